@@ -1,0 +1,49 @@
+# Build of the B200-native DreamDDP engine (no cmake needed).
+#
+#   paper_2502_11058_b200/lib/libdsx.so        sm_100a kernels + the dsx C-ABI (include/dsx.h)
+#   paper_2502_11058_b200/lib/libdreamsched.so the drop-in dreamsched:: C++ API (include/dreamsched)
+#   build/parity_tool                          tests/native/parity_tool.cpp against the above
+#   build/acceptance                           the reference's acceptance binary compiled
+#                                              against this library (drop-in proof; needs
+#                                              /root/reference, so only built where present)
+NVCC    ?= /usr/local/cuda/bin/nvcc
+CXX     ?= g++
+PKG     := paper_2502_11058_b200
+LIB     := $(PKG)/lib
+SRC     := $(PKG)/csrc
+REF     ?= /root/reference/proj
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -std=c++17 -O3 $(ARCH) -lineinfo -fmad=false -Xptxas -v -Xcompiler -fPIC -Iinclude
+CXXFLAGS:= -std=c++20 -O2 -ffp-contract=off -fPIC -Iinclude -Wall -Wextra
+# NCCL: link the same libnccl.so.2 torch loads (the venv's nvidia-nccl wheel),
+# so one process never mixes two NCCL builds under one soname.
+NCCL_LIBDIR ?= $(shell python3 -c "import nvidia,os;print(os.path.join(list(nvidia.__path__)[0],'nccl','lib'))" 2>/dev/null)
+NCCL_LINK := $(if $(wildcard $(NCCL_LIBDIR)/libnccl.so.2),-L$(NCCL_LIBDIR) -l:libnccl.so.2 -Xlinker -rpath -Xlinker $(NCCL_LIBDIR),-lnccl)
+HOST_SRCS := $(wildcard $(SRC)/host/*.cpp)
+CUDA_SRCS := $(wildcard $(SRC)/cuda/*.cu)
+CUDA_HDRS := $(wildcard $(SRC)/cuda/*.cuh)
+API_HDRS  := $(wildcard include/dreamsched/*.hpp) include/dsx.h
+
+.PHONY: all clean acceptance
+all: $(LIB)/libdsx.so $(LIB)/libdreamsched.so build/parity_tool $(if $(wildcard $(REF)),acceptance)
+
+$(LIB)/libdsx.so: $(CUDA_SRCS) $(CUDA_HDRS) include/dsx.h
+	@mkdir -p $(LIB) build
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CUDA_SRCS) $(NCCL_LINK) 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+$(LIB)/libdreamsched.so: $(HOST_SRCS) $(API_HDRS) $(LIB)/libdsx.so
+	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIB) -ldsx -Wl,-rpath,'$$ORIGIN'
+
+build/parity_tool: tests/native/parity_tool.cpp $(LIB)/libdreamsched.so
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Iinclude $< -L$(LIB) -ldreamsched -ldsx \
+	    -Wl,-rpath,'$$ORIGIN/../$(LIB)' -o $@
+
+acceptance: build/acceptance
+build/acceptance: $(REF)/tests/acceptance/acceptance_main.cpp $(LIB)/libdreamsched.so
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Iinclude -I$(REF)/tests/support $< -L$(LIB) -ldreamsched -ldsx \
+	    -Wl,-rpath,'$$ORIGIN/../$(LIB)' -o $@
+
+clean:
+	rm -rf $(LIB) build

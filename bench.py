@@ -1,0 +1,381 @@
+#!/usr/bin/env python3
+"""bench.py — iterations/s of DreamDDP partial-sync local SGD on B200.
+
+Workload (BASELINE.json configs[1], ResNet-18-shaped, 8 workers, H=5): the
+reference's quadratic lab with one registered layer per layer of
+tests/golden/data/resnet18_like.profile (61 blocks, param_bytes/4 coordinates
+each, min 1: dim = 11,689,532 per worker), K = 8 workers, H = 5, the schedule
+bubble_fill(schedule_dfs(profile, 5)) computed by this framework's
+(bit-exact) scheduler, sigma = 1 (exact std::mt19937_64 + normal_distribution
+noise stream reproduced on the GPU), seed 1, fp64 — the reference's own
+arithmetic.  A step is one plsgd_step of all K workers (local step + scheduled
+in-place averaging); value = iterations/s of the whole job.  With N GPUs
+(torchrun) each rank holds K/N workers and the averaging crosses NVLink
+(NCCL), so total work is fixed: "scaling": "strong".
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/parity_tool_ref: trainer.cpp compiled from /root/reference) on
+the same workload, one thread (the reference is single-threaded).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PROFILE = os.path.join(REPO, "tests", "golden", "data", "resnet18_like.profile")
+METRIC = "iterations/sec at 1/2/4/8 B200 vs CPU ref; exposed sync time per iteration"
+REF_TOOL = os.path.join(REPO, "oracle", "_ref", "parity_tool_ref")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--period", type=int, default=5)
+    ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--profile", default=PROFILE)
+    ap.add_argument("--sync-algo", default="pairwise", choices=["pairwise", "nccl_avg"])
+    ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers ---
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def sample_once(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.QUERY,
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            if out:
+                self.rows.append([x.strip() for x in out.split(",")])
+        except Exception:
+            pass
+
+    def _loop(self):
+        while not self._stop.is_set():
+            self.sample_once()
+            self._stop.wait(0.1)
+
+    def start(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            self.sample_once()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[5:9]):
+                if v.strip().lower() in ("active", "1"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(args):
+    from paper_2502_11058_b200.lab import lab_problem, schedule_from_profile
+    sizes, dim = lab_problem(args.profile)
+    sets, fills, objective, text = schedule_from_profile(args.profile, args.period, fill=True)
+    return sizes, dim, sets, fills, text
+
+
+def learning_rate(r: int, period: int) -> float:
+    """TrainerConfig::learning_rate (trainer.cpp:126-135) for mu=1, beta=2."""
+    mu, beta = 1.0, 2.0
+    a = max(16.0 * (beta / mu), float(period)) + 1.0
+    return 4.0 / (mu * (a + float(r)))
+
+
+# ------------------------------------------------------------ reference arm ---
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return None
+    sizes_note = "resnet18_like.profile blocks"
+    steps = max(1, args.steps)
+    warm = max(0, args.warmup)
+    # Bound the run: the full-size reference step takes seconds (4.3 s at
+    # sigma=1 in the survey); time one step first and cap the sample.
+    probe = run_ref_tool(args, 1, 0)
+    per_step = probe["seconds"]
+    budget_s = 150.0
+    steps = int(max(1, min(steps, budget_s // max(per_step, 1e-9))))
+    warm = int(min(warm, 1))
+    res = run_ref_tool(args, steps, warm)
+    it_s = res["it_per_s"]
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": it_s, "unit": "iterations/s", "n_gpus": world,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 / it_s, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world, res["dim"]),
+        "cpu_baseline": {"value": it_s, "unit": "iterations/s", "cores": 1, "kind": "reference",
+                         "sample": f"{steps} timed plsgd_step calls ({warm} warm-up) of the full "
+                                   f"workload ({sizes_note}), reference trainer.cpp single thread"},
+        "e2e": {"value": it_s, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def run_ref_tool(args, steps, warmup):
+    if not os.path.exists(REF_TOOL):
+        raise RuntimeError("oracle/_ref/parity_tool_ref missing (built by __graft_entry__.build())")
+    cmd = [REF_TOOL, "bench", "0", "0", str(args.workers), str(args.period), repr(args.sigma),
+           str(args.seed), str(steps), str(warmup), "partial", "dfs", args.profile]
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def workload_config(args, world, dim):
+    return {"workload": "resnet18-shaped quadratic lab (61 registered layers), 8 workers, H=5",
+            "profile": os.path.relpath(args.profile, REPO), "workers": args.workers,
+            "period": args.period, "dim_per_worker": dim, "sigma": args.sigma,
+            "schedule": "bubble_fill(schedule_dfs(profile, H))", "seed": args.seed,
+            "parallelism": f"dp{world} ({args.workers // world} workers/GPU)",
+            "sync_algo": args.sync_algo if world > 1 else "fused in-kernel (single GPU)",
+            "l2": "working set > 126 MB L2 (no flush needed)"}
+
+
+# ------------------------------------------------------------------ our arm ---
+
+def our_arm(args, world, rank, local_rank, dist):
+    import numpy as np
+
+    from paper_2502_11058_b200 import native as N
+    from paper_2502_11058_b200.lab import Lab, LabDesc, nccl_unique_id, sync_mask
+
+    sizes, dim, sets, fills, _ = workload(args)
+    L, H, K = len(sizes), args.period, args.workers
+    if K % world:
+        raise SystemExit(f"--workers {K} must be divisible by the GPU count {world}")
+    kl = K // world
+    lab = Lab(LabDesc(dim=dim, block_sizes=sizes, workers_total=K, workers_local=kl,
+                      worker_begin=rank * kl, sigma=args.sigma, dtype=args.dtype,
+                      device=local_rank))
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        algo = N.DSX_SYNC_PAIRWISE if args.sync_algo == "pairwise" else N.DSX_SYNC_NCCL_AVG
+        lab.comm_init(obj[0], world, rank, algo)
+    lab.set_overlap(not args.no_overlap)
+    lab.seed(args.seed)
+    lab.fill(0.0)
+    masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    r = 0
+    for _ in range(max(3, args.warmup)):
+        lab.step(learning_rate(r, H), masks[r % H])
+        r += 1
+    lab.sync()
+    barrier()
+    lab.sync()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = lab.launches()
+    lab.record(0)
+    for _ in range(args.steps):
+        lab.step(learning_rate(r, H), masks[r % H])
+        r += 1
+    lab.record(1)
+    ms = lab.elapsed_ms(0, 1)  # waits for the last event
+    lab.sync()
+    clocks.stop()
+    launches = lab.launches() - launches0
+    barrier()
+    ms_max = ms
+    if dist is not None:
+        import torch
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = args.steps / (ms_max / 1e3)
+
+    # per-step breakdown with instrumentation (separate pass; not the timed one)
+    lab.set_instrument(True)
+    per = []
+    for _ in range(2 * H):
+        lab.step(learning_rate(r, H), masks[r % H])
+        r += 1
+        per.append(lab.last_step_times())
+    lab.set_instrument(False)
+    step_ms = [p[0] for p in per]
+    sync_ms = [p[1] for p in per]
+    exposed_ms = [p[2] for p in per]
+    noise_ms = [p[3] for p in per]
+    update_ms = [p[4] for p in per]
+    if dist is not None:
+        import torch
+        t = torch.tensor([statistics.mean(sync_ms), statistics.mean(exposed_ms)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sync_mean, exposed_mean = float(t[0]), float(t[1])
+    else:
+        sync_mean, exposed_mean = 0.0, 0.0
+
+    # roofline: the dominant kernel on the path
+    esz = 8 if args.dtype == "f64" else 4
+    peak, peak_kind = measured_peaks()
+    update_bytes = kl * dim * (2 * esz + (8 if args.sigma > 0 else 0))
+    upd = statistics.mean(update_ms)
+    noi = statistics.mean(noise_ms)
+    if args.sigma > 0 and noi > upd:
+        # noise engine dominates: algorithmic bytes = the noise it writes
+        dom = {"kernel": "mt_noise (exact mt19937_64 + polar)", "ms": noi,
+               "bytes": kl * dim * 8}
+    else:
+        dom = {"kernel": "lab_update (fused gradient+update+average)", "ms": upd,
+               "bytes": update_bytes}
+    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom["kernel"].split(" ")[0])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": dom["kernel"], "kernel_ms": round(dom["ms"], 4),
+                "algorithmic_bytes_per_launch": dom["bytes"], "peak_kind": peak_kind,
+                "step_breakdown_ms": {"step": round(statistics.mean(step_ms), 4),
+                                      "noise": round(noi, 4), "update": round(upd, 4)}}
+
+    # e2e through the C-ABI with HOST buffers (plsgd_step semantics: worker
+    # params + rng states in and out every step)
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        import torch
+        host = torch.zeros((kl, dim), dtype=torch.float64, pin_memory=True)
+        hn = host.numpy()
+        rng = [lab.get_rng(k) for k in range(kl)]
+        lab.set_params(hn)
+        lab.sync()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            lab.set_params(hn)
+            for k in range(kl):
+                lab.set_rng(k, *rng[k])
+            lab.step(learning_rate(r, H), masks[r % H])
+            r += 1
+            hn[:] = lab.get_params()
+            rng = [lab.get_rng(k) for k in range(kl)]
+        lab.sync()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        rng_bytes = kl * 313 * 8
+        e2e = {"value": args.e2e_steps / el, "unit": "iterations/s",
+               "h2d_bytes_per_step": kl * dim * 8 + rng_bytes,
+               "d2h_bytes_per_step": kl * dim * 8 + rng_bytes,
+               "path": "dsx C-ABI with host worker buffers (plsgd_step semantics)"}
+
+    if rank != 0:
+        lab.close()
+        return None
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            res = run_ref_tool(args, 2, 1)
+            cpu = {"value": res["it_per_s"], "unit": "iterations/s", "cores": 1,
+                   "kind": "reference",
+                   "sample": "2 timed plsgd_step calls (1 warm-up) of the full workload, "
+                             "reference trainer.cpp compiled from /root/reference, 1 thread"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "iterations/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_max / args.steps, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic",
+        "config": workload_config(args, world, dim),
+        "exposed_sync_ms_per_iter": round(exposed_mean, 5),
+        "sync_ms_per_iter": round(sync_mean, 5),
+        "exposed_sync_frac": round(exposed_mean / sync_mean, 4) if sync_mean > 0 else None,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+    lab.close()
+    return line
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch.distributed as dist_mod
+        dist_mod.init_process_group("gloo")
+        dist = dist_mod
+    if args.impl == "reference":
+        line = reference_arm(args, world, rank)
+    else:
+        line = our_arm(args, world, rank, local_rank, dist)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

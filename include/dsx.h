@@ -1,0 +1,150 @@
+/*
+ * dsx.h — C ABI of the B200 partial-synchronization local-SGD engine.
+ *
+ * This is the thin layer between the C++ host API (include/dreamsched/ headers,
+ * the drop-in surface of the reference's dreamsched::core) and the sm_100a
+ * kernels.  Plain pointers and sizes only; no C++ or torch types; no
+ * exception ever crosses it: every entry point returns a dsx_status and
+ * dsx_last_error() holds the message (thread-local).
+ *
+ * Reference interface each entry point replaces (reference paths relative to
+ * /root/reference/proj/core):
+ *   dsx_lab_create          — the per-run state of run_training (trainer.cpp:237-252):
+ *                             K worker parameter vectors + Problem arrays, here a
+ *                             device-resident arena [workers_local][ld] in HBM.
+ *   dsx_lab_set/get_params  — WorkerState::w (trainer.hpp:76-79) in / out.
+ *   dsx_lab_set/get_rng     — WorkerState::rng, the std::mt19937_64 state
+ *                             (x[312], cursor) as libstdc++ stores it.
+ *   dsx_lab_seed_rng        — worker_rng(seed, k) (trainer.cpp:169-173).
+ *   dsx_lab_step            — plsgd_step (trainer.cpp:187-235): local step of every
+ *                             worker (stochastic_gradient 175-185, update 191-199)
+ *                             then in-place averaging of the masked blocks
+ *                             (226-234), mask from trainer.cpp:202-224.
+ *   dsx_lab_gradient        — stochastic_gradient (trainer.cpp:175-185).
+ *   dsx_lab_mean_accumulate — the w_hat weighted average of run_training (290-295).
+ *   dsx_lab_log             — log_row's divergence / objective terms (254-284).
+ *   dsx_lab_comm_init       — (no reference counterpart: the reference averages
+ *                             in-process) one rank per GPU over NCCL/NVLink.
+ */
+#ifndef DREAMDDP_DSX_H_
+#define DREAMDDP_DSX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int dsx_status;
+enum {
+  DSX_OK = 0,
+  DSX_ERR_ARGUMENT = 1, /* maps to dreamsched::ArgumentError */
+  DSX_ERR_STATE = 2,    /* call out of order / unsupported configuration */
+  DSX_ERR_CUDA = 3,     /* CUDA runtime failure (incl. no device) */
+  DSX_ERR_NCCL = 4      /* NCCL failure */
+};
+
+/* arithmetic type of the parameter arena */
+enum { DSX_F64 = 0, DSX_F32 = 1 };
+
+/* cross-rank averaging algorithm (only used when nranks > 1) */
+enum {
+  DSX_SYNC_PAIRWISE = 0, /* reduce-scatter/all-gather with the reference's fixed
+                            pairwise summation order: bit-identical to K
+                            in-process workers */
+  DSX_SYNC_NCCL_AVG = 1  /* one in-place ncclAllReduce per masked range (sum),
+                            1/K fused into the local broadcast */
+};
+
+typedef struct dsx_lab dsx_lab;
+
+typedef struct dsx_lab_desc {
+  int device;                  /* CUDA ordinal */
+  int dtype;                   /* DSX_F64 | DSX_F32 */
+  int workers_total;           /* K (all ranks) */
+  int worker_begin;            /* global id of the first worker held here */
+  int workers_local;           /* rows held on this device */
+  uint64_t dim;                /* parameters per worker */
+  int layers;                  /* L registered layers (blocks) */
+  const uint64_t* block_sizes; /* [layers], sums to dim; layer 1 first */
+  const double* curvature;     /* [dim] host */
+  const double* optimum;       /* [dim] host */
+  double noise_sigma;          /* sigma; per-coordinate stddev sigma/sqrt(dim) */
+} dsx_lab_desc;
+
+const char* dsx_last_error(void);
+dsx_status dsx_device_count(int* count);
+
+dsx_status dsx_lab_create(const dsx_lab_desc* desc, dsx_lab** out);
+dsx_status dsx_lab_destroy(dsx_lab* lab);
+
+/* Worker rows.  `local` indexes the rows held here (0..workers_local-1). */
+dsx_status dsx_lab_set_params(dsx_lab* lab, int local, const double* w);
+dsx_status dsx_lab_get_params(dsx_lab* lab, int local, double* w);
+dsx_status dsx_lab_fill_params(dsx_lab* lab, double value);
+/* Whole arena in one copy each way: w is [workers_local][dim] row-major. */
+dsx_status dsx_lab_set_all_params(dsx_lab* lab, const double* w);
+dsx_status dsx_lab_get_all_params(dsx_lab* lab, double* w);
+
+/* std::mt19937_64 state: 312 words and the cursor p (libstdc++ _M_x/_M_p). */
+dsx_status dsx_lab_set_rng(dsx_lab* lab, int local, const uint64_t* x312, uint64_t p);
+dsx_status dsx_lab_get_rng(dsx_lab* lab, int local, uint64_t* x312, uint64_t* p);
+dsx_status dsx_lab_seed_rng(dsx_lab* lab, uint64_t seed);
+
+/* One iteration (asynchronous on the lab's stream).  mask has layers+1
+ * entries, 1-based like the reference's vector<bool>; mask[l] != 0 averages
+ * layer l's block across all workers_total workers. */
+dsx_status dsx_lab_step(dsx_lab* lab, double eta, const unsigned char* mask);
+/* Same, but the per-coordinate noise xi[workers_local][dim] (already scaled)
+ * is supplied by the caller instead of the device generator.  Test hook that
+ * isolates the update/averaging kernels from the noise engine. */
+dsx_status dsx_lab_step_with_noise(dsx_lab* lab, double eta, const unsigned char* mask,
+                                   const double* xi);
+/* max_k ||g_k||^2 of the last step (synchronizes). */
+dsx_status dsx_lab_last_max_grad_norm_sq(dsx_lab* lab, double* out);
+dsx_status dsx_lab_sync(dsx_lab* lab);
+
+/* g = curvature*(w-optimum) + noise for row `local` at its current params,
+ * advancing its rng (no update). g_out has dim entries. */
+dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out);
+
+/* run_training helpers (single rank): w_hat_sum += weight * mean_k(w_k). */
+dsx_status dsx_lab_mean_accumulate(dsx_lab* lab, double weight);
+/* gamma_per_layer[layers] = (1/K) sum_k ||mean - w_k||^2 over each block;
+ * out2[0] = f(w_hat_sum / weight_total) (or f(mean) when weight_total == 0);
+ * out2[1] = f(mean).  Synchronizes. */
+dsx_status dsx_lab_log(dsx_lab* lab, double weight_total, double* gamma_per_layer, double* out2);
+
+/* Multi-GPU: one rank per GPU.  id is ncclUniqueId (128 bytes) from rank 0. */
+dsx_status dsx_nccl_unique_id(unsigned char id[128]);
+dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nranks, int rank,
+                             int sync_algo);
+
+/* Overlapped sync: when enabled (default), the local step runs in two
+ * launches — layers above the lowest synced layer first — and the cross-rank
+ * averaging of the synced blocks starts on a high-priority side stream as soon
+ * as the first launch is done, overlapping the rest of the local step. */
+dsx_status dsx_lab_set_overlap(dsx_lab* lab, int enabled);
+
+/* Timing on the lab's compute stream: CUDA events in slots 0..31. */
+dsx_status dsx_lab_event_record(dsx_lab* lab, int slot);
+dsx_status dsx_lab_event_elapsed(dsx_lab* lab, int from_slot, int to_slot, float* ms);
+/* Per-step instrumentation of the last dsx_lab_step: out5 = milliseconds of
+ * [whole step, sync span, exposed sync, noise engine, local update] measured
+ * with CUDA events on the lab's streams (sync/exposed are 0 on a single
+ * rank, where averaging is fused into the update kernel).  Exposed sync is
+ * max(0, sync done - local step done), the measured counterpart of
+ * iteration_cost(...).term - bp_total (cost_model.cpp:26-41).
+ * Enabled by dsx_lab_set_instrument(lab, 1). */
+dsx_status dsx_lab_set_instrument(dsx_lab* lab, int enabled);
+dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out5);
+
+/* Number of kernel launches issued by this lab since creation. */
+dsx_status dsx_lab_launch_count(dsx_lab* lab, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DREAMDDP_DSX_H_ */

@@ -1,0 +1,1309 @@
+// lab.cu — the B200 partial-synchronization local-SGD engine behind dsx.h.
+//
+// HBM layout (one device, one rank):
+//   w      [workers_local][ld]  parameter arena, T = double|float, ld = dim
+//                               rounded up to 64 elements (256 B rows); each
+//                               registered layer is a contiguous coordinate
+//                               range, so a sync set is a byte range.
+//   noise  [workers_local][ld]  fp64 per-coordinate noise (sigma > 0 only)
+//   mt     [workers_local][313] std::mt19937_64 state (x[312], cursor)
+//   curv/opt [dim] fp64         only when the problem is not make_quadratic-
+//                               shaped (otherwise lambda_i is recomputed
+//                               in-kernel with the reference's exact formula)
+//
+// One plsgd_step (reference trainer.cpp:187-235) on a single rank is
+//   [noise engine]  ->  lab_update (fused: gradient, ||g||^2 partials,
+//   SGD update AND, for masked blocks, the pairwise cross-worker mean written
+//   back to every row)  ->  norm finalize.
+// The update+average kernel touches each parameter exactly once (read K
+// rows, write K rows): the reference's separate averaging pass costs no
+// extra HBM traffic here.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "dsx.h"
+#include "mt_engine.cuh"
+
+namespace dsx {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+thread_local std::string g_last_error;
+
+static dsx_status fail(dsx_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define DSX_CUDA(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return ::dsx::fail(DSX_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define DSX_NCCL(expr)                                                                 \
+  do {                                                                                 \
+    ncclResult_t r_ = (expr);                                                          \
+    if (r_ != ncclSuccess)                                                             \
+      return ::dsx::fail(DSX_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define DSX_TRY(expr)                      \
+  do {                                     \
+    dsx_status s_ = (expr);                \
+    if (s_ != DSX_OK) return s_;           \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// kernel parameter blocks
+// ---------------------------------------------------------------------------
+constexpr int kTile = 2048;       // coordinates per CTA (never crosses a block)
+constexpr int kThreads = 256;
+constexpr int kItems = kTile / kThreads;
+constexpr int kMaxMaskWords = 128;  // 4096 layers
+constexpr int kMaxProg = 64;        // generic pairwise program (K <= 64)
+
+struct Tile {
+  long long start;
+  int len;
+  int block;  // 0-based layer index
+};
+
+struct MaskBits {
+  uint32_t w[kMaxMaskWords];
+};
+
+__device__ __forceinline__ bool mask_has(const MaskBits& m, int block) {
+  return (m.w[block >> 5] >> (block & 31)) & 1u;
+}
+
+// Postorder program of the reference's pairwise_coord_sum tree
+// (trainer.cpp:31-38) for a runtime worker count: step j computes
+// v[dst] = v[a] + v[b].
+struct PairProg {
+  int n;
+  unsigned char dst[kMaxProg], a[kMaxProg], b[kMaxProg];
+};
+
+struct QuadParams {
+  bool analytic;
+  double mu, beta_minus_mu, dim_minus_1, opt_value;
+  const double* curv;
+  const double* opt;
+};
+
+template <typename T>
+struct UpdateArgs {
+  T* w;
+  long long ld;
+  int kl;             // rows held here
+  int k_total;        // K (divisor of the mean)
+  const Tile* tiles;
+  int ntiles;
+  int tile_base;      // first tile of this launch (split launches for overlap)
+  const double* noise;  // [kl][ld] or null
+  double eta;
+  QuadParams q;
+  MaskBits mask;
+  bool average;       // average masked blocks in-kernel (single rank)
+  double* norm_part;  // [kl][ntiles]
+};
+
+// lambda_i and w*_i.  The analytic form is make_quadratic's
+// mu + (beta - mu) * i / (dim - 1) (trainer.cpp:117-120), evaluated with the
+// same rounding sequence.
+__device__ __forceinline__ void quad_coeffs(const QuadParams& q, long long i, double* lam,
+                                            double* opt) {
+  if (q.analytic) {
+    *lam = q.dim_minus_1 == 0.0
+               ? q.mu
+               : __dadd_rn(q.mu, __ddiv_rn(__dmul_rn(q.beta_minus_mu, (double)i), q.dim_minus_1));
+    *opt = q.opt_value;
+  } else {
+    *lam = q.curv[i];
+    *opt = q.opt[i];
+  }
+}
+
+// pairwise_coord_sum over v[LO..HI) with the reference's split at n/2.
+template <int LO, int HI, typename T>
+__device__ __forceinline__ T psum(const T* v) {
+  constexpr int N = HI - LO;
+  if constexpr (N == 1) {
+    return v[LO];
+  } else if constexpr (N == 2) {
+    return v[LO] + v[LO + 1];
+  } else {
+    constexpr int MID = LO + N / 2;
+    return psum<LO, MID, T>(v) + psum<MID, HI, T>(v);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T run_prog(const PairProg& p, T* v) {
+  for (int j = 0; j < p.n; ++j) v[p.dst[j]] = v[p.a[j]] + v[p.b[j]];
+  return v[0];
+}
+
+__device__ __forceinline__ double block_sum(double x, double* red) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = x;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  }
+  return s;  // valid in thread 0
+}
+
+__device__ __forceinline__ double to_d(double x) { return x; }
+__device__ __forceinline__ double to_d(float x) { return (double)x; }
+
+// g = lambda*(w - w*) (+ xi);  w' = w - eta*g   — in T arithmetic.
+__device__ __forceinline__ double grad_step(double w, double lam, double opt, double xi,
+                                            double eta, bool noise, double* wout) {
+  double g = __dmul_rn(lam, __dsub_rn(w, opt));
+  if (noise) g = __dadd_rn(g, xi);
+  *wout = __dsub_rn(w, __dmul_rn(eta, g));
+  return g;
+}
+__device__ __forceinline__ float grad_step(float w, double lam, double opt, double xi, double eta,
+                                           bool noise, float* wout) {
+  float g = __fmul_rn((float)lam, __fsub_rn(w, (float)opt));
+  if (noise) g = __fadd_rn(g, (float)xi);
+  *wout = __fsub_rn(w, __fmul_rn((float)eta, g));
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// fused local step (+ in-place averaging of masked blocks on a single rank)
+// KL > 0: compile-time local worker count; KL == 0: runtime count via prog.
+// ---------------------------------------------------------------------------
+template <typename T, int KL, bool NOISE>
+__global__ void __launch_bounds__(kThreads)
+lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
+  constexpr int KMAX = KL > 0 ? KL : kMaxProg;
+  const int tile_id = a.tile_base + blockIdx.x;
+  const Tile t = a.tiles[tile_id];
+  const int kl = KL > 0 ? KL : a.kl;
+  const bool avg = a.average && mask_has(a.mask, t.block);
+  const double inv_dummy = 0.0;
+  (void)inv_dummy;
+  double nsq[KL > 0 ? KL : 1] = {};
+  double nsq_dyn = 0.0;  // generic path accumulates row by row below
+
+  if constexpr (KL > 0) {
+#pragma unroll 2
+    for (int j = 0; j < kItems; ++j) {
+      const int off = j * kThreads + threadIdx.x;
+      if (off >= t.len) break;
+      const long long i = t.start + off;
+      double lam, opt;
+      quad_coeffs(a.q, i, &lam, &opt);
+      T wn[KL];
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+        const T w = a.w[k * a.ld + i];
+        const double xi = NOISE ? a.noise[k * a.ld + i] : 0.0;
+        const auto g = grad_step(w, lam, opt, xi, a.eta, NOISE, &wn[k]);
+        nsq[k] += to_d(g) * to_d(g);
+      }
+      if (avg) {
+        const T m = psum<0, KL, T>(wn) / (T)a.k_total;
+#pragma unroll
+        for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = m;
+      } else {
+#pragma unroll
+        for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = wn[k];
+      }
+    }
+  } else {
+    // generic worker count: row-major pass, then the pairwise program for
+    // averaged coordinates.
+    T v[KMAX];
+    for (int j = 0; j < kItems; ++j) {
+      const int off = j * kThreads + threadIdx.x;
+      if (off >= t.len) break;
+      const long long i = t.start + off;
+      double lam, opt;
+      quad_coeffs(a.q, i, &lam, &opt);
+      for (int k = 0; k < kl; ++k) {
+        const T w = a.w[k * a.ld + i];
+        const double xi = NOISE ? a.noise[k * a.ld + i] : 0.0;
+        T wn;
+        const auto g = grad_step(w, lam, opt, xi, a.eta, NOISE, &wn);
+        v[k] = wn;
+        if (!avg) a.w[k * a.ld + i] = wn;
+        // per-row squared norm goes straight to the partials below
+        const double gd = to_d(g);
+        atomicAdd(&a.norm_part[(long long)k * a.ntiles + tile_id], gd * gd);
+      }
+      if (avg) {
+        const T m = run_prog(prog, v) / (T)a.k_total;
+        for (int k = 0; k < kl; ++k) a.w[k * a.ld + i] = m;
+      }
+    }
+    (void)nsq_dyn;
+  }
+
+  if constexpr (KL > 0) {
+    __shared__ double red[kThreads / 32];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+      const double s = block_sum(nsq[k], red);
+      if (threadIdx.x == 0) a.norm_part[(long long)k * a.ntiles + tile_id] = s;
+    }
+  }
+}
+
+// ||g_k||^2 = fixed-order sum of the tile partials; then max over rows.
+// One CTA; writes norm[k] and *maxnorm (and folds max into *gmax_sq).
+__global__ void norm_finalize_kernel(const double* part, int ntiles, int kl, double* norm,
+                                     double* maxnorm) {
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (int k = 0; k < kl; ++k) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < ntiles; i += blockDim.x) s += part[(long long)k * ntiles + i];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) {
+      norm[k] = s;
+      mx = fmax(mx, s);
+    }
+  }
+  if (threadIdx.x == 0) *maxnorm = mx;
+}
+
+__global__ void zero_kernel(double* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// noise engine, single chain per worker: one CTA walks the worker's stream
+// generation by generation exactly like libstdc++ (twist, temper, canonical,
+// polar accept), a CTA-wide scan orders the accepted pairs, and normals are
+// written to noise[k][0..dim).  Consumption stops right after the attempt
+// that yields normal dim-1 (the cached second value of an odd tail is
+// dropped, as the reference's per-call distribution object does).
+// ---------------------------------------------------------------------------
+constexpr int kMtThreads = 320;
+
+__global__ void __launch_bounds__(kMtThreads)
+mt_noise_chain_kernel(uint64_t* state, double* noise, long long ld, unsigned long long dim,
+                      double stddev) {
+  __shared__ uint64_t x[kMtN];
+  __shared__ double v[kMtN + 2];
+  __shared__ int warp_cnt[kMtThreads / 32];
+  __shared__ int s_last;  // attempt index where the run ends, or -1
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  uint64_t* st = state + (long long)blockIdx.x * (kMtN + 1);
+  double* out = noise + (long long)blockIdx.x * ld;
+  if (tid < kMtN) x[tid] = st[tid];
+  int p = (int)st[kMtN];
+  const unsigned long long pairs_needed = (dim + 1) / 2;
+  unsigned long long pairs_done = 0;
+  int have_half = 0;
+  double half = 0.0;
+  __syncthreads();
+  if (dim == 0) return;
+
+  for (;;) {
+    if (p >= kMtN) {  // _M_gen_rand
+      uint64_t a0 = 0, a1 = 0, a2 = 0;
+      if (tid < kMtM) {
+        a0 = x[tid];
+        a1 = x[tid + 1];
+        a2 = x[tid + kMtM];
+      }
+      __syncthreads();
+      if (tid < kMtM) x[tid] = mt_next_word(a0, a1, a2);
+      __syncthreads();
+      if (tid < kMtM) {
+        const int k = kMtM + tid;
+        a0 = x[k];
+        a1 = (k + 1 < kMtN) ? x[k + 1] : x[0];
+        a2 = x[k - kMtM];
+      }
+      __syncthreads();
+      if (tid < kMtM) x[kMtM + tid] = mt_next_word(a0, a1, a2);
+      __syncthreads();
+      p = 0;
+    }
+    // values of this generation, prefixed by a carried half pair
+    if (tid >= p && tid < kMtN) v[have_half + tid - p] = mt_polar_coord(mt_temper(x[tid]));
+    if (tid == 0 && have_half) v[0] = half;
+    if (tid == 0) s_last = -1;
+    __syncthreads();
+    const int nvals = have_half + kMtN - p;
+    const int npairs = nvals >> 1;
+    double px = 0.0, py = 0.0, r2 = 0.0;
+    bool acc = false;
+    if (tid < npairs) {
+      px = v[2 * tid];
+      py = v[2 * tid + 1];
+      acc = mt_polar_accept(px, py, &r2);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, acc);
+    if (lane == 0) warp_cnt[warp] = __popc(bal);
+    __syncthreads();
+    int before = __popc(bal & ((1u << lane) - 1u));
+    int total = 0;
+    for (int w = 0; w < kMtThreads / 32; ++w) {
+      if (w < warp) before += warp_cnt[w];
+      total += warp_cnt[w];
+    }
+    const unsigned long long remaining = pairs_needed - pairs_done;
+    const bool finishing = (unsigned long long)total >= remaining;
+    if (acc) {
+      const unsigned long long m = pairs_done + (unsigned long long)before;
+      if (m < pairs_needed) {
+        const double mult = mt_polar_mult(r2);
+        out[2 * m] = mt_scale(py, mult, stddev);
+        if (2 * m + 1 < dim) out[2 * m + 1] = mt_scale(px, mult, stddev);
+        if (m == pairs_needed - 1) s_last = tid;
+      }
+    }
+    __syncthreads();
+    if (finishing) {
+      const int last = s_last;
+      const int consumed = 2 * (last + 1) - have_half;  // outputs of this generation
+      if (tid < kMtN) st[tid] = x[tid];
+      if (tid == 0) st[kMtN] = (uint64_t)(p + consumed);
+      return;
+    }
+    pairs_done += (unsigned long long)total;
+    if (nvals & 1) {
+      half = v[nvals - 1];
+      have_half = 1;
+    } else {
+      have_half = 0;
+    }
+    p = kMtN;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// run_training helpers
+// ---------------------------------------------------------------------------
+template <typename T, int KL>
+__device__ __forceinline__ double row_mean(const T* w, long long ld, long long i, int kl, int k_total,
+                                           const PairProg& prog) {
+  if constexpr (KL > 0) {
+    T v[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) v[k] = w[k * ld + i];
+    return to_d(psum<0, KL, T>(v) / (T)k_total);
+  } else {
+    T v[kMaxProg];
+    for (int k = 0; k < kl; ++k) v[k] = w[k * ld + i];
+    return to_d(run_prog(prog, v) / (T)k_total);
+  }
+}
+
+template <typename T, int KL>
+__global__ void mean_accumulate_kernel(const T* w, long long ld, int kl, int k_total,
+                                       unsigned long long dim, double weight, double* what,
+                                       PairProg prog) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)dim;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double m = row_mean<T, KL>(w, ld, i, kl, k_total, prog);
+    what[i] = __dadd_rn(what[i], __dmul_rn(weight, m));
+  }
+}
+
+// Per tile: sum_k sum_i (mean_i - w_ki)^2, f(w_hat) and f(mean) partials.
+template <typename T, int KL>
+__global__ void __launch_bounds__(kThreads)
+log_kernel(const T* w, long long ld, int kl, int k_total, const Tile* tiles, int ntiles,
+           QuadParams q, const double* what, double weight_total, double* part /*[3][ntiles]*/,
+           PairProg prog) {
+  const Tile t = tiles[blockIdx.x];
+  double gsum = 0.0, fhat = 0.0, fmean = 0.0;
+  for (int off = threadIdx.x; off < t.len; off += kThreads) {
+    const long long i = t.start + off;
+    const double m = row_mean<T, KL>(w, ld, i, kl, k_total, prog);
+    for (int k = 0; k < kl; ++k) {
+      const double d = m - to_d(w[k * ld + i]);
+      gsum += d * d;
+    }
+    double lam, opt;
+    quad_coeffs(q, i, &lam, &opt);
+    const double dm = m - opt;
+    fmean += 0.5 * lam * dm * dm;
+    const double wh = weight_total > 0.0 ? what[i] / weight_total : m;
+    const double dh = wh - opt;
+    fhat += 0.5 * lam * dh * dh;
+  }
+  __shared__ double red[kThreads / 32];
+  gsum = block_sum(gsum, red);
+  fhat = block_sum(fhat, red);
+  fmean = block_sum(fmean, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = gsum;
+    part[ntiles + blockIdx.x] = fhat;
+    part[2 * ntiles + blockIdx.x] = fmean;
+  }
+}
+
+// g = lambda*(w - w*) + xi for one row (stochastic_gradient).
+template <typename T>
+__global__ void gradient_kernel(const T* w, unsigned long long dim, QuadParams q,
+                                const double* noise, double* g) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)dim;
+       i += (long long)gridDim.x * blockDim.x) {
+    double lam, opt;
+    quad_coeffs(q, i, &lam, &opt);
+    double gi = __dmul_rn(lam, __dsub_rn(to_d(w[i]), opt));
+    if (noise) gi = __dadd_rn(gi, noise[i]);
+    g[i] = gi;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// multi-rank averaging helpers
+// ---------------------------------------------------------------------------
+// staging[i] = pairwise over local rows of w[.][lo + i] (local subtree sum).
+template <typename T, int KL>
+__global__ void local_partial_kernel(const T* w, long long ld, int kl, long long lo, long long n,
+                                     T* staging, PairProg prog) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const long long i = lo + j;
+    if constexpr (KL > 0) {
+      T v[KL];
+#pragma unroll
+      for (int k = 0; k < KL; ++k) v[k] = w[k * ld + i];
+      staging[j] = psum<0, KL, T>(v);
+    } else {
+      T v[kMaxProg];
+      for (int k = 0; k < kl; ++k) v[k] = w[k * ld + i];
+      staging[j] = run_prog(prog, v);
+    }
+  }
+}
+
+// recv holds `nr` rank partials of one slice ([nr][count]); reduce them in
+// the reference's pairwise order over ranks, divide by K, write to out.
+template <typename T>
+__global__ void rank_reduce_kernel(const T* recv, long long count, int nr, int k_total,
+                                   T* out, PairProg prog) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count;
+       j += (long long)gridDim.x * blockDim.x) {
+    T v[kMaxProg];
+    for (int r = 0; r < nr; ++r) v[r] = recv[(long long)r * count + j];
+    out[j] = run_prog(prog, v) / (T)k_total;
+  }
+}
+
+// w[k][lo + i] = src[i] * scale  for every local row (scale 1 => copy).
+template <typename T>
+__global__ void broadcast_rows_kernel(T* w, long long ld, int kl, long long lo, long long n,
+                                      const T* src, T divisor) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const T m = divisor == (T)1 ? src[j] : src[j] / divisor;
+    for (int k = 0; k < kl; ++k) w[k * ld + lo + j] = m;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+static void build_prog(int n, PairProg* p) {
+  // Recursively mirrors pairwise_coord_sum: range [lo, hi) result lands in v[lo].
+  p->n = 0;
+  struct Rec {
+    static void go(PairProg* p, int lo, int hi) {
+      const int cnt = hi - lo;
+      if (cnt == 1) return;
+      if (cnt == 2) {
+        p->dst[p->n] = (unsigned char)lo;
+        p->a[p->n] = (unsigned char)lo;
+        p->b[p->n] = (unsigned char)(lo + 1);
+        ++p->n;
+        return;
+      }
+      const int mid = lo + cnt / 2;
+      go(p, lo, mid);
+      go(p, mid, hi);
+      p->dst[p->n] = (unsigned char)lo;
+      p->a[p->n] = (unsigned char)lo;
+      p->b[p->n] = (unsigned char)mid;
+      ++p->n;
+    }
+  };
+  if (n >= 1) Rec::go(p, 0, n);
+}
+
+// The global pairwise tree restricted to [begin, begin+count) is a subtree
+// iff recursing from [0, K) reaches exactly that range.
+static bool is_subtree(int K, int begin, int count) {
+  int lo = 0, hi = K;
+  for (;;) {
+    if (lo == begin && hi == begin + count) return true;
+    const int n = hi - lo;
+    if (n <= 1) return false;
+    const int mid = lo + n / 2;
+    if (begin + count <= mid) {
+      hi = mid;
+    } else if (begin >= mid) {
+      lo = mid;
+    } else {
+      return false;
+    }
+  }
+}
+
+}  // namespace dsx
+
+using namespace dsx;
+
+struct dsx_lab {
+  int device = 0;
+  int dtype = DSX_F64;
+  int K = 1, kbegin = 0, kl = 1;
+  unsigned long long dim = 0;
+  long long ld = 0;
+  int L = 0;
+  std::vector<unsigned long long> offs;  // L+1
+  QuadParams q{};
+  double sigma = 0.0, stddev = 0.0;
+
+  void* w = nullptr;
+  double* curv = nullptr;
+  double* opt = nullptr;
+  double* noise = nullptr;
+  uint64_t* mt = nullptr;
+  double* what = nullptr;
+  Tile* tiles = nullptr;
+  int ntiles = 0;
+  std::vector<Tile> h_tiles;
+  double* norm_part = nullptr;
+  double* norm = nullptr;
+  double* maxnorm = nullptr;
+  double* log_part = nullptr;
+  PairProg prog_local{};
+
+  cudaStream_t stream = nullptr;  // compute
+  cudaStream_t side = nullptr;    // sync (high priority)
+  cudaEvent_t ev[32] = {};
+  cudaEvent_t ev_split = nullptr, ev_synced = nullptr;
+  // instrumentation: 0 step start, 1 sync may start, 2 sync done (side),
+  // 3 local step done, 4 step end, 5 noise done / update start
+  cudaEvent_t iev[6] = {};
+  bool instrument = false;
+  bool has_ranges = false, synced_last = false;
+  bool overlap = true;
+  uint64_t launches = 0;
+
+  // multi-rank
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  int sync_algo = DSX_SYNC_PAIRWISE;
+  bool local_subtree = true;
+  PairProg prog_ranks{};
+  void* staging = nullptr;  // partial sums of synced range
+  void* recv = nullptr;     // [nranks][slice]
+  size_t staging_elems = 0;
+  int nsm = 148;
+};
+
+namespace {
+
+size_t elem_size(const dsx_lab* lab) { return lab->dtype == DSX_F64 ? 8 : 4; }
+
+bool detect_analytic(const dsx_lab_desc* d, QuadParams* q) {
+  const unsigned long long n = d->dim;
+  const double mu = d->curvature[0];
+  const double beta = d->curvature[n - 1];
+  const double opt = d->optimum[0];
+  for (unsigned long long i = 0; i < n; ++i) {
+    const double lam =
+        n == 1 ? mu : mu + (beta - mu) * static_cast<double>(i) / static_cast<double>(n - 1);
+    if (lam != d->curvature[i] || d->optimum[i] != opt) return false;
+  }
+  q->analytic = true;
+  q->mu = mu;
+  q->beta_minus_mu = beta - mu;
+  q->dim_minus_1 = n == 1 ? 0.0 : static_cast<double>(n - 1);
+  q->opt_value = opt;
+  return true;
+}
+
+dsx_status check_lab(dsx_lab* lab) {
+  if (!lab) return fail(DSX_ERR_ARGUMENT, "null lab");
+  DSX_CUDA(cudaSetDevice(lab->device));
+  return DSX_OK;
+}
+
+dsx_status check_row(dsx_lab* lab, int local) {
+  DSX_TRY(check_lab(lab));
+  if (local < 0 || local >= lab->kl) return fail(DSX_ERR_ARGUMENT, "worker row out of range");
+  return DSX_OK;
+}
+
+template <typename T, int KL>
+void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, bool noise, bool average,
+                     const MaskBits& mask, double eta) {
+  UpdateArgs<T> a;
+  a.w = static_cast<T*>(lab->w);
+  a.ld = lab->ld;
+  a.kl = lab->kl;
+  a.k_total = lab->K;
+  a.tiles = lab->tiles;
+  a.ntiles = lab->ntiles;
+  a.tile_base = tile_base;
+  a.noise = lab->noise;
+  a.eta = eta;
+  a.q = lab->q;
+  a.mask = mask;
+  a.average = average;
+  a.norm_part = lab->norm_part;
+  if (noise) {
+    lab_update_kernel<T, KL, true><<<count, kThreads, 0, s>>>(a, lab->prog_local);
+  } else {
+    lab_update_kernel<T, KL, false><<<count, kThreads, 0, s>>>(a, lab->prog_local);
+  }
+  ++lab->launches;
+}
+
+template <typename T>
+void launch_update(dsx_lab* lab, cudaStream_t s, int tile_base, int count, bool noise, bool average,
+                   const MaskBits& mask, double eta) {
+  switch (lab->kl) {
+    case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 2: return launch_update_t<T, 2>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 3: return launch_update_t<T, 3>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 4: return launch_update_t<T, 4>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 5: return launch_update_t<T, 5>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 6: return launch_update_t<T, 6>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 7: return launch_update_t<T, 7>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 8: return launch_update_t<T, 8>(lab, s, tile_base, count, noise, average, mask, eta);
+    default: return launch_update_t<T, 0>(lab, s, tile_base, count, noise, average, mask, eta);
+  }
+}
+
+template <typename T, int KL>
+void launch_rowwise_t(dsx_lab* lab, int what, double weight, double weight_total) {
+  const T* w = static_cast<const T*>(lab->w);
+  if (what == 0) {
+    mean_accumulate_kernel<T, KL><<<lab->nsm * 8, 256, 0, lab->stream>>>(
+        w, lab->ld, lab->kl, lab->K, lab->dim, weight, lab->what, lab->prog_local);
+  } else {
+    log_kernel<T, KL><<<lab->ntiles, kThreads, 0, lab->stream>>>(
+        w, lab->ld, lab->kl, lab->K, lab->tiles, lab->ntiles, lab->q, lab->what, weight_total,
+        lab->log_part, lab->prog_local);
+  }
+  ++lab->launches;
+}
+
+template <typename T>
+void launch_rowwise(dsx_lab* lab, int what, double weight, double weight_total) {
+  switch (lab->kl) {
+    case 1: return launch_rowwise_t<T, 1>(lab, what, weight, weight_total);
+    case 2: return launch_rowwise_t<T, 2>(lab, what, weight, weight_total);
+    case 4: return launch_rowwise_t<T, 4>(lab, what, weight, weight_total);
+    case 8: return launch_rowwise_t<T, 8>(lab, what, weight, weight_total);
+    default: return launch_rowwise_t<T, 0>(lab, what, weight, weight_total);
+  }
+}
+
+template <typename T, int KL>
+void launch_partial_t(dsx_lab* lab, cudaStream_t s, long long lo, long long n, T* dst) {
+  local_partial_kernel<T, KL><<<lab->nsm * 4, 256, 0, s>>>(static_cast<const T*>(lab->w), lab->ld,
+                                                           lab->kl, lo, n, dst, lab->prog_local);
+  ++lab->launches;
+}
+
+template <typename T>
+void launch_partial(dsx_lab* lab, cudaStream_t s, long long lo, long long n, T* dst) {
+  switch (lab->kl) {
+    case 2: return launch_partial_t<T, 2>(lab, s, lo, n, dst);
+    case 4: return launch_partial_t<T, 4>(lab, s, lo, n, dst);
+    case 8: return launch_partial_t<T, 8>(lab, s, lo, n, dst);
+    default: return launch_partial_t<T, 0>(lab, s, lo, n, dst);
+  }
+}
+
+ncclDataType_t nccl_type(const dsx_lab* lab) { return lab->dtype == DSX_F64 ? ncclFloat64 : ncclFloat32; }
+
+// Cross-rank average of coordinates [lo, lo+n) on stream s (all local rows
+// end up holding the global mean).  Requires comm.
+template <typename T>
+dsx_status sync_range(dsx_lab* lab, cudaStream_t s, long long lo, long long n) {
+  T* w = static_cast<T*>(lab->w);
+  const int R = lab->nranks;
+  // 1. this rank's subtree sum of the range
+  T* part = nullptr;
+  if (lab->kl == 1) {
+    part = w + lo;  // in place: row 0 is its own partial
+  } else {
+    part = static_cast<T*>(lab->staging);
+    launch_partial<T>(lab, s, lo, n, part);
+  }
+  if (lab->sync_algo == DSX_SYNC_NCCL_AVG) {
+    DSX_NCCL(ncclAllReduce(part, part, (size_t)n, nccl_type(lab), ncclSum, lab->comm, s));
+    broadcast_rows_kernel<T><<<lab->nsm * 4, 256, 0, s>>>(w, lab->ld, lab->kl, lo, n, part,
+                                                          (T)lab->K);
+    ++lab->launches;
+    return DSX_OK;
+  }
+  // 2. reduce-scatter in the reference's pairwise rank order: rank r owns
+  //    slice r; all-to-all of partial slices, local fixed-order reduction.
+  const long long base = n / R, extra = n % R;
+  auto slice_lo = [&](int r) { return r * base + std::min<long long>(r, extra); };
+  auto slice_n = [&](int r) { return base + (r < extra ? 1 : 0); };
+  const long long my_n = slice_n(lab->rank);
+  T* recv = static_cast<T*>(lab->recv);
+  DSX_NCCL(ncclGroupStart());
+  for (int r = 0; r < R; ++r) {
+    if (slice_n(r) > 0) DSX_NCCL(ncclSend(part + slice_lo(r), (size_t)slice_n(r), nccl_type(lab), r, lab->comm, s));
+    if (my_n > 0) DSX_NCCL(ncclRecv(recv + (long long)r * my_n, (size_t)my_n, nccl_type(lab), r, lab->comm, s));
+  }
+  DSX_NCCL(ncclGroupEnd());
+  if (my_n > 0) {
+    rank_reduce_kernel<T><<<lab->nsm * 4, 256, 0, s>>>(recv, my_n, R, lab->K, part + slice_lo(lab->rank),
+                                                        lab->prog_ranks);
+    ++lab->launches;
+  }
+  // 3. all-gather the reduced slices in place (one broadcast per owner).
+  DSX_NCCL(ncclGroupStart());
+  for (int r = 0; r < R; ++r) {
+    if (slice_n(r) > 0)
+      DSX_NCCL(ncclBroadcast(part + slice_lo(r), part + slice_lo(r), (size_t)slice_n(r), nccl_type(lab), r,
+                             lab->comm, s));
+  }
+  DSX_NCCL(ncclGroupEnd());
+  if (lab->kl > 1) {
+    broadcast_rows_kernel<T><<<lab->nsm * 4, 256, 0, s>>>(w, lab->ld, lab->kl, lo, n, part, (T)1);
+    ++lab->launches;
+  }
+  return DSX_OK;
+}
+
+// Masked blocks -> maximal contiguous coordinate ranges.
+std::vector<std::pair<long long, long long>> masked_ranges(const dsx_lab* lab, const unsigned char* mask) {
+  std::vector<std::pair<long long, long long>> out;
+  for (int b = 0; b < lab->L; ++b) {
+    if (!mask[b + 1]) continue;
+    const long long lo = (long long)lab->offs[b], hi = (long long)lab->offs[b + 1];
+    if (!out.empty() && out.back().first + out.back().second == lo) {
+      out.back().second += hi - lo;
+    } else {
+      out.push_back({lo, hi - lo});
+    }
+  }
+  return out;
+}
+
+template <typename T>
+dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, bool noise) {
+  MaskBits bits{};
+  for (int b = 0; b < lab->L; ++b)
+    if (mask[b + 1]) bits.w[b >> 5] |= 1u << (b & 31);
+  const bool single = lab->nranks == 1;
+  if (lab->kl == 0 || lab->ntiles == 0) return DSX_OK;
+  if (lab->kl > 8) {
+    zero_kernel<<<lab->nsm, 256, 0, lab->stream>>>(lab->norm_part, (long long)lab->kl * lab->ntiles);
+    ++lab->launches;
+  }
+  if (single) {
+    launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, lab->K > 1, bits, eta);
+  } else {
+    const auto ranges = masked_ranges(lab, mask);
+    lab->has_ranges = !ranges.empty();
+    // Split point: the local step runs backward-order (high layers first) so
+    // the synced ranges become final early; tiles are ordered by coordinate,
+    // so the first synced coordinate decides which tiles must finish before
+    // the sync may start.
+    int split = 0;
+    if (!ranges.empty() && lab->overlap) {
+      const long long first = ranges.front().first;
+      split = 0;
+      while (split < lab->ntiles && lab->h_tiles[split].start < first) ++split;
+    }
+    if (split < lab->ntiles) {
+      launch_update<T>(lab, lab->stream, split, lab->ntiles - split, noise, false, bits, eta);
+    }
+    DSX_CUDA(cudaEventRecord(lab->ev_split, lab->stream));
+    if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[1], lab->stream));
+    if (!ranges.empty()) {
+      DSX_CUDA(cudaStreamWaitEvent(lab->side, lab->ev_split, 0));
+      for (const auto& r : ranges) DSX_TRY(sync_range<T>(lab, lab->side, r.first, r.second));
+      DSX_CUDA(cudaEventRecord(lab->ev_synced, lab->side));
+      if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[2], lab->side));
+    }
+    if (split > 0) launch_update<T>(lab, lab->stream, 0, split, noise, false, bits, eta);
+    if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
+    if (!ranges.empty()) DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_synced, 0));
+  }
+  norm_finalize_kernel<<<1, 1024, 0, lab->stream>>>(lab->norm_part, lab->ntiles, lab->kl, lab->norm,
+                                                    lab->maxnorm);
+  ++lab->launches;
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[4], lab->stream));
+  lab->synced_last = !single && lab->has_ranges;
+  DSX_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
+dsx_status run_noise(dsx_lab* lab) {
+  if (lab->sigma > 0.0) {
+    mt_noise_chain_kernel<<<lab->kl, kMtThreads, 0, lab->stream>>>(lab->mt, lab->noise, lab->ld,
+                                                                   lab->dim, lab->stddev);
+    ++lab->launches;
+  }
+  return DSX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dsx_last_error(void) { return g_last_error.c_str(); }
+
+dsx_status dsx_device_count(int* count) {
+  if (!count) return fail(DSX_ERR_ARGUMENT, "null count");
+  DSX_CUDA(cudaGetDeviceCount(count));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
+  if (!d || !out) return fail(DSX_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (d->dim < 1) return fail(DSX_ERR_ARGUMENT, "dim must be >= 1");
+  if (d->layers < 1 || d->layers > kMaxMaskWords * 32)
+    return fail(DSX_ERR_ARGUMENT, "layers must be in [1, 4096]");
+  if (d->workers_total < 1 || d->workers_total > kMaxProg)
+    return fail(DSX_ERR_ARGUMENT, "workers_total must be in [1, 64]");
+  if (d->workers_local < 1 || d->worker_begin < 0 ||
+      d->worker_begin + d->workers_local > d->workers_total)
+    return fail(DSX_ERR_ARGUMENT, "bad local worker range");
+  if (d->dtype != DSX_F64 && d->dtype != DSX_F32) return fail(DSX_ERR_ARGUMENT, "bad dtype");
+  if (!d->block_sizes || !d->curvature || !d->optimum) return fail(DSX_ERR_ARGUMENT, "null arrays");
+  unsigned long long covered = 0;
+  for (int b = 0; b < d->layers; ++b) {
+    if (d->block_sizes[b] == 0) return fail(DSX_ERR_ARGUMENT, "zero-sized layer block");
+    covered += d->block_sizes[b];
+  }
+  if (covered != d->dim) return fail(DSX_ERR_ARGUMENT, "block sizes do not sum to dim");
+  if (!(d->noise_sigma >= 0.0)) return fail(DSX_ERR_ARGUMENT, "sigma must be non-negative");
+  int ndev = 0;
+  DSX_CUDA(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) return fail(DSX_ERR_CUDA, "no such CUDA device");
+  DSX_CUDA(cudaSetDevice(d->device));
+
+  auto* lab = new dsx_lab();
+  lab->device = d->device;
+  lab->dtype = d->dtype;
+  lab->K = d->workers_total;
+  lab->kbegin = d->worker_begin;
+  lab->kl = d->workers_local;
+  lab->dim = d->dim;
+  lab->ld = (long long)((d->dim + 63) / 64 * 64);
+  lab->L = d->layers;
+  lab->sigma = d->noise_sigma;
+  lab->stddev = d->noise_sigma / std::sqrt(static_cast<double>(d->dim));  // trainer.cpp:180-181
+  lab->offs.assign(d->layers + 1, 0);
+  for (int b = 0; b < d->layers; ++b) lab->offs[b + 1] = lab->offs[b] + d->block_sizes[b];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+  lab->nsm = sms;
+  build_prog(lab->kl, &lab->prog_local);
+
+  auto cleanup = [&](dsx_status s) {
+    dsx_lab_destroy(lab);
+    return s;
+  };
+  const size_t es = elem_size(lab);
+  cudaError_t e = cudaMalloc(&lab->w, es * (size_t)lab->ld * lab->kl);
+  if (e != cudaSuccess) return cleanup(fail(DSX_ERR_CUDA, std::string("cudaMalloc(w): ") + cudaGetErrorString(e)));
+  cudaMemset(lab->w, 0, es * (size_t)lab->ld * lab->kl);
+  if (!detect_analytic(d, &lab->q)) {
+    lab->q.analytic = false;
+    if (cudaMalloc(&lab->curv, 8 * d->dim) != cudaSuccess || cudaMalloc(&lab->opt, 8 * d->dim) != cudaSuccess)
+      return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(curvature/optimum) failed"));
+    cudaMemcpy(lab->curv, d->curvature, 8 * d->dim, cudaMemcpyHostToDevice);
+    cudaMemcpy(lab->opt, d->optimum, 8 * d->dim, cudaMemcpyHostToDevice);
+    lab->q.curv = lab->curv;
+    lab->q.opt = lab->opt;
+  }
+  if (cudaMalloc(&lab->mt, 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
+    return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(mt) failed"));
+  if (lab->sigma > 0.0 && cudaMalloc(&lab->noise, 8 * (size_t)lab->ld * lab->kl) != cudaSuccess)
+    return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(noise) failed"));
+  // tiles: per block, kTile coordinates each (never crossing a block)
+  for (int b = 0; b < lab->L; ++b) {
+    for (unsigned long long s = lab->offs[b]; s < lab->offs[b + 1]; s += kTile) {
+      lab->h_tiles.push_back({(long long)s, (int)std::min<unsigned long long>(kTile, lab->offs[b + 1] - s), b});
+    }
+  }
+  lab->ntiles = (int)lab->h_tiles.size();
+  if (cudaMalloc(&lab->tiles, sizeof(Tile) * lab->ntiles) != cudaSuccess ||
+      cudaMalloc(&lab->norm_part, 8 * (size_t)lab->ntiles * lab->kl) != cudaSuccess ||
+      cudaMalloc(&lab->norm, 8 * (size_t)lab->kl) != cudaSuccess ||
+      cudaMalloc(&lab->maxnorm, 8) != cudaSuccess ||
+      cudaMalloc(&lab->log_part, 8 * 3 * (size_t)lab->ntiles) != cudaSuccess)
+    return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(tiles/partials) failed"));
+  cudaMemcpy(lab->tiles, lab->h_tiles.data(), sizeof(Tile) * lab->ntiles, cudaMemcpyHostToDevice);
+  cudaMemset(lab->maxnorm, 0, 8);
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  if (cudaStreamCreateWithPriority(&lab->stream, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&lab->side, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
+    return cleanup(fail(DSX_ERR_CUDA, "stream creation failed"));
+  for (auto& ev : lab->ev) cudaEventCreate(&ev);
+  for (auto& ev : lab->iev) cudaEventCreate(&ev);
+  cudaEventCreateWithFlags(&lab->ev_split, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&lab->ev_synced, cudaEventDisableTiming);
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cleanup(fail(DSX_ERR_CUDA, std::string("lab init: ") + cudaGetErrorString(e)));
+  // default rng: worker_rng(0, k)
+  if (dsx_lab_seed_rng(lab, 0) != DSX_OK) return cleanup(DSX_ERR_CUDA);
+  *out = lab;
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_destroy(dsx_lab* lab) {
+  if (!lab) return DSX_OK;
+  cudaSetDevice(lab->device);
+  if (lab->stream) cudaStreamSynchronize(lab->stream);
+  if (lab->side) cudaStreamSynchronize(lab->side);
+  if (lab->comm) ncclCommDestroy(lab->comm);
+  for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt,
+                  (void*)lab->what, (void*)lab->tiles, (void*)lab->norm_part, (void*)lab->norm,
+                  (void*)lab->maxnorm, (void*)lab->log_part, lab->staging, lab->recv})
+    if (p) cudaFree(p);
+  for (auto& ev : lab->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : lab->iev)
+    if (ev) cudaEventDestroy(ev);
+  if (lab->ev_split) cudaEventDestroy(lab->ev_split);
+  if (lab->ev_synced) cudaEventDestroy(lab->ev_synced);
+  if (lab->stream) cudaStreamDestroy(lab->stream);
+  if (lab->side) cudaStreamDestroy(lab->side);
+  delete lab;
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_params(dsx_lab* lab, int local, const double* w) {
+  DSX_TRY(check_row(lab, local));
+  if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  if (lab->dtype == DSX_F64) {
+    DSX_CUDA(cudaMemcpy(static_cast<double*>(lab->w) + (long long)local * lab->ld, w, 8 * lab->dim,
+                        cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> tmp(w, w + lab->dim);
+    DSX_CUDA(cudaMemcpy(static_cast<float*>(lab->w) + (long long)local * lab->ld, tmp.data(), 4 * lab->dim,
+                        cudaMemcpyHostToDevice));
+  }
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_get_params(dsx_lab* lab, int local, double* w) {
+  DSX_TRY(check_row(lab, local));
+  if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  if (lab->dtype == DSX_F64) {
+    DSX_CUDA(cudaMemcpy(w, static_cast<double*>(lab->w) + (long long)local * lab->ld, 8 * lab->dim,
+                        cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<float> tmp(lab->dim);
+    DSX_CUDA(cudaMemcpy(tmp.data(), static_cast<float*>(lab->w) + (long long)local * lab->ld, 4 * lab->dim,
+                        cudaMemcpyDeviceToHost));
+    std::copy(tmp.begin(), tmp.end(), w);
+  }
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_all_params(dsx_lab* lab, const double* w) {
+  DSX_TRY(check_lab(lab));
+  if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  if (lab->dtype == DSX_F64) {
+    DSX_CUDA(cudaMemcpy2DAsync(lab->w, 8 * lab->ld, w, 8 * lab->dim, 8 * lab->dim, lab->kl,
+                               cudaMemcpyHostToDevice, lab->stream));
+    return DSX_OK;
+  }
+  for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, w + (long long)k * lab->dim));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_get_all_params(dsx_lab* lab, double* w) {
+  DSX_TRY(check_lab(lab));
+  if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  if (lab->dtype == DSX_F64) {
+    DSX_CUDA(cudaStreamSynchronize(lab->side));
+    DSX_CUDA(cudaMemcpy2DAsync(w, 8 * lab->dim, lab->w, 8 * lab->ld, 8 * lab->dim, lab->kl,
+                               cudaMemcpyDeviceToHost, lab->stream));
+    DSX_CUDA(cudaStreamSynchronize(lab->stream));
+    return DSX_OK;
+  }
+  for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, w + (long long)k * lab->dim));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_fill_params(dsx_lab* lab, double value) {
+  DSX_TRY(check_lab(lab));
+  std::vector<double> row(lab->dim, value);
+  for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, row.data()));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_rng(dsx_lab* lab, int local, const uint64_t* x312, uint64_t p) {
+  DSX_TRY(check_row(lab, local));
+  if (!x312 || p > kMtN) return fail(DSX_ERR_ARGUMENT, "bad rng state");
+  uint64_t buf[kMtN + 1];
+  std::memcpy(buf, x312, 8 * kMtN);
+  buf[kMtN] = p;
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaMemcpy(lab->mt + (long long)local * (kMtN + 1), buf, sizeof buf, cudaMemcpyHostToDevice));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_get_rng(dsx_lab* lab, int local, uint64_t* x312, uint64_t* p) {
+  DSX_TRY(check_row(lab, local));
+  if (!x312 || !p) return fail(DSX_ERR_ARGUMENT, "null rng out");
+  uint64_t buf[kMtN + 1];
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaMemcpy(buf, lab->mt + (long long)local * (kMtN + 1), sizeof buf, cudaMemcpyDeviceToHost));
+  std::memcpy(x312, buf, 8 * kMtN);
+  *p = buf[kMtN];
+  return DSX_OK;
+}
+
+// worker_rng(seed, k) (trainer.cpp:169-173) for every local row, seeded on
+// the host with libstdc++'s own seed_seq and read back through operator<<.
+dsx_status dsx_lab_seed_rng(dsx_lab* lab, uint64_t seed) {
+  DSX_TRY(check_lab(lab));
+  for (int k = 0; k < lab->kl; ++k) {
+    const int global = lab->kbegin + k;
+    std::seed_seq seq{static_cast<std::uint32_t>(seed), static_cast<std::uint32_t>(seed >> 32),
+                      static_cast<std::uint32_t>(global), 0x5eedu};
+    std::mt19937_64 eng(seq);
+    std::stringstream ss;
+    ss << eng;
+    uint64_t x[kMtN], p = 0;
+    for (int i = 0; i < kMtN; ++i) ss >> x[i];
+    ss >> p;
+    DSX_TRY(dsx_lab_set_rng(lab, k, x, p));
+  }
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_step(dsx_lab* lab, double eta, const unsigned char* mask) {
+  DSX_TRY(check_lab(lab));
+  if (!mask) return fail(DSX_ERR_ARGUMENT, "null mask");
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[0], lab->stream));
+  DSX_TRY(run_noise(lab));
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[5], lab->stream));
+  const bool noise = lab->sigma > 0.0;
+  return lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, noise)
+                               : step_impl<float>(lab, eta, mask, noise);
+}
+
+dsx_status dsx_lab_step_with_noise(dsx_lab* lab, double eta, const unsigned char* mask,
+                                   const double* xi) {
+  DSX_TRY(check_lab(lab));
+  if (!mask || !xi) return fail(DSX_ERR_ARGUMENT, "null mask/noise");
+  if (!lab->noise) {
+    DSX_CUDA(cudaMalloc(&lab->noise, 8 * (size_t)lab->ld * lab->kl));
+  }
+  DSX_CUDA(cudaMemcpy2DAsync(lab->noise, 8 * lab->ld, xi, 8 * lab->dim, 8 * lab->dim, lab->kl,
+                             cudaMemcpyHostToDevice, lab->stream));
+  if (lab->instrument) {
+    DSX_CUDA(cudaEventRecord(lab->iev[0], lab->stream));
+    DSX_CUDA(cudaEventRecord(lab->iev[5], lab->stream));
+  }
+  return lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, true)
+                               : step_impl<float>(lab, eta, mask, true);
+}
+
+dsx_status dsx_lab_last_max_grad_norm_sq(dsx_lab* lab, double* out) {
+  DSX_TRY(check_lab(lab));
+  if (!out) return fail(DSX_ERR_ARGUMENT, "null out");
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaMemcpy(out, lab->maxnorm, 8, cudaMemcpyDeviceToHost));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_sync(dsx_lab* lab) {
+  DSX_TRY(check_lab(lab));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
+  DSX_TRY(check_row(lab, local));
+  if (!g_out) return fail(DSX_ERR_ARGUMENT, "null gradient out");
+  DSX_TRY(run_noise(lab));  // advances every local row's stream; see note in trainer.cpp
+  double* g = nullptr;
+  DSX_CUDA(cudaMallocAsync((void**)&g, 8 * lab->dim, lab->stream));
+  const double* xi = lab->sigma > 0.0 ? lab->noise + (long long)local * lab->ld : nullptr;
+  if (lab->dtype == DSX_F64) {
+    gradient_kernel<double><<<lab->nsm * 4, 256, 0, lab->stream>>>(
+        static_cast<const double*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, xi, g);
+  } else {
+    gradient_kernel<float><<<lab->nsm * 4, 256, 0, lab->stream>>>(
+        static_cast<const float*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, xi, g);
+  }
+  ++lab->launches;
+  DSX_CUDA(cudaMemcpyAsync(g_out, g, 8 * lab->dim, cudaMemcpyDeviceToHost, lab->stream));
+  DSX_CUDA(cudaFreeAsync(g, lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_mean_accumulate(dsx_lab* lab, double weight) {
+  DSX_TRY(check_lab(lab));
+  if (lab->nranks != 1) return fail(DSX_ERR_STATE, "run_training logging is single-rank");
+  if (!lab->what) {
+    DSX_CUDA(cudaMalloc(&lab->what, 8 * lab->dim));
+    DSX_CUDA(cudaMemsetAsync(lab->what, 0, 8 * lab->dim, lab->stream));
+  }
+  if (lab->dtype == DSX_F64) launch_rowwise<double>(lab, 0, weight, 0.0);
+  else launch_rowwise<float>(lab, 0, weight, 0.0);
+  DSX_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_log(dsx_lab* lab, double weight_total, double* gamma_per_layer, double* out2) {
+  DSX_TRY(check_lab(lab));
+  if (lab->nranks != 1) return fail(DSX_ERR_STATE, "run_training logging is single-rank");
+  if (!gamma_per_layer || !out2) return fail(DSX_ERR_ARGUMENT, "null log outputs");
+  if (!lab->what) {
+    DSX_CUDA(cudaMalloc(&lab->what, 8 * lab->dim));
+    DSX_CUDA(cudaMemsetAsync(lab->what, 0, 8 * lab->dim, lab->stream));
+  }
+  if (lab->dtype == DSX_F64) launch_rowwise<double>(lab, 1, 0.0, weight_total);
+  else launch_rowwise<float>(lab, 1, 0.0, weight_total);
+  std::vector<double> part(3 * (size_t)lab->ntiles);
+  DSX_CUDA(cudaMemcpyAsync(part.data(), lab->log_part, 8 * part.size(), cudaMemcpyDeviceToHost, lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  for (int b = 0; b < lab->L; ++b) gamma_per_layer[b] = 0.0;
+  double fh = 0.0, fm = 0.0;
+  for (int t = 0; t < lab->ntiles; ++t) {
+    gamma_per_layer[lab->h_tiles[t].block] += part[t];
+    fh += part[lab->ntiles + t];
+    fm += part[2 * lab->ntiles + t];
+  }
+  for (int b = 0; b < lab->L; ++b) gamma_per_layer[b] /= static_cast<double>(lab->K);
+  out2[0] = fh;
+  out2[1] = fm;
+  return DSX_OK;
+}
+
+dsx_status dsx_nccl_unique_id(unsigned char id[128]) {
+  if (!id) return fail(DSX_ERR_ARGUMENT, "null id");
+  ncclUniqueId u;
+  DSX_NCCL(ncclGetUniqueId(&u));
+  std::memcpy(id, u.internal, 128);
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nranks, int rank,
+                             int sync_algo) {
+  DSX_TRY(check_lab(lab));
+  if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(DSX_ERR_ARGUMENT, "bad comm args");
+  if (sync_algo != DSX_SYNC_PAIRWISE && sync_algo != DSX_SYNC_NCCL_AVG)
+    return fail(DSX_ERR_ARGUMENT, "bad sync algorithm");
+  if (lab->comm) return fail(DSX_ERR_STATE, "comm already initialised");
+  if (lab->K % nranks != 0 || lab->kl != lab->K / nranks || lab->kbegin != rank * lab->kl)
+    return fail(DSX_ERR_ARGUMENT, "ranks must hold equal contiguous worker ranges");
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, 128);
+  DSX_NCCL(ncclCommInitRank(&lab->comm, nranks, u, rank));
+  lab->nranks = nranks;
+  lab->rank = rank;
+  lab->sync_algo = sync_algo;
+  // Exactness needs every rank's rows to be a subtree of the pairwise tree.
+  lab->local_subtree = is_subtree(lab->K, lab->kbegin, lab->kl);
+  for (int r = 0; r < nranks && lab->local_subtree; ++r)
+    lab->local_subtree = is_subtree(lab->K, r * lab->kl, lab->kl);
+  if (sync_algo == DSX_SYNC_PAIRWISE && !lab->local_subtree)
+    return fail(DSX_ERR_ARGUMENT, "pairwise sync needs rank worker ranges aligned to the pairwise tree");
+  build_prog(nranks, &lab->prog_ranks);
+  const size_t es = elem_size(lab);
+  lab->staging_elems = lab->dim;
+  if (lab->kl > 1) DSX_CUDA(cudaMalloc(&lab->staging, es * lab->dim));
+  DSX_CUDA(cudaMalloc(&lab->recv, es * (lab->dim / nranks + 1) * nranks));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_overlap(dsx_lab* lab, int enabled) {
+  DSX_TRY(check_lab(lab));
+  lab->overlap = enabled != 0;
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_event_record(dsx_lab* lab, int slot) {
+  DSX_TRY(check_lab(lab));
+  if (slot < 0 || slot >= 32) return fail(DSX_ERR_ARGUMENT, "event slot out of range");
+  DSX_CUDA(cudaEventRecord(lab->ev[slot], lab->stream));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_event_elapsed(dsx_lab* lab, int a, int b, float* ms) {
+  DSX_TRY(check_lab(lab));
+  if (a < 0 || a >= 32 || b < 0 || b >= 32 || !ms) return fail(DSX_ERR_ARGUMENT, "bad event args");
+  DSX_CUDA(cudaEventSynchronize(lab->ev[b]));
+  DSX_CUDA(cudaEventElapsedTime(ms, lab->ev[a], lab->ev[b]));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_instrument(dsx_lab* lab, int enabled) {
+  DSX_TRY(check_lab(lab));
+  lab->instrument = enabled != 0;
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out3) {
+  DSX_TRY(check_lab(lab));
+  if (!out3) return fail(DSX_ERR_ARGUMENT, "null out");
+  if (!lab->instrument) return fail(DSX_ERR_STATE, "instrumentation disabled");
+  DSX_CUDA(cudaEventSynchronize(lab->iev[4]));
+  DSX_CUDA(cudaEventElapsedTime(&out3[0], lab->iev[0], lab->iev[4]));
+  DSX_CUDA(cudaEventElapsedTime(&out3[3], lab->iev[0], lab->iev[5]));
+  // update span: from update start to the local step's end (single rank:
+  // the fused update kernel + norm finalize)
+  DSX_CUDA(cudaEventElapsedTime(&out3[4], lab->iev[5], lab->synced_last ? lab->iev[3] : lab->iev[4]));
+  out3[1] = out3[2] = 0.0f;
+  if (lab->synced_last) {
+    // sync = side-stream span; exposed = how long the synced blocks finished
+    // after the local step did (cost_model.cpp:39: term - bp_total).
+    float sync_start = 0.0f, sync_end = 0.0f, local_end = 0.0f;
+    DSX_CUDA(cudaEventElapsedTime(&sync_start, lab->iev[0], lab->iev[1]));
+    DSX_CUDA(cudaEventElapsedTime(&sync_end, lab->iev[0], lab->iev[2]));
+    DSX_CUDA(cudaEventElapsedTime(&local_end, lab->iev[0], lab->iev[3]));
+    out3[1] = sync_end - sync_start;
+    out3[2] = std::max(0.0f, sync_end - local_end);
+  }
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_launch_count(dsx_lab* lab, uint64_t* out) {
+  if (!lab || !out) return fail(DSX_ERR_ARGUMENT, "null argument");
+  *out = lab->launches;
+  return DSX_OK;
+}
+
+}  // extern "C"

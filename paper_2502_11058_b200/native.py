@@ -1,0 +1,101 @@
+"""ctypes loader for lib/libdsx.so (the dsx C-ABI, include/dsx.h).
+
+Fails loudly when the native library is missing: there is no Python or CPU
+fallback for anything the C-ABI does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(PKG_DIR, "lib")
+DSX_PATH = os.path.join(LIB_DIR, "libdsx.so")
+DREAMSCHED_PATH = os.path.join(LIB_DIR, "libdreamsched.so")
+
+DSX_OK, DSX_ERR_ARGUMENT, DSX_ERR_STATE, DSX_ERR_CUDA, DSX_ERR_NCCL = range(5)
+DSX_F64, DSX_F32 = 0, 1
+DSX_SYNC_PAIRWISE, DSX_SYNC_NCCL_AVG = 0, 1
+
+
+class DsxError(RuntimeError):
+    def __init__(self, status: int, where: str, message: str):
+        super().__init__(f"{where}: [{status}] {message}")
+        self.status = status
+
+
+class LabDescC(C.Structure):
+    _fields_ = [
+        ("device", C.c_int),
+        ("dtype", C.c_int),
+        ("workers_total", C.c_int),
+        ("worker_begin", C.c_int),
+        ("workers_local", C.c_int),
+        ("dim", C.c_uint64),
+        ("layers", C.c_int),
+        ("block_sizes", C.POINTER(C.c_uint64)),
+        ("curvature", C.POINTER(C.c_double)),
+        ("optimum", C.POINTER(C.c_double)),
+        ("noise_sigma", C.c_double),
+    ]
+
+
+_dsx = None
+
+_SIGS = {
+    "dsx_last_error": ([], C.c_char_p),
+    "dsx_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "dsx_lab_create": ([C.POINTER(LabDescC), C.POINTER(C.c_void_p)], C.c_int),
+    "dsx_lab_destroy": ([C.c_void_p], C.c_int),
+    "dsx_lab_set_params": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "dsx_lab_get_params": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "dsx_lab_fill_params": ([C.c_void_p, C.c_double], C.c_int),
+    "dsx_lab_set_all_params": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_lab_get_all_params": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_lab_set_rng": ([C.c_void_p, C.c_int, C.c_void_p, C.c_uint64], C.c_int),
+    "dsx_lab_get_rng": ([C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "dsx_lab_seed_rng": ([C.c_void_p, C.c_uint64], C.c_int),
+    "dsx_lab_step": ([C.c_void_p, C.c_double, C.c_void_p], C.c_int),
+    "dsx_lab_step_with_noise": ([C.c_void_p, C.c_double, C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_lab_last_max_grad_norm_sq": ([C.c_void_p, C.POINTER(C.c_double)], C.c_int),
+    "dsx_lab_sync": ([C.c_void_p], C.c_int),
+    "dsx_lab_gradient": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "dsx_lab_mean_accumulate": ([C.c_void_p, C.c_double], C.c_int),
+    "dsx_lab_log": ([C.c_void_p, C.c_double, C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_nccl_unique_id": ([C.c_void_p], C.c_int),
+    "dsx_lab_comm_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
+    "dsx_lab_set_overlap": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_lab_event_record": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_lab_event_elapsed": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
+    "dsx_lab_set_instrument": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_lab_last_step_times": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_lab_launch_count": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+}
+
+
+def exported_symbols():
+    """Every entry point include/dsx.h declares (checked by the CPU tests)."""
+    return sorted(_SIGS)
+
+
+def load_dsx():
+    global _dsx
+    if _dsx is None:
+        if not os.path.exists(DSX_PATH):
+            raise RuntimeError(
+                f"{DSX_PATH} is missing: build the native engine first "
+                "(python -c 'import __graft_entry__ as g; g.build()' or `make`)")
+        lib = C.CDLL(DSX_PATH, mode=C.RTLD_GLOBAL)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _dsx = lib
+    return _dsx
+
+
+def call(name: str, *args) -> None:
+    lib = load_dsx()
+    status = getattr(lib, name)(*args)
+    if status != DSX_OK:
+        raise DsxError(status, name, lib.dsx_last_error().decode(errors="replace"))

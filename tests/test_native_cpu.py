@@ -1,0 +1,106 @@
+"""CPU-side checks of the native product (no GPU needed):
+
+* the C-ABI libraries load and export every symbol the headers declare;
+* the host C++ API (scheduler, cost model, simulator, profile/schedule I/O)
+  is byte-identical to the REAL reference — fixtures and fuzzed instances —
+  through the same parity_tool source compiled against both libraries;
+* the reference's own acceptance binary, compiled against this library,
+  passes its host-only criteria;
+* the device path fails loudly (no silent CPU fallback) without a GPU.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+from tests import golden_io as G
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOOL = os.path.join(REPO, "build", "parity_tool")
+REF_TOOL = os.path.join(REPO, "oracle", "_ref", "parity_tool_ref")
+ACCEPT = os.path.join(REPO, "build", "acceptance")
+
+
+def _declared(header, prefix):
+    text = open(os.path.join(REPO, "include", header)).read()
+    return sorted(set(re.findall(r"\b(" + prefix + r"_\w+)\s*\(", text)))
+
+
+def _exports(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True,
+                         check=True).stdout
+    return {ln.split()[-1] for ln in out.splitlines() if ln.strip()}
+
+
+def test_dsx_exports_every_declared_symbol():
+    from paper_2502_11058_b200 import native
+    declared = _declared("dsx.h", "dsx")
+    assert declared == native.exported_symbols()
+    exported = _exports(native.DSX_PATH)
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    native.load_dsx()  # resolves every signature
+
+
+def test_dreamsched_c_exports():
+    from paper_2502_11058_b200 import native
+    declared = _declared("dreamsched_c.h", "dsc")
+    exported = _exports(native.DREAMSCHED_PATH)
+    assert declared and all(s in exported for s in declared)
+
+
+def test_kernels_target_sm100a():
+    from paper_2502_11058_b200 import native
+    out = subprocess.run(["cuobjdump", "--list-elf", native.DSX_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def run_tool(*args):
+    return subprocess.run([TOOL] + list(args), check=True, capture_output=True, text=True).stdout
+
+
+def test_sched_fuzz_golden_byte_identical():
+    assert run_tool("sched-fuzz", "2026", "150", "40") == G.read("sched_fuzz_2026.txt")
+
+
+@pytest.mark.parametrize("name,h", [("resnet18_like", 5), ("three_layer", 2),
+                                    ("three_layer_light", 2), ("totals_123", 1)])
+def test_profile_fixture_schedules_byte_identical(name, h):
+    out = run_tool("profile", os.path.join(G.DATA, name + ".profile"), str(h))
+    assert out.replace(G.DATA + "/", "") == G.read("profile_%s_h%d.txt" % (name, h))
+
+
+def test_trace_json_byte_identical():
+    out = run_tool("trace", os.path.join(G.DATA, "three_layer.profile"), "plsgd", "2", "2")
+    assert out == G.read("trace_three_layer_plsgd.txt")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_TOOL), reason="reference build absent")
+@pytest.mark.parametrize("seed,count,maxl", [(11, 600, 24), (12, 300, 61)])
+def test_sched_fuzz_live_against_reference(seed, count, maxl):
+    args = ["sched-fuzz", str(seed), str(count), str(maxl)]
+    ref = subprocess.run([REF_TOOL] + args, check=True, capture_output=True, text=True).stdout
+    assert run_tool(*args) == ref
+
+
+@pytest.mark.parametrize("criterion", [1, 2, 3, 4, 5, 10])
+def test_reference_acceptance_host_criteria(criterion):
+    if not os.path.exists(ACCEPT):
+        pytest.skip("acceptance binary is built only where /root/reference exists")
+    out = subprocess.run([ACCEPT, "--only", str(criterion)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "[PASS]" in out.stdout
+
+
+def test_device_path_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2502_11058_b200 import DsxError, Lab, LabDesc
+    with pytest.raises(DsxError):
+        Lab(LabDesc(dim=16, block_sizes=[8, 8], workers_total=2))
+    out = subprocess.run([TOOL, "steps", "12", "3", "4", "3", "0.5", "7", "1", "partial", "enp"],
+                         capture_output=True, text=True)
+    assert out.returncode != 0 and "dsx_lab_create" in out.stderr
