@@ -140,6 +140,11 @@ dsx_status dsx_lab_event_elapsed(dsx_lab* lab, int from_slot, int to_slot, float
 dsx_status dsx_lab_set_instrument(dsx_lab* lab, int enabled);
 dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out5);
 
+/* Host-only self-test of the MT19937-64 jump-ahead used by the parallel
+ * noise engine: *ok = 1 when jumping J outputs by polynomial equals running
+ * the recurrence (no GPU needed). */
+dsx_status dsx_mt_jump_selftest(unsigned long long jump, int* ok);
+
 /* Number of kernel launches issued by this lab since creation. */
 dsx_status dsx_lab_launch_count(dsx_lab* lab, uint64_t* out);
 

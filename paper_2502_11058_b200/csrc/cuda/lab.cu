@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <sstream>
@@ -32,6 +33,7 @@
 
 #include "dsx.h"
 #include "mt_engine.cuh"
+#include "noise_engine.cuh"
 
 namespace dsx {
 
@@ -112,7 +114,8 @@ struct UpdateArgs {
   const Tile* tiles;
   int ntiles;
   int tile_base;      // first tile of this launch (split launches for overlap)
-  const double* noise;  // [kl][ld] or null
+  const double* noise;  // [kl][ld] flat noise (NM == 1)
+  NoiseView nv;         // segmented engine output (NM == 2)
   double eta;
   QuadParams q;
   MaskBits mask;
@@ -192,18 +195,43 @@ __device__ __forceinline__ float grad_step(float w, double lam, double opt, doub
 // fused local step (+ in-place averaging of masked blocks on a single rank)
 // KL > 0: compile-time local worker count; KL == 0: runtime count via prog.
 // ---------------------------------------------------------------------------
-template <typename T, int KL, bool NOISE>
+// Segmented engine lookup: normal i of worker k lives in segment s with
+// pfx[s] <= i/2 < pfx[s+1], at slot offset 2*(i/2 - pfx[s]) + (i&1).
+__device__ __forceinline__ int seg_search(const unsigned long long* pf, int P, unsigned long long m) {
+  int lo = 0, hi = P;  // answer in [0, P]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pf[mid] <= m) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double seg_noise(const NoiseView& nv, int k, int seg, long long i) {
+  const unsigned long long* pf = nv.pfx + (long long)k * (nv.P + 2);
+  const unsigned long long m = (unsigned long long)i >> 1;
+  return nv.slots[((long long)k * (nv.P + 1) + seg) * nv.cap + 2 * (long long)(m - pf[seg]) + (i & 1)];
+}
+
+// NM: 0 no noise, 1 flat noise buffer, 2 segmented engine output.
+template <typename T, int KL, int NM>
 __global__ void __launch_bounds__(kThreads)
 lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   constexpr int KMAX = KL > 0 ? KL : kMaxProg;
+  constexpr bool NOISE = NM != 0;
   const int tile_id = a.tile_base + blockIdx.x;
   const Tile t = a.tiles[tile_id];
   const int kl = KL > 0 ? KL : a.kl;
   const bool avg = a.average && mask_has(a.mask, t.block);
-  const double inv_dummy = 0.0;
-  (void)inv_dummy;
-  double nsq[KL > 0 ? KL : 1] = {};
-  double nsq_dyn = 0.0;  // generic path accumulates row by row below
+  double nsq[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) nsq[k] = 0.0;
+  // per-worker current segment (monotone along this thread's elements)
+  int seg[KL > 0 ? KL : 1];
+  if constexpr (NM == 2 && KL > 0) {
+    const unsigned long long m0 = (unsigned long long)(t.start + threadIdx.x) >> 1;
+#pragma unroll
+    for (int k = 0; k < KL; ++k) seg[k] = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P, m0);
+  }
 
   if constexpr (KL > 0) {
 #pragma unroll 2
@@ -217,7 +245,14 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
 #pragma unroll
       for (int k = 0; k < KL; ++k) {
         const T w = a.w[k * a.ld + i];
-        const double xi = NOISE ? a.noise[k * a.ld + i] : 0.0;
+        double xi = 0.0;
+        if constexpr (NM == 1) xi = a.noise[k * a.ld + i];
+        if constexpr (NM == 2) {
+          const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
+          const unsigned long long m = (unsigned long long)i >> 1;
+          while (m >= pf[seg[k] + 1]) ++seg[k];
+          xi = seg_noise(a.nv, k, seg[k], i);
+        }
         const auto g = grad_step(w, lam, opt, xi, a.eta, NOISE, &wn[k]);
         nsq[k] += to_d(g) * to_d(g);
       }
@@ -231,7 +266,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
       }
     }
   } else {
-    // generic worker count: row-major pass, then the pairwise program for
+    // generic worker count: row pass, then the pairwise program for
     // averaged coordinates.
     T v[KMAX];
     for (int j = 0; j < kItems; ++j) {
@@ -242,49 +277,49 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
       quad_coeffs(a.q, i, &lam, &opt);
       for (int k = 0; k < kl; ++k) {
         const T w = a.w[k * a.ld + i];
-        const double xi = NOISE ? a.noise[k * a.ld + i] : 0.0;
+        double xi = 0.0;
+        if constexpr (NM == 1) xi = a.noise[k * a.ld + i];
+        if constexpr (NM == 2) {
+          const int s = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
+                                   (unsigned long long)i >> 1);
+          xi = seg_noise(a.nv, k, s, i);
+        }
         T wn;
         const auto g = grad_step(w, lam, opt, xi, a.eta, NOISE, &wn);
         v[k] = wn;
         if (!avg) a.w[k * a.ld + i] = wn;
-        // per-row squared norm goes straight to the partials below
-        const double gd = to_d(g);
-        atomicAdd(&a.norm_part[(long long)k * a.ntiles + tile_id], gd * gd);
+        nsq[k] += to_d(g) * to_d(g);
       }
       if (avg) {
         const T m = run_prog(prog, v) / (T)a.k_total;
         for (int k = 0; k < kl; ++k) a.w[k * a.ld + i] = m;
       }
     }
-    (void)nsq_dyn;
   }
 
-  if constexpr (KL > 0) {
+  {
     __shared__ double red[kThreads / 32];
-#pragma unroll
-    for (int k = 0; k < KL; ++k) {
+    for (int k = 0; k < kl; ++k) {
       const double s = block_sum(nsq[k], red);
       if (threadIdx.x == 0) a.norm_part[(long long)k * a.ntiles + tile_id] = s;
     }
   }
 }
 
-// ||g_k||^2 = fixed-order sum of the tile partials; then max over rows.
-// One CTA; writes norm[k] and *maxnorm (and folds max into *gmax_sq).
-__global__ void norm_finalize_kernel(const double* part, int ntiles, int kl, double* norm,
-                                     double* maxnorm) {
+// ||g_k||^2 = fixed-order sum of the tile partials (one CTA per worker row),
+// then the max over rows (atomicMax on the bit pattern: non-negative doubles
+// order like their uint64 images, so the result is order-independent).
+__global__ void __launch_bounds__(1024)
+norm_finalize_kernel(const double* part, int ntiles, double* norm, unsigned long long* maxnorm) {
   __shared__ double red[32];
-  double mx = 0.0;
-  for (int k = 0; k < kl; ++k) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < ntiles; i += blockDim.x) s += part[(long long)k * ntiles + i];
-    s = block_sum(s, red);
-    if (threadIdx.x == 0) {
-      norm[k] = s;
-      mx = fmax(mx, s);
-    }
+  const int k = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < ntiles; i += blockDim.x) s += part[(long long)k * ntiles + i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    norm[k] = s;
+    atomicMax(maxnorm, (unsigned long long)__double_as_longlong(s));
   }
-  if (threadIdx.x == 0) *maxnorm = mx;
 }
 
 __global__ void zero_kernel(double* p, long long n) {
@@ -464,14 +499,18 @@ log_kernel(const T* w, long long ld, int kl, int k_total, const Tile* tiles, int
 
 // g = lambda*(w - w*) + xi for one row (stochastic_gradient).
 template <typename T>
-__global__ void gradient_kernel(const T* w, unsigned long long dim, QuadParams q,
-                                const double* noise, double* g) {
+__global__ void gradient_kernel(const T* w, unsigned long long dim, QuadParams q, int nm,
+                                const double* flat, NoiseView nv, int k, double* g) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)dim;
        i += (long long)gridDim.x * blockDim.x) {
     double lam, opt;
     quad_coeffs(q, i, &lam, &opt);
     double gi = __dmul_rn(lam, __dsub_rn(to_d(w[i]), opt));
-    if (noise) gi = __dadd_rn(gi, noise[i]);
+    if (nm == 1) gi = __dadd_rn(gi, flat[i]);
+    if (nm == 2) {
+      const int s = seg_search(nv.pfx + (long long)k * (nv.P + 2), nv.P, (unsigned long long)i >> 1);
+      gi = __dadd_rn(gi, seg_noise(nv, k, s, i));
+    }
     g[i] = gi;
   }
 }
@@ -609,6 +648,8 @@ struct dsx_lab {
   // 3 local step done, 4 step end, 5 noise done / update start
   cudaEvent_t iev[6] = {};
   bool instrument = false;
+  dsx::NoiseEngine* engine = nullptr;  // parallel exact noise (sigma > 0)
+  bool use_chain = false;
   bool has_ranges = false, synced_last = false;
   bool overlap = true;
   uint64_t launches = 0;
@@ -660,9 +701,9 @@ dsx_status check_row(dsx_lab* lab, int local) {
 }
 
 template <typename T, int KL>
-void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, bool noise, bool average,
+void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int nm, bool average,
                      const MaskBits& mask, double eta) {
-  UpdateArgs<T> a;
+  UpdateArgs<T> a{};
   a.w = static_cast<T*>(lab->w);
   a.ld = lab->ld;
   a.kl = lab->kl;
@@ -676,16 +717,19 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, boo
   a.mask = mask;
   a.average = average;
   a.norm_part = lab->norm_part;
-  if (noise) {
-    lab_update_kernel<T, KL, true><<<count, kThreads, 0, s>>>(a, lab->prog_local);
+  if (lab->engine) a.nv = lab->engine->view();
+  if (nm == 2) {
+    lab_update_kernel<T, KL, 2><<<count, kThreads, 0, s>>>(a, lab->prog_local);
+  } else if (nm == 1) {
+    lab_update_kernel<T, KL, 1><<<count, kThreads, 0, s>>>(a, lab->prog_local);
   } else {
-    lab_update_kernel<T, KL, false><<<count, kThreads, 0, s>>>(a, lab->prog_local);
+    lab_update_kernel<T, KL, 0><<<count, kThreads, 0, s>>>(a, lab->prog_local);
   }
   ++lab->launches;
 }
 
 template <typename T>
-void launch_update(dsx_lab* lab, cudaStream_t s, int tile_base, int count, bool noise, bool average,
+void launch_update(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int noise, bool average,
                    const MaskBits& mask, double eta) {
   switch (lab->kl) {
     case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta);
@@ -814,16 +858,12 @@ std::vector<std::pair<long long, long long>> masked_ranges(const dsx_lab* lab, c
 }
 
 template <typename T>
-dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, bool noise) {
+dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int noise) {
   MaskBits bits{};
   for (int b = 0; b < lab->L; ++b)
     if (mask[b + 1]) bits.w[b >> 5] |= 1u << (b & 31);
   const bool single = lab->nranks == 1;
   if (lab->kl == 0 || lab->ntiles == 0) return DSX_OK;
-  if (lab->kl > 8) {
-    zero_kernel<<<lab->nsm, 256, 0, lab->stream>>>(lab->norm_part, (long long)lab->kl * lab->ntiles);
-    ++lab->launches;
-  }
   if (single) {
     launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, lab->K > 1, bits, eta);
   } else {
@@ -854,8 +894,9 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, bool n
     if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
     if (!ranges.empty()) DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_synced, 0));
   }
-  norm_finalize_kernel<<<1, 1024, 0, lab->stream>>>(lab->norm_part, lab->ntiles, lab->kl, lab->norm,
-                                                    lab->maxnorm);
+  DSX_CUDA(cudaMemsetAsync(lab->maxnorm, 0, 8, lab->stream));
+  norm_finalize_kernel<<<lab->kl, 1024, 0, lab->stream>>>(
+      lab->norm_part, lab->ntiles, lab->norm, reinterpret_cast<unsigned long long*>(lab->maxnorm));
   ++lab->launches;
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[4], lab->stream));
   lab->synced_last = !single && lab->has_ranges;
@@ -863,12 +904,22 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, bool n
   return DSX_OK;
 }
 
-dsx_status run_noise(dsx_lab* lab) {
-  if (lab->sigma > 0.0) {
+// Generates this step's noise; returns the update kernels' noise mode.
+dsx_status run_noise(dsx_lab* lab, int* mode) {
+  *mode = 0;
+  if (lab->sigma <= 0.0) return DSX_OK;
+  if (lab->use_chain) {  // DSX_NOISE_CHAIN=1: the single-chain reference engine
     mt_noise_chain_kernel<<<lab->kl, kMtThreads, 0, lab->stream>>>(lab->mt, lab->noise, lab->ld,
                                                                    lab->dim, lab->stddev);
     ++lab->launches;
+    *mode = 1;
+    return DSX_OK;
   }
+  std::string err;
+  const uint64_t before = lab->engine->launches();
+  if (!lab->engine->run(lab->mt, lab->stddev, lab->stream, &err)) return fail(DSX_ERR_CUDA, err);
+  lab->launches += lab->engine->launches() - before;
+  *mode = 2;
   return DSX_OK;
 }
 
@@ -946,8 +997,18 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
   }
   if (cudaMalloc(&lab->mt, 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
     return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(mt) failed"));
-  if (lab->sigma > 0.0 && cudaMalloc(&lab->noise, 8 * (size_t)lab->ld * lab->kl) != cudaSuccess)
-    return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(noise) failed"));
+  if (lab->sigma > 0.0) {
+    const char* chain = std::getenv("DSX_NOISE_CHAIN");
+    lab->use_chain = chain && chain[0] == '1';
+    if (lab->use_chain) {
+      if (cudaMalloc(&lab->noise, 8 * (size_t)lab->ld * lab->kl) != cudaSuccess)
+        return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(noise) failed"));
+    } else {
+      lab->engine = new dsx::NoiseEngine();
+      std::string err;
+      if (!lab->engine->init(lab->dim, lab->kl, lab->nsm, &err)) return cleanup(fail(DSX_ERR_CUDA, err));
+    }
+  }
   // tiles: per block, kTile coordinates each (never crossing a block)
   for (int b = 0; b < lab->L; ++b) {
     for (unsigned long long s = lab->offs[b]; s < lab->offs[b + 1]; s += kTile) {
@@ -986,6 +1047,7 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   if (lab->stream) cudaStreamSynchronize(lab->stream);
   if (lab->side) cudaStreamSynchronize(lab->side);
   if (lab->comm) ncclCommDestroy(lab->comm);
+  delete lab->engine;
   for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt,
                   (void*)lab->what, (void*)lab->tiles, (void*)lab->norm_part, (void*)lab->norm,
                   (void*)lab->maxnorm, (void*)lab->log_part, lab->staging, lab->recv})
@@ -1112,9 +1174,9 @@ dsx_status dsx_lab_step(dsx_lab* lab, double eta, const unsigned char* mask) {
   DSX_TRY(check_lab(lab));
   if (!mask) return fail(DSX_ERR_ARGUMENT, "null mask");
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[0], lab->stream));
-  DSX_TRY(run_noise(lab));
+  int noise = 0;
+  DSX_TRY(run_noise(lab, &noise));
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[5], lab->stream));
-  const bool noise = lab->sigma > 0.0;
   return lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, noise)
                                : step_impl<float>(lab, eta, mask, noise);
 }
@@ -1132,8 +1194,8 @@ dsx_status dsx_lab_step_with_noise(dsx_lab* lab, double eta, const unsigned char
     DSX_CUDA(cudaEventRecord(lab->iev[0], lab->stream));
     DSX_CUDA(cudaEventRecord(lab->iev[5], lab->stream));
   }
-  return lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, true)
-                               : step_impl<float>(lab, eta, mask, true);
+  return lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, 1)
+                               : step_impl<float>(lab, eta, mask, 1);
 }
 
 dsx_status dsx_lab_last_max_grad_norm_sq(dsx_lab* lab, double* out) {
@@ -1155,16 +1217,20 @@ dsx_status dsx_lab_sync(dsx_lab* lab) {
 dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
   DSX_TRY(check_row(lab, local));
   if (!g_out) return fail(DSX_ERR_ARGUMENT, "null gradient out");
-  DSX_TRY(run_noise(lab));  // advances every local row's stream; see note in trainer.cpp
+  int nm = 0;
+  DSX_TRY(run_noise(lab, &nm));  // advances every local row's stream
   double* g = nullptr;
   DSX_CUDA(cudaMallocAsync((void**)&g, 8 * lab->dim, lab->stream));
-  const double* xi = lab->sigma > 0.0 ? lab->noise + (long long)local * lab->ld : nullptr;
+  const double* xi = nm == 1 ? lab->noise + (long long)local * lab->ld : nullptr;
+  const NoiseView nv = lab->engine ? lab->engine->view() : NoiseView{};
   if (lab->dtype == DSX_F64) {
     gradient_kernel<double><<<lab->nsm * 4, 256, 0, lab->stream>>>(
-        static_cast<const double*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, xi, g);
+        static_cast<const double*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, nm, xi, nv,
+        local, g);
   } else {
     gradient_kernel<float><<<lab->nsm * 4, 256, 0, lab->stream>>>(
-        static_cast<const float*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, xi, g);
+        static_cast<const float*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, nm, xi, nv,
+        local, g);
   }
   ++lab->launches;
   DSX_CUDA(cudaMemcpyAsync(g_out, g, 8 * lab->dim, cudaMemcpyDeviceToHost, lab->stream));
@@ -1297,6 +1363,31 @@ dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out3) {
     out3[1] = sync_end - sync_start;
     out3[2] = std::max(0.0f, sync_end - local_end);
   }
+  return DSX_OK;
+}
+
+// Host-only check of the MT19937-64 jump-ahead: the window at stream
+// offset 1+J computed by the characteristic-polynomial jump equals the one
+// produced by running the recurrence.  Needs no GPU.
+dsx_status dsx_mt_jump_selftest(unsigned long long jump, int* ok) {
+  if (!ok) return fail(DSX_ERR_ARGUMENT, "null ok");
+  if (jump > 50'000'000ull) return fail(DSX_ERR_ARGUMENT, "jump too large for the direct check");
+  std::mt19937_64 eng(12345u);
+  for (int i = 0; i < 1000; ++i) eng();
+  std::stringstream ss;
+  ss << eng;
+  uint64_t x[kMtN];
+  for (int i = 0; i < kMtN; ++i) ss >> x[i];
+  if (dsx::mt_char_poly().empty()) return fail(DSX_ERR_STATE, "characteristic polynomial unavailable");
+  const std::vector<uint64_t> jumped = dsx::mt_jump_host(x, dsx::mt_jump_poly(jump));
+  std::vector<uint64_t> y(x, x + kMtN);
+  y.reserve(jump + 2 * kMtN + 2);
+  while (y.size() < jump + 1 + kMtN) {
+    const size_t k = y.size() - kMtN;
+    y.push_back(mt_next_word(y[k], y[k + 1], y[k + kMtM]));
+  }
+  *ok = 1;
+  for (int j = 0; j < kMtN; ++j) *ok &= jumped[j] == y[1 + jump + j];
   return DSX_OK;
 }
 

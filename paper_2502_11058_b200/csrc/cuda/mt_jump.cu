@@ -1,0 +1,638 @@
+// mt_jump.cu — the parallel, stream-exact noise engine (see noise_engine.cuh).
+//
+// Host: the MT19937-64 characteristic polynomial (Berlekamp-Massey over
+// GF(2)) and jump polynomials c_s = x^(s*S - 1) mod phi.
+// Device: prefix -> jump -> segment -> finish kernels, one CUDA stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <sstream>
+
+#include "mt_engine.cuh"
+#include "noise_engine.cuh"
+
+#if defined(__x86_64__)
+#include <wmmintrin.h>
+#endif
+
+namespace dsx {
+
+namespace {
+
+constexpr int kDeg = 19937;               // deg phi
+constexpr int kPolyWords = 312;            // ceil(19938 / 64)
+constexpr int kPrefixWords = 65 * kMtN;    // Y[0 .. 20280): >= 1 + 19940 + 311 + 10
+constexpr int kJumpBits = 19940;           // c padded to a multiple of 10
+constexpr int kCkWords = kMtN + 4;         // x[312], carry flag, carry bits, local count, pad
+constexpr int kThreads = 320;
+
+using Poly = std::vector<uint64_t>;
+
+// ---- host GF(2) polynomial arithmetic -----------------------------------
+
+void xor_shifted(uint64_t* dst, size_t dst_words, const uint64_t* src, size_t src_words, size_t shift) {
+  const size_t ws = shift / 64, bs = shift % 64;
+  for (size_t i = 0; i < src_words; ++i) {
+    const uint64_t v = src[i];
+    if (!v) continue;
+    if (i + ws < dst_words) dst[i + ws] ^= v << bs;
+    if (bs && i + ws + 1 < dst_words) dst[i + ws + 1] ^= v >> (64 - bs);
+  }
+}
+
+bool get_bit(const uint64_t* p, size_t i) { return (p[i / 64] >> (i % 64)) & 1u; }
+
+// reduce r (any length, degree < 64*len) modulo phi in place; result in the
+// low kPolyWords words.
+void reduce(Poly& r, const Poly& phi) {
+  // byte table of v(x) * phi(x), v in [0, 256)
+  static std::vector<Poly> table;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    table.assign(256, Poly(kPolyWords + 1, 0));
+    for (int v = 1; v < 256; ++v)
+      for (int b = 0; b < 8; ++b)
+        if ((v >> b) & 1) xor_shifted(table[v].data(), kPolyWords + 1, phi.data(), kPolyWords, b);
+  });
+  const long top = (long)r.size() * 64 - 1;
+  long t = top;
+  for (; t - 7 >= kDeg; t -= 8) {
+    // byte of r at bits [t-7, t]
+    const size_t lo = (size_t)(t - 7);
+    uint64_t v = r[lo / 64] >> (lo % 64);
+    if (lo % 64 > 56 && lo / 64 + 1 < r.size()) v |= r[lo / 64 + 1] << (64 - lo % 64);
+    v &= 0xff;
+    if (v) xor_shifted(r.data(), r.size(), table[v].data(), kPolyWords + 1, lo - kDeg);
+  }
+  for (; t >= kDeg; --t)
+    if (get_bit(r.data(), (size_t)t)) xor_shifted(r.data(), r.size(), phi.data(), kPolyWords, (size_t)t - kDeg);
+  r.resize(kPolyWords);
+}
+
+#if defined(__x86_64__)
+__attribute__((target("pclmul,sse2"))) void clmul_words(const uint64_t* a, const uint64_t* b, uint64_t* out,
+                                                        size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    if (!a[i]) continue;
+    const __m128i av = _mm_set_epi64x(0, (long long)a[i]);
+    for (size_t j = 0; j < n; ++j) {
+      const __m128i bv = _mm_set_epi64x(0, (long long)b[j]);
+      const __m128i p = _mm_clmulepi64_si128(av, bv, 0x00);
+      out[i + j] ^= (uint64_t)_mm_cvtsi128_si64(p);
+      out[i + j + 1] ^= (uint64_t)_mm_cvtsi128_si64(_mm_unpackhi_epi64(p, p));
+    }
+  }
+}
+#endif
+
+void clmul_portable(const uint64_t* a, const uint64_t* b, uint64_t* out, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    for (int bit = 0; bit < 64; ++bit) {
+      if (!((a[i] >> bit) & 1)) continue;
+      xor_shifted(out + i, 2 * n - i, b, n, (size_t)bit);
+    }
+  }
+}
+
+Poly mulmod(const Poly& a, const Poly& b, const Poly& phi) {
+  Poly prod(2 * kPolyWords + 1, 0);
+#if defined(__x86_64__)
+  if (__builtin_cpu_supports("pclmul")) {
+    clmul_words(a.data(), b.data(), prod.data(), kPolyWords);
+  } else {
+    clmul_portable(a.data(), b.data(), prod.data(), kPolyWords);
+  }
+#else
+  clmul_portable(a.data(), b.data(), prod.data(), kPolyWords);
+#endif
+  reduce(prod, phi);
+  return prod;
+}
+
+Poly sqrmod(const Poly& a, const Poly& phi) {
+  Poly sq(2 * kPolyWords + 1, 0);
+  for (size_t i = 0; i < kPolyWords; ++i) {
+    uint64_t v = a[i];
+    uint64_t lo = 0, hi = 0;
+    for (int b = 0; b < 32; ++b) {
+      lo |= ((v >> b) & 1ull) << (2 * b);
+      hi |= ((v >> (b + 32)) & 1ull) << (2 * b);
+    }
+    sq[2 * i] = lo;
+    sq[2 * i + 1] = hi;
+  }
+  reduce(sq, phi);
+  return sq;
+}
+
+Poly x_pow(unsigned long long J, const Poly& phi) {
+  Poly r(kPolyWords, 0);
+  r[0] = 1;
+  for (int bit = 63; bit >= 0; --bit) {
+    r = sqrmod(r, phi);
+    if ((J >> bit) & 1ull) {  // r *= x
+      Poly t(kPolyWords + 1, 0);
+      xor_shifted(t.data(), t.size(), r.data(), kPolyWords, 1);
+      reduce(t, phi);
+      r = t;
+    }
+  }
+  return r;
+}
+
+// Y[0..n) from a generation-aligned 312-word array.
+void host_sequence(const uint64_t* x, size_t n, std::vector<uint64_t>& y) {
+  y.assign(x, x + kMtN);
+  y.reserve(n);
+  while (y.size() < n) {
+    const size_t k = y.size() - kMtN;
+    y.push_back(mt_next_word(y[k], y[k + 1], y[k + kMtM]));
+  }
+}
+
+Poly compute_char_poly() {
+  // Bit 0 of Y[1..] of an arbitrary stream; its minimal polynomial is phi.
+  std::mt19937_64 eng(5489u);
+  std::stringstream ss;
+  ss << eng;
+  uint64_t x[kMtN];
+  for (int i = 0; i < kMtN; ++i) ss >> x[i];
+  const size_t N = 2 * kDeg + 256;
+  std::vector<uint64_t> y;
+  host_sequence(x, N + 2, y);
+  // reversed bit sequence: rev[k] = s_{N-1-k}, s_n = Y[1+n] & 1
+  const size_t RW = (N + 63) / 64 + 2;
+  std::vector<uint64_t> rev(RW, 0);
+  for (size_t n = 0; n < N; ++n)
+    if (y[1 + n] & 1) {
+      const size_t k = N - 1 - n;
+      rev[k / 64] |= 1ull << (k % 64);
+    }
+  const size_t CW = (N + 63) / 64 + 2;
+  std::vector<uint64_t> C(CW, 0), B(CW, 0), T;
+  C[0] = B[0] = 1;
+  size_t L = 0, m = 1;
+  for (size_t n = 0; n < N; ++n) {
+    // d = sum_{i=0..L} C_i s_{n-i} = sum_i C_i rev[N-1-n+i]
+    const size_t off = N - 1 - n;
+    uint64_t acc = 0;
+    const size_t words = L / 64 + 1;
+    for (size_t w = 0; w < words; ++w) {
+      const size_t bit = off + 64 * w;
+      uint64_t r = rev[bit / 64] >> (bit % 64);
+      if (bit % 64 && bit / 64 + 1 < RW) r |= rev[bit / 64 + 1] << (64 - bit % 64);
+      uint64_t c = C[w];
+      if (w == words - 1 && (L % 64) != 63) c &= (2ull << (L % 64)) - 1;
+      acc ^= c & r;
+    }
+    const bool d = __builtin_popcountll(acc) & 1;
+    if (!d) {
+      ++m;
+    } else if (2 * L <= n) {
+      T = C;
+      xor_shifted(C.data(), CW, B.data(), CW, m);
+      L = n + 1 - L;
+      B = T;
+      m = 1;
+    } else {
+      xor_shifted(C.data(), CW, B.data(), CW, m);
+      ++m;
+    }
+  }
+  Poly phi(kPolyWords, 0);
+  if (L != (size_t)kDeg) return Poly();  // signals failure
+  // phi_k = C_{L-k}
+  for (size_t k = 0; k <= L; ++k)
+    if (get_bit(C.data(), L - k)) phi[k / 64] |= 1ull << (k % 64);
+  return phi;
+}
+
+}  // namespace
+
+const std::vector<uint64_t>& mt_char_poly() {
+  static Poly phi;
+  static std::once_flag once;
+  std::call_once(once, [] { phi = compute_char_poly(); });
+  return phi;
+}
+
+std::vector<uint64_t> mt_jump_poly(unsigned long long J) { return x_pow(J, mt_char_poly()); }
+
+std::vector<uint64_t> mt_jump_host(const uint64_t* x312, const std::vector<uint64_t>& c) {
+  std::vector<uint64_t> y;
+  host_sequence(x312, kPrefixWords, y);
+  std::vector<uint64_t> out(kMtN, 0);
+  for (int i = 0; i < kDeg; ++i)
+    if (get_bit(c.data(), (size_t)i))
+      for (int j = 0; j < kMtN; ++j) out[j] ^= y[1 + i + j];
+  return out;
+}
+
+// ---- device ----------------------------------------------------------------
+
+namespace {
+
+struct Smem {
+  uint64_t x[kMtN];
+  double v[kMtN + 2];
+  int wcnt[kThreads / 32];
+  int misc[4];
+};
+
+__device__ __forceinline__ void block_twist(uint64_t* x) {
+  const int tid = threadIdx.x;
+  uint64_t a0 = 0, a1 = 0, a2 = 0;
+  if (tid < kMtM) {
+    a0 = x[tid];
+    a1 = x[tid + 1];
+    a2 = x[tid + kMtM];
+  }
+  __syncthreads();
+  if (tid < kMtM) x[tid] = mt_next_word(a0, a1, a2);
+  __syncthreads();
+  if (tid < kMtM) {
+    const int k = kMtM + tid;
+    a0 = x[k];
+    a1 = (k + 1 < kMtN) ? x[k + 1] : x[0];
+    a2 = x[k - kMtM];
+  }
+  __syncthreads();
+  if (tid < kMtM) x[kMtM + tid] = mt_next_word(a0, a1, a2);
+  __syncthreads();
+}
+
+// One generation's outputs [lo, hi) with a carried half pair: fills v,
+// evaluates this thread's attempt (tid < npairs), returns the CTA total and
+// the thread's rank among accepted attempts.  Updates the carry.
+struct PairEval {
+  bool acc;
+  int rank;
+  int total;
+  int npairs;
+  double px, py, r2;
+};
+
+__device__ __forceinline__ PairEval eval_generation(Smem& sm, int lo, int hi, int& have_half,
+                                                    double& half) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid >= lo && tid < hi) sm.v[have_half + tid - lo] = mt_polar_coord(mt_temper(sm.x[tid]));
+  if (tid == 0 && have_half) sm.v[0] = half;
+  __syncthreads();
+  const int nvals = have_half + (hi - lo);
+  PairEval e;
+  e.npairs = nvals >> 1;
+  e.acc = false;
+  e.px = e.py = e.r2 = 0.0;
+  if (tid < e.npairs) {
+    e.px = sm.v[2 * tid];
+    e.py = sm.v[2 * tid + 1];
+    e.acc = mt_polar_accept(e.px, e.py, &e.r2);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, e.acc);
+  if (lane == 0) sm.wcnt[warp] = __popc(bal);
+  __syncthreads();
+  int before = __popc(bal & ((1u << lane) - 1u));
+  int total = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) before += sm.wcnt[w];
+    total += sm.wcnt[w];
+  }
+  e.rank = before;
+  e.total = total;
+  if (nvals & 1) {
+    half = sm.v[nvals - 1];
+    have_half = 1;
+  } else {
+    have_half = 0;
+  }
+  __syncthreads();  // v / wcnt reusable
+  return e;
+}
+
+// Normalizes the cursor (p == 312 -> twist) and writes Y[0..kPrefixWords).
+__global__ void __launch_bounds__(kThreads)
+mt_prefix_kernel(const uint64_t* mt, uint64_t* ybuf, uint64_t* win, int P, int* pnorm) {
+  __shared__ uint64_t x[kMtN];
+  const int w = blockIdx.x, tid = threadIdx.x;
+  const uint64_t* st = mt + (long long)w * (kMtN + 1);
+  if (tid < kMtN) x[tid] = st[tid];
+  int p = (int)st[kMtN];
+  __syncthreads();
+  if (p >= kMtN) {
+    block_twist(x);
+    p = 0;
+  }
+  uint64_t* y = ybuf + (long long)w * kPrefixWords;
+  for (int g = 0; g < kPrefixWords / kMtN; ++g) {
+    if (g) block_twist(x);
+    if (tid < kMtN) {
+      y[g * kMtN + tid] = x[tid];
+      if (g == 0) win[(long long)w * P * kMtN + tid] = x[tid];
+    }
+  }
+  if (tid == 0) pnorm[w] = p;
+}
+
+// Segment start windows W_{sS} = sum_i c_s[i] W_{1+i}: one warp per jump,
+// lane l owns window words [10l, 10l+10) with a sliding register window.
+constexpr int kJumpWarps = 8;
+
+__global__ void __launch_bounds__(kJumpWarps * 32)
+mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 + 1]*/, uint64_t* win, int P) {
+  extern __shared__ uint64_t ys[];
+  const int w = blockIdx.y;
+  const uint64_t* y = ybuf + (long long)w * kPrefixWords;
+  for (int i = threadIdx.x; i < kPrefixWords; i += blockDim.x) ys[i] = y[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = 1 + blockIdx.x * kJumpWarps + warp;
+  if (s >= P) return;
+  constexpr int kCW = kJumpBits / 32 + 1;
+  const uint32_t* c = cbits + (long long)(s - 1) * kCW;
+  const int j0 = 10 * lane;  // lanes 0..31 cover 0..319 (>= 312 ignored)
+  uint64_t acc[10], win_r[10];
+#pragma unroll
+  for (int q = 0; q < 10; ++q) {
+    acc[q] = 0;
+    win_r[q] = ys[1 + j0 + q];
+  }
+  uint32_t cw = 0;
+  for (int i0 = 0; i0 < kJumpBits; i0 += 10) {
+#pragma unroll
+    for (int u = 0; u < 10; ++u) {
+      const int i = i0 + u;
+      if ((i & 31) == 0 || u == 0) cw = c[i >> 5];
+      if ((cw >> (i & 31)) & 1u) {
+#pragma unroll
+        for (int q = 0; q < 10; ++q) acc[q] ^= win_r[(u + q) % 10];
+      }
+      // slide: logical slot 0 (= win_r[u]) leaves, Y[1 + (i+1) + j0 + 9] enters
+      win_r[u] = ys[1 + i + 1 + j0 + 9];
+    }
+  }
+  uint64_t* out = win + ((long long)w * P + s) * kMtN;
+#pragma unroll
+  for (int q = 0; q < 10; ++q)
+    if (j0 + q < kMtN) out[j0 + q] = acc[q];
+}
+
+__device__ __forceinline__ void store_ck(uint64_t* ck, const uint64_t* x, int have_half, double half,
+                                         unsigned long long local) {
+  const int tid = threadIdx.x;
+  if (tid < kMtN) ck[tid] = x[tid];
+  if (tid == 0) {
+    ck[kMtN] = (uint64_t)have_half;
+    ck[kMtN + 1] = (uint64_t)__double_as_longlong(half);
+    ck[kMtN + 2] = local;
+  }
+}
+
+// One CTA per (segment, worker): S outputs from relative position sS + p.
+__global__ void __launch_bounds__(kThreads)
+mt_segment_kernel(const uint64_t* win, const int* pnorm, int P, int gens, int ck_every, int nck,
+                  double stddev, double* slots, long long cap, unsigned long long* cnt,
+                  uint64_t* ck, uint64_t* tail) {
+  __shared__ Smem sm;
+  const int s = blockIdx.x, w = blockIdx.y, tid = threadIdx.x;
+  if (tid < kMtN) sm.x[tid] = win[((long long)w * P + s) * kMtN + tid];
+  const int p = pnorm[w];
+  const int ngen = gens + (p > 0 ? 1 : 0);
+  double* out = slots + ((long long)w * (P + 1) + s) * cap;
+  uint64_t* ckw = ck + ((long long)w * P + s) * (long long)nck * kCkWords;
+  int have_half = 0;
+  double half = 0.0;
+  unsigned long long local = 0;
+  __syncthreads();
+  for (int q = 0; q < ngen; ++q) {
+    if (q) block_twist(sm.x);
+    if (q % ck_every == 0) store_ck(ckw + (long long)(q / ck_every) * kCkWords, sm.x, have_half, half, local);
+    const int lo = q == 0 ? p : 0;
+    const int hi = (q == gens) ? p : kMtN;  // only reached when p > 0
+    const PairEval e = eval_generation(sm, lo, hi, have_half, half);
+    if (e.acc) {
+      const unsigned long long m = local + (unsigned long long)e.rank;
+      const double mult = mt_polar_mult(e.r2);
+      out[2 * m] = mt_scale(e.py, mult, stddev);
+      out[2 * m + 1] = mt_scale(e.px, mult, stddev);
+    }
+    local += (unsigned long long)e.total;
+  }
+  if (tid == 0) cnt[(long long)w * P + s] = local;
+  // end state for an overflow continuation: the last processed array, next
+  // offset = p (or 312 when p == 0: twist first)
+  store_ck(tail + ((long long)w * P + s) * kCkWords, sm.x, have_half, half, local);
+}
+
+// Walks generations from a checkpoint until the target pair; writes the new
+// rng state.  Also serves the (rare) overflow continuation.
+__global__ void __launch_bounds__(kThreads)
+mt_finish_kernel(uint64_t* mt, const int* pnorm, int P, int gens, int ck_every, int nck,
+                 unsigned long long pairs_needed, double stddev, double* slots, long long cap,
+                 const unsigned long long* cnt, unsigned long long* pfx, const uint64_t* ck,
+                 const uint64_t* tail, int* status) {
+  __shared__ Smem sm;
+  __shared__ unsigned long long s_pfx_target[3];
+  const int w = blockIdx.x, tid = threadIdx.x;
+  const int p = pnorm[w];
+  unsigned long long* pf = pfx + (long long)w * (P + 2);
+  if (tid == 0) {
+    unsigned long long run = 0;
+    int star = -1;
+    for (int s = 0; s < P; ++s) {
+      pf[s] = run;
+      const unsigned long long c = cnt[(long long)w * P + s];
+      if (star < 0 && run + c >= pairs_needed) star = s;
+      run += c;
+    }
+    pf[P] = run;
+    pf[P + 1] = run;
+    s_pfx_target[0] = (unsigned long long)(star < 0 ? P : star);
+    s_pfx_target[1] = run;
+  }
+  __syncthreads();
+  const int star = (int)s_pfx_target[0];
+  const unsigned long long total = s_pfx_target[1];
+  int have_half = 0, q = 0, lo = 0, hi = kMtN;
+  double half = 0.0;
+  unsigned long long local = 0, target = 0;
+  double* out = nullptr;
+  bool overflow = star >= P;
+  if (!overflow) {
+    target = pairs_needed - 1 - pf[star];
+    // last checkpoint at or before the target pair
+    const uint64_t* base = ck + ((long long)w * P + star) * (long long)nck * kCkWords;
+    int c = 0;
+    for (int k = 1; k < nck; ++k) {
+      if (k * ck_every >= gens + (p > 0 ? 1 : 0)) break;
+      if (base[(long long)k * kCkWords + kMtN + 2] <= target) c = k;
+    }
+    const uint64_t* cp = base + (long long)c * kCkWords;
+    if (tid < kMtN) sm.x[tid] = cp[tid];
+    have_half = (int)cp[kMtN];
+    half = __longlong_as_double((long long)cp[kMtN + 1]);
+    local = cp[kMtN + 2];
+    q = c * ck_every;
+  } else {
+    // continue after the last segment: its final array, next offset p
+    const uint64_t* tp = tail + ((long long)w * P + (P - 1)) * kCkWords;
+    if (tid < kMtN) sm.x[tid] = tp[tid];
+    have_half = (int)tp[kMtN];
+    half = __longlong_as_double((long long)tp[kMtN + 1]);
+    local = 0;
+    target = pairs_needed - 1 - total;
+    out = slots + ((long long)w * (P + 1) + P) * cap;
+    q = -1;  // marks continuation
+  }
+  __syncthreads();
+  bool first = true;
+  for (;;) {
+    if (!overflow) {
+      if (!first) block_twist(sm.x);
+      lo = q == 0 ? p : 0;
+      hi = (q == gens) ? p : kMtN;
+    } else {
+      if (first && p > 0) {
+        lo = p;  // rest of the last segment's final array
+      } else {
+        block_twist(sm.x);
+        lo = 0;
+      }
+      hi = kMtN;
+    }
+    first = false;
+    const int carry_in = have_half;
+    const PairEval e = eval_generation(sm, lo, hi, have_half, half);
+    if (overflow && e.acc) {
+      const unsigned long long m = local + (unsigned long long)e.rank;
+      if (2 * m + 1 < (unsigned long long)cap) {
+        const double mult = mt_polar_mult(e.r2);
+        out[2 * m] = mt_scale(e.py, mult, stddev);
+        out[2 * m + 1] = mt_scale(e.px, mult, stddev);
+      }
+    }
+    if (local + (unsigned long long)e.total > target) {
+      // the attempt with rank (target - local) ends this step's consumption
+      if (e.acc && (unsigned long long)e.rank == target - local) {
+        const int end_off = lo - carry_in + 2 * tid + 2;  // one past its second output
+        sm.misc[0] = end_off;
+      }
+      __syncthreads();
+      uint64_t* st = mt + (long long)w * (kMtN + 1);
+      if (tid < kMtN) st[tid] = sm.x[tid];
+      if (tid == 0) {
+        st[kMtN] = (uint64_t)sm.misc[0];
+        if (overflow) {
+          pf[P + 1] = total + target + 1;
+          status[w] = (2 * (target + 1) <= (unsigned long long)cap) ? 0 : 1;
+        } else {
+          status[w] = 0;
+        }
+      }
+      return;
+    }
+    local += (unsigned long long)e.total;
+    if (!overflow) ++q;
+  }
+}
+
+}  // namespace
+
+NoiseEngine::~NoiseEngine() {
+  for (void* p : {(void*)ybuf_, (void*)win_, (void*)jidx_, (void*)joff_, (void*)slots_, (void*)cnt_,
+                  (void*)pfx_, (void*)ck_, (void*)tail_, (void*)status_})
+    if (p) cudaFree(p);
+}
+
+bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err) {
+  dim_ = dim;
+  kl_ = kl;
+  // outputs one step needs: 2 per attempt, M / (pi/4) attempts, + 8 sd + slack
+  const double M = (double)((dim + 1) / 2);
+  const double pa = 0.78539816339744831;
+  const double attempts = M / pa + 8.0 * std::sqrt(M * (1.0 - pa)) / pa + 1024.0;
+  const double E = 2.0 * attempts;
+  const double min_seg = 312.0 * 64.0;
+  int P = (int)std::ceil(E / min_seg);
+  P = std::max(1, std::min(P, (int)std::ceil(4.0 * nsm / kl)));
+  long long gens = (long long)std::ceil(E / P / 312.0);
+  if (gens < 1) gens = 1;
+  S_ = gens * 312;
+  P_ = (int)std::ceil(E / (double)S_);
+  gens_ = (int)gens;
+  ck_every_ = 16;
+  nck_ = (gens_ + 1 + ck_every_ - 1) / ck_every_ + 1;
+  cap_ = S_ + 16;
+
+  const std::vector<uint64_t>& phi = mt_char_poly();
+  if (phi.empty()) {
+    *err = "MT19937-64 characteristic polynomial: Berlekamp-Massey did not reach degree 19937";
+    return false;
+  }
+  // jump bitsets for s = 1..P-1: c_s = x^(sS-1) mod phi
+  constexpr int kCW = kJumpBits / 32 + 1;
+  std::vector<uint32_t> bits((size_t)std::max(1, P_ - 1) * kCW, 0);
+  if (P_ > 1) {
+    Poly c = x_pow((unsigned long long)S_ - 1, phi);
+    const Poly step = x_pow((unsigned long long)S_, phi);
+    for (int s = 1; s < P_; ++s) {
+      if (s > 1) c = mulmod(c, step, phi);
+      uint32_t* dst = bits.data() + (size_t)(s - 1) * kCW;
+      for (int i = 0; i < kDeg; ++i)
+        if (get_bit(c.data(), (size_t)i)) dst[i >> 5] |= 1u << (i & 31);
+    }
+  }
+  auto alloc = [&](void** p, size_t bytes) {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      *err = "noise engine: cudaMalloc failed";
+      return false;
+    }
+    return true;
+  };
+  if (!alloc((void**)&ybuf_, 8ull * kPrefixWords * kl) || !alloc((void**)&win_, 8ull * kMtN * P_ * kl) ||
+      !alloc((void**)&jidx_, bits.size() * 4) ||
+      !alloc((void**)&slots_, 8ull * cap_ * (P_ + 1) * kl) || !alloc((void**)&cnt_, 8ull * P_ * kl) ||
+      !alloc((void**)&pfx_, 8ull * (P_ + 2) * kl) ||
+      !alloc((void**)&ck_, 8ull * kCkWords * nck_ * P_ * kl) ||
+      !alloc((void**)&tail_, 8ull * kCkWords * P_ * kl) || !alloc((void**)&status_, 4ull * kl) ||
+      !alloc((void**)&joff_, 4ull * kl))
+    return false;
+  cudaMemcpy(jidx_, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemset(status_, 0, 4ull * kl);
+  if (cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8 * kPrefixWords) != cudaSuccess) {
+    *err = "noise engine: cannot opt in to 162 KB shared memory";
+    return false;
+  }
+  return true;
+}
+
+bool NoiseEngine::run(uint64_t* mt, double stddev, void* stream_ptr, std::string* err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  int* pnorm = joff_;  // [kl] normalized cursors
+  mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt, ybuf_, win_, P_, pnorm);
+  ++launches_;
+  if (P_ > 1) {
+    dim3 grid((P_ - 1 + kJumpWarps - 1) / kJumpWarps, kl_);
+    mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(
+        ybuf_, reinterpret_cast<const uint32_t*>(jidx_), win_, P_);
+    ++launches_;
+  }
+  mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(win_, pnorm, P_, gens_, ck_every_, nck_,
+                                                             stddev, slots_, cap_, cnt_, ck_, tail_);
+  mt_finish_kernel<<<kl_, kThreads, 0, stream>>>(mt, pnorm, P_, gens_, ck_every_, nck_, (dim_ + 1) / 2,
+                                                 stddev, slots_, cap_, cnt_, pfx_, ck_, tail_, status_);
+  launches_ += 2;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("noise engine launch: ") + cudaGetErrorString(e);
+    return false;
+  }
+  return true;
+}
+
+}  // namespace dsx

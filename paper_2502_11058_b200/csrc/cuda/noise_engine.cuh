@@ -1,0 +1,74 @@
+// noise_engine.cuh — parallel, stream-exact reproduction of the reference's
+// per-worker gradient noise (std::mt19937_64 + std::normal_distribution,
+// trainer.cpp:179-183) on sm_100a.
+//
+// A worker's step consumes a contiguous run of its Mersenne-twister stream;
+// how long the run is depends on the polar method's rejections, i.e. on the
+// stream itself (never on the parameters).  The engine cuts the run into P
+// segments of S outputs (S a multiple of 312), reaches each segment's start
+// state with an MT19937-64 jump-ahead — W_{1+J} = sum_i c_i W_{1+i} over
+// GF(2) with c = x^J mod phi, phi the characteristic polynomial of the
+// twister (computed once by Berlekamp-Massey on the host) — and lets one CTA
+// per segment generate, accept/reject and transform its attempts.  A
+// finisher scans the per-segment accepted-pair counts, pins the exact attempt
+// that produces normal dim-1, and writes back the worker's new
+// (x[312], cursor) state.  The update kernel maps coordinate i -> (segment,
+// slot) through the scanned counts.  Every accept/reject and every stream
+// position is bit-identical to libstdc++; see mt_engine.cuh for the per-draw
+// arithmetic.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dsx {
+
+struct NoiseView {
+  const double* slots;              // [kl][P+1][cap]
+  const unsigned long long* pfx;    // [kl][P+2] exclusive pair prefix per segment
+  long long cap;                    // slot capacity (doubles)
+  int P;                            // segments (slot P = overflow)
+};
+
+class NoiseEngine {
+ public:
+  // dim: normals per worker per step; kl: local workers; nsm: SM count.
+  NoiseEngine() = default;
+  ~NoiseEngine();
+  bool init(unsigned long long dim, int kl, int nsm, std::string* err);
+  // Generates this step's noise for all local workers from mt[kl][313] and
+  // advances the states.  stddev = sigma / sqrt(dim).
+  bool run(uint64_t* mt, double stddev, void* stream, std::string* err);
+  NoiseView view() const { return {slots_, pfx_, cap_, P_}; }
+  int segments() const { return P_; }
+  long long segment_outputs() const { return S_; }
+  uint64_t launches() const { return launches_; }
+
+ private:
+  unsigned long long dim_ = 0;
+  int kl_ = 0, P_ = 1, gens_ = 1, ck_every_ = 16, nck_ = 1;
+  long long S_ = 0, cap_ = 0;
+  uint64_t* ybuf_ = nullptr;       // [kl][kPrefixWords]
+  uint64_t* win_ = nullptr;        // [kl][P][312]
+  uint16_t* jidx_ = nullptr;       // set-bit indexes of c_s, s = 1..P-1
+  int* joff_ = nullptr;            // [P] offsets into jidx (joff[0] unused)
+  double* slots_ = nullptr;        // [kl][P+1][cap]
+  unsigned long long* cnt_ = nullptr;  // [kl][P]
+  unsigned long long* pfx_ = nullptr;  // [kl][P+2]
+  uint64_t* ck_ = nullptr;         // [kl][P][nck][kCkWords]
+  uint64_t* tail_ = nullptr;       // [kl][P][kCkWords] segment end states
+  int* status_ = nullptr;          // [kl] 0 ok, else overflow failure
+  uint64_t launches_ = 0;
+};
+
+// Host-side MT19937-64 jump machinery (exposed for the CPU self-test).
+// Characteristic polynomial phi (degree 19937) as 312 little-endian words.
+const std::vector<uint64_t>& mt_char_poly();
+// c = x^J mod phi.
+std::vector<uint64_t> mt_jump_poly(unsigned long long J);
+// Applies c to the window starting at Y[1] of a sequence whose first 312
+// words are x (generation-aligned state): returns Y[1+J .. 1+J+311].
+std::vector<uint64_t> mt_jump_host(const uint64_t* x312, const std::vector<uint64_t>& c);
+
+}  // namespace dsx

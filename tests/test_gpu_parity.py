@@ -194,3 +194,35 @@ def test_reference_acceptance_on_gpu(criterion):
     out = subprocess.run([ACCEPT, "--only", str(criterion)], capture_output=True, text=True,
                          timeout=900)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("dim,K,advance", [(1, 1, 0), (2, 2, 1), (400001, 3, 0), (250000, 2, 3),
+                                           (1234567, 1, 0)])
+def test_parallel_noise_engine_segments_exact(dim, K, advance):
+    """The jump-ahead engine (many segments for large dims) reproduces the
+    stream exactly, including odd starting cursors (a std::mt19937_64 that
+    was advanced by an odd number of draws before the step)."""
+    from paper_2502_11058_b200 import Lab, LabDesc
+    from paper_2502_11058_b200.lab import sync_mask
+    seed = 77
+    L = 4 if dim >= 4 else 1
+    curv, sizes = O.make_quadratic(dim, L)
+    lab = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, sigma=1.0))
+    rngs = [O.worker_rng(seed, k) for k in range(K)]
+    for k in range(K):
+        for _ in range(advance + k):
+            O.lib().orc_mt_next(O.C.byref(rngs[k]))
+        lab.set_rng(k, np.array(list(rngs[k].x), dtype=np.uint64), int(rngs[k].p))
+    w = np.zeros((K, dim))
+    lab.set_params(w)
+    sets = O.enp(L, 2 if L >= 2 else 1)
+    H = len(sets)
+    for r in range(3):
+        eta = O.learning_rate(r, 1.0, 2.0, H)
+        mask = sync_mask("partial", H, r, L, sets)
+        lab.step(eta, mask)
+        O.plsgd_step(w, rngs, curv, np.ones(dim), 1.0, sizes, eta, mask)
+    assert rel_err(lab.get_params(), w) <= 1e-12
+    for k in range(K):
+        assert lab.rng_text(k) == O.mt_state_text(rngs[k])
+    lab.close()

@@ -104,3 +104,14 @@ def test_device_path_fails_loudly_without_gpu():
     out = subprocess.run([TOOL, "steps", "12", "3", "4", "3", "0.5", "7", "1", "partial", "enp"],
                          capture_output=True, text=True)
     assert out.returncode != 0 and "dsx_lab_create" in out.stderr
+
+
+@pytest.mark.parametrize("jump", [1, 311, 312, 19936, 19937, 100003, 2000000])
+def test_mt_jump_ahead_matches_recurrence(jump):
+    """The GF(2) characteristic-polynomial jump used by the parallel noise
+    engine equals running std::mt19937_64's recurrence (host-only)."""
+    import ctypes as C
+    from paper_2502_11058_b200 import native
+    ok = C.c_int(0)
+    native.call("dsx_mt_jump_selftest", jump, C.byref(ok))
+    assert ok.value == 1
