@@ -140,6 +140,12 @@ dsx_status dsx_lab_event_elapsed(dsx_lab* lab, int from_slot, int to_slot, float
 dsx_status dsx_lab_set_instrument(dsx_lab* lab, int enabled);
 dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out5);
 
+/* Host-only: *pairwise_exact = 1 when splitting workers_total workers into
+ * nranks equal contiguous ranges keeps each range a subtree of the
+ * reference's pairwise summation tree (trainer.cpp:31-38), i.e. when
+ * DSX_SYNC_PAIRWISE reproduces the in-process result bit-for-bit. */
+dsx_status dsx_sync_plan(int workers_total, int nranks, int* pairwise_exact);
+
 /* Host-only self-test of the MT19937-64 jump-ahead used by the parallel
  * noise engine: *ok = 1 when jumping J outputs by polynomial equals running
  * the recurrence (no GPU needed). */

@@ -1366,6 +1366,21 @@ dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out3) {
   return DSX_OK;
 }
 
+// Host-only: can `nranks` equal contiguous worker ranges reproduce the
+// reference's pairwise summation order (each range a subtree)?
+dsx_status dsx_sync_plan(int workers_total, int nranks, int* pairwise_exact) {
+  if (!pairwise_exact || workers_total < 1 || nranks < 1) return fail(DSX_ERR_ARGUMENT, "bad plan args");
+  if (workers_total % nranks) {
+    *pairwise_exact = 0;
+    return DSX_OK;
+  }
+  const int kl = workers_total / nranks;
+  int ok = 1;
+  for (int r = 0; r < nranks; ++r) ok &= is_subtree(workers_total, r * kl, kl) ? 1 : 0;
+  *pairwise_exact = ok;
+  return DSX_OK;
+}
+
 // Host-only check of the MT19937-64 jump-ahead: the window at stream
 // offset 1+J computed by the characteristic-polynomial jump equals the one
 // produced by running the recurrence.  Needs no GPU.

@@ -71,6 +71,7 @@ _SIGS = {
     "dsx_lab_last_step_times": ([C.c_void_p, C.c_void_p], C.c_int),
     "dsx_lab_launch_count": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
     "dsx_mt_jump_selftest": ([C.c_ulonglong, C.POINTER(C.c_int)], C.c_int),
+    "dsx_sync_plan": ([C.c_int, C.c_int, C.POINTER(C.c_int)], C.c_int),
 }
 
 
