@@ -40,9 +40,9 @@ build/parity_tool: tests/native/parity_tool.cpp $(LIB)/libdreamsched.so
 	    -Wl,-rpath,'$$ORIGIN/../$(LIB)' -o $@
 
 acceptance: build/acceptance
-build/acceptance: $(REF)/tests/acceptance/acceptance_main.cpp $(LIB)/libdreamsched.so
+build/acceptance: $(REF)/tests/acceptance/acceptance_main.cpp tests/native/eager_init.cpp $(LIB)/libdreamsched.so
 	@mkdir -p build
-	$(CXX) -std=c++20 -O2 -Iinclude -I$(REF)/tests/support $< -L$(LIB) -ldreamsched -ldsx \
+	$(CXX) -std=c++20 -O2 -Iinclude -I$(REF)/tests/support $< tests/native/eager_init.cpp -L$(LIB) -ldreamsched -ldsx \
 	    -Wl,-rpath,'$$ORIGIN/../$(LIB)' -o $@
 
 clean:

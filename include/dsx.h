@@ -75,6 +75,9 @@ typedef struct dsx_lab_desc {
 
 const char* dsx_last_error(void);
 dsx_status dsx_device_count(int* count);
+/* Creates the CUDA context on DREAMSCHED_DEVICE (default 0) and the noise
+ * engine's host tables; optional (everything is created lazily otherwise). */
+dsx_status dsx_warmup(void);
 
 dsx_status dsx_lab_create(const dsx_lab_desc* desc, dsx_lab** out);
 dsx_status dsx_lab_destroy(dsx_lab* lab);

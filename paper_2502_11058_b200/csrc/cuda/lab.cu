@@ -225,12 +225,30 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   double nsq[KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) nsq[k] = 0.0;
-  // per-worker current segment (monotone along this thread's elements)
-  int seg[KL > 0 ? KL : 1];
+  // Engine noise of coordinate i lives at slot_seg[i - 2*pfx[seg]]: per tile
+  // and worker the tile spans at most two segments (segments hold >= 7.8k
+  // pairs, a tile 1024), so one boundary + two rebased base pointers suffice.
+  __shared__ const double* s_base[KL > 0 ? KL : 1][2];
+  __shared__ unsigned long long s_bound[KL > 0 ? KL : 1];
+  __shared__ int s_simple;
   if constexpr (NM == 2 && KL > 0) {
-    const unsigned long long m0 = (unsigned long long)(t.start + threadIdx.x) >> 1;
-#pragma unroll
-    for (int k = 0; k < KL; ++k) seg[k] = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P, m0);
+    if (threadIdx.x == 0) s_simple = 1;
+    __syncthreads();
+    if (threadIdx.x < KL) {
+      const int k = threadIdx.x;
+      const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
+      const unsigned long long m0 = (unsigned long long)t.start >> 1;
+      const unsigned long long m1 = (unsigned long long)(t.start + t.len - 1) >> 1;
+      const int s0 = seg_search(pf, a.nv.P, m0);
+      const int s1 = s0 < a.nv.P ? s0 + 1 : s0;
+      const double* slot0 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s0) * a.nv.cap;
+      const double* slot1 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s1) * a.nv.cap;
+      s_base[k][0] = slot0 - 2 * (long long)pf[s0];
+      s_base[k][1] = slot1 - 2 * (long long)pf[s1];
+      s_bound[k] = s0 < a.nv.P ? pf[s0 + 1] : ~0ull;
+      if (s1 < a.nv.P && m1 >= pf[s1 + 1]) s_simple = 0;  // spans 3+ segments
+    }
+    __syncthreads();
   }
 
   if constexpr (KL > 0) {
@@ -248,10 +266,13 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
         double xi = 0.0;
         if constexpr (NM == 1) xi = a.noise[k * a.ld + i];
         if constexpr (NM == 2) {
-          const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
-          const unsigned long long m = (unsigned long long)i >> 1;
-          while (m >= pf[seg[k] + 1]) ++seg[k];
-          xi = seg_noise(a.nv, k, seg[k], i);
+          if (s_simple) {
+            xi = s_base[k][((unsigned long long)i >> 1) >= s_bound[k]][i];
+          } else {
+            const int sg = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
+                                      (unsigned long long)i >> 1);
+            xi = seg_noise(a.nv, k, sg, i);
+          }
         }
         const auto g = grad_step(w, lam, opt, xi, a.eta, NOISE, &wn[k]);
         nsq[k] += to_d(g) * to_d(g);
@@ -928,6 +949,15 @@ dsx_status run_noise(dsx_lab* lab, int* mode) {
 extern "C" {
 
 const char* dsx_last_error(void) { return g_last_error.c_str(); }
+
+dsx_status dsx_warmup(void) {
+  const char* env = std::getenv("DREAMSCHED_DEVICE");
+  const int dev = env ? std::atoi(env) : 0;
+  (void)dsx::mt_char_poly();
+  DSX_CUDA(cudaSetDevice(dev));
+  DSX_CUDA(cudaFree(nullptr));
+  return DSX_OK;
+}
 
 dsx_status dsx_device_count(int* count) {
   if (!count) return fail(DSX_ERR_ARGUMENT, "null count");

@@ -26,7 +26,7 @@ namespace {
 constexpr int kDeg = 19937;               // deg phi
 constexpr int kPolyWords = 312;            // ceil(19938 / 64)
 constexpr int kPrefixWords = 65 * kMtN;    // Y[0 .. 20280): >= 1 + 19940 + 311 + 10
-constexpr int kJumpBits = 19940;           // c padded to a multiple of 10
+constexpr int kJumpBits = 19952;           // c padded to a multiple of 16
 constexpr int kCkWords = kMtN + 4;         // x[312], carry flag, carry bits, local count, pad
 constexpr int kThreads = 320;
 
@@ -314,6 +314,22 @@ __device__ __forceinline__ PairEval eval_generation(Smem& sm, int lo, int hi, in
   return e;
 }
 
+// dst = the generation after src (separate buffers, 2 barriers).  Phase A
+// (k < 156) reads only src; phase B (k >= 156) also reads the new dst[k-156]
+// and, for k = 311, dst[0] — exactly _M_gen_rand's in-place order.
+__device__ __forceinline__ void twist_into(const uint64_t* src, uint64_t* dst) {
+  const int tid = threadIdx.x;
+  if (tid < kMtM) dst[tid] = mt_next_word(src[tid], src[tid + 1], src[tid + kMtM]);
+  __syncthreads();
+  if (tid < kMtM) {
+    const int k = kMtM + tid;
+    dst[k] = mt_next_word(src[k], (k + 1 < kMtN) ? src[k + 1] : dst[0], dst[tid]);
+  }
+  __syncthreads();
+}
+
+constexpr int kRound = 4;  // generations per segment-kernel round
+
 // Normalizes the cursor (p == 312 -> twist) and writes Y[0..kPrefixWords).
 __global__ void __launch_bounds__(kThreads)
 mt_prefix_kernel(const uint64_t* mt, uint64_t* ybuf, uint64_t* win, int P, int* pnorm) {
@@ -340,7 +356,15 @@ mt_prefix_kernel(const uint64_t* mt, uint64_t* ybuf, uint64_t* win, int P, int* 
 
 // Segment start windows W_{sS} = sum_i c_s[i] W_{1+i}: one warp per jump,
 // lane l owns window words [10l, 10l+10) with a sliding register window.
-constexpr int kJumpWarps = 8;
+// One warp per jump; lane l (< 29) owns window words [11 l, 11 l + 11): an odd
+// stride, so the 64-bit shared loads of a warp hit distinct banks.  The
+// sliding window lives in a 16-register ring: the word entering the window
+// is loaded 5 iterations before it is first used, hiding the shared-memory
+// latency with only 4 warps per SM (the 162 KB prefix allows one CTA).
+constexpr int kJumpWarps = 4;
+constexpr int kJA = 11;              // accumulator words per lane
+constexpr int kJQ = 16;              // ring size = kJA + prefetch distance
+constexpr int kJLanes = (kMtN + kJA - 1) / kJA;  // 29
 
 __global__ void __launch_bounds__(kJumpWarps * 32)
 mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 + 1]*/, uint64_t* win, int P) {
@@ -354,31 +378,32 @@ mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 
   if (s >= P) return;
   constexpr int kCW = kJumpBits / 32 + 1;
   const uint32_t* c = cbits + (long long)(s - 1) * kCW;
-  const int j0 = 10 * lane;  // lanes 0..31 cover 0..319 (>= 312 ignored)
-  uint64_t acc[10], win_r[10];
+  const int j0 = lane < kJLanes ? kJA * lane : 0;  // idle lanes recompute lane 0
+  const uint64_t* yb = ys + 1 + j0;
+  uint64_t acc[kJA], ring[kJQ];
 #pragma unroll
-  for (int q = 0; q < 10; ++q) {
-    acc[q] = 0;
-    win_r[q] = ys[1 + j0 + q];
-  }
-  uint32_t cw = 0;
-  for (int i0 = 0; i0 < kJumpBits; i0 += 10) {
+  for (int q = 0; q < kJA; ++q) acc[q] = 0;
 #pragma unroll
-    for (int u = 0; u < 10; ++u) {
-      const int i = i0 + u;
-      if ((i & 31) == 0 || u == 0) cw = c[i >> 5];
-      if ((cw >> (i & 31)) & 1u) {
+  for (int q = 0; q < kJQ; ++q) ring[q] = yb[q];
+  // invariant at iteration i (u = i mod kJQ): ring[(u + q) % kJQ] = Y[1 + j0 + i + q]
+  // for q < kJQ; the window is q < kJA.
+  for (int i0 = 0; i0 < kJumpBits; i0 += kJQ) {
+    const uint32_t cw = c[i0 >> 5] >> (i0 & 31);  // kJQ bits of c, i0 % 16 == 0
 #pragma unroll
-        for (int q = 0; q < 10; ++q) acc[q] ^= win_r[(u + q) % 10];
+    for (int u = 0; u < kJQ; ++u) {
+      if ((cw >> u) & 1u) {
+#pragma unroll
+        for (int q = 0; q < kJA; ++q) acc[q] ^= ring[(u + q) % kJQ];
       }
-      // slide: logical slot 0 (= win_r[u]) leaves, Y[1 + (i+1) + j0 + 9] enters
-      win_r[u] = ys[1 + i + 1 + j0 + 9];
+      ring[u] = yb[i0 + u + kJQ];  // enters as q = kJQ-1 at iteration i+1
     }
   }
   uint64_t* out = win + ((long long)w * P + s) * kMtN;
+  if (lane < kJLanes) {
 #pragma unroll
-  for (int q = 0; q < 10; ++q)
-    if (j0 + q < kMtN) out[j0 + q] = acc[q];
+    for (int q = 0; q < kJA; ++q)
+      if (j0 + q < kMtN) out[j0 + q] = acc[q];
+  }
 }
 
 __device__ __forceinline__ void store_ck(uint64_t* ck, const uint64_t* x, int have_half, double half,
@@ -394,38 +419,112 @@ __device__ __forceinline__ void store_ck(uint64_t* ck, const uint64_t* x, int ha
 
 // One CTA per (segment, worker): S outputs from relative position sS + p.
 __global__ void __launch_bounds__(kThreads)
-mt_segment_kernel(const uint64_t* win, const int* pnorm, int P, int gens, int ck_every, int nck,
-                  double stddev, double* slots, long long cap, unsigned long long* cnt,
-                  uint64_t* ck, uint64_t* tail) {
-  __shared__ Smem sm;
-  const int s = blockIdx.x, w = blockIdx.y, tid = threadIdx.x;
-  if (tid < kMtN) sm.x[tid] = win[((long long)w * P + s) * kMtN + tid];
-  const int p = pnorm[w];
+mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
+                  int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
+                  double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
+                  uint64_t* tail) {
+  // kRound generations per round: each round twists kRound arrays into a
+  // ring (2 barriers per twist, separate source/destination), then tempers,
+  // pairs, scans and transforms all of them at once — 2 pair slots per
+  // thread instead of ~0.5, and 3 barriers per round instead of 3 per
+  // generation.
+  constexpr int R = kRound;
+  constexpr int kSlots = (R * kMtN / 2 + kThreads - 1) / kThreads;  // pair slots per thread
+  __shared__ uint64_t ring[R + 1][kMtN];
+  __shared__ double v[R * kMtN + 2];
+  __shared__ int wcnt[kSlots][kThreads / 32];
+  const int s = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int p;
+  if (s == 0) {
+    // segment 0 starts from the worker's live state (no prefix needed)
+    const uint64_t* st = win_state + (long long)w * (kMtN + 1);
+    if (tid < kMtN) ring[R][tid] = st[tid];
+    p = (int)st[kMtN];
+    __syncthreads();
+    if (p >= kMtN) {
+      twist_into(ring[R], ring[0]);
+      p = 0;
+    } else if (tid < kMtN) {
+      ring[0][tid] = ring[R][tid];
+    }
+    if (tid == 0) pnorm_out[w] = p;
+  } else {
+    if (tid < kMtN) ring[0][tid] = win[((long long)w * P + s) * kMtN + tid];
+    p = pnorm_in[w];
+  }
+  __syncthreads();
   const int ngen = gens + (p > 0 ? 1 : 0);
   double* out = slots + ((long long)w * (P + 1) + s) * cap;
   uint64_t* ckw = ck + ((long long)w * P + s) * (long long)nck * kCkWords;
   int have_half = 0;
   double half = 0.0;
   unsigned long long local = 0;
-  __syncthreads();
-  for (int q = 0; q < ngen; ++q) {
-    if (q) block_twist(sm.x);
-    if (q % ck_every == 0) store_ck(ckw + (long long)(q / ck_every) * kCkWords, sm.x, have_half, half, local);
-    const int lo = q == 0 ? p : 0;
-    const int hi = (q == gens) ? p : kMtN;  // only reached when p > 0
-    const PairEval e = eval_generation(sm, lo, hi, have_half, half);
-    if (e.acc) {
-      const unsigned long long m = local + (unsigned long long)e.rank;
-      const double mult = mt_polar_mult(e.r2);
-      out[2 * m] = mt_scale(e.py, mult, stddev);
-      out[2 * m + 1] = mt_scale(e.px, mult, stddev);
+  int cur = 0;  // ring slot holding the first generation of this round
+  for (int q = 0; q < ngen; q += R) {
+    const int rg = min(R, ngen - q);
+    if (q) twist_into(ring[(cur + R) % (R + 1)], ring[cur]);  // after the previous round's last
+    if (q % ck_every == 0) store_ck(ckw + (long long)(q / ck_every) * kCkWords, ring[cur], have_half, half, local);
+    for (int g = 1; g < rg; ++g) twist_into(ring[(cur + g - 1) % (R + 1)], ring[(cur + g) % (R + 1)]);
+    // values of generations q .. q+rg-1 (with their [lo, hi) windows)
+    int nvals = have_half;
+    for (int g = 0; g < rg; ++g) {
+      const int gen = q + g;
+      const int lo = gen == 0 ? p : 0;
+      const int hi = (gen == gens) ? p : kMtN;
+      const uint64_t* x = ring[(cur + g) % (R + 1)];
+      if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(x[tid]));
+      nvals += hi - lo;
     }
-    local += (unsigned long long)e.total;
+    if (tid == 0 && have_half) v[0] = half;
+    __syncthreads();
+    const int npairs = nvals >> 1;
+    bool acc[kSlots];
+    double r2[kSlots];
+    int before[kSlots];
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+      const int a = tid + u * kThreads;
+      acc[u] = false;
+      r2[u] = 0.0;
+      if (a < npairs) acc[u] = mt_polar_accept(v[2 * a], v[2 * a + 1], &r2[u]);
+      const unsigned bal = __ballot_sync(0xffffffffu, acc[u]);
+      if (lane == 0) wcnt[u][warp] = __popc(bal);
+      before[u] = __popc(bal & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+    int total = 0;
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+      int b = total;
+      for (int ww = 0; ww < kThreads / 32; ++ww) {
+        if (ww < warp) b += wcnt[u][ww];
+        total += wcnt[u][ww];
+      }
+      before[u] += b;
+    }
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+      if (!acc[u]) continue;
+      const int a = tid + u * kThreads;
+      const unsigned long long m = local + (unsigned long long)before[u];
+      const double mult = mt_polar_mult(r2[u]);
+      out[2 * m] = mt_scale(v[2 * a + 1], mult, stddev);
+      out[2 * m + 1] = mt_scale(v[2 * a], mult, stddev);
+    }
+    local += (unsigned long long)total;
+    if (nvals & 1) {
+      half = v[nvals - 1];
+      have_half = 1;
+    } else {
+      have_half = 0;
+    }
+    cur = (cur + rg - 1) % (R + 1);  // slot of this round's last generation ...
+    __syncthreads();
+    if (q + R < ngen) cur = (cur + 1) % (R + 1);  // ... next round starts one slot on
   }
   if (tid == 0) cnt[(long long)w * P + s] = local;
-  // end state for an overflow continuation: the last processed array, next
-  // offset = p (or 312 when p == 0: twist first)
-  store_ck(tail + ((long long)w * P + s) * kCkWords, sm.x, have_half, half, local);
+  // end state for an overflow continuation: the last processed array
+  store_ck(tail + ((long long)w * P + s) * kCkWords, ring[cur], have_half, half, local);
 }
 
 // Walks generations from a checkpoint until the target pair; writes the new
@@ -599,7 +698,7 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
       !alloc((void**)&pfx_, 8ull * (P_ + 2) * kl) ||
       !alloc((void**)&ck_, 8ull * kCkWords * nck_ * P_ * kl) ||
       !alloc((void**)&tail_, 8ull * kCkWords * P_ * kl) || !alloc((void**)&status_, 4ull * kl) ||
-      !alloc((void**)&joff_, 4ull * kl))
+      !alloc((void**)&joff_, 8ull * kl))
     return false;
   cudaMemcpy(jidx_, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice);
   cudaMemset(status_, 0, 4ull * kl);
@@ -613,18 +712,20 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
 
 bool NoiseEngine::run(uint64_t* mt, double stddev, void* stream_ptr, std::string* err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
-  int* pnorm = joff_;  // [kl] normalized cursors
-  mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt, ybuf_, win_, P_, pnorm);
-  ++launches_;
+  int* pnorm = joff_;              // [kl] cursor normalized by the prefix kernel
+  int* pnorm2 = joff_ + kl_;       // [kl] the same, written by segment 0
   if (P_ > 1) {
+    mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt, ybuf_, win_, P_, pnorm);
+    ++launches_;
     dim3 grid((P_ - 1 + kJumpWarps - 1) / kJumpWarps, kl_);
     mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(
         ybuf_, reinterpret_cast<const uint32_t*>(jidx_), win_, P_);
     ++launches_;
   }
-  mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(win_, pnorm, P_, gens_, ck_every_, nck_,
-                                                             stddev, slots_, cap_, cnt_, ck_, tail_);
-  mt_finish_kernel<<<kl_, kThreads, 0, stream>>>(mt, pnorm, P_, gens_, ck_every_, nck_, (dim_ + 1) / 2,
+  mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(mt, win_, pnorm, pnorm2, P_, gens_,
+                                                             ck_every_, nck_, stddev, slots_, cap_,
+                                                             cnt_, ck_, tail_);
+  mt_finish_kernel<<<kl_, kThreads, 0, stream>>>(mt, pnorm2, P_, gens_, ck_every_, nck_, (dim_ + 1) / 2,
                                                  stddev, slots_, cap_, cnt_, pfx_, ck_, tail_, status_);
   launches_ += 2;
   const cudaError_t e = cudaGetLastError();

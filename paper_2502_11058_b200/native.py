@@ -45,6 +45,7 @@ _dsx = None
 _SIGS = {
     "dsx_last_error": ([], C.c_char_p),
     "dsx_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "dsx_warmup": ([], C.c_int),
     "dsx_lab_create": ([C.POINTER(LabDescC), C.POINTER(C.c_void_p)], C.c_int),
     "dsx_lab_destroy": ([C.c_void_p], C.c_int),
     "dsx_lab_set_params": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
