@@ -671,6 +671,13 @@ struct dsx_lab {
   bool instrument = false;
   dsx::NoiseEngine* engine = nullptr;  // parallel exact noise (sigma > 0)
   bool use_chain = false;
+  // noise pipelining: the engine runs on nstream one step ahead, into the
+  // buffer set the update is not reading; two rng-state buffers keep the
+  // committed state (visible through get_rng) apart from a prefetched one.
+  cudaStream_t nstream = nullptr;
+  cudaEvent_t ev_noise[2] = {}, ev_upd[2] = {};
+  int mt_commit = 0, cur_set = 0, next_set = 0, pf_set = -1, pf_state = 0;
+  bool pipeline = true;
   bool has_ranges = false, synced_last = false;
   bool overlap = true;
   uint64_t launches = 0;
@@ -738,7 +745,7 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.mask = mask;
   a.average = average;
   a.norm_part = lab->norm_part;
-  if (lab->engine) a.nv = lab->engine->view();
+  if (lab->engine) a.nv = lab->engine->view(lab->cur_set);
   if (nm == 2) {
     lab_update_kernel<T, KL, 2><<<count, kThreads, 0, s>>>(a, lab->prog_local);
   } else if (nm == 1) {
@@ -925,22 +932,71 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int no
   return DSX_OK;
 }
 
-// Generates this step's noise; returns the update kernels' noise mode.
+uint64_t* mt_state(dsx_lab* lab, int idx) { return lab->mt + (long long)idx * lab->kl * (kMtN + 1); }
+
+// Launches the engine on the noise stream: states mt_commit -> other buffer,
+// normals into `set`, after the last update that read `set` finished.
+dsx_status launch_engine(dsx_lab* lab, int set, int* out_state) {
+  std::string err;
+  DSX_CUDA(cudaStreamWaitEvent(lab->nstream, lab->ev_upd[set], 0));
+  const int dst = 1 - lab->mt_commit;
+  const uint64_t before = lab->engine->launches();
+  if (!lab->engine->run(mt_state(lab, lab->mt_commit), mt_state(lab, dst), set, lab->stddev,
+                        lab->nstream, &err))
+    return fail(DSX_ERR_CUDA, err);
+  lab->launches += lab->engine->launches() - before;
+  DSX_CUDA(cudaEventRecord(lab->ev_noise[set], lab->nstream));
+  *out_state = dst;
+  return DSX_OK;
+}
+
+// Drops a speculatively generated next-step noise (the rng state it started
+// from is about to change or be read by the caller).
+dsx_status invalidate_prefetch(dsx_lab* lab) {
+  if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
+  lab->pf_set = -1;
+  return DSX_OK;
+}
+
+// Makes this step's noise available to the compute stream; returns the
+// update kernels' noise mode and selects lab->cur_set.
 dsx_status run_noise(dsx_lab* lab, int* mode) {
   *mode = 0;
   if (lab->sigma <= 0.0) return DSX_OK;
   if (lab->use_chain) {  // DSX_NOISE_CHAIN=1: the single-chain reference engine
-    mt_noise_chain_kernel<<<lab->kl, kMtThreads, 0, lab->stream>>>(lab->mt, lab->noise, lab->ld,
-                                                                   lab->dim, lab->stddev);
+    mt_noise_chain_kernel<<<lab->kl, kMtThreads, 0, lab->stream>>>(mt_state(lab, lab->mt_commit),
+                                                                   lab->noise, lab->ld, lab->dim,
+                                                                   lab->stddev);
     ++lab->launches;
     *mode = 1;
     return DSX_OK;
   }
-  std::string err;
-  const uint64_t before = lab->engine->launches();
-  if (!lab->engine->run(lab->mt, lab->stddev, lab->stream, &err)) return fail(DSX_ERR_CUDA, err);
-  lab->launches += lab->engine->launches() - before;
+  if (lab->pf_set >= 0) {  // generated during the previous step
+    lab->cur_set = lab->pf_set;
+    lab->mt_commit = lab->pf_state;
+    lab->pf_set = -1;
+  } else {
+    lab->cur_set = lab->next_set;
+    int st = 0;
+    DSX_TRY(launch_engine(lab, lab->cur_set, &st));
+    lab->mt_commit = st;
+  }
+  lab->next_set = 1 - lab->cur_set;
+  DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_noise[lab->cur_set], 0));
   *mode = 2;
+  return DSX_OK;
+}
+
+// After the update of this step was enqueued: generate the next step's noise
+// on the noise stream so it overlaps this step's (HBM-bound) update.
+dsx_status after_update(dsx_lab* lab, int mode) {
+  if (mode != 2) return DSX_OK;
+  DSX_CUDA(cudaEventRecord(lab->ev_upd[lab->cur_set], lab->stream));
+  if (!lab->pipeline) return DSX_OK;
+  int st = 0;
+  DSX_TRY(launch_engine(lab, lab->next_set, &st));
+  lab->pf_set = lab->next_set;
+  lab->pf_state = st;
   return DSX_OK;
 }
 
@@ -1025,7 +1081,7 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
     lab->q.curv = lab->curv;
     lab->q.opt = lab->opt;
   }
-  if (cudaMalloc(&lab->mt, 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
+  if (cudaMalloc(&lab->mt, 2 * 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
     return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(mt) failed"));
   if (lab->sigma > 0.0) {
     const char* chain = std::getenv("DSX_NOISE_CHAIN");
@@ -1063,6 +1119,16 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
   for (auto& ev : lab->iev) cudaEventCreate(&ev);
   cudaEventCreateWithFlags(&lab->ev_split, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&lab->ev_synced, cudaEventDisableTiming);
+  if (lab->engine) {
+    if (cudaStreamCreateWithPriority(&lab->nstream, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
+      return cleanup(fail(DSX_ERR_CUDA, "noise stream creation failed"));
+    for (int b = 0; b < 2; ++b) {
+      cudaEventCreateWithFlags(&lab->ev_noise[b], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&lab->ev_upd[b], cudaEventDisableTiming);
+    }
+    const char* pl = std::getenv("DSX_NOISE_PIPELINE");
+    lab->pipeline = !(pl && pl[0] == '0');
+  }
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cleanup(fail(DSX_ERR_CUDA, std::string("lab init: ") + cudaGetErrorString(e)));
   // default rng: worker_rng(0, k)
@@ -1076,6 +1142,7 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   cudaSetDevice(lab->device);
   if (lab->stream) cudaStreamSynchronize(lab->stream);
   if (lab->side) cudaStreamSynchronize(lab->side);
+  if (lab->nstream) cudaStreamSynchronize(lab->nstream);
   if (lab->comm) ncclCommDestroy(lab->comm);
   delete lab->engine;
   for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt,
@@ -1090,6 +1157,11 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   if (lab->ev_synced) cudaEventDestroy(lab->ev_synced);
   if (lab->stream) cudaStreamDestroy(lab->stream);
   if (lab->side) cudaStreamDestroy(lab->side);
+  if (lab->nstream) cudaStreamDestroy(lab->nstream);
+  for (int b = 0; b < 2; ++b) {
+    if (lab->ev_noise[b]) cudaEventDestroy(lab->ev_noise[b]);
+    if (lab->ev_upd[b]) cudaEventDestroy(lab->ev_upd[b]);
+  }
   delete lab;
   return DSX_OK;
 }
@@ -1166,7 +1238,9 @@ dsx_status dsx_lab_set_rng(dsx_lab* lab, int local, const uint64_t* x312, uint64
   std::memcpy(buf, x312, 8 * kMtN);
   buf[kMtN] = p;
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
-  DSX_CUDA(cudaMemcpy(lab->mt + (long long)local * (kMtN + 1), buf, sizeof buf, cudaMemcpyHostToDevice));
+  DSX_TRY(invalidate_prefetch(lab));
+  DSX_CUDA(cudaMemcpy(mt_state(lab, lab->mt_commit) + (long long)local * (kMtN + 1), buf, sizeof buf,
+                      cudaMemcpyHostToDevice));
   return DSX_OK;
 }
 
@@ -1175,7 +1249,10 @@ dsx_status dsx_lab_get_rng(dsx_lab* lab, int local, uint64_t* x312, uint64_t* p)
   if (!x312 || !p) return fail(DSX_ERR_ARGUMENT, "null rng out");
   uint64_t buf[kMtN + 1];
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
-  DSX_CUDA(cudaMemcpy(buf, lab->mt + (long long)local * (kMtN + 1), sizeof buf, cudaMemcpyDeviceToHost));
+  if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
+  // the committed state (after the last step's noise), not a prefetched one
+  DSX_CUDA(cudaMemcpy(buf, mt_state(lab, lab->mt_commit) + (long long)local * (kMtN + 1), sizeof buf,
+                      cudaMemcpyDeviceToHost));
   std::memcpy(x312, buf, 8 * kMtN);
   *p = buf[kMtN];
   return DSX_OK;
@@ -1207,8 +1284,9 @@ dsx_status dsx_lab_step(dsx_lab* lab, double eta, const unsigned char* mask) {
   int noise = 0;
   DSX_TRY(run_noise(lab, &noise));
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[5], lab->stream));
-  return lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, noise)
-                               : step_impl<float>(lab, eta, mask, noise);
+  DSX_TRY(lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, noise)
+                                : step_impl<float>(lab, eta, mask, noise));
+  return after_update(lab, noise);
 }
 
 dsx_status dsx_lab_step_with_noise(dsx_lab* lab, double eta, const unsigned char* mask,
@@ -1248,11 +1326,12 @@ dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
   DSX_TRY(check_row(lab, local));
   if (!g_out) return fail(DSX_ERR_ARGUMENT, "null gradient out");
   int nm = 0;
+  DSX_TRY(invalidate_prefetch(lab));
   DSX_TRY(run_noise(lab, &nm));  // advances every local row's stream
   double* g = nullptr;
   DSX_CUDA(cudaMallocAsync((void**)&g, 8 * lab->dim, lab->stream));
   const double* xi = nm == 1 ? lab->noise + (long long)local * lab->ld : nullptr;
-  const NoiseView nv = lab->engine ? lab->engine->view() : NoiseView{};
+  const NoiseView nv = lab->engine ? lab->engine->view(lab->cur_set) : NoiseView{};
   if (lab->dtype == DSX_F64) {
     gradient_kernel<double><<<lab->nsm * 4, 256, 0, lab->stream>>>(
         static_cast<const double*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, nm, xi, nv,

@@ -361,10 +361,19 @@ mt_prefix_kernel(const uint64_t* mt, uint64_t* ybuf, uint64_t* win, int P, int* 
 // sliding window lives in a 16-register ring: the word entering the window
 // is loaded 5 iterations before it is first used, hiding the shared-memory
 // latency with only 4 warps per SM (the 162 KB prefix allows one CTA).
-constexpr int kJumpWarps = 4;
-constexpr int kJA = 11;              // accumulator words per lane
-constexpr int kJQ = 16;              // ring size = kJA + prefetch distance
-constexpr int kJLanes = (kMtN + kJA - 1) / kJA;  // 29
+// A jump is split over kWarpsPerJump warps (a quarter of the 312 window
+// words each); lane l (< 26) of a quarter owns 3 consecutive words — an odd
+// stride, so a warp's 64-bit shared loads are bank-conflict free.  The
+// sliding window lives in an 8-register ring: the word entering the window
+// is loaded 5 iterations before it is first used.  kJumpsPerCta jumps of the
+// same worker share the CTA's 162 KB copy of the stream prefix.
+constexpr int kWarpsPerJump = 4;
+constexpr int kJumpsPerCta = 2;
+constexpr int kJumpWarps = kWarpsPerJump * kJumpsPerCta;
+constexpr int kJA = 3;               // accumulator words per lane
+constexpr int kJQ = 8;               // ring size = kJA + prefetch distance
+constexpr int kJWords = kMtN / kWarpsPerJump;    // 78 words per warp
+constexpr int kJLanes = kJWords / kJA;           // 26
 
 __global__ void __launch_bounds__(kJumpWarps * 32)
 mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 + 1]*/, uint64_t* win, int P) {
@@ -374,11 +383,11 @@ mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 
   for (int i = threadIdx.x; i < kPrefixWords; i += blockDim.x) ys[i] = y[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = 1 + blockIdx.x * kJumpWarps + warp;
+  const int s = 1 + blockIdx.x * kJumpsPerCta + warp / kWarpsPerJump;
   if (s >= P) return;
   constexpr int kCW = kJumpBits / 32 + 1;
   const uint32_t* c = cbits + (long long)(s - 1) * kCW;
-  const int j0 = lane < kJLanes ? kJA * lane : 0;  // idle lanes recompute lane 0
+  const int j0 = (warp % kWarpsPerJump) * kJWords + (lane < kJLanes ? kJA * lane : 0);
   const uint64_t* yb = ys + 1 + j0;
   uint64_t acc[kJA], ring[kJQ];
 #pragma unroll
@@ -388,7 +397,7 @@ mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 
   // invariant at iteration i (u = i mod kJQ): ring[(u + q) % kJQ] = Y[1 + j0 + i + q]
   // for q < kJQ; the window is q < kJA.
   for (int i0 = 0; i0 < kJumpBits; i0 += kJQ) {
-    const uint32_t cw = c[i0 >> 5] >> (i0 & 31);  // kJQ bits of c, i0 % 16 == 0
+    const uint32_t cw = c[i0 >> 5] >> (i0 & 31);  // kJQ bits of c, i0 % kJQ == 0
 #pragma unroll
     for (int u = 0; u < kJQ; ++u) {
       if ((cw >> u) & 1u) {
@@ -433,6 +442,8 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
   __shared__ uint64_t ring[R + 1][kMtN];
   __shared__ double v[R * kMtN + 2];
   __shared__ int wcnt[kSlots][kThreads / 32];
+  __shared__ int woff[kSlots][kThreads / 32];
+  __shared__ int woff_total;
   const int s = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int p;
   if (s == 0) {
@@ -492,16 +503,25 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
       before[u] = __popc(bal & ((1u << lane) - 1u));
     }
     __syncthreads();
-    int total = 0;
+    // exclusive scan of the kSlots*10 warp counts (slot-major = pair order)
+    // by warp 0; everyone then reads one offset per slot
+    constexpr int kCounts = kSlots * (kThreads / 32);
+    static_assert(kCounts <= 32, "scan fits one warp");
+    if (warp == 0) {
+      const int c = lane < kCounts ? (&wcnt[0][0])[lane] : 0;
+      int incl = c;
 #pragma unroll
-    for (int u = 0; u < kSlots; ++u) {
-      int b = total;
-      for (int ww = 0; ww < kThreads / 32; ++ww) {
-        if (ww < warp) b += wcnt[u][ww];
-        total += wcnt[u][ww];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
-      before[u] += b;
+      if (lane < kCounts) (&woff[0][0])[lane] = incl - c;
+      if (lane == 31) woff_total = incl;
     }
+    __syncthreads();
+    const int total = woff_total;
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) before[u] += woff[u][warp];
 #pragma unroll
     for (int u = 0; u < kSlots; ++u) {
       if (!acc[u]) continue;
@@ -656,8 +676,11 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
   const double attempts = M / pa + 8.0 * std::sqrt(M * (1.0 - pa)) / pa + 1024.0;
   const double E = 2.0 * attempts;
   const double min_seg = 312.0 * 64.0;
+  // ~2 jumps per SM (one CTA of kJumpsPerCta jumps per SM, a single wave)
+  // and >= 2 segment CTAs per SM; segments no shorter than 64 generations.
   int P = (int)std::ceil(E / min_seg);
-  P = std::max(1, std::min(P, (int)std::ceil(4.0 * nsm / kl)));
+  const int p_cap = std::max(1, (nsm / kl) * kJumpsPerCta + 1);
+  P = std::max(1, std::min(P, p_cap));
   long long gens = (long long)std::ceil(E / P / 312.0);
   if (gens < 1) gens = 1;
   S_ = gens * 312;
@@ -694,14 +717,14 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
   };
   if (!alloc((void**)&ybuf_, 8ull * kPrefixWords * kl) || !alloc((void**)&win_, 8ull * kMtN * P_ * kl) ||
       !alloc((void**)&jidx_, bits.size() * 4) ||
-      !alloc((void**)&slots_, 8ull * cap_ * (P_ + 1) * kl) || !alloc((void**)&cnt_, 8ull * P_ * kl) ||
-      !alloc((void**)&pfx_, 8ull * (P_ + 2) * kl) ||
+      !alloc((void**)&slots_, 2 * 8ull * cap_ * (P_ + 1) * kl) ||
+      !alloc((void**)&cnt_, 2 * 8ull * P_ * kl) || !alloc((void**)&pfx_, 2 * 8ull * (P_ + 2) * kl) ||
       !alloc((void**)&ck_, 8ull * kCkWords * nck_ * P_ * kl) ||
-      !alloc((void**)&tail_, 8ull * kCkWords * P_ * kl) || !alloc((void**)&status_, 4ull * kl) ||
+      !alloc((void**)&tail_, 8ull * kCkWords * P_ * kl) || !alloc((void**)&status_, 2 * 4ull * kl) ||
       !alloc((void**)&joff_, 8ull * kl))
     return false;
   cudaMemcpy(jidx_, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemset(status_, 0, 4ull * kl);
+  cudaMemset(status_, 0, 2 * 4ull * kl);
   if (cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            8 * kPrefixWords) != cudaSuccess) {
     *err = "noise engine: cannot opt in to 162 KB shared memory";
@@ -710,23 +733,28 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
   return true;
 }
 
-bool NoiseEngine::run(uint64_t* mt, double stddev, void* stream_ptr, std::string* err) {
+bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, double stddev,
+                      void* stream_ptr, std::string* err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   int* pnorm = joff_;              // [kl] cursor normalized by the prefix kernel
   int* pnorm2 = joff_ + kl_;       // [kl] the same, written by segment 0
+  double* slots = slots_ + (long long)set * (P_ + 1) * cap_ * kl_;
+  unsigned long long* cnt = cnt_ + (long long)set * P_ * kl_;
+  unsigned long long* pfx = pfx_ + (long long)set * (P_ + 2) * kl_;
+  int* status = status_ + set * kl_;
   if (P_ > 1) {
-    mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt, ybuf_, win_, P_, pnorm);
+    mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt_src, ybuf_, win_, P_, pnorm);
     ++launches_;
-    dim3 grid((P_ - 1 + kJumpWarps - 1) / kJumpWarps, kl_);
+    dim3 grid((P_ - 1 + kJumpsPerCta - 1) / kJumpsPerCta, kl_);
     mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(
         ybuf_, reinterpret_cast<const uint32_t*>(jidx_), win_, P_);
     ++launches_;
   }
-  mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(mt, win_, pnorm, pnorm2, P_, gens_,
-                                                             ck_every_, nck_, stddev, slots_, cap_,
-                                                             cnt_, ck_, tail_);
-  mt_finish_kernel<<<kl_, kThreads, 0, stream>>>(mt, pnorm2, P_, gens_, ck_every_, nck_, (dim_ + 1) / 2,
-                                                 stddev, slots_, cap_, cnt_, pfx_, ck_, tail_, status_);
+  mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
+                                                             ck_every_, nck_, stddev, slots, cap_,
+                                                             cnt, ck_, tail_);
+  mt_finish_kernel<<<kl_, kThreads, 0, stream>>>(mt_dst, pnorm2, P_, gens_, ck_every_, nck_, (dim_ + 1) / 2,
+                                                 stddev, slots, cap_, cnt, pfx, ck_, tail_, status);
   launches_ += 2;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

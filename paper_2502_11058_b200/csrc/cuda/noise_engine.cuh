@@ -37,10 +37,16 @@ class NoiseEngine {
   NoiseEngine() = default;
   ~NoiseEngine();
   bool init(unsigned long long dim, int kl, int nsm, std::string* err);
-  // Generates this step's noise for all local workers from mt[kl][313] and
-  // advances the states.  stddev = sigma / sqrt(dim).
-  bool run(uint64_t* mt, double stddev, void* stream, std::string* err);
-  NoiseView view() const { return {slots_, pfx_, cap_, P_}; }
+  // Generates one step's noise for all local workers from the states
+  // mt_src[kl][313] into buffer set `set` (0/1, double-buffered so the next
+  // step's noise can be produced while the current update reads the other
+  // set) and writes the advanced states to mt_dst.  stddev = sigma/sqrt(dim).
+  bool run(const uint64_t* mt_src, uint64_t* mt_dst, int set, double stddev, void* stream,
+           std::string* err);
+  NoiseView view(int set) const {
+    return {slots_ + (long long)set * (P_ + 1) * cap_ * kl_,
+            pfx_ + (long long)set * (P_ + 2) * kl_, cap_, P_};
+  }
   int segments() const { return P_; }
   long long segment_outputs() const { return S_; }
   uint64_t launches() const { return launches_; }
