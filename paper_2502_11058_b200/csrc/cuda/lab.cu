@@ -195,6 +195,17 @@ __device__ __forceinline__ float grad_step(float w, double lam, double opt, doub
 // fused local step (+ in-place averaging of masked blocks on a single rank)
 // KL > 0: compile-time local worker count; KL == 0: runtime count via prog.
 // ---------------------------------------------------------------------------
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+
 // Segmented engine lookup: normal i of worker k lives in segment s with
 // pfx[s] <= i/2 < pfx[s+1], at slot offset 2*(i/2 - pfx[s]) + (i&1).
 __device__ __forceinline__ int seg_search(const unsigned long long* pf, int P, unsigned long long m) {
@@ -252,38 +263,86 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   }
 
   if constexpr (KL > 0) {
-#pragma unroll 2
-    for (int j = 0; j < kItems; ++j) {
-      const int off = j * kThreads + threadIdx.x;
-      if (off >= t.len) break;
-      const long long i = t.start + off;
+    // Coordinate pairs (i, i+1), i even: 16-byte (fp64) / 8-byte (fp32)
+    // vector loads/stores of every row and of the engine noise (its
+    // segments start at even coordinates, so a pair never straddles one).
+    // An odd tile start / end is handled as a scalar head / tail.
+    using V2 = typename Vec2<T>::type;
+    const long long first = t.start + (t.start & 1);
+    const long long end = t.start + t.len;
+    const int npairs = (int)((end - first) >> 1);
+    auto noise_at = [&](int k, long long i) -> double {
+      if constexpr (NM == 1) return a.noise[k * a.ld + i];
+      if constexpr (NM == 2) {
+        if (s_simple) return s_base[k][((unsigned long long)i >> 1) >= s_bound[k]][i];
+        const int sg = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
+                                  (unsigned long long)i >> 1);
+        return seg_noise(a.nv, k, sg, i);
+      }
+      return 0.0;
+    };
+    auto scalar = [&](long long i) {
       double lam, opt;
       quad_coeffs(a.q, i, &lam, &opt);
       T wn[KL];
 #pragma unroll
       for (int k = 0; k < KL; ++k) {
-        const T w = a.w[k * a.ld + i];
-        double xi = 0.0;
-        if constexpr (NM == 1) xi = a.noise[k * a.ld + i];
-        if constexpr (NM == 2) {
-          if (s_simple) {
-            xi = s_base[k][((unsigned long long)i >> 1) >= s_bound[k]][i];
-          } else {
-            const int sg = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
-                                      (unsigned long long)i >> 1);
-            xi = seg_noise(a.nv, k, sg, i);
-          }
-        }
-        const auto g = grad_step(w, lam, opt, xi, a.eta, NOISE, &wn[k]);
+        const auto g = grad_step(a.w[k * a.ld + i], lam, opt, noise_at(k, i), a.eta, NOISE, &wn[k]);
         nsq[k] += to_d(g) * to_d(g);
       }
-      if (avg) {
-        const T m = psum<0, KL, T>(wn) / (T)a.k_total;
+      const T m = avg ? psum<0, KL, T>(wn) / (T)a.k_total : T(0);
 #pragma unroll
-        for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = m;
+      for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = avg ? m : wn[k];
+    };
+    if (threadIdx.x == 0 && first != t.start) scalar(t.start);
+    if (threadIdx.x == 1 && first + 2 * (long long)npairs < end) scalar(end - 1);
+#pragma unroll 2
+    for (int j = 0; j < kItems / 2; ++j) {
+      const int pr = j * kThreads + threadIdx.x;
+      if (pr >= npairs) break;
+      const long long i = first + 2 * (long long)pr;
+      double lam0, opt0, lam1, opt1;
+      quad_coeffs(a.q, i, &lam0, &opt0);
+      quad_coeffs(a.q, i + 1, &lam1, &opt1);
+      T w0[KL], w1[KL];
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+        const V2 w = *reinterpret_cast<const V2*>(a.w + k * a.ld + i);
+        double x0 = 0.0, x1 = 0.0;
+        if constexpr (NM == 1) {
+          const double2 xv = *reinterpret_cast<const double2*>(a.noise + k * a.ld + i);
+          x0 = xv.x;
+          x1 = xv.y;
+        }
+        if constexpr (NM == 2) {
+          if (s_simple) {
+            const double2 xv = *reinterpret_cast<const double2*>(
+                s_base[k][((unsigned long long)i >> 1) >= s_bound[k]] + i);
+            x0 = xv.x;
+            x1 = xv.y;
+          } else {
+            x0 = noise_at(k, i);
+            x1 = noise_at(k, i + 1);
+          }
+        }
+        const auto g0 = grad_step(w.x, lam0, opt0, x0, a.eta, NOISE, &w0[k]);
+        const auto g1 = grad_step(w.y, lam1, opt1, x1, a.eta, NOISE, &w1[k]);
+        nsq[k] += to_d(g0) * to_d(g0) + to_d(g1) * to_d(g1);
+      }
+      if (avg) {
+        V2 m;
+        m.x = psum<0, KL, T>(w0) / (T)a.k_total;
+        m.y = psum<0, KL, T>(w1) / (T)a.k_total;
+#pragma unroll
+        for (int k = 0; k < KL; ++k) *reinterpret_cast<V2*>(a.w + k * a.ld + i) = m;
       } else {
 #pragma unroll
-        for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = wn[k];
+        for (int k = 0; k < KL; ++k) {
+          V2 o;
+          o.x = w0[k];
+          o.y = w1[k];
+          *reinterpret_cast<V2*>(a.w + k * a.ld + i) = o;
+        }
       }
     }
   } else {
