@@ -90,6 +90,13 @@ dsx_status dsx_lab_fill_params(dsx_lab* lab, double value);
 dsx_status dsx_lab_set_all_params(dsx_lab* lab, const double* w);
 dsx_status dsx_lab_get_all_params(dsx_lab* lab, double* w);
 
+/* Every local worker's parameters w[workers_local][dim] and/or rng states
+ * rng[workers_local][313] (x[312] then the cursor) in one transfer each —
+ * plsgd_step's host WorkerState round trip.  Either pointer may be NULL.
+ * Both calls return with the copies complete. */
+dsx_status dsx_lab_set_state(dsx_lab* lab, const double* w, const uint64_t* rng);
+dsx_status dsx_lab_get_state(dsx_lab* lab, double* w, uint64_t* rng);
+
 /* std::mt19937_64 state: 312 words and the cursor p (libstdc++ _M_x/_M_p). */
 dsx_status dsx_lab_set_rng(dsx_lab* lab, int local, const uint64_t* x312, uint64_t p);
 dsx_status dsx_lab_get_rng(dsx_lab* lab, int local, uint64_t* x312, uint64_t* p);
@@ -129,6 +136,12 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
  * averaging of the synced blocks starts on a high-priority side stream as soon
  * as the first launch is done, overlapping the rest of the local step. */
 dsx_status dsx_lab_set_overlap(dsx_lab* lab, int enabled);
+
+/* Noise pipelining (default on): the exact noise engine generates step r+1's
+ * noise on its own high-priority stream while step r's update runs; the rng
+ * state visible through dsx_lab_get_rng stays the committed one.  Disabling
+ * serializes noise and update (used to time each alone). */
+dsx_status dsx_lab_set_pipeline(dsx_lab* lab, int enabled);
 
 /* Timing on the lab's compute stream: CUDA events in slots 0..31. */
 dsx_status dsx_lab_event_record(dsx_lab* lab, int slot);

@@ -1269,6 +1269,48 @@ dsx_status dsx_lab_set_all_params(dsx_lab* lab, const double* w) {
   return DSX_OK;
 }
 
+dsx_status dsx_lab_set_state(dsx_lab* lab, const double* w, const uint64_t* rng) {
+  DSX_TRY(check_lab(lab));
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  if (rng) DSX_TRY(invalidate_prefetch(lab));
+  if (w) {
+    if (lab->dtype == DSX_F64) {
+      DSX_CUDA(cudaMemcpy2DAsync(lab->w, 8 * lab->ld, w, 8 * lab->dim, 8 * lab->dim, lab->kl,
+                                 cudaMemcpyHostToDevice, lab->stream));
+    } else {
+      for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, w + (long long)k * lab->dim));
+    }
+  }
+  if (rng) {
+    for (int k = 0; k < lab->kl; ++k)
+      if (rng[(long long)k * (kMtN + 1) + kMtN] > kMtN) return fail(DSX_ERR_ARGUMENT, "bad rng cursor");
+    DSX_CUDA(cudaMemcpyAsync(mt_state(lab, lab->mt_commit), rng, 8ull * (kMtN + 1) * lab->kl,
+                             cudaMemcpyHostToDevice, lab->stream));
+  }
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_get_state(dsx_lab* lab, double* w, uint64_t* rng) {
+  DSX_TRY(check_lab(lab));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
+  if (w) {
+    if (lab->dtype == DSX_F64) {
+      DSX_CUDA(cudaMemcpy2DAsync(w, 8 * lab->dim, lab->w, 8 * lab->ld, 8 * lab->dim, lab->kl,
+                                 cudaMemcpyDeviceToHost, lab->stream));
+    } else {
+      for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, w + (long long)k * lab->dim));
+    }
+  }
+  if (rng) {
+    DSX_CUDA(cudaMemcpyAsync(rng, mt_state(lab, lab->mt_commit), 8ull * (kMtN + 1) * lab->kl,
+                             cudaMemcpyDeviceToHost, lab->stream));
+  }
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  return DSX_OK;
+}
+
 dsx_status dsx_lab_get_all_params(dsx_lab* lab, double* w) {
   DSX_TRY(check_lab(lab));
   if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
@@ -1480,6 +1522,13 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   lab->staging_elems = lab->dim;
   if (lab->kl > 1) DSX_CUDA(cudaMalloc(&lab->staging, es * lab->dim));
   DSX_CUDA(cudaMalloc(&lab->recv, es * (lab->dim / nranks + 1) * nranks));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_pipeline(dsx_lab* lab, int enabled) {
+  DSX_TRY(check_lab(lab));
+  if (!enabled) DSX_TRY(invalidate_prefetch(lab));
+  lab->pipeline = enabled != 0;
   return DSX_OK;
 }
 

@@ -145,6 +145,9 @@ class Lab:
         buf = C.create_string_buffer(uid, 128)
         N.call("dsx_lab_comm_init", self.h, buf, nranks, rank, algo)
 
+    def set_pipeline(self, on: bool) -> None:
+        N.call("dsx_lab_set_pipeline", self.h, int(on))
+
     def set_overlap(self, on: bool) -> None:
         N.call("dsx_lab_set_overlap", self.h, int(on))
 

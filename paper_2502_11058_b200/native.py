@@ -53,6 +53,8 @@ _SIGS = {
     "dsx_lab_fill_params": ([C.c_void_p, C.c_double], C.c_int),
     "dsx_lab_set_all_params": ([C.c_void_p, C.c_void_p], C.c_int),
     "dsx_lab_get_all_params": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_lab_set_state": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_lab_get_state": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "dsx_lab_set_rng": ([C.c_void_p, C.c_int, C.c_void_p, C.c_uint64], C.c_int),
     "dsx_lab_get_rng": ([C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
     "dsx_lab_seed_rng": ([C.c_void_p, C.c_uint64], C.c_int),
@@ -66,6 +68,7 @@ _SIGS = {
     "dsx_nccl_unique_id": ([C.c_void_p], C.c_int),
     "dsx_lab_comm_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
     "dsx_lab_set_overlap": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_lab_set_pipeline": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_lab_event_record": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_lab_event_elapsed": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "dsx_lab_set_instrument": ([C.c_void_p, C.c_int], C.c_int),

@@ -1,0 +1,88 @@
+"""Multi-GPU parity script (run under torchrun, one rank per GPU).
+
+K workers are split into equal contiguous ranges over the ranks; every step
+averages the scheduled layers across ranks over NCCL (dsx_lab_comm_init).
+Rank 0 gathers all worker parameters and rng states and compares them with
+the C oracle's in-process K-worker run (trainer.cpp semantics): bit-exact
+for DSX_SYNC_PAIRWISE.  Exit code 0 = pass.  Used by
+tests/test_gpu_multigpu.py; also runnable by hand:
+
+  torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/multigpu_parity.py
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch.distributed as dist
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+from oracle import pyoracle as O  # noqa: E402
+from paper_2502_11058_b200 import native as N  # noqa: E402
+from paper_2502_11058_b200.lab import Lab, LabDesc, nccl_unique_id, sync_mask  # noqa: E402
+
+
+def run(algo, overlap, dim=200003, L=12, K=8, H=4, sigma=1.0, seed=5, steps=7):
+    world, rank = dist.get_world_size(), dist.get_rank()
+    kl = K // world
+    curv, sizes = O.make_quadratic(dim, L)
+    lab = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, workers_local=kl,
+                      worker_begin=rank * kl, sigma=sigma, device=int(os.environ.get("LOCAL_RANK", 0))))
+    uid = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    lab.comm_init(uid[0], world, rank, algo)
+    lab.set_overlap(overlap)
+    lab.seed(seed)
+    lab.fill(0.0)
+    sets = O.enp(L, H)
+    for r in range(steps):
+        lab.step(O.learning_rate(r, 1.0, 2.0, H), sync_mask("partial", H, r, L, sets))
+    w = lab.get_params()
+    rngs = [lab.rng_text(k) for k in range(kl)]
+    lab.close()
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (w, rngs))
+    if rank != 0:
+        return None
+    W = np.concatenate([g[0] for g in gathered])
+    R = [t for g in gathered for t in g[1]]
+    ref = np.zeros((K, dim))
+    orngs = [O.worker_rng(seed, k) for k in range(K)]
+    for r in range(steps):
+        eta = O.learning_rate(r, 1.0, 2.0, H)
+        O.plsgd_step(ref, orngs, curv, np.ones(dim), sigma, sizes, eta,
+                     O.sync_mask("partial", H, r, L, sets))
+    err = float(np.max(np.abs(W - ref) / np.maximum(np.abs(ref), 1e-300)))
+    rng_ok = all(R[k] == O.mt_state_text(orngs[k]) for k in range(K))
+    return {"algo": algo, "overlap": overlap, "max_rel_err": err, "bit_exact": bool(np.array_equal(W, ref)),
+            "rng_exact": rng_ok}
+
+
+def main():
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo")
+    results = []
+    for algo, overlap in [(N.DSX_SYNC_PAIRWISE, True), (N.DSX_SYNC_PAIRWISE, False),
+                          (N.DSX_SYNC_NCCL_AVG, True)]:
+        res = run(algo, overlap)
+        if res is not None:
+            results.append(res)
+    ok = True
+    if dist.get_rank() == 0:
+        world = dist.get_world_size()
+        for res in results:
+            exact_required = res["algo"] == N.DSX_SYNC_PAIRWISE or world <= 2
+            res["pass"] = res["rng_exact"] and (res["bit_exact"] if exact_required
+                                                else res["max_rel_err"] <= 1e-12)
+            ok &= res["pass"]
+        print(json.dumps({"world": world, "results": results, "pass": ok}), flush=True)
+    okt = [ok]
+    dist.broadcast_object_list(okt, src=0)
+    dist.destroy_process_group()
+    sys.exit(0 if okt[0] else 1)
+
+
+if __name__ == "__main__":
+    main()
