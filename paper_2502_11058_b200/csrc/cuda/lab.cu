@@ -75,6 +75,7 @@ constexpr int kThreads = 256;
 constexpr int kItems = kTile / kThreads;
 constexpr int kMaxMaskWords = 128;  // 4096 layers
 constexpr int kMaxProg = 64;        // generic pairwise program (K <= 64)
+constexpr int kMaxChunks = 8;
 
 struct Tile {
   long long start;
@@ -121,6 +122,7 @@ struct UpdateArgs {
   MaskBits mask;
   bool average;       // average masked blocks in-kernel (single rank)
   double* norm_part;  // [kl][ntiles]
+  T* partial_out;     // multi-rank: subtree sums of synced tiles (else null)
 };
 
 // lambda_i and w*_i.  The analytic form is make_quadratic's
@@ -233,6 +235,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   const Tile t = a.tiles[tile_id];
   const int kl = KL > 0 ? KL : a.kl;
   const bool avg = a.average && mask_has(a.mask, t.block);
+  const bool part = KL > 1 && a.partial_out != nullptr && mask_has(a.mask, t.block);
   double nsq[KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) nsq[k] = 0.0;
@@ -290,6 +293,10 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
         const auto g = grad_step(a.w[k * a.ld + i], lam, opt, noise_at(k, i), a.eta, NOISE, &wn[k]);
         nsq[k] += to_d(g) * to_d(g);
       }
+      if (part) {
+        a.partial_out[i] = psum<0, KL, T>(wn);
+        return;
+      }
       const T m = avg ? psum<0, KL, T>(wn) / (T)a.k_total : T(0);
 #pragma unroll
       for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = avg ? m : wn[k];
@@ -335,6 +342,13 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
         m.y = psum<0, KL, T>(w1) / (T)a.k_total;
 #pragma unroll
         for (int k = 0; k < KL; ++k) *reinterpret_cast<V2*>(a.w + k * a.ld + i) = m;
+      } else if (part) {
+        // multi-rank synced tile: only this rank's subtree sum leaves the
+        // kernel; the rows are rewritten by the cross-rank average
+        V2 m;
+        m.x = psum<0, KL, T>(w0);
+        m.y = psum<0, KL, T>(w1);
+        *reinterpret_cast<V2*>(a.partial_out + i) = m;
       } else {
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
@@ -642,6 +656,66 @@ __global__ void broadcast_rows_kernel(T* w, long long ld, int kl, long long lo, 
   }
 }
 
+// Cross-rank in-place average over NVLink peer memory: x[q] is rank q's
+// exchange buffer (its subtree sums, or its only worker row), mapped into
+// this process with CUDA IPC.  This rank owns slice [a, b) of the chunk: it
+// loads every rank's value (P2P reads), sums them in the reference's
+// pairwise rank order, divides by K and stores the mean into every rank's
+// buffer (P2P writes).  One kernel = reduce-scatter + all-gather, exact.
+struct PeerPtrs {
+  void* p[kMaxProg];
+};
+
+template <typename T, int W>
+__global__ void __launch_bounds__(256)
+p2p_average_kernel(PeerPtrs peers, long long a, long long b, int k_total, PairProg prog) {
+  using V2 = typename Vec2<T>::type;
+  // vector body on even coordinates, scalar head/tail
+  const long long first = a + (a & 1);
+  const long long npairs = (b - first) >> 1;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = tid; j < npairs; j += stride) {
+    const long long i = first + 2 * j;
+    T vx[W > 0 ? W : kMaxProg], vy[W > 0 ? W : kMaxProg];
+    const int nr = W > 0 ? W : prog.n + 1;
+#pragma unroll
+    for (int q = 0; q < (W > 0 ? W : kMaxProg); ++q) {
+      if (q >= nr) break;
+      const V2 v = *reinterpret_cast<const V2*>(static_cast<const T*>(peers.p[q]) + i);
+      vx[q] = v.x;
+      vy[q] = v.y;
+    }
+    V2 m;
+    if constexpr (W > 0) {
+      m.x = psum<0, W, T>(vx) / (T)k_total;
+      m.y = psum<0, W, T>(vy) / (T)k_total;
+    } else {
+      m.x = run_prog(prog, vx) / (T)k_total;
+      m.y = run_prog(prog, vy) / (T)k_total;
+    }
+#pragma unroll
+    for (int q = 0; q < (W > 0 ? W : kMaxProg); ++q) {
+      if (q >= nr) break;
+      *reinterpret_cast<V2*>(static_cast<T*>(peers.p[q]) + i) = m;
+    }
+  }
+  if (tid < 2) {  // odd head (a) / tail (b-1)
+    const long long i = tid == 0 ? a : b - 1;
+    const bool take = tid == 0 ? (first != a && a < b) : (first + 2 * npairs < b && b - 1 >= first);
+    if (take) {
+      T v[W > 0 ? W : kMaxProg];
+      const int nr = W > 0 ? W : prog.n + 1;
+      for (int q = 0; q < nr; ++q) v[q] = static_cast<const T*>(peers.p[q])[i];
+      T m;
+      if constexpr (W > 0) m = psum<0, W, T>(v) / (T)k_total;
+      else m = run_prog(prog, v) / (T)k_total;
+      for (int q = 0; q < nr; ++q) static_cast<T*>(peers.p[q])[i] = m;
+    }
+  }
+  __threadfence_system();
+}
+
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
@@ -745,6 +819,12 @@ struct dsx_lab {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   int sync_algo = DSX_SYNC_PAIRWISE;
+  bool p2p = false;            // NVLink peer-memory average available
+  PeerPtrs peers{};            // every rank's exchange buffer, mapped here
+  std::vector<void*> opened;   // IPC mappings to close
+  int* bar = nullptr;          // 4-byte barrier all-reduce scratch
+  int chunks = 4;              // overlap groups per step
+  cudaEvent_t ev_chunk[8] = {};
   bool local_subtree = true;
   PairProg prog_ranks{};
   void* staging = nullptr;  // partial sums of synced range
@@ -789,7 +869,7 @@ dsx_status check_row(dsx_lab* lab, int local) {
 
 template <typename T, int KL>
 void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int nm, bool average,
-                     const MaskBits& mask, double eta) {
+                     const MaskBits& mask, double eta, T* partial_out) {
   UpdateArgs<T> a{};
   a.w = static_cast<T*>(lab->w);
   a.ld = lab->ld;
@@ -804,6 +884,7 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.mask = mask;
   a.average = average;
   a.norm_part = lab->norm_part;
+  a.partial_out = partial_out;
   if (lab->engine) a.nv = lab->engine->view(lab->cur_set);
   if (nm == 2) {
     lab_update_kernel<T, KL, 2><<<count, kThreads, 0, s>>>(a, lab->prog_local);
@@ -817,17 +898,17 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
 
 template <typename T>
 void launch_update(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int noise, bool average,
-                   const MaskBits& mask, double eta) {
+                   const MaskBits& mask, double eta, T* partial_out = nullptr) {
   switch (lab->kl) {
-    case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta);
-    case 2: return launch_update_t<T, 2>(lab, s, tile_base, count, noise, average, mask, eta);
-    case 3: return launch_update_t<T, 3>(lab, s, tile_base, count, noise, average, mask, eta);
-    case 4: return launch_update_t<T, 4>(lab, s, tile_base, count, noise, average, mask, eta);
-    case 5: return launch_update_t<T, 5>(lab, s, tile_base, count, noise, average, mask, eta);
-    case 6: return launch_update_t<T, 6>(lab, s, tile_base, count, noise, average, mask, eta);
-    case 7: return launch_update_t<T, 7>(lab, s, tile_base, count, noise, average, mask, eta);
-    case 8: return launch_update_t<T, 8>(lab, s, tile_base, count, noise, average, mask, eta);
-    default: return launch_update_t<T, 0>(lab, s, tile_base, count, noise, average, mask, eta);
+    case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 2: return launch_update_t<T, 2>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 3: return launch_update_t<T, 3>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 4: return launch_update_t<T, 4>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 5: return launch_update_t<T, 5>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 6: return launch_update_t<T, 6>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 7: return launch_update_t<T, 7>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 8: return launch_update_t<T, 8>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    default: return launch_update_t<T, 0>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
   }
 }
 
@@ -944,6 +1025,92 @@ std::vector<std::pair<long long, long long>> masked_ranges(const dsx_lab* lab, c
   return out;
 }
 
+// Multi-rank step with the NVLink peer-memory average: the local step runs
+// in `chunks` tile groups from the top layer down (backward order); as soon
+// as a group is updated the side stream averages its synced coordinates
+// across ranks (one p2p_average_kernel per range), overlapping the update
+// of the groups below.  Cross-rank ordering uses 4-byte NCCL all-reduces as
+// barriers: before a group's average (every rank's subtree sums are final)
+// and after it (every rank's peer writes landed).
+template <typename T>
+dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, const MaskBits& bits,
+                          int noise) {
+  const auto ranges = masked_ranges(lab, mask);
+  lab->has_ranges = !ranges.empty();
+  const int G = lab->overlap ? std::max(1, std::min(lab->chunks, lab->ntiles)) : 1;
+  T* part = lab->kl > 1 ? static_cast<T*>(lab->staging) : nullptr;
+  const bool fused_partial = lab->kl > 1 && lab->kl <= 8;
+  auto barrier = [&]() -> dsx_status {
+    DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+    return DSX_OK;
+  };
+  const int R = lab->nranks;
+  bool any = false, started = false;
+  std::vector<std::pair<long long, long long>> pending;  // ranges awaiting the row broadcast
+  for (int g = 0; g < G; ++g) {
+    // group g = tiles [tb, te), counted from the top
+    const int te = lab->ntiles - (int)((long long)lab->ntiles * g / G);
+    const int tb = lab->ntiles - (int)((long long)lab->ntiles * (g + 1) / G);
+    if (te <= tb) continue;
+    launch_update<T>(lab, lab->stream, tb, te - tb, noise, false, bits, eta, fused_partial ? part : nullptr);
+    if (g == 0 && lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[1], lab->stream));
+    const long long lo = lab->h_tiles[tb].start;
+    const long long hi = lab->h_tiles[te - 1].start + lab->h_tiles[te - 1].len;
+    std::vector<std::pair<long long, long long>> sub;
+    for (const auto& r : ranges) {
+      const long long a = std::max(lo, r.first), b = std::min(hi, r.first + r.second);
+      if (a < b) sub.push_back({a, b - a});
+    }
+    if (sub.empty()) continue;
+    DSX_CUDA(cudaEventRecord(lab->ev_chunk[g % kMaxChunks], lab->stream));
+    DSX_CUDA(cudaStreamWaitEvent(lab->side, lab->ev_chunk[g % kMaxChunks], 0));
+    if (lab->kl > 1 && !fused_partial)
+      for (const auto& r : sub) launch_partial<T>(lab, lab->side, r.first, r.second, part + r.first);
+    DSX_TRY(barrier());  // this group's subtree sums final on every rank
+    started = true;
+    if (!pending.empty()) {  // previous group's averages landed (barrier above)
+      for (const auto& r : pending) {
+        broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->side>>>(static_cast<T*>(lab->w), lab->ld,
+                                                                       lab->kl, r.first, r.second,
+                                                                       part + r.first, (T)1);
+        ++lab->launches;
+      }
+      pending.clear();
+    }
+    for (const auto& r : sub) {
+      const long long base = r.second / R, extra = r.second % R;
+      const long long a = r.first + lab->rank * base + std::min<long long>(lab->rank, extra);
+      const long long n = base + (lab->rank < extra ? 1 : 0);
+      if (n <= 0) continue;
+      const int blocks = (int)std::min<long long>(lab->nsm * 4, (n / 2 + 255) / 256 + 1);
+      switch (R) {
+        case 2: p2p_average_kernel<T, 2><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks); break;
+        case 4: p2p_average_kernel<T, 4><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks); break;
+        case 8: p2p_average_kernel<T, 8><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks); break;
+        default: p2p_average_kernel<T, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks);
+      }
+      ++lab->launches;
+    }
+    if (lab->kl > 1) pending.insert(pending.end(), sub.begin(), sub.end());
+    any = true;
+  }
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
+  if (any) {
+    DSX_TRY(barrier());  // the last group's peer writes landed everywhere
+    for (const auto& r : pending) {
+      broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->side>>>(static_cast<T*>(lab->w), lab->ld,
+                                                                     lab->kl, r.first, r.second,
+                                                                     part + r.first, (T)1);
+      ++lab->launches;
+    }
+    DSX_CUDA(cudaEventRecord(lab->ev_synced, lab->side));
+    if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[2], lab->side));
+    DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_synced, 0));
+  }
+  (void)started;
+  return DSX_OK;
+}
+
 template <typename T>
 dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int noise) {
   MaskBits bits{};
@@ -953,6 +1120,8 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int no
   if (lab->kl == 0 || lab->ntiles == 0) return DSX_OK;
   if (single) {
     launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, lab->K > 1, bits, eta);
+  } else if (lab->p2p && lab->sync_algo == DSX_SYNC_PAIRWISE) {
+    DSX_TRY(step_multi_p2p<T>(lab, eta, mask, bits, noise));
   } else {
     const auto ranges = masked_ranges(lab, mask);
     lab->has_ranges = !ranges.empty();
@@ -1204,6 +1373,10 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   if (lab->nstream) cudaStreamSynchronize(lab->nstream);
   if (lab->comm) ncclCommDestroy(lab->comm);
   delete lab->engine;
+  for (void* p : lab->opened) cudaIpcCloseMemHandle(p);
+  if (lab->bar) cudaFree(lab->bar);
+  for (auto& ev : lab->ev_chunk)
+    if (ev) cudaEventDestroy(ev);
   for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt,
                   (void*)lab->what, (void*)lab->tiles, (void*)lab->norm_part, (void*)lab->norm,
                   (void*)lab->maxnorm, (void*)lab->log_part, lab->staging, lab->recv})
@@ -1522,6 +1695,56 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   lab->staging_elems = lab->dim;
   if (lab->kl > 1) DSX_CUDA(cudaMalloc(&lab->staging, es * lab->dim));
   DSX_CUDA(cudaMalloc(&lab->recv, es * (lab->dim / nranks + 1) * nranks));
+  DSX_CUDA(cudaMalloc(&lab->bar, 4));
+  DSX_CUDA(cudaMemset(lab->bar, 0, 4));
+  for (auto& ev : lab->ev_chunk) DSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  if (const char* c = std::getenv("DSX_SYNC_CHUNKS")) lab->chunks = std::max(1, std::min(kMaxChunks, std::atoi(c)));
+
+  // NVLink peer-memory exchange: map every rank's exchange buffer (its only
+  // worker row, or its subtree-sum staging) through CUDA IPC.  All ranks must
+  // agree on using it, so the per-rank outcome is min-reduced.
+  const char* p2p_env = std::getenv("DSX_P2P");
+  int ok = (p2p_env && p2p_env[0] == '0') || nranks > kMaxProg ? 0 : 1;
+  void* xbuf = lab->kl == 1 ? lab->w : lab->staging;
+  cudaIpcMemHandle_t mine{};
+  if (ok && cudaIpcGetMemHandle(&mine, xbuf) != cudaSuccess) ok = 0;
+  char* d_handles = nullptr;
+  int* d_ok = nullptr;
+  DSX_CUDA(cudaMalloc(&d_handles, sizeof(cudaIpcMemHandle_t) * nranks));
+  DSX_CUDA(cudaMalloc(&d_ok, 4));
+  DSX_CUDA(cudaMemcpy(d_handles + sizeof(cudaIpcMemHandle_t) * rank, &mine, sizeof mine, cudaMemcpyHostToDevice));
+  DSX_CUDA(cudaMemcpy(d_ok, &ok, 4, cudaMemcpyHostToDevice));
+  DSX_NCCL(ncclAllGather(d_handles + sizeof(cudaIpcMemHandle_t) * rank, d_handles, sizeof(cudaIpcMemHandle_t),
+                         ncclChar, lab->comm, lab->side));
+  DSX_NCCL(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, lab->comm, lab->side));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  std::vector<cudaIpcMemHandle_t> handles(nranks);
+  DSX_CUDA(cudaMemcpy(handles.data(), d_handles, sizeof(cudaIpcMemHandle_t) * nranks, cudaMemcpyDeviceToHost));
+  DSX_CUDA(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
+  int local_ok = ok;
+  if (ok) {
+    for (int q = 0; q < nranks; ++q) {
+      if (q == rank) {
+        lab->peers.p[q] = xbuf;
+        continue;
+      }
+      void* ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, handles[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        local_ok = 0;
+        break;
+      }
+      lab->opened.push_back(ptr);
+      lab->peers.p[q] = ptr;
+    }
+  }
+  DSX_CUDA(cudaMemcpy(d_ok, &local_ok, 4, cudaMemcpyHostToDevice));
+  DSX_NCCL(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, lab->comm, lab->side));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  DSX_CUDA(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_handles);
+  cudaFree(d_ok);
+  lab->p2p = ok != 0;
   return DSX_OK;
 }
 

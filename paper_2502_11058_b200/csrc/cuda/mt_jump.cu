@@ -427,23 +427,27 @@ __device__ __forceinline__ void store_ck(uint64_t* ck, const uint64_t* x, int ha
 }
 
 // One CTA per (segment, worker): S outputs from relative position sS + p.
+//
+// kRound generations per round.  ring[0..R-1] receive this round's arrays
+// (ring[0] twisted from ring[R], which holds the previous round's last
+// array; chained twists after that, 2 barriers each), all R*312 outputs are
+// tempered and paired at once (2 pair slots per thread), one warp scans the
+// accepted counts, and accepted pairs are transformed and stored as one
+// 16-byte (y*mult, x*mult) pair.  Ring slots are compile-time constants, and
+// interior rounds (every generation complete) take a branch-free path.
 __global__ void __launch_bounds__(kThreads)
 mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
                   int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
                   double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
                   uint64_t* tail) {
-  // kRound generations per round: each round twists kRound arrays into a
-  // ring (2 barriers per twist, separate source/destination), then tempers,
-  // pairs, scans and transforms all of them at once — 2 pair slots per
-  // thread instead of ~0.5, and 3 barriers per round instead of 3 per
-  // generation.
   constexpr int R = kRound;
   constexpr int kSlots = (R * kMtN / 2 + kThreads - 1) / kThreads;  // pair slots per thread
+  constexpr int kCounts = kSlots * (kThreads / 32);
+  static_assert(kCounts <= 32, "scan fits one warp");
   __shared__ uint64_t ring[R + 1][kMtN];
   __shared__ double v[R * kMtN + 2];
-  __shared__ int wcnt[kSlots][kThreads / 32];
-  __shared__ int woff[kSlots][kThreads / 32];
-  __shared__ int woff_total;
+  __shared__ int wcnt[kCounts];
+  __shared__ int woff[kCounts + 1];
   const int s = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int p;
   if (s == 0) {
@@ -470,24 +474,38 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
   int have_half = 0;
   double half = 0.0;
   unsigned long long local = 0;
-  int cur = 0;  // ring slot holding the first generation of this round
+  int last = 0;  // ring slot of the last processed generation
   for (int q = 0; q < ngen; q += R) {
     const int rg = min(R, ngen - q);
-    if (q) twist_into(ring[(cur + R) % (R + 1)], ring[cur]);  // after the previous round's last
-    if (q % ck_every == 0) store_ck(ckw + (long long)(q / ck_every) * kCkWords, ring[cur], have_half, half, local);
-    for (int g = 1; g < rg; ++g) twist_into(ring[(cur + g - 1) % (R + 1)], ring[(cur + g) % (R + 1)]);
-    // values of generations q .. q+rg-1 (with their [lo, hi) windows)
-    int nvals = have_half;
-    for (int g = 0; g < rg; ++g) {
-      const int gen = q + g;
-      const int lo = gen == 0 ? p : 0;
-      const int hi = (gen == gens) ? p : kMtN;
-      const uint64_t* x = ring[(cur + g) % (R + 1)];
-      if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(x[tid]));
-      nvals += hi - lo;
+    if (q) twist_into(ring[R], ring[0]);
+    if (q % ck_every == 0) store_ck(ckw + (long long)(q / ck_every) * kCkWords, ring[0], have_half, half, local);
+#pragma unroll
+    for (int g = 1; g < R; ++g)
+      if (g < rg) twist_into(ring[g - 1], ring[g]);
+    int nvals;
+    if (q > 0 && q + R <= gens) {  // interior: R complete generations
+#pragma unroll
+      for (int g = 0; g < R; ++g)
+        if (tid < kMtN) v[have_half + g * kMtN + tid] = mt_polar_coord(mt_temper(ring[g][tid]));
+      nvals = have_half + R * kMtN;
+    } else {
+      nvals = have_half;
+#pragma unroll
+      for (int g = 0; g < R; ++g) {
+        if (g < rg) {
+          const int gen = q + g;
+          const int lo = gen == 0 ? p : 0;
+          const int hi = (gen == gens) ? p : kMtN;
+          if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(ring[g][tid]));
+          nvals += hi - lo;
+        }
+      }
     }
     if (tid == 0 && have_half) v[0] = half;
     __syncthreads();
+    last = rg - 1;
+    // carry the round's last array to ring[R] for the next round's first twist
+    if (q + R < ngen && tid < kMtN) ring[R][tid] = ring[R - 1][tid];
     const int npairs = nvals >> 1;
     bool acc[kSlots];
     double r2[kSlots];
@@ -499,37 +517,34 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
       r2[u] = 0.0;
       if (a < npairs) acc[u] = mt_polar_accept(v[2 * a], v[2 * a + 1], &r2[u]);
       const unsigned bal = __ballot_sync(0xffffffffu, acc[u]);
-      if (lane == 0) wcnt[u][warp] = __popc(bal);
+      if (lane == 0) wcnt[u * (kThreads / 32) + warp] = __popc(bal);
       before[u] = __popc(bal & ((1u << lane) - 1u));
     }
     __syncthreads();
-    // exclusive scan of the kSlots*10 warp counts (slot-major = pair order)
-    // by warp 0; everyone then reads one offset per slot
-    constexpr int kCounts = kSlots * (kThreads / 32);
-    static_assert(kCounts <= 32, "scan fits one warp");
-    if (warp == 0) {
-      const int c = lane < kCounts ? (&wcnt[0][0])[lane] : 0;
+    if (warp == 0) {  // exclusive scan, slot-major = pair order
+      const int c = lane < kCounts ? wcnt[lane] : 0;
       int incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += t;
       }
-      if (lane < kCounts) (&woff[0][0])[lane] = incl - c;
-      if (lane == 31) woff_total = incl;
+      if (lane < kCounts) woff[lane] = incl - c;
+      if (lane == 31) woff[kCounts] = incl;
     }
     __syncthreads();
-    const int total = woff_total;
-#pragma unroll
-    for (int u = 0; u < kSlots; ++u) before[u] += woff[u][warp];
+    const int total = woff[kCounts];
 #pragma unroll
     for (int u = 0; u < kSlots; ++u) {
-      if (!acc[u]) continue;
-      const int a = tid + u * kThreads;
-      const unsigned long long m = local + (unsigned long long)before[u];
-      const double mult = mt_polar_mult(r2[u]);
-      out[2 * m] = mt_scale(v[2 * a + 1], mult, stddev);
-      out[2 * m + 1] = mt_scale(v[2 * a], mult, stddev);
+      if (acc[u]) {
+        const int a = tid + u * kThreads;
+        const unsigned long long m = local + (unsigned long long)(before[u] + woff[u * (kThreads / 32) + warp]);
+        const double mult = mt_polar_mult(r2[u]);
+        double2 o;
+        o.x = mt_scale(v[2 * a + 1], mult, stddev);
+        o.y = mt_scale(v[2 * a], mult, stddev);
+        *reinterpret_cast<double2*>(out + 2 * m) = o;
+      }
     }
     local += (unsigned long long)total;
     if (nvals & 1) {
@@ -538,13 +553,15 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
     } else {
       have_half = 0;
     }
-    cur = (cur + rg - 1) % (R + 1);  // slot of this round's last generation ...
     __syncthreads();
-    if (q + R < ngen) cur = (cur + 1) % (R + 1);  // ... next round starts one slot on
   }
   if (tid == 0) cnt[(long long)w * P + s] = local;
   // end state for an overflow continuation: the last processed array
-  store_ck(tail + ((long long)w * P + s) * kCkWords, ring[cur], have_half, half, local);
+  const uint64_t* lastx = ring[0];
+#pragma unroll
+  for (int g = 1; g < R; ++g)
+    if (g == last) lastx = ring[g];
+  store_ck(tail + ((long long)w * P + s) * kCkWords, lastx, have_half, half, local);
 }
 
 // Walks generations from a checkpoint until the target pair; writes the new

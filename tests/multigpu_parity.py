@@ -48,6 +48,15 @@ def run(algo, overlap, dim=200003, L=12, K=8, H=4, sigma=1.0, seed=5, steps=7):
         return None
     W = np.concatenate([g[0] for g in gathered])
     R = [t for g in gathered for t in g[1]]
+    # the same K workers on one GPU (in-kernel averaging, same device noise)
+    one = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, sigma=sigma,
+                      device=int(os.environ.get("LOCAL_RANK", 0))))
+    one.seed(seed)
+    one.fill(0.0)
+    for r in range(steps):
+        one.step(O.learning_rate(r, 1.0, 2.0, H), sync_mask("partial", H, r, L, sets))
+    W1 = one.get_params()
+    one.close()
     ref = np.zeros((K, dim))
     orngs = [O.worker_rng(seed, k) for k in range(K)]
     for r in range(steps):
@@ -56,7 +65,12 @@ def run(algo, overlap, dim=200003, L=12, K=8, H=4, sigma=1.0, seed=5, steps=7):
                      O.sync_mask("partial", H, r, L, sets))
     err = float(np.max(np.abs(W - ref) / np.maximum(np.abs(ref), 1e-300)))
     rng_ok = all(R[k] == O.mt_state_text(orngs[k]) for k in range(K))
-    return {"algo": algo, "overlap": overlap, "max_rel_err": err, "bit_exact": bool(np.array_equal(W, ref)),
+    # vs the oracle: equal up to the last ulp of log() in the polar transform
+    # (CUDA's vs glibc's); vs the single-GPU run (same device noise): the
+    # cross-rank averaging itself must be bit-identical.
+    return {"algo": algo, "overlap": overlap, "max_rel_err_vs_oracle": err,
+            "bit_exact_vs_single_gpu": bool(np.array_equal(W, W1)),
+            "max_rel_err_vs_single_gpu": float(np.max(np.abs(W - W1) / np.maximum(np.abs(W1), 1e-300))),
             "rng_exact": rng_ok}
 
 
@@ -74,8 +88,9 @@ def main():
         world = dist.get_world_size()
         for res in results:
             exact_required = res["algo"] == N.DSX_SYNC_PAIRWISE or world <= 2
-            res["pass"] = res["rng_exact"] and (res["bit_exact"] if exact_required
-                                                else res["max_rel_err"] <= 1e-12)
+            res["pass"] = (res["rng_exact"] and res["max_rel_err_vs_oracle"] <= 1e-12 and
+                           (res["bit_exact_vs_single_gpu"] if exact_required
+                            else res["max_rel_err_vs_single_gpu"] <= 1e-12))
             ok &= res["pass"]
         print(json.dumps({"world": world, "results": results, "pass": ok}), flush=True)
     okt = [ok]
