@@ -143,6 +143,18 @@ dsx_status dsx_lab_set_overlap(dsx_lab* lab, int enabled);
  * serializes noise and update (used to time each alone). */
 dsx_status dsx_lab_set_pipeline(dsx_lab* lab, int enabled);
 
+/* Bandwidth-throttled sync (the paper's low-bandwidth regime): every synced
+ * layer additionally occupies the FIFO sync stream for latency +
+ * layer_bytes/bandwidth seconds (comm_time, profile.cpp:103-110), issued
+ * when the layer's local step is done.  bandwidth <= 0 switches it off. */
+dsx_status dsx_lab_set_link(dsx_lab* lab, double bandwidth, double latency);
+
+/* CUDA-event layer profiler: t_bp[l] = device seconds of layer l's local
+ * step (state untouched), t_comm[l] = seconds of its cross-rank average
+ * (multi-rank), or the throttled link's model, or -1 (not measured).
+ * Median of `reps`.  Feeds dsc_write_profile -> schedule_dfs. */
+dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm);
+
 /* Timing on the lab's compute stream: CUDA events in slots 0..31. */
 dsx_status dsx_lab_event_record(dsx_lab* lab, int slot);
 dsx_status dsx_lab_event_elapsed(dsx_lab* lab, int from_slot, int to_slot, float* ms);

@@ -416,6 +416,18 @@ norm_finalize_kernel(const double* part, int ntiles, double* norm, unsigned long
   }
 }
 
+// Bandwidth-throttled link emulation: occupies the sync stream for `ns`
+// nanoseconds (globaltimer), the modelled transfer time of the layers just
+// synced on a link of the profile's alpha-beta kind (profile.cpp:103-110).
+__global__ void link_spin_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 __global__ void zero_kernel(double* p, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -819,6 +831,8 @@ struct dsx_lab {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   int sync_algo = DSX_SYNC_PAIRWISE;
+  double link_bw = 0.0, link_lat = 0.0;  // throttled link (bw <= 0: off)
+  std::vector<cudaEvent_t> layer_ev;     // per-layer "BP done" events (throttled mode)
   bool p2p = false;            // NVLink peer-memory average available
   PeerPtrs peers{};            // every rank's exchange buffer, mapped here
   std::vector<void*> opened;   // IPC mappings to close
@@ -1025,6 +1039,62 @@ std::vector<std::pair<long long, long long>> masked_ranges(const dsx_lab* lab, c
   return out;
 }
 
+// Modelled link time of the synced layers overlapping [lo, lo+n): per layer
+// latency + bytes/bandwidth, like comm_time() (profile.cpp:103-110).
+unsigned long long link_ns(const dsx_lab* lab, const unsigned char* mask, long long lo, long long n) {
+  double sec = 0.0;
+  const size_t es = lab->dtype == DSX_F64 ? 8 : 4;
+  for (int b = 0; b < lab->L; ++b) {
+    if (!mask[b + 1]) continue;
+    const long long a = std::max<long long>(lo, (long long)lab->offs[b]);
+    const long long e = std::min<long long>(lo + n, (long long)lab->offs[b + 1]);
+    if (a >= e) continue;
+    sec += lab->link_lat + (double)((e - a) * (long long)es) / lab->link_bw;
+  }
+  return (unsigned long long)(sec * 1e9);
+}
+
+// Single GPU with a throttled link: the local step runs layer by layer in
+// backward order (L..1) on the compute stream and each synced layer's
+// modelled transfer occupies the FIFO sync stream from the moment its
+// update is done — the discrete-event model of simulator.cpp:145-157
+// executed for real.  The averaging itself stays fused in the update kernel.
+template <typename T>
+dsx_status step_single_throttled(dsx_lab* lab, double eta, const unsigned char* mask,
+                                 const MaskBits& bits, int noise) {
+  if ((int)lab->layer_ev.size() < lab->L) {
+    const size_t old = lab->layer_ev.size();
+    lab->layer_ev.resize(lab->L);
+    for (size_t i = old; i < lab->layer_ev.size(); ++i)
+      DSX_CUDA(cudaEventCreateWithFlags(&lab->layer_ev[i], cudaEventDisableTiming));
+  }
+  // tile range of each layer
+  int te = lab->ntiles;
+  bool any = false;
+  for (int b = lab->L - 1; b >= 0; --b) {
+    int tb = te;
+    while (tb > 0 && lab->h_tiles[tb - 1].block == b) --tb;
+    if (te > tb) launch_update<T>(lab, lab->stream, tb, te - tb, noise, lab->K > 1, bits, eta);
+    te = tb;
+    if (!mask[b + 1]) continue;
+    DSX_CUDA(cudaEventRecord(lab->layer_ev[b], lab->stream));
+    if (!any && lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[1], lab->stream));
+    DSX_CUDA(cudaStreamWaitEvent(lab->side, lab->layer_ev[b], 0));
+    const unsigned long long ns = link_ns(lab, mask, (long long)lab->offs[b], (long long)(lab->offs[b + 1] - lab->offs[b]));
+    link_spin_kernel<<<1, 1, 0, lab->side>>>(ns);
+    ++lab->launches;
+    any = true;
+  }
+  lab->has_ranges = any;
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
+  if (any) {
+    DSX_CUDA(cudaEventRecord(lab->ev_synced, lab->side));
+    if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[2], lab->side));
+    DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_synced, 0));
+  }
+  return DSX_OK;
+}
+
 // Multi-rank step with the NVLink peer-memory average: the local step runs
 // in `chunks` tile groups from the top layer down (backward order); as soon
 // as a group is updated the side stream averages its synced coordinates
@@ -1091,6 +1161,12 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
       }
       ++lab->launches;
     }
+    if (lab->link_bw > 0.0) {
+      unsigned long long ns = 0;
+      for (const auto& r : sub) ns += link_ns(lab, mask, r.first, r.second);
+      link_spin_kernel<<<1, 1, 0, lab->side>>>(ns);
+      ++lab->launches;
+    }
     if (lab->kl > 1) pending.insert(pending.end(), sub.begin(), sub.end());
     any = true;
   }
@@ -1118,7 +1194,9 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int no
     if (mask[b + 1]) bits.w[b >> 5] |= 1u << (b & 31);
   const bool single = lab->nranks == 1;
   if (lab->kl == 0 || lab->ntiles == 0) return DSX_OK;
-  if (single) {
+  if (single && lab->link_bw > 0.0) {
+    DSX_TRY(step_single_throttled<T>(lab, eta, mask, bits, noise));
+  } else if (single) {
     launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, lab->K > 1, bits, eta);
   } else if (lab->p2p && lab->sync_algo == DSX_SYNC_PAIRWISE) {
     DSX_TRY(step_multi_p2p<T>(lab, eta, mask, bits, noise));
@@ -1374,6 +1452,8 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   if (lab->comm) ncclCommDestroy(lab->comm);
   delete lab->engine;
   for (void* p : lab->opened) cudaIpcCloseMemHandle(p);
+  for (auto& ev : lab->layer_ev)
+    if (ev) cudaEventDestroy(ev);
   if (lab->bar) cudaFree(lab->bar);
   for (auto& ev : lab->ev_chunk)
     if (ev) cudaEventDestroy(ev);
@@ -1745,6 +1825,99 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   cudaFree(d_handles);
   cudaFree(d_ok);
   lab->p2p = ok != 0;
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_link(dsx_lab* lab, double bandwidth, double latency) {
+  DSX_TRY(check_lab(lab));
+  if (!(latency >= 0.0)) return fail(DSX_ERR_ARGUMENT, "latency must be >= 0");
+  lab->link_bw = bandwidth > 0.0 ? bandwidth : 0.0;
+  lab->link_lat = latency;
+  return DSX_OK;
+}
+
+// CUDA-event layer profiler: per registered layer, the
+// device time of its local step (gradient + update over the layer's tiles,
+// eta = 0 and no noise so the state is untouched) and, on multiple ranks,
+// of its cross-rank average (on a saved-and-restored arena).  Median of
+// `reps` repetitions, seconds.  t_comm[l] < 0 means "not measured" (single
+// rank without a throttled link: use the link model).
+dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm) {
+  DSX_TRY(check_lab(lab));
+  if (!t_bp || reps < 1) return fail(DSX_ERR_ARGUMENT, "bad profile args");
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
+  MaskBits none{};
+  cudaEvent_t e0, e1;
+  DSX_CUDA(cudaEventCreate(&e0));
+  DSX_CUDA(cudaEventCreate(&e1));
+  std::vector<float> ts(reps);
+  int tb = 0;
+  for (int b = 0; b < lab->L; ++b) {
+    int te = tb;
+    while (te < lab->ntiles && lab->h_tiles[te].block == b) ++te;
+    for (int r = 0; r < reps; ++r) {
+      DSX_CUDA(cudaEventRecord(e0, lab->stream));
+      if (lab->dtype == DSX_F64) launch_update<double>(lab, lab->stream, tb, te - tb, 0, false, none, 0.0);
+      else launch_update<float>(lab, lab->stream, tb, te - tb, 0, false, none, 0.0);
+      DSX_CUDA(cudaEventRecord(e1, lab->stream));
+      DSX_CUDA(cudaEventSynchronize(e1));
+      DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
+    }
+    std::sort(ts.begin(), ts.end());
+    t_bp[b] = ts[reps / 2] * 1e-3;
+    tb = te;
+  }
+  if (t_comm) {
+    std::vector<unsigned char> one(lab->L + 1, 0);
+    for (int b = 0; b < lab->L; ++b) {
+      t_comm[b] = -1.0;
+      if (lab->link_bw > 0.0) {
+        std::fill(one.begin(), one.end(), 0);
+        one[b + 1] = 1;
+        t_comm[b] = (double)link_ns(lab, one.data(), (long long)lab->offs[b],
+                                    (long long)(lab->offs[b + 1] - lab->offs[b])) * 1e-9;
+      }
+    }
+    if (lab->nranks > 1 && lab->p2p && lab->link_bw <= 0.0) {
+      // measure the real NVLink average per layer on a backup of the arena
+      const size_t es = elem_size(lab);
+      void* backup = nullptr;
+      const size_t bytes = es * (size_t)lab->ld * lab->kl;
+      DSX_CUDA(cudaMalloc(&backup, bytes));
+      DSX_CUDA(cudaMemcpyAsync(backup, lab->w, bytes, cudaMemcpyDeviceToDevice, lab->side));
+      for (int b = 0; b < lab->L; ++b) {
+        const long long lo = (long long)lab->offs[b], n = (long long)(lab->offs[b + 1] - lab->offs[b]);
+        for (int r = 0; r < reps; ++r) {
+          DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+          DSX_CUDA(cudaEventRecord(e0, lab->side));
+          const int R = lab->nranks;
+          const long long base = n / R, extra = n % R;
+          const long long a = lo + lab->rank * base + std::min<long long>(lab->rank, extra);
+          const long long m = base + (lab->rank < extra ? 1 : 0);
+          if (m > 0) {
+            const int blocks = (int)std::min<long long>(lab->nsm * 4, (m / 2 + 255) / 256 + 1);
+            if (lab->dtype == DSX_F64)
+              p2p_average_kernel<double, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + m, lab->K, lab->prog_ranks);
+            else
+              p2p_average_kernel<float, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + m, lab->K, lab->prog_ranks);
+          }
+          DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+          DSX_CUDA(cudaEventRecord(e1, lab->side));
+          DSX_CUDA(cudaEventSynchronize(e1));
+          DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
+        }
+        std::sort(ts.begin(), ts.end());
+        t_comm[b] = ts[reps / 2] * 1e-3;
+      }
+      DSX_CUDA(cudaMemcpyAsync(lab->w, backup, bytes, cudaMemcpyDeviceToDevice, lab->side));
+      DSX_CUDA(cudaStreamSynchronize(lab->side));
+      cudaFree(backup);
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return DSX_OK;
 }
 

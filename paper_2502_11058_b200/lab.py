@@ -167,6 +167,17 @@ class Lab:
         N.call("dsx_lab_event_elapsed", self.h, a, b, C.byref(out))
         return out.value
 
+    def set_link(self, bandwidth: float, latency: float = 0.0) -> None:
+        """Throttled sync link (bytes/s, s); bandwidth <= 0 disables."""
+        N.call("dsx_lab_set_link", self.h, bandwidth, latency)
+
+    def profile(self, reps: int = 5):
+        """CUDA-event layer profiler -> (t_bp[L], t_comm[L] or -1) in seconds."""
+        t_bp = np.empty(self.L)
+        t_comm = np.empty(self.L)
+        N.call("dsx_lab_profile", self.h, reps, t_bp.ctypes.data, t_comm.ctypes.data)
+        return t_bp, t_comm
+
     def launches(self) -> int:
         out = C.c_uint64()
         N.call("dsx_lab_launch_count", self.h, C.byref(out))
@@ -275,3 +286,23 @@ def lab_problem(profile_path: str):
     pb, _, _ = profile_layers(profile_path)
     sizes = [max(1, b // 4) for b in pb]
     return sizes, int(sum(sizes))
+
+
+def write_profile(path: str, param_bytes, t_fp, t_bp, t_comm=None, bandwidth: float = 1.0,
+                  latency: float = 0.0, names=None) -> None:
+    """Measured per-layer times -> "dreamsched-profile v1" file through the
+    drop-in library's write_profile (profile.cpp:160-174 semantics: times
+    rounded to integer microseconds)."""
+    N.load_dsx()
+    lib = _dsc()
+    L = len(param_bytes)
+    pb = (C.c_uint64 * L)(*[int(x) for x in param_bytes])
+    fp = (C.c_double * L)(*[float(x) for x in t_fp])
+    bp = (C.c_double * L)(*[float(x) for x in t_bp])
+    cm = (C.c_double * L)(*[float(x) for x in t_comm]) if t_comm is not None else None
+    nm = (C.c_char_p * L)(*[(n if isinstance(n, bytes) else str(n).encode()) for n in
+                            (names or [f"layer{i + 1}" for i in range(L)])])
+    rc = lib.dsc_write_profile(path.encode(), L, nm, pb, fp, bp, cm, C.c_double(bandwidth),
+                               C.c_double(latency))
+    if rc != 0:
+        raise RuntimeError(lib.dsc_last_error().decode())
