@@ -70,9 +70,8 @@ static dsx_status fail(dsx_status code, const std::string& msg) {
 // ---------------------------------------------------------------------------
 // kernel parameter blocks
 // ---------------------------------------------------------------------------
-constexpr int kTile = 2048;       // coordinates per CTA (never crosses a block)
+constexpr int kTile = 4096;       // default coordinates per CTA (never crosses a block; DSX_TILE)
 constexpr int kThreads = 256;
-constexpr int kItems = kTile / kThreads;
 constexpr int kMaxMaskWords = 128;  // 4096 layers
 constexpr int kMaxProg = 64;        // generic pairwise program (K <= 64)
 constexpr int kMaxChunks = 8;
@@ -304,9 +303,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     if (threadIdx.x == 0 && first != t.start) scalar(t.start);
     if (threadIdx.x == 1 && first + 2 * (long long)npairs < end) scalar(end - 1);
 #pragma unroll 2
-    for (int j = 0; j < kItems / 2; ++j) {
-      const int pr = j * kThreads + threadIdx.x;
-      if (pr >= npairs) break;
+    for (int pr = threadIdx.x; pr < npairs; pr += kThreads) {
       const long long i = first + 2 * (long long)pr;
       double lam0, opt0, lam1, opt1;
       quad_coeffs(a.q, i, &lam0, &opt0);
@@ -363,9 +360,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     // generic worker count: row pass, then the pairwise program for
     // averaged coordinates.
     T v[KMAX];
-    for (int j = 0; j < kItems; ++j) {
-      const int off = j * kThreads + threadIdx.x;
-      if (off >= t.len) break;
+    for (int off = threadIdx.x; off < t.len; off += kThreads) {
       const long long i = t.start + off;
       double lam, opt;
       quad_coeffs(a.q, i, &lam, &opt);
@@ -1233,7 +1228,7 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int no
       lab->norm_part, lab->ntiles, lab->norm, reinterpret_cast<unsigned long long*>(lab->maxnorm));
   ++lab->launches;
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[4], lab->stream));
-  lab->synced_last = !single && lab->has_ranges;
+  lab->synced_last = (!single || lab->link_bw > 0.0) && lab->has_ranges;
   DSX_CUDA(cudaGetLastError());
   return DSX_OK;
 }
@@ -1401,10 +1396,12 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
       if (!lab->engine->init(lab->dim, lab->kl, lab->nsm, &err)) return cleanup(fail(DSX_ERR_CUDA, err));
     }
   }
-  // tiles: per block, kTile coordinates each (never crossing a block)
+  // tiles: per block, `tile` coordinates each (never crossing a block)
+  long long tile = kTile;
+  if (const char* e = std::getenv("DSX_TILE")) tile = std::max(256LL, std::atoll(e) / 2 * 2);
   for (int b = 0; b < lab->L; ++b) {
-    for (unsigned long long s = lab->offs[b]; s < lab->offs[b + 1]; s += kTile) {
-      lab->h_tiles.push_back({(long long)s, (int)std::min<unsigned long long>(kTile, lab->offs[b + 1] - s), b});
+    for (unsigned long long s = lab->offs[b]; s < lab->offs[b + 1]; s += tile) {
+      lab->h_tiles.push_back({(long long)s, (int)std::min<unsigned long long>(tile, lab->offs[b + 1] - s), b});
     }
   }
   lab->ntiles = (int)lab->h_tiles.size();

@@ -276,6 +276,35 @@ int cmd_train(const std::string& path) {
   return 0;
 }
 
+// Per-call latency of the host-state API on a tiny problem (the shape of
+// the reference acceptance criterion 6): microseconds per call.
+int cmd_apibench() {
+  const Problem problem = make_quadratic(64, 4, 1.0, 2.0, 1.0);
+  TrainerConfig config;
+  config.workers = 4;
+  config.period = 1;
+  config.schedule = Schedule::single_set(4);
+  config.seed = 7;
+  std::vector<WorkerState> workers(4);
+  for (int k = 0; k < 4; ++k) {
+    workers[static_cast<std::size_t>(k)].w.assign(64, 0.0);
+    workers[static_cast<std::size_t>(k)].rng = worker_rng(7, k);
+  }
+  std::vector<double> ref(64, 0.0);
+  std::mt19937_64 stream = worker_rng(7, 0);
+  plsgd_step(workers, 0, config, problem);  // warm (creates the device state)
+  (void)stochastic_gradient(problem, ref, stream);
+  auto t0 = std::chrono::steady_clock::now();
+  for (long long r = 1; r <= 100; ++r) plsgd_step(workers, r, config, problem);
+  auto t1 = std::chrono::steady_clock::now();
+  for (int i = 0; i < 100; ++i) (void)stochastic_gradient(problem, ref, stream);
+  auto t2 = std::chrono::steady_clock::now();
+  std::printf("{\"plsgd_step_us\": %.1f, \"stochastic_gradient_us\": %.1f}\n",
+              std::chrono::duration<double, std::micro>(t1 - t0).count() / 100.0,
+              std::chrono::duration<double, std::micro>(t2 - t1).count() / 100.0);
+  return 0;
+}
+
 // CPU timing of plsgd_step: one JSON line.
 int cmd_bench(int argc, char** argv) {
   // bench dim blocks K H sigma seed steps warmup mode schedule [profile]
@@ -328,6 +357,7 @@ int main(int argc, char** argv) {
     if (cmd == "steps") return cmd_steps(argc, argv);
     if (cmd == "train" && argc >= 3) return cmd_train(argv[2]);
     if (cmd == "bench") return cmd_bench(argc, argv);
+    if (cmd == "apibench") return cmd_apibench();
   } catch (const Error& e) {
     std::cerr << "error: " << e.what() << "\n";
     return 1;
