@@ -70,7 +70,7 @@ static dsx_status fail(dsx_status code, const std::string& msg) {
 // ---------------------------------------------------------------------------
 // kernel parameter blocks
 // ---------------------------------------------------------------------------
-constexpr int kTile = 4096;       // default coordinates per CTA (never crosses a block; DSX_TILE)
+constexpr int kTile = 8192;       // default coordinates per CTA (never crosses a block; DSX_TILE)
 constexpr int kThreads = 256;
 constexpr int kMaxMaskWords = 128;  // 4096 layers
 constexpr int kMaxProg = 64;        // generic pairwise program (K <= 64)
@@ -792,6 +792,7 @@ struct dsx_lab {
   double* noise = nullptr;
   uint64_t* mt = nullptr;
   double* what = nullptr;
+  double* grad_buf = nullptr;  // dsx_lab_gradient output staging
   Tile* tiles = nullptr;
   int ntiles = 0;
   std::vector<Tile> h_tiles;
@@ -1454,7 +1455,7 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   if (lab->bar) cudaFree(lab->bar);
   for (auto& ev : lab->ev_chunk)
     if (ev) cudaEventDestroy(ev);
-  for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt,
+  for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt, (void*)lab->grad_buf,
                   (void*)lab->what, (void*)lab->tiles, (void*)lab->norm_part, (void*)lab->norm,
                   (void*)lab->maxnorm, (void*)lab->log_part, lab->staging, lab->recv})
     if (p) cudaFree(p);
@@ -1680,7 +1681,8 @@ dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
   DSX_TRY(invalidate_prefetch(lab));
   DSX_TRY(run_noise(lab, &nm));  // advances every local row's stream
   double* g = nullptr;
-  DSX_CUDA(cudaMallocAsync((void**)&g, 8 * lab->dim, lab->stream));
+  if (!lab->grad_buf) DSX_CUDA(cudaMalloc(&lab->grad_buf, 8 * lab->dim));
+  g = lab->grad_buf;
   const double* xi = nm == 1 ? lab->noise + (long long)local * lab->ld : nullptr;
   const NoiseView nv = lab->engine ? lab->engine->view(lab->cur_set) : NoiseView{};
   if (lab->dtype == DSX_F64) {
@@ -1694,7 +1696,6 @@ dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
   }
   ++lab->launches;
   DSX_CUDA(cudaMemcpyAsync(g_out, g, 8 * lab->dim, cudaMemcpyDeviceToHost, lab->stream));
-  DSX_CUDA(cudaFreeAsync(g, lab->stream));
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
   return DSX_OK;
 }
