@@ -297,21 +297,20 @@ def our_arm(args, world, rank, local_rank, dist):
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
         import torch
+        # pinned host buffers: every worker's parameters and engine state go
+        # in and come back every step, one transfer each way
         host = torch.zeros((kl, dim), dtype=torch.float64, pin_memory=True)
-        hn = host.numpy()
-        rng = [lab.get_rng(k) for k in range(kl)]
-        lab.set_params(hn)
+        host_rng = torch.zeros((kl, 313), dtype=torch.int64, pin_memory=True)
+        wp, rp = host.data_ptr(), host_rng.data_ptr()
+        N.call("dsx_lab_get_state", lab.h, wp, rp)
         lab.sync()
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            lab.set_params(hn)
-            for k in range(kl):
-                lab.set_rng(k, *rng[k])
+            N.call("dsx_lab_set_state", lab.h, wp, rp)
             lab.step(learning_rate(r, H), masks[r % H])
             r += 1
-            hn[:] = lab.get_params()
-            rng = [lab.get_rng(k) for k in range(kl)]
+            N.call("dsx_lab_get_state", lab.h, wp, rp)
         lab.sync()
         el = time.perf_counter() - t0
         if dist is not None:

@@ -435,7 +435,7 @@ __device__ __forceinline__ void store_ck(uint64_t* ck, const uint64_t* x, int ha
 // accepted counts, and accepted pairs are transformed and stored as one
 // 16-byte (y*mult, x*mult) pair.  Ring slots are compile-time constants, and
 // interior rounds (every generation complete) take a branch-free path.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
                   int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
                   double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
