@@ -78,10 +78,14 @@ def main():
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     dist.init_process_group("gloo")
     results = []
-    for algo, overlap in [(N.DSX_SYNC_PAIRWISE, True), (N.DSX_SYNC_PAIRWISE, False),
-                          (N.DSX_SYNC_NCCL_AVG, True)]:
-        res = run(algo, overlap)
+    world = dist.get_world_size()
+    cases = [(N.DSX_SYNC_PAIRWISE, True, 8), (N.DSX_SYNC_PAIRWISE, False, 8),
+             (N.DSX_SYNC_NCCL_AVG, True, 8),
+             (N.DSX_SYNC_PAIRWISE, True, world)]  # one worker per GPU (in-place exchange)
+    for algo, overlap, K in cases:
+        res = run(algo, overlap, K=K)
         if res is not None:
+            res["K"] = K
             results.append(res)
     ok = True
     if dist.get_rank() == 0:
