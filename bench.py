@@ -284,7 +284,11 @@ def our_arm(args, world, rank, local_rank, dist):
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom["kernel"].split(" ")[0])
+            # dram bytes per launch from the committed ncu capture
+            # (profiles/r01_ncu_summary.md), for this kernel and noise mode;
+            # the capture is single-GPU with all 8 workers, so it applies at N=1
+            rec = json.load(open(tpath)).get(dom["kernel"].split(" ")[0], {})
+            traffic = rec.get("sigma1" if args.sigma > 0 else "sigma0") if world == 1 else None
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -86,7 +86,7 @@ struct MaskBits {
   uint32_t w[kMaxMaskWords];
 };
 
-__device__ __forceinline__ bool mask_has(const MaskBits& m, int block) {
+__host__ __device__ __forceinline__ bool mask_has(const MaskBits& m, int block) {
   return (m.w[block >> 5] >> (block & 31)) & 1u;
 }
 
@@ -122,6 +122,8 @@ struct UpdateArgs {
   bool average;       // average masked blocks in-kernel (single rank)
   double* norm_part;  // [kl][ntiles]
   T* partial_out;     // multi-rank: subtree sums of synced tiles (else null)
+  const T* mean_in;   // multi-rank: cross-rank means of the layers in `stale`
+  MaskBits stale;     // layers whose rows are stale: every row equals mean_in
 };
 
 // lambda_i and w*_i.  The analytic form is make_quadratic's
@@ -235,6 +237,11 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   const int kl = KL > 0 ? KL : a.kl;
   const bool avg = a.average && mask_has(a.mask, t.block);
   const bool part = KL > 1 && a.partial_out != nullptr && mask_has(a.mask, t.block);
+  // lazy broadcast: after a cross-rank average the mean lives once in the
+  // exchange buffer; all kl rows are logically equal to it, so it is read
+  // once instead of kl times (and the rows are never written back while the
+  // layer keeps being synced)
+  const bool stale = KL > 1 && a.mean_in != nullptr && mask_has(a.stale, t.block);
   double nsq[KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) nsq[k] = 0.0;
@@ -289,7 +296,8 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
       T wn[KL];
 #pragma unroll
       for (int k = 0; k < KL; ++k) {
-        const auto g = grad_step(a.w[k * a.ld + i], lam, opt, noise_at(k, i), a.eta, NOISE, &wn[k]);
+        const auto g = grad_step(stale ? a.mean_in[i] : a.w[k * a.ld + i], lam, opt, noise_at(k, i),
+                                 a.eta, NOISE, &wn[k]);
         nsq[k] += to_d(g) * to_d(g);
       }
       if (part) {
@@ -311,7 +319,8 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
       T w0[KL], w1[KL];
 #pragma unroll
       for (int k = 0; k < KL; ++k) {
-        const V2 w = *reinterpret_cast<const V2*>(a.w + k * a.ld + i);
+        const V2 w = stale ? *reinterpret_cast<const V2*>(a.mean_in + i)
+                           : *reinterpret_cast<const V2*>(a.w + k * a.ld + i);
         double x0 = 0.0, x1 = 0.0;
         if constexpr (NM == 1) {
           const double2 xv = *reinterpret_cast<const double2*>(a.noise + k * a.ld + i);
@@ -834,6 +843,9 @@ struct dsx_lab {
   std::vector<void*> opened;   // IPC mappings to close
   int* bar = nullptr;          // 4-byte barrier all-reduce scratch
   int chunks = 4;              // overlap groups per step
+  bool lazy = true;            // lazy broadcast of cross-rank means (DSX_LAZY=0: off)
+  MaskBits stale_bits{};       // layers whose rows are stale (mean in staging)
+  bool stale_any = false;
   cudaEvent_t ev_chunk[8] = {};
   bool local_subtree = true;
   PairProg prog_ranks{};
@@ -895,6 +907,8 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.average = average;
   a.norm_part = lab->norm_part;
   a.partial_out = partial_out;
+  a.mean_in = lab->stale_any ? static_cast<const T*>(lab->staging) : nullptr;
+  a.stale = lab->stale_bits;
   if (lab->engine) a.nv = lab->engine->view(lab->cur_set);
   if (nm == 2) {
     lab_update_kernel<T, KL, 2><<<count, kThreads, 0, s>>>(a, lab->prog_local);
@@ -1106,6 +1120,9 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
   const int G = lab->overlap ? std::max(1, std::min(lab->chunks, lab->ntiles)) : 1;
   T* part = lab->kl > 1 ? static_cast<T*>(lab->staging) : nullptr;
   const bool fused_partial = lab->kl > 1 && lab->kl <= 8;
+  // lazy broadcast (fused path): the synced layers' rows stay stale, their
+  // mean lives in the exchange buffer and the next update reads it there
+  const bool lazy = fused_partial && lab->lazy;
   auto barrier = [&]() -> dsx_status {
     DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
     return DSX_OK;
@@ -1134,7 +1151,7 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
       for (const auto& r : sub) launch_partial<T>(lab, lab->side, r.first, r.second, part + r.first);
     DSX_TRY(barrier());  // this group's subtree sums final on every rank
     started = true;
-    if (!pending.empty()) {  // previous group's averages landed (barrier above)
+    if (!pending.empty() && !lazy) {  // previous group's averages landed (barrier above)
       for (const auto& r : pending) {
         broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->side>>>(static_cast<T*>(lab->w), lab->ld,
                                                                        lab->kl, r.first, r.second,
@@ -1169,17 +1186,25 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
   if (any) {
     DSX_TRY(barrier());  // the last group's peer writes landed everywhere
-    for (const auto& r : pending) {
-      broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->side>>>(static_cast<T*>(lab->w), lab->ld,
-                                                                     lab->kl, r.first, r.second,
-                                                                     part + r.first, (T)1);
-      ++lab->launches;
+    if (!lazy) {
+      for (const auto& r : pending) {
+        broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->side>>>(static_cast<T*>(lab->w), lab->ld,
+                                                                       lab->kl, r.first, r.second,
+                                                                       part + r.first, (T)1);
+        ++lab->launches;
+      }
     }
     DSX_CUDA(cudaEventRecord(lab->ev_synced, lab->side));
     if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[2], lab->side));
     DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_synced, 0));
   }
   (void)started;
+  if (lazy) {
+    // this step's synced layers are stale now (the previous stale set was
+    // consumed: unsynced tiles rewrote their rows, synced ones are stale again)
+    lab->stale_bits = bits;
+    lab->stale_any = any;
+  }
   return DSX_OK;
 }
 
@@ -1235,6 +1260,34 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int no
 }
 
 uint64_t* mt_state(dsx_lab* lab, int idx) { return lab->mt + (long long)idx * lab->kl * (kMtN + 1); }
+
+// Writes the lazily kept cross-rank means back into every local row (before
+// anything reads or partially overwrites the rows).
+template <typename T>
+dsx_status materialize_t(dsx_lab* lab) {
+  DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_synced, 0));
+  for (int b = 0; b < lab->L; ++b) {
+    if (!mask_has(lab->stale_bits, b)) continue;
+    const long long lo = (long long)lab->offs[b], n = (long long)(lab->offs[b + 1] - lab->offs[b]);
+    broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->stream>>>(
+        static_cast<T*>(lab->w), lab->ld, lab->kl, lo, n, static_cast<const T*>(lab->staging) + lo, (T)1);
+    ++lab->launches;
+  }
+  lab->stale_bits = MaskBits{};
+  lab->stale_any = false;
+  DSX_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
+dsx_status materialize(dsx_lab* lab) {
+  if (!lab->stale_any) return DSX_OK;
+  return lab->dtype == DSX_F64 ? materialize_t<double>(lab) : materialize_t<float>(lab);
+}
+
+void drop_stale(dsx_lab* lab) {  // every row is about to be overwritten
+  lab->stale_bits = MaskBits{};
+  lab->stale_any = false;
+}
 
 // Launches the engine on the noise stream: states mt_commit -> other buffer,
 // normals into `set`, after the last update that read `set` finished.
@@ -1479,6 +1532,7 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
 dsx_status dsx_lab_set_params(dsx_lab* lab, int local, const double* w) {
   DSX_TRY(check_row(lab, local));
   if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  DSX_TRY(materialize(lab));  // the other rows keep their (lazy) values
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
   if (lab->dtype == DSX_F64) {
     DSX_CUDA(cudaMemcpy(static_cast<double*>(lab->w) + (long long)local * lab->ld, w, 8 * lab->dim,
@@ -1494,6 +1548,7 @@ dsx_status dsx_lab_set_params(dsx_lab* lab, int local, const double* w) {
 dsx_status dsx_lab_get_params(dsx_lab* lab, int local, double* w) {
   DSX_TRY(check_row(lab, local));
   if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  DSX_TRY(materialize(lab));
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
   DSX_CUDA(cudaStreamSynchronize(lab->side));
   if (lab->dtype == DSX_F64) {
@@ -1511,6 +1566,8 @@ dsx_status dsx_lab_get_params(dsx_lab* lab, int local, double* w) {
 dsx_status dsx_lab_set_all_params(dsx_lab* lab, const double* w) {
   DSX_TRY(check_lab(lab));
   if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  drop_stale(lab);
   if (lab->dtype == DSX_F64) {
     DSX_CUDA(cudaMemcpy2DAsync(lab->w, 8 * lab->ld, w, 8 * lab->dim, 8 * lab->dim, lab->kl,
                                cudaMemcpyHostToDevice, lab->stream));
@@ -1523,6 +1580,8 @@ dsx_status dsx_lab_set_all_params(dsx_lab* lab, const double* w) {
 dsx_status dsx_lab_set_state(dsx_lab* lab, const double* w, const uint64_t* rng) {
   DSX_TRY(check_lab(lab));
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  if (w) drop_stale(lab);
   if (rng) DSX_TRY(invalidate_prefetch(lab));
   if (w) {
     if (lab->dtype == DSX_F64) {
@@ -1544,6 +1603,7 @@ dsx_status dsx_lab_set_state(dsx_lab* lab, const double* w, const uint64_t* rng)
 
 dsx_status dsx_lab_get_state(dsx_lab* lab, double* w, uint64_t* rng) {
   DSX_TRY(check_lab(lab));
+  if (w) DSX_TRY(materialize(lab));
   DSX_CUDA(cudaStreamSynchronize(lab->side));
   if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
   if (w) {
@@ -1565,6 +1625,7 @@ dsx_status dsx_lab_get_state(dsx_lab* lab, double* w, uint64_t* rng) {
 dsx_status dsx_lab_get_all_params(dsx_lab* lab, double* w) {
   DSX_TRY(check_lab(lab));
   if (!w) return fail(DSX_ERR_ARGUMENT, "null params");
+  DSX_TRY(materialize(lab));
   if (lab->dtype == DSX_F64) {
     DSX_CUDA(cudaStreamSynchronize(lab->side));
     DSX_CUDA(cudaMemcpy2DAsync(w, 8 * lab->dim, lab->w, 8 * lab->ld, 8 * lab->dim, lab->kl,
@@ -1678,6 +1739,7 @@ dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
   DSX_TRY(check_row(lab, local));
   if (!g_out) return fail(DSX_ERR_ARGUMENT, "null gradient out");
   int nm = 0;
+  DSX_TRY(materialize(lab));
   DSX_TRY(invalidate_prefetch(lab));
   DSX_TRY(run_noise(lab, &nm));  // advances every local row's stream
   double* g = nullptr;
@@ -1777,6 +1839,7 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   DSX_CUDA(cudaMemset(lab->bar, 0, 4));
   for (auto& ev : lab->ev_chunk) DSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   if (const char* c = std::getenv("DSX_SYNC_CHUNKS")) lab->chunks = std::max(1, std::min(kMaxChunks, std::atoi(c)));
+  if (const char* z = std::getenv("DSX_LAZY")) lab->lazy = z[0] != '0';
 
   // NVLink peer-memory exchange: map every rank's exchange buffer (its only
   // worker row, or its subtree-sum staging) through CUDA IPC.  All ranks must
@@ -1843,6 +1906,7 @@ dsx_status dsx_lab_set_link(dsx_lab* lab, double bandwidth, double latency) {
 dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm) {
   DSX_TRY(check_lab(lab));
   if (!t_bp || reps < 1) return fail(DSX_ERR_ARGUMENT, "bad profile args");
+  DSX_TRY(materialize(lab));
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
   DSX_CUDA(cudaStreamSynchronize(lab->side));
   if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
