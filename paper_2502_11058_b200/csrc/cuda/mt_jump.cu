@@ -693,11 +693,15 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
   const double attempts = M / pa + 8.0 * std::sqrt(M * (1.0 - pa)) / pa + 1024.0;
   const double E = 2.0 * attempts;
   const double min_seg = 312.0 * 64.0;
-  // ~2 jumps per SM (one CTA of kJumpsPerCta jumps per SM, a single wave)
-  // and >= 2 segment CTAs per SM; segments no shorter than 64 generations.
-  int P = (int)std::ceil(E / min_seg);
-  const int p_cap = std::max(1, (nsm / kl) * kJumpsPerCta + 1);
-  P = std::max(1, std::min(P, p_cap));
+  // Segment count: the segment kernel is latency-bound per CTA (measured
+  // ~2.24 ns per output, so T_seg ~ 2.24e-3 us * E / P) and jumps cost
+  // ~1.3 us of whole-GPU time each (T_jump ~ 1.3 us * kl * (P-1)); their sum
+  // is minimal at P* = sqrt(1.72e-3 * E / kl).  Capped so segment CTAs fit
+  // one wave at 2 per SM; segments no shorter than 64 generations.
+  int P = (int)std::lround(std::sqrt(1.72e-3 * E / kl));
+  P = std::min(P, (int)std::ceil(E / min_seg));
+  P = std::min(P, std::max(1, 2 * nsm / kl));
+  P = std::max(1, P);
   long long gens = (long long)std::ceil(E / P / 312.0);
   if (gens < 1) gens = 1;
   S_ = gens * 312;
