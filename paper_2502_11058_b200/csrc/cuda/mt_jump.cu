@@ -448,6 +448,8 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
   __shared__ double v[R * kMtN + 2];
   __shared__ int wcnt[kCounts];
   __shared__ int woff[kCounts + 1];
+  __shared__ short acc_pair[R * kMtN / 2 + 1];
+  __shared__ double acc_r2[R * kMtN / 2 + 1];
   const int s = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int p;
   if (s == 0) {
@@ -534,17 +536,24 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
     }
     __syncthreads();
     const int total = woff[kCounts];
+    // compact the accepted attempts (rank order) so the fp64 polar transform
+    // runs on fully populated warps
 #pragma unroll
     for (int u = 0; u < kSlots; ++u) {
       if (acc[u]) {
-        const int a = tid + u * kThreads;
-        const unsigned long long m = local + (unsigned long long)(before[u] + woff[u * (kThreads / 32) + warp]);
-        const double mult = mt_polar_mult(r2[u]);
-        double2 o;
-        o.x = mt_scale(v[2 * a + 1], mult, stddev);
-        o.y = mt_scale(v[2 * a], mult, stddev);
-        *reinterpret_cast<double2*>(out + 2 * m) = o;
+        const int j = before[u] + woff[u * (kThreads / 32) + warp];
+        acc_pair[j] = (short)(tid + u * kThreads);
+        acc_r2[j] = r2[u];
       }
+    }
+    __syncthreads();
+    for (int j = tid; j < total; j += kThreads) {
+      const int a = acc_pair[j];
+      const double mult = mt_polar_mult(acc_r2[j]);
+      double2 o;
+      o.x = mt_scale(v[2 * a + 1], mult, stddev);
+      o.y = mt_scale(v[2 * a], mult, stddev);
+      *reinterpret_cast<double2*>(out + 2 * (local + (unsigned long long)j)) = o;
     }
     local += (unsigned long long)total;
     if (nvals & 1) {
