@@ -573,6 +573,212 @@ mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pno
   store_ck(tail + ((long long)w * P + s) * kCkWords, lastx, have_half, half, local);
 }
 
+// Warp-specialized segment kernel (the default).  Warp 0 is the twister: it
+// produces the generation arrays into a double-buffered ring (R arrays per
+// half) with warp-level sync only, one round ahead; warps 1..10 consume a
+// round at a time (temper, polar accept, scan, compaction, fp64 transform)
+// and never wait on twist barriers.  Producer/consumer hand-off uses named
+// barriers: FULL_h (producer arrives once half h is written), EMPTY_h
+// (consumers arrive once they stopped reading half h).  Consumer-only sync
+// uses named barrier kBarCons over the 320 consumer threads.
+constexpr int kWsR = 4;                       // generations per round
+constexpr int kWsThreads = 32 + kThreads;     // producer warp + 320 consumers
+constexpr int kBarFull = 1, kBarEmpty = 3, kBarCons = 5;
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// dst = next generation of src, by one warp (phase A then phase B).
+__device__ __forceinline__ void warp_twist(const uint64_t* src, uint64_t* dst, int lane) {
+  for (int k = lane; k < kMtM; k += 32) dst[k] = mt_next_word(src[k], src[k + 1], src[k + kMtM]);
+  __syncwarp();
+  for (int k = kMtM + lane; k < kMtN; k += 32)
+    dst[k] = mt_next_word(src[k], (k + 1 < kMtN) ? src[k + 1] : dst[0], dst[k - kMtM]);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWsThreads, 2)
+mt_segment_ws_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
+                     int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
+                     double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
+                     uint64_t* tail) {
+  constexpr int R = kWsR;
+  constexpr int kSlots = (R * kMtN / 2 + kThreads - 1) / kThreads;  // pair slots per consumer
+  constexpr int kCounts = kSlots * (kThreads / 32);
+  static_assert(kCounts <= 32, "scan fits one warp");
+  __shared__ uint64_t ring[2][R][kMtN];
+  __shared__ uint64_t boot[kMtN];
+  __shared__ double v[R * kMtN + 2];
+  __shared__ int wcnt[kCounts];
+  __shared__ int woff[kCounts + 1];
+  __shared__ short acc_pair[R * kMtN / 2 + 1];
+  __shared__ double acc_r2[R * kMtN / 2 + 1];
+  __shared__ int s_p;
+  const int s = blockIdx.x, w = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    // ---------------- producer: generations into the ring ----------------
+    int p;
+    if (s == 0) {
+      const uint64_t* st = win_state + (long long)w * (kMtN + 1);
+      for (int k = lane; k < kMtN; k += 32) boot[k] = st[k];
+      p = (int)st[kMtN];
+      __syncwarp();
+      if (p >= kMtN) {
+        warp_twist(boot, ring[0][0], lane);
+        p = 0;
+      } else {
+        for (int k = lane; k < kMtN; k += 32) ring[0][0][k] = boot[k];
+      }
+      if (lane == 0) pnorm_out[w] = p;
+    } else {
+      for (int k = lane; k < kMtN; k += 32) ring[0][0][k] = win[((long long)w * P + s) * kMtN + k];
+      p = pnorm_in[w];
+    }
+    if (lane == 0) s_p = p;
+    __syncwarp();
+    const int ngen = gens + (p > 0 ? 1 : 0);
+    const int rounds = (ngen + R - 1) / R;
+    for (int k = 0; k < rounds; ++k) {
+      const int h = k & 1;
+      if (k >= 2) named_sync(kBarEmpty + h, kWsThreads);  // consumers done with round k-2
+      const int rg = min(R, ngen - k * R);
+      for (int g = 0; g < rg; ++g) {
+        if (k == 0 && g == 0) continue;  // gen 0 already in place
+        const uint64_t* src = g ? ring[h][g - 1] : ring[1 - h][R - 1];
+        warp_twist(src, ring[h][g], lane);
+      }
+      __threadfence_block();
+      named_arrive(kBarFull + h, kWsThreads);
+    }
+    return;
+  }
+
+  // ---------------- consumers (320 threads) ----------------
+  const int tid = threadIdx.x - 32, cw = tid >> 5;
+  named_sync(kBarFull + 0, kWsThreads);  // round 0 ready (also publishes s_p)
+  const int p = s_p;
+  const int ngen = gens + (p > 0 ? 1 : 0);
+  const int rounds = (ngen + R - 1) / R;
+  double* out = slots + ((long long)w * (P + 1) + s) * cap;
+  uint64_t* ckw = ck + ((long long)w * P + s) * (long long)nck * kCkWords;
+  int have_half = 0;
+  double half = 0.0;
+  unsigned long long local = 0;
+  for (int k = 0; k < rounds; ++k) {
+    const int h = k & 1;
+    const int q = k * R;
+    if (k) named_sync(kBarFull + h, kWsThreads);
+    const int rg = min(R, ngen - q);
+    if (q % ck_every == 0) {
+      uint64_t* c = ckw + (long long)(q / ck_every) * kCkWords;
+      if (tid < kMtN) c[tid] = ring[h][0][tid];
+      if (tid == 0) {
+        c[kMtN] = (uint64_t)have_half;
+        c[kMtN + 1] = (uint64_t)__double_as_longlong(half);
+        c[kMtN + 2] = local;
+      }
+    }
+    int nvals;
+    if (q > 0 && q + R <= gens) {  // interior: R complete generations
+#pragma unroll
+      for (int g = 0; g < R; ++g)
+        if (tid < kMtN) v[have_half + g * kMtN + tid] = mt_polar_coord(mt_temper(ring[h][g][tid]));
+      nvals = have_half + R * kMtN;
+    } else {
+      nvals = have_half;
+#pragma unroll
+      for (int g = 0; g < R; ++g) {
+        if (g < rg) {
+          const int gen = q + g;
+          const int lo = gen == 0 ? p : 0;
+          const int hi = (gen == gens) ? p : kMtN;
+          if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(ring[h][g][tid]));
+          nvals += hi - lo;
+        }
+      }
+    }
+    if (k == rounds - 1) {  // end state for an overflow continuation
+      uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
+      if (tid < kMtN) c[tid] = ring[h][rg - 1][tid];
+    }
+    if (tid == 0 && have_half) v[0] = half;
+    named_arrive(kBarEmpty + h, kWsThreads);  // done reading ring half h
+    named_sync(kBarCons, kThreads);
+    const int npairs = nvals >> 1;
+    bool acc[kSlots];
+    double r2[kSlots];
+    int before[kSlots];
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+      const int a = tid + u * kThreads;
+      acc[u] = false;
+      r2[u] = 0.0;
+      if (a < npairs) acc[u] = mt_polar_accept(v[2 * a], v[2 * a + 1], &r2[u]);
+      const unsigned bal = __ballot_sync(0xffffffffu, acc[u]);
+      if (lane == 0) wcnt[u * (kThreads / 32) + cw] = __popc(bal);
+      before[u] = __popc(bal & ((1u << lane) - 1u));
+    }
+    named_sync(kBarCons, kThreads);
+    if (cw == 0) {
+      const int c = lane < kCounts ? wcnt[lane] : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < kCounts) woff[lane] = incl - c;
+      if (lane == 31) woff[kCounts] = incl;
+    }
+    named_sync(kBarCons, kThreads);
+    const int total = woff[kCounts];
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+      if (acc[u]) {
+        const int j = before[u] + woff[u * (kThreads / 32) + cw];
+        acc_pair[j] = (short)(tid + u * kThreads);
+        acc_r2[j] = r2[u];
+      }
+    }
+    named_sync(kBarCons, kThreads);
+    // two independent polar transforms per iteration (ILP over the fp64 chains)
+    for (int j = tid; j < total; j += 2 * kThreads) {
+      const int j2 = j + kThreads;
+      const bool two = j2 < total;
+      const int a = acc_pair[j];
+      const int a2 = two ? acc_pair[j2] : a;
+      const double m1 = mt_polar_mult(acc_r2[j]);
+      const double m2 = mt_polar_mult(two ? acc_r2[j2] : acc_r2[j]);
+      double2 o;
+      o.x = mt_scale(v[2 * a + 1], m1, stddev);
+      o.y = mt_scale(v[2 * a], m1, stddev);
+      *reinterpret_cast<double2*>(out + 2 * (local + (unsigned long long)j)) = o;
+      if (two) {
+        o.x = mt_scale(v[2 * a2 + 1], m2, stddev);
+        o.y = mt_scale(v[2 * a2], m2, stddev);
+        *reinterpret_cast<double2*>(out + 2 * (local + (unsigned long long)j2)) = o;
+      }
+    }
+    local += (unsigned long long)total;
+    if (nvals & 1) {
+      half = v[nvals - 1];
+      have_half = 1;
+    } else {
+      have_half = 0;
+    }
+    named_sync(kBarCons, kThreads);  // v / acc lists reusable
+  }
+  if (tid == 0) {
+    cnt[(long long)w * P + s] = local;
+    uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
+    c[kMtN] = (uint64_t)have_half;
+    c[kMtN + 1] = (uint64_t)__double_as_longlong(half);
+    c[kMtN + 2] = local;
+  }
+}
+
 // Walks generations from a checkpoint until the target pair; writes the new
 // rng state.  Also serves the (rare) overflow continuation.
 __global__ void __launch_bounds__(kThreads)
@@ -780,9 +986,19 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, double 
         ybuf_, reinterpret_cast<const uint32_t*>(jidx_), win_, P_);
     ++launches_;
   }
-  mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
-                                                             ck_every_, nck_, stddev, slots, cap_,
-                                                             cnt, ck_, tail_);
+  static const bool ws = [] {
+    const char* e = std::getenv("DSX_SEG_WS");
+    return !(e && e[0] == '0');
+  }();
+  if (ws) {
+    mt_segment_ws_kernel<<<dim3(P_, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
+                                                                    ck_every_, nck_, stddev, slots, cap_,
+                                                                    cnt, ck_, tail_);
+  } else {
+    mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
+                                                               ck_every_, nck_, stddev, slots, cap_,
+                                                               cnt, ck_, tail_);
+  }
   mt_finish_kernel<<<kl_, kThreads, 0, stream>>>(mt_dst, pnorm2, P_, gens_, ck_every_, nck_, (dim_ + 1) / 2,
                                                  stddev, slots, cap_, cnt, pfx, ck_, tail_, status);
   launches_ += 2;
