@@ -10,6 +10,8 @@
  *   dsc_profile_layers   — per-layer param_bytes / t_fp / t_bp of a profile.
  *   dsc_write_profile    — write_profile (profile.cpp:160) from measured
  *                          per-layer times (the CUDA-event profiler's output).
+ *   dsc_compare_modes / dsc_simulate_trace — the simulator's predictions,
+ *                          set beside the measured GPU timeline.
  */
 #ifndef DREAMDDP_DREAMSCHED_C_H_
 #define DREAMDDP_DREAMSCHED_C_H_
@@ -34,6 +36,13 @@ int dsc_write_profile(const char* path, int layers, const char* const* names,
                       const uint64_t* param_bytes, const double* t_fp, const double* t_bp,
                       const double* t_comm /* nullable: link model */, double bandwidth,
                       double latency);
+
+/* compare_modes (simulator.cpp:212-229): the four-mode report text. */
+int dsc_compare_modes(const char* profile_path, int period, long long iters, char* out, size_t cap);
+/* simulate_run (simulator.cpp:76-184) of one mode (plsgd: the DFS + fill
+ * schedule) -> trace-event JSON text and the makespan. */
+int dsc_simulate_trace(const char* profile_path, const char* mode, int period, long long iters,
+                       char* out, size_t cap, double* makespan);
 
 #ifdef __cplusplus
 }

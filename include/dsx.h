@@ -179,6 +179,15 @@ dsx_status dsx_sync_plan(int workers_total, int nranks, int* pairwise_exact);
  * the recurrence (no GPU needed). */
 dsx_status dsx_mt_jump_selftest(unsigned long long jump, int* ok);
 
+/* Measured timeline of the last instrumented single-GPU step with a
+ * throttled link: bp[2l], bp[2l+1] = start/end ms of layer l's local step,
+ * comm[2l], comm[2l+1] = start/end ms of its transfer on the FIFO link (-1
+ * if not synced), relative to the step start — simulate_run's events,
+ * measured (simulator.cpp:145-157).  With overlap disabled
+ * (dsx_lab_set_overlap(lab, 0)) transfers start after the whole local step
+ * (the ssgd mode). */
+dsx_status dsx_lab_last_timeline(dsx_lab* lab, float* bp, float* comm);
+
 /* Number of kernel launches issued by this lab since creation. */
 dsx_status dsx_lab_launch_count(dsx_lab* lab, uint64_t* out);
 

@@ -838,6 +838,8 @@ struct dsx_lab {
   int sync_algo = DSX_SYNC_PAIRWISE;
   double link_bw = 0.0, link_lat = 0.0;  // throttled link (bw <= 0: off)
   std::vector<cudaEvent_t> layer_ev;     // per-layer "BP done" events (throttled mode)
+  std::vector<cudaEvent_t> tl_ev;        // [4L] timeline: BP start/end, COMM start/end
+  std::vector<unsigned char> tl_mask;    // mask of the step the timeline belongs to
   bool p2p = false;            // NVLink peer-memory average available
   PeerPtrs peers{};            // every rank's exchange buffer, mapped here
   std::vector<void*> opened;   // IPC mappings to close
@@ -1078,22 +1080,50 @@ dsx_status step_single_throttled(dsx_lab* lab, double eta, const unsigned char* 
     for (size_t i = old; i < lab->layer_ev.size(); ++i)
       DSX_CUDA(cudaEventCreateWithFlags(&lab->layer_ev[i], cudaEventDisableTiming));
   }
+  // measured timeline (dsx_lab_last_timeline): timing events around every
+  // layer's local step and modelled transfer
+  const bool tl = lab->instrument;
+  if (tl && (int)lab->tl_ev.size() < 4 * lab->L) {
+    const size_t old = lab->tl_ev.size();
+    lab->tl_ev.resize(4 * lab->L);
+    for (size_t i = old; i < lab->tl_ev.size(); ++i) DSX_CUDA(cudaEventCreate(&lab->tl_ev[i]));
+  }
+  if (tl) lab->tl_mask.assign(mask, mask + lab->L + 1);
   // tile range of each layer
   int te = lab->ntiles;
   bool any = false;
+  std::vector<int> deferred;  // no-overlap (ssgd): transfers start after the whole local step
+  auto transfer = [&](int b) -> dsx_status {
+    if (tl) DSX_CUDA(cudaEventRecord(lab->tl_ev[4 * b + 2], lab->side));
+    const unsigned long long ns =
+        link_ns(lab, mask, (long long)lab->offs[b], (long long)(lab->offs[b + 1] - lab->offs[b]));
+    link_spin_kernel<<<1, 1, 0, lab->side>>>(ns);
+    ++lab->launches;
+    if (tl) DSX_CUDA(cudaEventRecord(lab->tl_ev[4 * b + 3], lab->side));
+    return DSX_OK;
+  };
   for (int b = lab->L - 1; b >= 0; --b) {
     int tb = te;
     while (tb > 0 && lab->h_tiles[tb - 1].block == b) --tb;
+    if (tl) DSX_CUDA(cudaEventRecord(lab->tl_ev[4 * b + 0], lab->stream));
     if (te > tb) launch_update<T>(lab, lab->stream, tb, te - tb, noise, lab->K > 1, bits, eta);
+    if (tl) DSX_CUDA(cudaEventRecord(lab->tl_ev[4 * b + 1], lab->stream));
     te = tb;
     if (!mask[b + 1]) continue;
-    DSX_CUDA(cudaEventRecord(lab->layer_ev[b], lab->stream));
     if (!any && lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[1], lab->stream));
-    DSX_CUDA(cudaStreamWaitEvent(lab->side, lab->layer_ev[b], 0));
-    const unsigned long long ns = link_ns(lab, mask, (long long)lab->offs[b], (long long)(lab->offs[b + 1] - lab->offs[b]));
-    link_spin_kernel<<<1, 1, 0, lab->side>>>(ns);
-    ++lab->launches;
     any = true;
+    if (!lab->overlap) {
+      deferred.push_back(b);
+      continue;
+    }
+    DSX_CUDA(cudaEventRecord(lab->layer_ev[b], lab->stream));
+    DSX_CUDA(cudaStreamWaitEvent(lab->side, lab->layer_ev[b], 0));
+    DSX_TRY(transfer(b));
+  }
+  if (!deferred.empty()) {
+    DSX_CUDA(cudaEventRecord(lab->ev_split, lab->stream));
+    DSX_CUDA(cudaStreamWaitEvent(lab->side, lab->ev_split, 0));
+    for (int b : deferred) DSX_TRY(transfer(b));
   }
   lab->has_ranges = any;
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
@@ -1504,6 +1534,8 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   delete lab->engine;
   for (void* p : lab->opened) cudaIpcCloseMemHandle(p);
   for (auto& ev : lab->layer_ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : lab->tl_ev)
     if (ev) cudaEventDestroy(ev);
   if (lab->bar) cudaFree(lab->bar);
   for (auto& ev : lab->ev_chunk)
@@ -2014,6 +2046,29 @@ dsx_status dsx_lab_event_elapsed(dsx_lab* lab, int a, int b, float* ms) {
 dsx_status dsx_lab_set_instrument(dsx_lab* lab, int enabled) {
   DSX_TRY(check_lab(lab));
   lab->instrument = enabled != 0;
+  return DSX_OK;
+}
+
+// Measured timeline of the last instrumented single-GPU throttled step: per
+// layer l (0-based), bp[2l..2l+1] = start/end ms of its local step on the
+// compute lane, comm[2l..2l+1] = start/end ms of its transfer on the link
+// lane (-1 when not synced), relative to the step start.  The same events
+// as simulate_run's timeline (simulator.cpp:145-157), measured.
+dsx_status dsx_lab_last_timeline(dsx_lab* lab, float* bp, float* comm) {
+  DSX_TRY(check_lab(lab));
+  if (!bp || !comm) return fail(DSX_ERR_ARGUMENT, "null timeline out");
+  if (!lab->instrument || (int)lab->tl_ev.size() < 4 * lab->L || (int)lab->tl_mask.size() != lab->L + 1)
+    return fail(DSX_ERR_STATE, "no instrumented throttled step recorded");
+  DSX_CUDA(cudaEventSynchronize(lab->iev[4]));
+  for (int b = 0; b < lab->L; ++b) {
+    DSX_CUDA(cudaEventElapsedTime(&bp[2 * b], lab->iev[0], lab->tl_ev[4 * b]));
+    DSX_CUDA(cudaEventElapsedTime(&bp[2 * b + 1], lab->iev[0], lab->tl_ev[4 * b + 1]));
+    comm[2 * b] = comm[2 * b + 1] = -1.0f;
+    if (lab->tl_mask[b + 1]) {
+      DSX_CUDA(cudaEventElapsedTime(&comm[2 * b], lab->iev[0], lab->tl_ev[4 * b + 2]));
+      DSX_CUDA(cudaEventElapsedTime(&comm[2 * b + 1], lab->iev[0], lab->tl_ev[4 * b + 3]));
+    }
+  }
   return DSX_OK;
 }
 

@@ -2,6 +2,7 @@
 #include "dreamsched_c.h"
 
 #include <cstring>
+#include <optional>
 #include <sstream>
 #include <string>
 
@@ -10,6 +11,7 @@
 #include "dreamsched/profile.hpp"
 #include "dreamsched/schedule.hpp"
 #include "dreamsched/scheduler.hpp"
+#include "dreamsched/simulator.hpp"
 
 namespace {
 thread_local std::string g_error;
@@ -82,6 +84,38 @@ int dsc_write_profile(const char* path, int layers, const char* const* names,
     p.link = {bandwidth, latency};
     p.validate();
     dreamsched::save_profile(p, path);
+  });
+}
+
+namespace {
+void copy_out(const std::string& t, char* out, size_t cap) {
+  if (t.size() + 1 > cap) throw dreamsched::ArgumentError("output buffer too small");
+  std::memcpy(out, t.c_str(), t.size() + 1);
+}
+}  // namespace
+
+int dsc_compare_modes(const char* profile_path, int period, long long iters, char* out, size_t cap) {
+  return guarded([&] {
+    const dreamsched::ModelProfile profile = dreamsched::load_profile(profile_path);
+    std::ostringstream text;
+    dreamsched::write_mode_report(dreamsched::compare_modes(profile, period, iters), text);
+    copy_out(text.str(), out, cap);
+  });
+}
+
+int dsc_simulate_trace(const char* profile_path, const char* mode, int period, long long iters,
+                       char* out, size_t cap, double* makespan) {
+  return guarded([&] {
+    const dreamsched::ModelProfile profile = dreamsched::load_profile(profile_path);
+    const dreamsched::Mode m = dreamsched::parse_mode(mode);
+    std::optional<dreamsched::Schedule> sched;
+    if (m == dreamsched::Mode::kPlsgd)
+      sched = dreamsched::bubble_fill(dreamsched::schedule_dfs(profile, period).best, profile);
+    const dreamsched::Timeline tl = dreamsched::simulate_run(profile, m, sched, iters, period);
+    std::ostringstream text;
+    dreamsched::write_trace(tl, text);
+    copy_out(text.str(), out, cap);
+    if (makespan) *makespan = tl.makespan;
   });
 }
 

@@ -1,0 +1,146 @@
+"""Four training modes on the GPU vs the simulator's prediction (SURVEY §8f
+#2 and #4).
+
+The loop the paper describes, executed for real on one B200:
+  1. the CUDA-event layer profiler measures every registered layer's local
+     step (dsx_lab_profile),
+  2. the measured times + an alpha-beta link become a "dreamsched-profile v1"
+     file (write_profile),
+  3. the bit-exact scheduler turns it into the plsgd schedule
+     (schedule_dfs + bubble_fill), and simulate_run predicts each mode,
+  4. each mode runs on the GPU with the throttled link — ssgd (all layers
+     every step, transfers after the local step), wfbp (all layers, each
+     transfer as soon as its layer is done), flsgd (everything every H steps,
+     after the local step), plsgd (the schedule, overlapped) — and the
+     measured per-layer timeline is exported in the simulator's trace schema.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import tempfile
+
+import numpy as np
+
+from . import native as N
+from .lab import Lab, LabDesc, _dsc, schedule_from_profile, sync_mask, write_profile
+
+MODES = ("ssgd", "wfbp", "flsgd", "plsgd")
+
+
+def simulate(profile_path: str, mode: str, period: int, iters: int):
+    """simulate_run of one mode -> (makespan seconds, trace JSON text)."""
+    N.load_dsx()
+    lib = _dsc()
+    buf = C.create_string_buffer(64 << 20)
+    mk = C.c_double()
+    rc = lib.dsc_simulate_trace(profile_path.encode(), mode.encode(), period, C.c_longlong(iters),
+                                buf, C.c_size_t(len(buf)), C.byref(mk))
+    if rc != 0:
+        raise RuntimeError(lib.dsc_last_error().decode())
+    return mk.value, buf.value.decode()
+
+
+def compare(profile_path: str, period: int, iters: int) -> str:
+    """compare_modes + write_mode_report text (the four predicted makespans,
+    S1, S2)."""
+    N.load_dsx()
+    lib = _dsc()
+    buf = C.create_string_buffer(1 << 20)
+    rc = lib.dsc_compare_modes(profile_path.encode(), period, C.c_longlong(iters), buf,
+                               C.c_size_t(len(buf)))
+    if rc != 0:
+        raise RuntimeError(lib.dsc_last_error().decode())
+    return buf.value.decode()
+
+
+def trace_json(mode: str, steps) -> str:
+    """Measured timeline -> the simulator's trace-event JSON schema
+    (simulator.cpp:186-203): complete events, microsecond ts/dur rounded half
+    to even, pid = mode, tid = lane."""
+    events = []
+    for it, (bp, comm) in enumerate(steps, start=1):
+        L = len(bp) // 2
+        for l in range(L):
+            events.append((bp[2 * l], bp[2 * l + 1], f"BP L{l + 1}", "compute", it, l + 1))
+            if comm[2 * l] >= 0:
+                events.append((comm[2 * l], comm[2 * l + 1], f"COMM L{l + 1}", "link", it, l + 1))
+    events.sort(key=lambda e: e[0])
+    recs = []
+    for s, e, name, lane, it, layer in events:
+        ts = int(round(s * 1e3))
+        recs.append({"name": name, "ph": "X", "ts": ts, "dur": int(round(e * 1e3)) - ts, "pid": mode,
+                     "tid": lane, "args": {"iteration": it, "layer": layer}})
+    return json.dumps(recs, indent=1) + "\n"
+
+
+def run(block_sizes, workers=4, period=4, bandwidth=None, latency=5e-6, comm_ratio=2.0, iters=None,
+        device=0, out_dir=None, reps=5):
+    """Returns {mode: {measured_s, predicted_s}} + speedups; writes traces to
+    out_dir when given.  bandwidth None: chosen so the full model's transfer
+    takes comm_ratio x the measured local step (a comm-bound setting, where
+    the modes differ)."""
+    L = len(block_sizes)
+    dim = int(sum(block_sizes))
+    iters = iters or 2 * period
+    lab = Lab(LabDesc(dim=dim, block_sizes=list(block_sizes), workers_total=workers, sigma=0.0,
+                      device=device))
+    lab.seed(1)
+    lab.fill(0.0)
+    t_bp, _ = lab.profile(reps=reps)
+    if bandwidth is None:
+        bandwidth = dim * 8 / max(comm_ratio * float(np.sum(t_bp)) - L * latency, 1e-6)
+    tmp = tempfile.mkdtemp(prefix="dreamddp_modes_")
+    prof = os.path.join(tmp, "measured.profile")
+    write_profile(prof, [int(s) * 8 for s in block_sizes], np.zeros(L), t_bp, None, bandwidth,
+                  latency)
+    sets, fills, objective, sched_text = schedule_from_profile(prof, period)
+    lab.set_link(bandwidth, latency)
+    lab.set_pipeline(False)
+    res = {"profile": prof, "schedule": sched_text, "layers": L, "workers": workers,
+           "period": period, "bandwidth_Bps": bandwidth, "latency_s": latency, "iters": iters,
+           "t_bp_total_s": float(np.sum(np.round(t_bp * 1e6) * 1e-6)), "modes": {}}
+    everything = np.ones(L + 1, dtype=np.uint8)
+    nothing = np.zeros(L + 1, dtype=np.uint8)
+    for mode in MODES:
+        predicted, sim_trace = simulate(prof, mode, period, iters)
+        lab.set_overlap(mode in ("wfbp", "plsgd"))
+        lab.set_instrument(True)
+        steps = []
+        total_ms = 0.0
+        for r in range(iters):
+            if mode in ("ssgd", "wfbp"):
+                mask = everything
+            elif mode == "flsgd":
+                mask = everything if (r + 1) % period == 0 or r + 1 == iters else nothing
+            else:
+                mask = sync_mask("partial", period, r, L, sets, fills)
+            lab.step(1e-3, mask)
+            step_ms = lab.last_step_times()[0]
+            total_ms += step_ms
+            bp = np.empty(2 * L, dtype=np.float32)
+            comm = np.empty(2 * L, dtype=np.float32)
+            N.call("dsx_lab_last_timeline", lab.h, bp.ctypes.data, comm.ctypes.data)
+            steps.append((bp, comm, step_ms))
+        # stack the per-step timelines back to back (each step starts after
+        # the previous one ended, like the simulator's iteration barrier)
+        offset, stacked = 0.0, []
+        for bp, comm, step_ms in steps:
+            stacked.append((bp + offset, np.where(comm >= 0, comm + offset, -1.0)))
+            offset += step_ms
+        res["modes"][mode] = {"measured_s": total_ms * 1e-3, "predicted_s": predicted}
+        if out_dir:
+            os.makedirs(out_dir, exist_ok=True)
+            with open(os.path.join(out_dir, f"trace_measured_{mode}.json"), "w") as f:
+                f.write(trace_json(mode, stacked))
+            with open(os.path.join(out_dir, f"trace_simulated_{mode}.json"), "w") as f:
+                f.write(sim_trace)
+    lab.set_link(0.0, 0.0)
+    lab.set_instrument(False)
+    lab.close()
+    m = res["modes"]
+    for kind in ("measured_s", "predicted_s"):
+        res["S1_" + kind.split("_")[0]] = m["wfbp"][kind] / m["plsgd"][kind]
+        res["S2_" + kind.split("_")[0]] = m["flsgd"][kind] / m["plsgd"][kind]
+    return res

@@ -71,6 +71,7 @@ _SIGS = {
     "dsx_lab_set_pipeline": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_lab_set_link": ([C.c_void_p, C.c_double, C.c_double], C.c_int),
     "dsx_lab_profile": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_lab_last_timeline": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "dsx_lab_event_record": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_lab_event_elapsed": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "dsx_lab_set_instrument": ([C.c_void_p, C.c_int], C.c_int),

@@ -77,6 +77,33 @@ def test_trace_json_byte_identical():
     assert out == G.read("trace_three_layer_plsgd.txt")
 
 
+def test_c_abi_simulator_matches_trace_fixture():
+    """dsc_simulate_trace + dsc_compare_modes (the C-ABI the four-mode GPU
+    runner uses) reproduce the reference's trace + mode report byte for byte."""
+    from paper_2502_11058_b200 import modes
+    prof = os.path.join(G.DATA, "three_layer.profile")
+    makespan, trace = modes.simulate(prof, "plsgd", 2, 2)
+    assert trace + modes.compare(prof, 2, 2) == G.read("trace_three_layer_plsgd.txt")
+    assert makespan == 9.0
+
+
+def test_measured_trace_schema_matches_simulator():
+    """The measured-timeline export uses the simulator's trace schema."""
+    import json
+
+    import numpy as np
+
+    from paper_2502_11058_b200 import modes
+    # one step, 2 layers: BP L2 [0,1] ms, BP L1 [1,2] ms, COMM L1 [2,4] ms
+    bp = np.array([1.0, 2.0, 0.0, 1.0], dtype=np.float32)
+    comm = np.array([2.0, 4.0, -1.0, -1.0], dtype=np.float32)
+    got = json.loads(modes.trace_json("plsgd", [(bp, comm)]))
+    sim = json.loads(modes.simulate(os.path.join(G.DATA, "three_layer.profile"), "plsgd", 2, 2)[1])
+    assert {tuple(sorted(e)) for e in got} == {tuple(sorted(e)) for e in sim if "layer" in e["args"]}
+    assert [(e["name"], e["ts"], e["dur"], e["tid"]) for e in got] == [
+        ("BP L2", 0, 1000, "compute"), ("BP L1", 1000, 1000, "compute"), ("COMM L1", 2000, 2000, "link")]
+
+
 @pytest.mark.skipif(not os.path.exists(REF_TOOL), reason="reference build absent")
 @pytest.mark.parametrize("seed,count,maxl", [(11, 600, 24), (12, 300, 61)])
 def test_sched_fuzz_live_against_reference(seed, count, maxl):
