@@ -547,9 +547,12 @@ mt_noise_chain_kernel(uint64_t* state, double* noise, long long ld, unsigned lon
 // ---------------------------------------------------------------------------
 // run_training helpers
 // ---------------------------------------------------------------------------
+// worker_mean (trainer.cpp:40-50) of coordinate i: pairwise over the local
+// rows, or (multi-rank) the cross-rank mean already reduced into gm.
 template <typename T, int KL>
 __device__ __forceinline__ double row_mean(const T* w, long long ld, long long i, int kl, int k_total,
-                                           const PairProg& prog) {
+                                           const PairProg& prog, const T* gm) {
+  if (gm) return to_d(gm[i]);
   if constexpr (KL > 0) {
     T v[KL];
 #pragma unroll
@@ -565,10 +568,10 @@ __device__ __forceinline__ double row_mean(const T* w, long long ld, long long i
 template <typename T, int KL>
 __global__ void mean_accumulate_kernel(const T* w, long long ld, int kl, int k_total,
                                        unsigned long long dim, double weight, double* what,
-                                       PairProg prog) {
+                                       PairProg prog, const T* gm) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)dim;
        i += (long long)gridDim.x * blockDim.x) {
-    const double m = row_mean<T, KL>(w, ld, i, kl, k_total, prog);
+    const double m = row_mean<T, KL>(w, ld, i, kl, k_total, prog, gm);
     what[i] = __dadd_rn(what[i], __dmul_rn(weight, m));
   }
 }
@@ -578,12 +581,12 @@ template <typename T, int KL>
 __global__ void __launch_bounds__(kThreads)
 log_kernel(const T* w, long long ld, int kl, int k_total, const Tile* tiles, int ntiles,
            QuadParams q, const double* what, double weight_total, double* part /*[3][ntiles]*/,
-           PairProg prog) {
+           PairProg prog, const T* gm) {
   const Tile t = tiles[blockIdx.x];
   double gsum = 0.0, fhat = 0.0, fmean = 0.0;
   for (int off = threadIdx.x; off < t.len; off += kThreads) {
     const long long i = t.start + off;
-    const double m = row_mean<T, KL>(w, ld, i, kl, k_total, prog);
+    const double m = row_mean<T, KL>(w, ld, i, kl, k_total, prog, gm);
     for (int k = 0; k < kl; ++k) {
       const double d = m - to_d(w[k * ld + i]);
       gsum += d * d;
@@ -853,6 +856,7 @@ struct dsx_lab {
   PairProg prog_ranks{};
   void* staging = nullptr;  // partial sums of synced range
   void* recv = nullptr;     // [nranks][slice]
+  void* gmean = nullptr;    // run_training logging: [nranks][dim] subtree sums -> mean in row 0
   size_t staging_elems = 0;
   int nsm = 148;
 };
@@ -939,27 +943,27 @@ void launch_update(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int n
 }
 
 template <typename T, int KL>
-void launch_rowwise_t(dsx_lab* lab, int what, double weight, double weight_total) {
+void launch_rowwise_t(dsx_lab* lab, int what, double weight, double weight_total, const T* gm) {
   const T* w = static_cast<const T*>(lab->w);
   if (what == 0) {
     mean_accumulate_kernel<T, KL><<<lab->nsm * 8, 256, 0, lab->stream>>>(
-        w, lab->ld, lab->kl, lab->K, lab->dim, weight, lab->what, lab->prog_local);
+        w, lab->ld, lab->kl, lab->K, lab->dim, weight, lab->what, lab->prog_local, gm);
   } else {
     log_kernel<T, KL><<<lab->ntiles, kThreads, 0, lab->stream>>>(
         w, lab->ld, lab->kl, lab->K, lab->tiles, lab->ntiles, lab->q, lab->what, weight_total,
-        lab->log_part, lab->prog_local);
+        lab->log_part, lab->prog_local, gm);
   }
   ++lab->launches;
 }
 
 template <typename T>
-void launch_rowwise(dsx_lab* lab, int what, double weight, double weight_total) {
+void launch_rowwise(dsx_lab* lab, int what, double weight, double weight_total, const T* gm) {
   switch (lab->kl) {
-    case 1: return launch_rowwise_t<T, 1>(lab, what, weight, weight_total);
-    case 2: return launch_rowwise_t<T, 2>(lab, what, weight, weight_total);
-    case 4: return launch_rowwise_t<T, 4>(lab, what, weight, weight_total);
-    case 8: return launch_rowwise_t<T, 8>(lab, what, weight, weight_total);
-    default: return launch_rowwise_t<T, 0>(lab, what, weight, weight_total);
+    case 1: return launch_rowwise_t<T, 1>(lab, what, weight, weight_total, gm);
+    case 2: return launch_rowwise_t<T, 2>(lab, what, weight, weight_total, gm);
+    case 4: return launch_rowwise_t<T, 4>(lab, what, weight, weight_total, gm);
+    case 8: return launch_rowwise_t<T, 8>(lab, what, weight, weight_total, gm);
+    default: return launch_rowwise_t<T, 0>(lab, what, weight, weight_total, gm);
   }
 }
 
@@ -1314,6 +1318,38 @@ dsx_status materialize(dsx_lab* lab) {
   return lab->dtype == DSX_F64 ? materialize_t<double>(lab) : materialize_t<float>(lab);
 }
 
+// run_training logging on several ranks: worker_mean over ALL K workers,
+// exact — each rank's local subtree sum is all-gathered and reduced in the
+// reference's pairwise rank order (the same tree the step's average uses).
+// Returns the [dim] mean (row 0 of the gather buffer), on lab->stream.
+template <typename T>
+dsx_status global_mean(dsx_lab* lab, const T** out) {
+  DSX_TRY(materialize(lab));
+  const long long D = (long long)lab->dim;
+  if (!lab->gmean) DSX_CUDA(cudaMalloc(&lab->gmean, sizeof(T) * D * lab->nranks));
+  T* all = static_cast<T*>(lab->gmean);
+  launch_partial<T>(lab, lab->stream, 0, D, all + lab->rank * D);
+  DSX_NCCL(ncclAllGather(all + lab->rank * D, all, (size_t)D, nccl_type(lab), lab->comm, lab->stream));
+  // in place: element j of row 0 is written after its thread read column j
+  rank_reduce_kernel<T><<<lab->nsm * 4, 256, 0, lab->stream>>>(all, D, lab->nranks, lab->K, all,
+                                                               lab->prog_ranks);
+  ++lab->launches;
+  DSX_CUDA(cudaGetLastError());
+  *out = all;
+  return DSX_OK;
+}
+
+// mean_accumulate (what = 0) / log (what = 1) over the (global) worker mean
+template <typename T>
+dsx_status rowwise(dsx_lab* lab, int what, double weight, double weight_total) {
+  const T* gm = nullptr;
+  if (lab->nranks > 1) DSX_TRY(global_mean<T>(lab, &gm));
+  else DSX_TRY(materialize(lab));
+  launch_rowwise<T>(lab, what, weight, weight_total, gm);
+  DSX_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
 void drop_stale(dsx_lab* lab) {  // every row is about to be overwritten
   lab->stale_bits = MaskBits{};
   lab->stale_any = false;
@@ -1542,7 +1578,7 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
     if (ev) cudaEventDestroy(ev);
   for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt, (void*)lab->grad_buf,
                   (void*)lab->what, (void*)lab->tiles, (void*)lab->norm_part, (void*)lab->norm,
-                  (void*)lab->maxnorm, (void*)lab->log_part, lab->staging, lab->recv})
+                  (void*)lab->maxnorm, (void*)lab->log_part, lab->staging, lab->recv, lab->gmean})
     if (p) cudaFree(p);
   for (auto& ev : lab->ev)
     if (ev) cudaEventDestroy(ev);
@@ -1794,29 +1830,30 @@ dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
   return DSX_OK;
 }
 
+// Multi-rank: every rank keeps the same w_hat (it accumulates the global
+// mean); the per-layer Gamma partials of the local rows are summed over
+// ranks, the objectives are identical on every rank.
 dsx_status dsx_lab_mean_accumulate(dsx_lab* lab, double weight) {
   DSX_TRY(check_lab(lab));
-  if (lab->nranks != 1) return fail(DSX_ERR_STATE, "run_training logging is single-rank");
   if (!lab->what) {
     DSX_CUDA(cudaMalloc(&lab->what, 8 * lab->dim));
     DSX_CUDA(cudaMemsetAsync(lab->what, 0, 8 * lab->dim, lab->stream));
   }
-  if (lab->dtype == DSX_F64) launch_rowwise<double>(lab, 0, weight, 0.0);
-  else launch_rowwise<float>(lab, 0, weight, 0.0);
-  DSX_CUDA(cudaGetLastError());
-  return DSX_OK;
+  return lab->dtype == DSX_F64 ? rowwise<double>(lab, 0, weight, 0.0) : rowwise<float>(lab, 0, weight, 0.0);
 }
 
 dsx_status dsx_lab_log(dsx_lab* lab, double weight_total, double* gamma_per_layer, double* out2) {
   DSX_TRY(check_lab(lab));
-  if (lab->nranks != 1) return fail(DSX_ERR_STATE, "run_training logging is single-rank");
   if (!gamma_per_layer || !out2) return fail(DSX_ERR_ARGUMENT, "null log outputs");
   if (!lab->what) {
     DSX_CUDA(cudaMalloc(&lab->what, 8 * lab->dim));
     DSX_CUDA(cudaMemsetAsync(lab->what, 0, 8 * lab->dim, lab->stream));
   }
-  if (lab->dtype == DSX_F64) launch_rowwise<double>(lab, 1, 0.0, weight_total);
-  else launch_rowwise<float>(lab, 1, 0.0, weight_total);
+  DSX_TRY(lab->dtype == DSX_F64 ? rowwise<double>(lab, 1, 0.0, weight_total)
+                                : rowwise<float>(lab, 1, 0.0, weight_total));
+  if (lab->nranks > 1)
+    DSX_NCCL(ncclAllReduce(lab->log_part, lab->log_part, (size_t)lab->ntiles, ncclFloat64, ncclSum, lab->comm,
+                           lab->stream));
   std::vector<double> part(3 * (size_t)lab->ntiles);
   DSX_CUDA(cudaMemcpyAsync(part.data(), lab->log_part, 8 * part.size(), cudaMemcpyDeviceToHost, lab->stream));
   DSX_CUDA(cudaStreamSynchronize(lab->stream));

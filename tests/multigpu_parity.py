@@ -74,6 +74,53 @@ def run(algo, overlap, dim=200003, L=12, K=8, H=4, sigma=1.0, seed=5, steps=7):
             "rng_exact": rng_ok}
 
 
+def _train_log(lab, L, H, sets, iters, stride):
+    """run_training's loop (trainer.cpp:286-301) over the lab API: w_hat
+    accumulation before every step, Gamma^l / f(w_hat) / f(mean) rows."""
+    g, fh, fm = lab.log(0.0)
+    rows, weight_total = [np.concatenate([g, [fh, fm]])], 0.0
+    for r in range(iters):
+        p_r = (3.0 + r) * (3.0 + r)
+        lab.mean_accumulate(p_r)
+        weight_total += p_r
+        lab.step(O.learning_rate(r, 1.0, 2.0, H), sync_mask("partial", H, r, L, sets))
+        if (r + 1) % stride == 0 or r + 1 == iters:
+            g, fh, fm = lab.log(weight_total)
+            rows.append(np.concatenate([g, [fh, fm]]))
+    return np.array(rows)
+
+
+def run_train_log(K=8, dim=100003, L=10, H=3, sigma=1.0, seed=9, iters=7, stride=2):
+    """Multi-rank run_training logging vs the same loop on
+    one GPU: the worker mean is exact on both, the Gamma partials are summed
+    in a different order (<= 1e-10 relative)."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    kl = K // world
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    _, sizes = O.make_quadratic(dim, L)
+    sets = O.enp(L, H)
+    lab = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, workers_local=kl,
+                      worker_begin=rank * kl, sigma=sigma, device=dev))
+    uid = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    lab.comm_init(uid[0], world, rank)
+    lab.seed(seed)
+    lab.fill(0.0)
+    multi = _train_log(lab, L, H, sets, iters, stride)
+    lab.close()
+    if rank != 0:
+        return None
+    one = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, sigma=sigma, device=dev))
+    one.seed(seed)
+    one.fill(0.0)
+    single = _train_log(one, L, H, sets, iters, stride)
+    one.close()
+    err = float(np.max(np.abs(multi - single) / np.maximum(np.abs(single), 1e-300)))
+    return {"case": "run_training_log", "K": K, "rows": int(single.shape[0]),
+            "max_rel_err_vs_single_gpu": err,
+            "pass": err <= 1e-10 and bool(np.all(single[:, -2:] > 0)) and bool(np.any(single[1:, :L] > 0))}
+
+
 def main():
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     dist.init_process_group("gloo")
@@ -87,6 +134,7 @@ def main():
         if res is not None:
             res["K"] = K
             results.append(res)
+    logs = [run_train_log(K=8), run_train_log(K=world)]
     ok = True
     if dist.get_rank() == 0:
         world = dist.get_world_size()
@@ -95,6 +143,9 @@ def main():
             res["pass"] = (res["rng_exact"] and res["max_rel_err_vs_oracle"] <= 1e-12 and
                            (res["bit_exact_vs_single_gpu"] if exact_required
                             else res["max_rel_err_vs_single_gpu"] <= 1e-12))
+            ok &= res["pass"]
+        for res in logs:
+            results.append(res)
             ok &= res["pass"]
         print(json.dumps({"world": world, "results": results, "pass": ok}), flush=True)
     okt = [ok]

@@ -13,14 +13,19 @@ pytestmark = pytest.mark.gpu
 
 def test_four_modes_measured_vs_simulated(tmp_path):
     from paper_2502_11058_b200 import modes
-    L, dim, H = 12, 3_000_000, 4
+    L, dim, H = 12, 12_000_000, 4
     _, sizes = O.make_quadratic(dim, L)
-    res = modes.run(list(sizes), workers=4, period=H, comm_ratio=2.0, iters=2 * H,
+    iters = 2 * H
+    res = modes.run(list(sizes), workers=4, period=H, comm_ratio=2.0, iters=iters,
                     out_dir=str(tmp_path))
     m = res["modes"]
-    # the measured makespans follow the simulator's (same profile, same link)
+    # the measured makespans follow the simulator's (same profile, same link);
+    # the simulator does not model the per-layer launch gaps (a few us each)
     for mode in modes.MODES:
-        assert m[mode]["measured_s"] == pytest.approx(m[mode]["predicted_s"], rel=0.35), (mode, res)
+        assert m[mode]["measured_s"] == pytest.approx(m[mode]["predicted_s"], rel=0.3,
+                                                      abs=iters * L * 15e-6), (mode, res)
+    assert res["S1_measured"] == pytest.approx(res["S1_predicted"], rel=0.3)
+    assert res["S2_measured"] == pytest.approx(res["S2_predicted"], rel=0.3)
     # and its ordering: plsgd beats wfbp and flsgd in a comm-bound setting
     assert res["S1_predicted"] > 1.0 and res["S2_predicted"] > 1.0
     assert m["plsgd"]["measured_s"] < m["wfbp"]["measured_s"]
