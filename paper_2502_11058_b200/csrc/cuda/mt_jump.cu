@@ -779,6 +779,236 @@ mt_segment_ws_kernel(const uint64_t* win_state, const uint64_t* win, const int* 
   }
 }
 
+// Segment kernel v5 (the default).  Same contract as mt_segment_ws_kernel,
+// rebalanced after ncu showed consumers stalled on the single twister warp
+// (~12 % of samples) and on the uneven per-round transform split (~8 %):
+//  * kProdWarps twister warps split every generation's two phases (a 64-
+//    thread named barrier between phases) — half the producer latency;
+//  * interior rounds read the pair coordinates straight from the ring (the
+//    ring half is R*312 contiguous words, so output n of the round is word
+//    n), no staging array and no barrier between temper and accept;
+//  * every consumer warp scans the 20 per-warp accepted counts itself (one
+//    barrier instead of scan + two barriers);
+//  * accepted pairs go to a shared FIFO and are transformed in full chunks
+//    of 320 (or 640 with 2-way ILP), the remainder carried to the next round,
+//    so no warp idles at the end of a round with a half-empty transform.
+constexpr int kProdWarps = 2;
+constexpr int kProdThreads = 32 * kProdWarps;
+constexpr int kWs2Threads = kProdThreads + kThreads;
+constexpr int kBarProd = 6;
+constexpr int kQCap = 1024;  // FIFO capacity: < 320 carried + 624 new per round
+
+__global__ void __launch_bounds__(kWs2Threads, 2)
+mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
+                      int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
+                      double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
+                      uint64_t* tail) {
+  constexpr int R = kWsR;
+  constexpr int kPairSlots = 2;  // 624 pairs of an interior round over 320 threads
+  constexpr int kCounts = kPairSlots * (kThreads / 32);
+  static_assert(R * kMtN / 2 <= kPairSlots * kThreads, "pair slots");
+  static_assert(kCounts <= 32, "scan fits one warp");
+  __shared__ __align__(16) uint64_t ring[2][R * kMtN];
+  __shared__ __align__(16) double v[R * kMtN + 2];  // boundary rounds only (and the boot state)
+  __shared__ __align__(16) double2 fifo[kQCap];
+  __shared__ int wcnt[2][kCounts];
+  __shared__ double s_half[2];
+  __shared__ int s_p;
+  const int s = blockIdx.x, w = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* boot = reinterpret_cast<uint64_t*>(v);
+
+  if (warp < kProdWarps) {
+    // ---------------- producers: generations into the ring ----------------
+    const int pt = threadIdx.x;
+    int p;
+    if (s == 0) {
+      const uint64_t* st = win_state + (long long)w * (kMtN + 1);
+      for (int k = pt; k < kMtN; k += kProdThreads) boot[k] = st[k];
+      p = (int)st[kMtN];
+      named_sync(kBarProd, kProdThreads);
+      if (p >= kMtN) {
+        for (int k = pt; k < kMtM; k += kProdThreads) ring[0][k] = mt_next_word(boot[k], boot[k + 1], boot[k + kMtM]);
+        named_sync(kBarProd, kProdThreads);
+        for (int k = kMtM + pt; k < kMtN; k += kProdThreads)
+          ring[0][k] = mt_next_word(boot[k], (k + 1 < kMtN) ? boot[k + 1] : ring[0][0], ring[0][k - kMtM]);
+        p = 0;
+      } else {
+        for (int k = pt; k < kMtN; k += kProdThreads) ring[0][k] = boot[k];
+      }
+      if (pt == 0) pnorm_out[w] = p;
+    } else {
+      for (int k = pt; k < kMtN; k += kProdThreads) ring[0][k] = win[((long long)w * P + s) * kMtN + k];
+      p = pnorm_in[w];
+    }
+    if (pt == 0) s_p = p;
+    named_sync(kBarProd, kProdThreads);
+    const int ngen = gens + (p > 0 ? 1 : 0);
+    const int rounds = (ngen + R - 1) / R;
+    for (int k = 0; k < rounds; ++k) {
+      const int h = k & 1;
+      if (k >= 2) named_sync(kBarEmpty + h, kWs2Threads);  // consumers done with round k-2
+      const int rg = min(R, ngen - k * R);
+      for (int g = 0; g < rg; ++g) {
+        if (k == 0 && g == 0) continue;  // gen 0 already in place
+        const uint64_t* src = g ? &ring[h][(g - 1) * kMtN] : &ring[1 - h][(R - 1) * kMtN];
+        uint64_t* dst = &ring[h][g * kMtN];
+        for (int i = pt; i < kMtM; i += kProdThreads) dst[i] = mt_next_word(src[i], src[i + 1], src[i + kMtM]);
+        named_sync(kBarProd, kProdThreads);
+        for (int i = kMtM + pt; i < kMtN; i += kProdThreads)
+          dst[i] = mt_next_word(src[i], (i + 1 < kMtN) ? src[i + 1] : dst[0], dst[i - kMtM]);
+        named_sync(kBarProd, kProdThreads);
+      }
+      __threadfence_block();
+      named_arrive(kBarFull + h, kWs2Threads);
+    }
+    return;
+  }
+
+  // ---------------- consumers (320 threads) ----------------
+  const int tid = threadIdx.x - kProdThreads, cw = tid >> 5;
+  if (tid == 0) s_half[0] = 0.0;
+  named_sync(kBarFull + 0, kWs2Threads);  // round 0 ready (also publishes s_p)
+  const int p = s_p;
+  const int ngen = gens + (p > 0 ? 1 : 0);
+  const int rounds = (ngen + R - 1) / R;
+  double* out = slots + ((long long)w * (P + 1) + s) * cap;
+  uint64_t* ckw = ck + ((long long)w * P + s) * (long long)nck * kCkWords;
+  int hh = 0;                      // a carried half pair enters this round
+  unsigned long long local = 0;    // accepted pairs pushed to the FIFO
+  unsigned long long head = 0;     // accepted pairs transformed and stored
+  auto transform = [&](unsigned long long g) {
+    const double2 xy = fifo[g % kQCap];
+    double r2;
+    mt_polar_accept(xy.x, xy.y, &r2);
+    const double m = mt_polar_mult(r2);
+    double2 o;
+    o.x = mt_scale(xy.y, m, stddev);
+    o.y = mt_scale(xy.x, m, stddev);
+    *reinterpret_cast<double2*>(out + 2 * g) = o;
+  };
+  for (int k = 0; k < rounds; ++k) {
+    const int h = k & 1;
+    const int q = k * R;
+    if (k) named_sync(kBarFull + h, kWs2Threads);
+    const int rg = min(R, ngen - q);
+    const double half_in = s_half[h];
+    if (q % ck_every == 0) {
+      uint64_t* c = ckw + (long long)(q / ck_every) * kCkWords;
+      if (tid < kMtN) c[tid] = ring[h][tid];
+      if (tid == 0) {
+        c[kMtN] = (uint64_t)hh;
+        c[kMtN + 1] = (uint64_t)__double_as_longlong(half_in);
+        c[kMtN + 2] = local;
+      }
+    }
+    if (k == rounds - 1) {  // end state for an overflow continuation
+      uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
+      if (tid < kMtN) c[tid] = ring[h][(rg - 1) * kMtN + tid];
+    }
+    bool acc[kPairSlots];
+    double px[kPairSlots], py[kPairSlots];
+    int npairs, hh_next;
+    if (q > 0 && q + R <= gens) {
+      // interior: R complete generations; round output n is ring word n
+      const uint64_t* rw = ring[h];
+      npairs = (hh + R * kMtN) >> 1;
+      hh_next = (hh + R * kMtN) & 1;
+#pragma unroll
+      for (int u = 0; u < kPairSlots; ++u) {
+        const int a = tid + u * kThreads;
+        acc[u] = false;
+        px[u] = py[u] = 0.0;
+        if (a < npairs) {
+          const int n0 = 2 * a - hh;
+          px[u] = n0 < 0 ? half_in : mt_polar_coord(mt_temper(rw[n0]));
+          py[u] = mt_polar_coord(mt_temper(rw[n0 + 1]));
+          double r2;
+          acc[u] = mt_polar_accept(px[u], py[u], &r2);
+        }
+      }
+      if (hh_next && tid == kThreads - 1) s_half[1 - h] = mt_polar_coord(mt_temper(rw[R * kMtN - 1]));
+      named_arrive(kBarEmpty + h, kWs2Threads);  // done reading ring half h
+    } else {
+      // boundary round (the segment's first / last): partial generations
+      int nvals = hh;
+#pragma unroll
+      for (int g = 0; g < R; ++g) {
+        if (g < rg) {
+          const int gen = q + g;
+          const int lo = gen == 0 ? p : 0;
+          const int hi = (gen == gens) ? p : kMtN;
+          if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(ring[h][g * kMtN + tid]));
+          nvals += hi - lo;
+        }
+      }
+      if (tid == 0 && hh) v[0] = half_in;
+      named_arrive(kBarEmpty + h, kWs2Threads);
+      named_sync(kBarCons, kThreads);  // v complete
+      npairs = nvals >> 1;
+      hh_next = nvals & 1;
+#pragma unroll
+      for (int u = 0; u < kPairSlots; ++u) {
+        const int a = tid + u * kThreads;
+        acc[u] = false;
+        px[u] = py[u] = 0.0;
+        if (a < npairs) {
+          px[u] = v[2 * a];
+          py[u] = v[2 * a + 1];
+          double r2;
+          acc[u] = mt_polar_accept(px[u], py[u], &r2);
+        }
+      }
+      if (hh_next && tid == 0) s_half[1 - h] = v[nvals - 1];
+    }
+    // accepted counts per (slot, warp), slot-major = pair order
+    int before[kPairSlots];
+#pragma unroll
+    for (int u = 0; u < kPairSlots; ++u) {
+      const unsigned bal = __ballot_sync(0xffffffffu, acc[u]);
+      if (lane == 0) wcnt[h][u * (kThreads / 32) + cw] = __popc(bal);
+      before[u] = __popc(bal & ((1u << lane) - 1u));
+    }
+    named_sync(kBarCons, kThreads);
+    // every warp scans the counts itself
+    const int c = lane < kCounts ? wcnt[h][lane] : 0;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, kCounts - 1);
+#pragma unroll
+    for (int u = 0; u < kPairSlots; ++u) {
+      const int idx = u * (kThreads / 32) + cw;
+      const int excl = __shfl_sync(0xffffffffu, incl - c, idx);
+      if (acc[u]) fifo[(local + (unsigned long long)(excl + before[u])) % kQCap] = make_double2(px[u], py[u]);
+    }
+    local += (unsigned long long)total;
+    hh = hh_next;
+    named_sync(kBarCons, kThreads);  // FIFO entries visible
+    while (local - head >= 2 * kThreads) {
+      const unsigned long long g = head + (unsigned long long)tid;
+      transform(g);
+      transform(g + kThreads);
+      head += 2 * kThreads;
+    }
+    if (local - head >= kThreads) {
+      transform(head + (unsigned long long)tid);
+      head += kThreads;
+    }
+  }
+  for (unsigned long long g = head + (unsigned long long)tid; g < local; g += kThreads) transform(g);
+  if (tid == 0) {
+    cnt[(long long)w * P + s] = local;
+    uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
+    c[kMtN] = (uint64_t)hh;
+    c[kMtN + 1] = (uint64_t)__double_as_longlong(s_half[rounds & 1]);
+    c[kMtN + 2] = local;
+  }
+}
+
 // Walks generations from a checkpoint until the target pair; writes the new
 // rng state.  Also serves the (rare) overflow continuation.
 __global__ void __launch_bounds__(kThreads)
@@ -986,11 +1216,16 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, double 
         ybuf_, reinterpret_cast<const uint32_t*>(jidx_), win_, P_);
     ++launches_;
   }
-  static const bool ws = [] {
+  // DSX_SEG_WS: 2 (default) v5 kernel, 1 single-twister warp-specialized, 0 v3
+  static const int ws = [] {
     const char* e = std::getenv("DSX_SEG_WS");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 2;
   }();
-  if (ws) {
+  if (ws == 2) {
+    mt_segment_ws2_kernel<<<dim3(P_, kl_), kWs2Threads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
+                                                                     ck_every_, nck_, stddev, slots, cap_,
+                                                                     cnt, ck_, tail_);
+  } else if (ws == 1) {
     mt_segment_ws_kernel<<<dim3(P_, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
                                                                     ck_every_, nck_, stddev, slots, cap_,
                                                                     cnt, ck_, tail_);
