@@ -188,6 +188,8 @@ def workload_config(args, world, dim):
 # ------------------------------------------------------------------ our arm ---
 
 def our_arm(args, world, rank, local_rank, dist):
+    import ctypes as C
+
     import numpy as np
 
     from paper_2502_11058_b200 import native as N
@@ -313,13 +315,15 @@ def our_arm(args, world, rank, local_rank, dist):
         wp, rp = host.data_ptr(), host_rng.data_ptr()
         N.call("dsx_lab_get_state", lab.h, wp, rp)
         lab.sync()
+        # dsx_lab_step_host: plsgd_step on host rows, transfers pipelined
+        # against the update (chunk c+1 in, chunk c updated, chunk c-1 out)
+        rows = (C.c_void_p * kl)(*[wp + k * dim * 8 for k in range(kl)])
+        masks_c = [np.ascontiguousarray(m, dtype=np.uint8) for m in masks]
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            N.call("dsx_lab_set_state", lab.h, wp, rp)
-            lab.step(learning_rate(r, H), masks[r % H])
+            N.call("dsx_lab_step_host", lab.h, learning_rate(r, H), masks_c[r % H].ctypes.data, rows, rp)
             r += 1
-            N.call("dsx_lab_get_state", lab.h, wp, rp)
         lab.sync()
         el = time.perf_counter() - t0
         if dist is not None:
@@ -330,7 +334,7 @@ def our_arm(args, world, rank, local_rank, dist):
         e2e = {"value": args.e2e_steps / el, "unit": "iterations/s",
                "h2d_bytes_per_step": kl * dim * 8 + rng_bytes,
                "d2h_bytes_per_step": kl * dim * 8 + rng_bytes,
-               "path": "dsx C-ABI with host worker buffers (plsgd_step semantics)"}
+               "path": "dsx_lab_step_host: host worker rows + rng states in/out every step, chunked H2D/update/D2H overlap"}
 
     if rank != 0:
         lab.close()

@@ -97,6 +97,23 @@ dsx_status dsx_lab_get_all_params(dsx_lab* lab, double* w);
 dsx_status dsx_lab_set_state(dsx_lab* lab, const double* w, const uint64_t* rng);
 dsx_status dsx_lab_get_state(dsx_lab* lab, double* w, uint64_t* rng);
 
+/* One plsgd_step (trainer.cpp:187-235) on HOST-resident worker state:
+ * rows[k] is worker k's dim parameters (read, then overwritten with the
+ * result), rng[workers_local][313] the engine states in/out.  Replaces
+ * set_state + step + get_state: the parameter transfers are split into
+ * coordinate chunks and pipelined — chunk c+1 host->device, chunk c's fused
+ * update and chunk c-1 device->host run concurrently (two copy engines), so
+ * the call costs about one direction's PCIe time instead of both.  Rows in
+ * pinned memory (cudaHostAlloc / dsx_host_alloc) get the overlap; pageable
+ * rows are still correct.  Single rank, fp64; other labs take the
+ * set_state/step/get_state path inside the call.  Returns with every copy
+ * complete. */
+dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask, double* const* rows,
+                             uint64_t* rng);
+/* Pinned host memory for rows / rng buffers (cudaHostAlloc, portable). */
+dsx_status dsx_host_alloc(size_t bytes, void** out);
+dsx_status dsx_host_free(void* p);
+
 /* std::mt19937_64 state: 312 words and the cursor p (libstdc++ _M_x/_M_p). */
 dsx_status dsx_lab_set_rng(dsx_lab* lab, int local, const uint64_t* x312, uint64_t p);
 dsx_status dsx_lab_get_rng(dsx_lab* lab, int local, uint64_t* x312, uint64_t* p);

@@ -857,6 +857,10 @@ struct dsx_lab {
   void* staging = nullptr;  // partial sums of synced range
   void* recv = nullptr;     // [nranks][slice]
   void* gmean = nullptr;    // run_training logging: [nranks][dim] subtree sums -> mean in row 0
+  // host-state step (dsx_lab_step_host): copy-engine streams + per-chunk events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  int host_chunks = 24;
   size_t staging_elems = 0;
   int nsm = 148;
 };
@@ -1584,6 +1588,11 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : lab->iev)
     if (ev) cudaEventDestroy(ev);
+  for (auto* v : {&lab->ev_in, &lab->ev_out})
+    for (auto& ev : *v)
+      if (ev) cudaEventDestroy(ev);
+  if (lab->h2d) cudaStreamDestroy(lab->h2d);
+  if (lab->d2h) cudaStreamDestroy(lab->d2h);
   if (lab->ev_split) cudaEventDestroy(lab->ev_split);
   if (lab->ev_synced) cudaEventDestroy(lab->ev_synced);
   if (lab->stream) cudaStreamDestroy(lab->stream);
@@ -1687,6 +1696,122 @@ dsx_status dsx_lab_get_state(dsx_lab* lab, double* w, uint64_t* rng) {
                              cudaMemcpyDeviceToHost, lab->stream));
   }
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask, double* const* rows,
+                             uint64_t* rng) {
+  DSX_TRY(check_lab(lab));
+  if (!mask || !rows || !rng) return fail(DSX_ERR_ARGUMENT, "null step_host argument");
+  for (int k = 0; k < lab->kl; ++k) {
+    if (!rows[k]) return fail(DSX_ERR_ARGUMENT, "null worker row");
+    if (rng[(long long)k * (kMtN + 1) + kMtN] > kMtN) return fail(DSX_ERR_ARGUMENT, "bad rng cursor");
+  }
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  drop_stale(lab);
+  DSX_TRY(invalidate_prefetch(lab));
+  const long long D = (long long)lab->dim;
+  if (lab->dtype != DSX_F64 || lab->nranks != 1 || lab->link_bw > 0.0 || lab->use_chain) {
+    // the staged path: whole rows in, one step, whole rows out
+    for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, rows[k]));
+    DSX_CUDA(cudaMemcpy(mt_state(lab, lab->mt_commit), rng, 8ull * (kMtN + 1) * lab->kl, cudaMemcpyHostToDevice));
+    const bool pl = lab->pipeline;
+    lab->pipeline = false;
+    const dsx_status st = dsx_lab_step(lab, eta, mask);
+    lab->pipeline = pl;
+    DSX_TRY(st);
+    for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, rows[k]));
+    return dsx_lab_get_state(lab, nullptr, rng);
+  }
+  if (!lab->h2d) {
+    DSX_CUDA(cudaStreamCreateWithFlags(&lab->h2d, cudaStreamNonBlocking));
+    DSX_CUDA(cudaStreamCreateWithFlags(&lab->d2h, cudaStreamNonBlocking));
+  }
+  if (const char* c = std::getenv("DSX_HOST_CHUNKS")) lab->host_chunks = std::max(1, std::atoi(c));
+  const int C = std::max(1, std::min(lab->host_chunks, lab->ntiles));
+  while ((int)lab->ev_in.size() < C) {
+    cudaEvent_t a, b;
+    DSX_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    DSX_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    lab->ev_in.push_back(a);
+    lab->ev_out.push_back(b);
+  }
+  // engine states first (small), then the noise engine overlaps the first
+  // parameter chunks' transfer
+  DSX_CUDA(cudaMemcpy(mt_state(lab, lab->mt_commit), rng, 8ull * (kMtN + 1) * lab->kl, cudaMemcpyHostToDevice));
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[0], lab->stream));
+  int noise = 0;
+  DSX_TRY(run_noise(lab, &noise));
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[5], lab->stream));
+  MaskBits bits{};
+  for (int b = 0; b < lab->L; ++b)
+    if (mask[b + 1]) bits.w[b >> 5] |= 1u << (b & 31);
+  double* w = static_cast<double*>(lab->w);
+  // rows at a constant host pitch (one [kl][pitch] buffer) move as one 2D
+  // copy per chunk and direction
+  long long pitch = lab->kl > 1 ? (long long)(rows[1] - rows[0]) : (long long)D;
+  for (int k = 1; k < lab->kl && pitch >= D; ++k)
+    if (rows[k] - rows[k - 1] != pitch) pitch = 0;
+  const bool strided = pitch >= D;
+  // (every stream touching the rows was drained above)
+  for (int c = 0; c < C; ++c) {
+    const int tb = (int)((long long)lab->ntiles * c / C), te = (int)((long long)lab->ntiles * (c + 1) / C);
+    if (te <= tb) continue;
+    const long long lo = lab->h_tiles[tb].start;
+    const long long hi = te < lab->ntiles ? lab->h_tiles[te].start : D;
+    if (strided) {
+      DSX_CUDA(cudaMemcpy2DAsync(w + lo, 8 * lab->ld, rows[0] + lo, 8 * pitch, 8ull * (hi - lo), lab->kl,
+                                 cudaMemcpyHostToDevice, lab->h2d));
+    } else {
+      for (int k = 0; k < lab->kl; ++k)
+        DSX_CUDA(cudaMemcpyAsync(w + (long long)k * lab->ld + lo, rows[k] + lo, 8ull * (hi - lo),
+                                 cudaMemcpyHostToDevice, lab->h2d));
+    }
+    DSX_CUDA(cudaEventRecord(lab->ev_in[c], lab->h2d));
+    DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_in[c], 0));
+    launch_update<double>(lab, lab->stream, tb, te - tb, noise, lab->K > 1, bits, eta);
+    DSX_CUDA(cudaEventRecord(lab->ev_out[c], lab->stream));
+    DSX_CUDA(cudaStreamWaitEvent(lab->d2h, lab->ev_out[c], 0));
+    if (strided) {
+      DSX_CUDA(cudaMemcpy2DAsync(rows[0] + lo, 8 * pitch, w + lo, 8 * lab->ld, 8ull * (hi - lo), lab->kl,
+                                 cudaMemcpyDeviceToHost, lab->d2h));
+    } else {
+      for (int k = 0; k < lab->kl; ++k)
+        DSX_CUDA(cudaMemcpyAsync(rows[k] + lo, w + (long long)k * lab->ld + lo, 8ull * (hi - lo),
+                                 cudaMemcpyDeviceToHost, lab->d2h));
+    }
+  }
+  lab->has_ranges = false;
+  lab->synced_last = false;
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
+  DSX_CUDA(cudaMemsetAsync(lab->maxnorm, 0, 8, lab->stream));
+  norm_finalize_kernel<<<lab->kl, 1024, 0, lab->stream>>>(
+      lab->norm_part, lab->ntiles, lab->norm, reinterpret_cast<unsigned long long*>(lab->maxnorm));
+  ++lab->launches;
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[4], lab->stream));
+  const bool pl = lab->pipeline;
+  lab->pipeline = false;  // the next call brings its own rng state
+  const dsx_status st = after_update(lab, noise);
+  lab->pipeline = pl;
+  DSX_TRY(st);
+  DSX_CUDA(cudaMemcpyAsync(rng, mt_state(lab, lab->mt_commit), 8ull * (kMtN + 1) * lab->kl,
+                           cudaMemcpyDeviceToHost, lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->d2h));
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
+dsx_status dsx_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(DSX_ERR_ARGUMENT, "null out");
+  *out = nullptr;
+  DSX_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+  return DSX_OK;
+}
+
+dsx_status dsx_host_free(void* p) {
+  if (p) DSX_CUDA(cudaFreeHost(p));
   return DSX_OK;
 }
 

@@ -226,3 +226,46 @@ def test_parallel_noise_engine_segments_exact(dim, K, advance):
     for k in range(K):
         assert lab.rng_text(k) == O.mt_state_text(rngs[k])
     lab.close()
+
+
+@pytest.mark.parametrize("pinned,chunks", [(True, None), (False, None), (True, "1"), (True, "7")])
+def test_step_host_matches_device_resident_steps(pinned, chunks, monkeypatch):
+    """dsx_lab_step_host (chunked, overlapped host round trip) == set_state +
+    step + get_state, bit for bit, including the rng states."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2502_11058_b200 import Lab, LabDesc
+    from paper_2502_11058_b200 import native as N
+    from paper_2502_11058_b200.lab import sync_mask
+    if chunks:
+        monkeypatch.setenv("DSX_HOST_CHUNKS", chunks)
+    K, dim, L, H, seed = 8, 300007, 11, 4, 21
+    curv, sizes = O.make_quadratic(dim, L)
+    sets = O.enp(L, H)
+    a = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, sigma=1.0))
+    b = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, sigma=1.0))
+    for lab in (a, b):
+        lab.set_pipeline(False)
+        lab.seed(seed)
+    w0 = np.random.default_rng(3).normal(size=(K, dim))
+    host = torch.from_numpy(w0.copy())
+    if pinned:
+        host = host.pin_memory()
+    rng = torch.zeros((K, 313), dtype=torch.int64)
+    N.call("dsx_lab_get_state", a.h, None, rng.data_ptr())
+    rows = (C.c_void_p * K)(*[host.data_ptr() + k * dim * 8 for k in range(K)])
+    b.set_params(w0)
+    for r in range(2 * H):
+        eta = O.learning_rate(r, 1.0, 2.0, H)
+        mask = np.ascontiguousarray(sync_mask("partial", H, r, L, sets))
+        N.call("dsx_lab_step_host", a.h, eta, mask.ctypes.data, rows, rng.data_ptr())
+        b.step(eta, mask)
+        assert a.max_grad_norm_sq() == b.max_grad_norm_sq()
+    assert np.array_equal(host.numpy(), b.get_params())
+    want = torch.zeros((K, 313), dtype=torch.int64)
+    N.call("dsx_lab_get_state", b.h, None, want.data_ptr())
+    assert torch.equal(rng, want)
+    a.close()
+    b.close()
