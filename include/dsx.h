@@ -184,6 +184,10 @@ dsx_status dsx_lab_event_elapsed(dsx_lab* lab, int from_slot, int to_slot, float
  * Enabled by dsx_lab_set_instrument(lab, 1). */
 dsx_status dsx_lab_set_instrument(dsx_lab* lab, int enabled);
 dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out5);
+/* Noise engine alone: device milliseconds of one run generating `steps`
+ * steps (1 or the lab's batch length, *batch_out), median of `reps`, from the
+ * committed rng state; the generated noise is discarded (state untouched). */
+dsx_status dsx_lab_engine_time(dsx_lab* lab, int steps, int reps, float* ms, int* batch_out);
 
 /* Host-only: *pairwise_exact = 1 when splitting workers_total workers into
  * nranks equal contiguous ranges keeps each range a subtree of the

@@ -75,6 +75,7 @@ constexpr int kThreads = 256;
 constexpr int kMaxMaskWords = 128;  // 4096 layers
 constexpr int kMaxProg = 64;        // generic pairwise program (K <= 64)
 constexpr int kMaxChunks = 8;
+constexpr int kNoiseBatch = 4;   // steps per noise-engine run when pipelining (DSX_NOISE_BATCH)
 
 struct Tile {
   long long start;
@@ -209,8 +210,9 @@ struct Vec2<float> {
   using type = float2;
 };
 
-// Segmented engine lookup: normal i of worker k lives in segment s with
-// pfx[s] <= i/2 < pfx[s+1], at slot offset 2*(i/2 - pfx[s]) + (i&1).
+// Segmented engine lookup: normal i of worker k (in the run's step t, whose
+// first pair is base = t*ceil(dim/2)) is pair m = base + i/2; it lives in
+// segment s with pfx[s] <= m < pfx[s+1], at slot offset 2*(m - pfx[s]) + (i&1).
 __device__ __forceinline__ int seg_search(const unsigned long long* pf, int P, unsigned long long m) {
   int lo = 0, hi = P;  // answer in [0, P]
   while (lo < hi) {
@@ -222,7 +224,7 @@ __device__ __forceinline__ int seg_search(const unsigned long long* pf, int P, u
 
 __device__ __forceinline__ double seg_noise(const NoiseView& nv, int k, int seg, long long i) {
   const unsigned long long* pf = nv.pfx + (long long)k * (nv.P + 2);
-  const unsigned long long m = (unsigned long long)i >> 1;
+  const unsigned long long m = nv.base + ((unsigned long long)i >> 1);
   return nv.slots[((long long)k * (nv.P + 1) + seg) * nv.cap + 2 * (long long)(m - pf[seg]) + (i & 1)];
 }
 
@@ -257,15 +259,16 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     if (threadIdx.x < KL) {
       const int k = threadIdx.x;
       const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
-      const unsigned long long m0 = (unsigned long long)t.start >> 1;
-      const unsigned long long m1 = (unsigned long long)(t.start + t.len - 1) >> 1;
+      const unsigned long long m0 = a.nv.base + ((unsigned long long)t.start >> 1);
+      const unsigned long long m1 = a.nv.base + ((unsigned long long)(t.start + t.len - 1) >> 1);
       const int s0 = seg_search(pf, a.nv.P, m0);
       const int s1 = s0 < a.nv.P ? s0 + 1 : s0;
       const double* slot0 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s0) * a.nv.cap;
       const double* slot1 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s1) * a.nv.cap;
-      s_base[k][0] = slot0 - 2 * (long long)pf[s0];
-      s_base[k][1] = slot1 - 2 * (long long)pf[s1];
-      s_bound[k] = s0 < a.nv.P ? pf[s0 + 1] : ~0ull;
+      // rebased so that s_base[k][.] + i addresses coordinate i's normal
+      s_base[k][0] = slot0 - 2 * (long long)pf[s0] + 2 * (long long)a.nv.base;
+      s_base[k][1] = slot1 - 2 * (long long)pf[s1] + 2 * (long long)a.nv.base;
+      s_bound[k] = s0 < a.nv.P ? pf[s0 + 1] - a.nv.base : ~0ull;
       if (s1 < a.nv.P && m1 >= pf[s1 + 1]) s_simple = 0;  // spans 3+ segments
     }
     __syncthreads();
@@ -285,7 +288,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
       if constexpr (NM == 2) {
         if (s_simple) return s_base[k][((unsigned long long)i >> 1) >= s_bound[k]][i];
         const int sg = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
-                                  (unsigned long long)i >> 1);
+                                  a.nv.base + ((unsigned long long)i >> 1));
         return seg_noise(a.nv, k, sg, i);
       }
       return 0.0;
@@ -379,7 +382,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
         if constexpr (NM == 1) xi = a.noise[k * a.ld + i];
         if constexpr (NM == 2) {
           const int s = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
-                                   (unsigned long long)i >> 1);
+                                   a.nv.base + ((unsigned long long)i >> 1));
           xi = seg_noise(a.nv, k, s, i);
         }
         T wn;
@@ -621,7 +624,7 @@ __global__ void gradient_kernel(const T* w, unsigned long long dim, QuadParams q
     double gi = __dmul_rn(lam, __dsub_rn(to_d(w[i]), opt));
     if (nm == 1) gi = __dadd_rn(gi, flat[i]);
     if (nm == 2) {
-      const int s = seg_search(nv.pfx + (long long)k * (nv.P + 2), nv.P, (unsigned long long)i >> 1);
+      const int s = seg_search(nv.pfx + (long long)k * (nv.P + 2), nv.P, nv.base + ((unsigned long long)i >> 1));
       gi = __dadd_rn(gi, seg_noise(nv, k, s, i));
     }
     g[i] = gi;
@@ -829,7 +832,13 @@ struct dsx_lab {
   // committed state (visible through get_rng) apart from a prefetched one.
   cudaStream_t nstream = nullptr;
   cudaEvent_t ev_noise[2] = {}, ev_upd[2] = {};
-  int mt_commit = 0, cur_set = 0, next_set = 0, pf_set = -1, pf_state = 0;
+  // rng-state slots [1 + 2*tmax][kl][313]: slot 0 = host-written, then per
+  // buffer set the state after each step of that set's engine run
+  int mt_commit = 0;                       // slot of the committed states
+  int tmax = 1;                            // steps per engine run (pipelined)
+  int cur_set = 0, cur_t = 0;              // noise the current step reads
+  int batch_set = -1, batch_t = 0, batch_n = 0;  // current run: set, next step, steps
+  int pf_set = -1, pf_n = 0;               // run prefetched into the other set
   bool pipeline = true;
   bool has_ranges = false, synced_last = false;
   bool overlap = true;
@@ -919,7 +928,7 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.partial_out = partial_out;
   a.mean_in = lab->stale_any ? static_cast<const T*>(lab->staging) : nullptr;
   a.stale = lab->stale_bits;
-  if (lab->engine) a.nv = lab->engine->view(lab->cur_set);
+  if (lab->engine) a.nv = lab->engine->view(lab->cur_set, lab->cur_t);
   if (nm == 2) {
     lab_update_kernel<T, KL, 2><<<count, kThreads, 0, s>>>(a, lab->prog_local);
   } else if (nm == 1) {
@@ -1359,32 +1368,37 @@ void drop_stale(dsx_lab* lab) {  // every row is about to be overwritten
   lab->stale_any = false;
 }
 
-// Launches the engine on the noise stream: states mt_commit -> other buffer,
-// normals into `set`, after the last update that read `set` finished.
-dsx_status launch_engine(dsx_lab* lab, int set, int* out_state) {
+int boundary_slot(const dsx_lab* lab, int set, int t) { return 1 + set * lab->tmax + t; }
+
+// Launches an engine run of `steps` steps on the noise stream: states in
+// slot src -> the set's boundary slots, normals into `set`, after the last
+// update that read `set` finished.
+dsx_status launch_engine(dsx_lab* lab, int set, int steps, int src) {
   std::string err;
   DSX_CUDA(cudaStreamWaitEvent(lab->nstream, lab->ev_upd[set], 0));
-  const int dst = 1 - lab->mt_commit;
   const uint64_t before = lab->engine->launches();
-  if (!lab->engine->run(mt_state(lab, lab->mt_commit), mt_state(lab, dst), set, lab->stddev,
-                        lab->nstream, &err))
+  if (!lab->engine->run(mt_state(lab, src), mt_state(lab, boundary_slot(lab, set, 0)), set, steps,
+                        lab->stddev, lab->nstream, &err))
     return fail(DSX_ERR_CUDA, err);
   lab->launches += lab->engine->launches() - before;
   DSX_CUDA(cudaEventRecord(lab->ev_noise[set], lab->nstream));
-  *out_state = dst;
   return DSX_OK;
 }
 
-// Drops a speculatively generated next-step noise (the rng state it started
-// from is about to change or be read by the caller).
+// Drops generated-but-unconsumed noise (the rest of the current run and a
+// prefetched run): the committed rng state is about to change.
 dsx_status invalidate_prefetch(dsx_lab* lab) {
   if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
   lab->pf_set = -1;
+  lab->batch_set = -1;
+  lab->batch_t = lab->batch_n = 0;
   return DSX_OK;
 }
 
 // Makes this step's noise available to the compute stream; returns the
-// update kernels' noise mode and selects lab->cur_set.
+// update kernels' noise mode and selects (cur_set, cur_t).  One engine run
+// covers tmax consecutive steps when pipelining (the jump-ahead is paid once
+// per run); the committed state advances to the state after this step.
 dsx_status run_noise(dsx_lab* lab, int* mode) {
   *mode = 0;
   if (lab->sigma <= 0.0) return DSX_OK;
@@ -1396,32 +1410,41 @@ dsx_status run_noise(dsx_lab* lab, int* mode) {
     *mode = 1;
     return DSX_OK;
   }
-  if (lab->pf_set >= 0) {  // generated during the previous step
-    lab->cur_set = lab->pf_set;
-    lab->mt_commit = lab->pf_state;
-    lab->pf_set = -1;
-  } else {
-    lab->cur_set = lab->next_set;
-    int st = 0;
-    DSX_TRY(launch_engine(lab, lab->cur_set, &st));
-    lab->mt_commit = st;
+  if (lab->batch_set < 0 || lab->batch_t >= lab->batch_n) {
+    if (lab->pf_set >= 0) {  // generated during the previous run's steps
+      lab->batch_set = lab->pf_set;
+      lab->batch_n = lab->pf_n;
+      lab->pf_set = -1;
+    } else {
+      const int commit_set = lab->mt_commit == 0 ? -1 : (lab->mt_commit - 1) / lab->tmax;
+      const int set = commit_set == 0 ? 1 : 0;
+      const int steps = lab->pipeline ? lab->tmax : 1;
+      DSX_TRY(launch_engine(lab, set, steps, lab->mt_commit));
+      lab->batch_set = set;
+      lab->batch_n = steps;
+    }
+    lab->batch_t = 0;
   }
-  lab->next_set = 1 - lab->cur_set;
+  lab->cur_set = lab->batch_set;
+  lab->cur_t = lab->batch_t;
+  lab->mt_commit = boundary_slot(lab, lab->batch_set, lab->batch_t);
+  ++lab->batch_t;
   DSX_CUDA(cudaStreamWaitEvent(lab->stream, lab->ev_noise[lab->cur_set], 0));
   *mode = 2;
   return DSX_OK;
 }
 
-// After the update of this step was enqueued: generate the next step's noise
-// on the noise stream so it overlaps this step's (HBM-bound) update.
+// After the update of this step was enqueued: start the next run on the
+// noise stream (from the current run's last state) so it overlaps this
+// run's (HBM-bound) updates.
 dsx_status after_update(dsx_lab* lab, int mode) {
   if (mode != 2) return DSX_OK;
   DSX_CUDA(cudaEventRecord(lab->ev_upd[lab->cur_set], lab->stream));
-  if (!lab->pipeline) return DSX_OK;
-  int st = 0;
-  DSX_TRY(launch_engine(lab, lab->next_set, &st));
-  lab->pf_set = lab->next_set;
-  lab->pf_state = st;
+  if (!lab->pipeline || lab->pf_set >= 0 || lab->batch_set < 0) return DSX_OK;
+  const int set = 1 - lab->batch_set;
+  DSX_TRY(launch_engine(lab, set, lab->tmax, boundary_slot(lab, lab->batch_set, lab->batch_n - 1)));
+  lab->pf_set = set;
+  lab->pf_n = lab->tmax;
   return DSX_OK;
 }
 
@@ -1506,7 +1529,11 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
     lab->q.curv = lab->curv;
     lab->q.opt = lab->opt;
   }
-  if (cudaMalloc(&lab->mt, 2 * 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
+  if (lab->sigma > 0.0) {
+    const char* nb = std::getenv("DSX_NOISE_BATCH");
+    lab->tmax = std::max(1, std::min(16, nb ? std::atoi(nb) : kNoiseBatch));
+  }
+  if (cudaMalloc(&lab->mt, (1 + 2 * (size_t)lab->tmax) * 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
     return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(mt) failed"));
   if (lab->sigma > 0.0) {
     const char* chain = std::getenv("DSX_NOISE_CHAIN");
@@ -1517,7 +1544,7 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
     } else {
       lab->engine = new dsx::NoiseEngine();
       std::string err;
-      if (!lab->engine->init(lab->dim, lab->kl, lab->nsm, &err)) return cleanup(fail(DSX_ERR_CUDA, err));
+      if (!lab->engine->init(lab->dim, lab->kl, lab->nsm, lab->tmax, &err)) return cleanup(fail(DSX_ERR_CUDA, err));
     }
   }
   // tiles: per block, `tile` coordinates each (never crossing a block)
@@ -1711,16 +1738,19 @@ dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask
   DSX_CUDA(cudaStreamSynchronize(lab->side));
   drop_stale(lab);
   DSX_TRY(invalidate_prefetch(lab));
+  // every call brings its own rng state: one-step engine runs, no prefetch
+  struct PipelineOff {
+    dsx_lab* l;
+    bool on;
+    ~PipelineOff() { l->pipeline = on; }
+  } guard{lab, lab->pipeline};
+  lab->pipeline = false;
   const long long D = (long long)lab->dim;
   if (lab->dtype != DSX_F64 || lab->nranks != 1 || lab->link_bw > 0.0 || lab->use_chain) {
     // the staged path: whole rows in, one step, whole rows out
     for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, rows[k]));
     DSX_CUDA(cudaMemcpy(mt_state(lab, lab->mt_commit), rng, 8ull * (kMtN + 1) * lab->kl, cudaMemcpyHostToDevice));
-    const bool pl = lab->pipeline;
-    lab->pipeline = false;
-    const dsx_status st = dsx_lab_step(lab, eta, mask);
-    lab->pipeline = pl;
-    DSX_TRY(st);
+    DSX_TRY(dsx_lab_step(lab, eta, mask));
     for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, rows[k]));
     return dsx_lab_get_state(lab, nullptr, rng);
   }
@@ -1790,11 +1820,7 @@ dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask
       lab->norm_part, lab->ntiles, lab->norm, reinterpret_cast<unsigned long long*>(lab->maxnorm));
   ++lab->launches;
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[4], lab->stream));
-  const bool pl = lab->pipeline;
-  lab->pipeline = false;  // the next call brings its own rng state
-  const dsx_status st = after_update(lab, noise);
-  lab->pipeline = pl;
-  DSX_TRY(st);
+  DSX_TRY(after_update(lab, noise));
   DSX_CUDA(cudaMemcpyAsync(rng, mt_state(lab, lab->mt_commit), 8ull * (kMtN + 1) * lab->kl,
                            cudaMemcpyDeviceToHost, lab->stream));
   DSX_CUDA(cudaStreamSynchronize(lab->d2h));
@@ -1939,7 +1965,7 @@ dsx_status dsx_lab_gradient(dsx_lab* lab, int local, double* g_out) {
   if (!lab->grad_buf) DSX_CUDA(cudaMalloc(&lab->grad_buf, 8 * lab->dim));
   g = lab->grad_buf;
   const double* xi = nm == 1 ? lab->noise + (long long)local * lab->ld : nullptr;
-  const NoiseView nv = lab->engine ? lab->engine->view(lab->cur_set) : NoiseView{};
+  const NoiseView nv = lab->engine ? lab->engine->view(lab->cur_set, lab->cur_t) : NoiseView{};
   if (lab->dtype == DSX_F64) {
     gradient_kernel<double><<<lab->nsm * 4, 256, 0, lab->stream>>>(
         static_cast<const double*>(lab->w) + (long long)local * lab->ld, lab->dim, lab->q, nm, xi, nv,
@@ -2232,6 +2258,36 @@ dsx_status dsx_lab_last_timeline(dsx_lab* lab, float* bp, float* comm) {
     }
   }
   return DSX_OK;
+}
+
+dsx_status dsx_lab_engine_time(dsx_lab* lab, int steps, int reps, float* ms, int* batch_out) {
+  DSX_TRY(check_lab(lab));
+  if (!ms || reps < 1) return fail(DSX_ERR_ARGUMENT, "bad engine_time args");
+  if (batch_out) *batch_out = lab->tmax;
+  *ms = 0.0f;
+  if (!lab->engine) return DSX_OK;
+  if (steps != 1 && steps != lab->tmax) return fail(DSX_ERR_ARGUMENT, "steps must be 1 or the batch length");
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_TRY(invalidate_prefetch(lab));
+  // run into the set that does not hold the committed state; it is dropped
+  const int commit_set = lab->mt_commit == 0 ? -1 : (lab->mt_commit - 1) / lab->tmax;
+  const int set = commit_set == 0 ? 1 : 0;
+  cudaEvent_t e0, e1;
+  DSX_CUDA(cudaEventCreate(&e0));
+  DSX_CUDA(cudaEventCreate(&e1));
+  std::vector<float> ts(reps);
+  for (int r = 0; r < reps; ++r) {
+    DSX_CUDA(cudaEventRecord(e0, lab->nstream));
+    DSX_TRY(launch_engine(lab, set, steps, lab->mt_commit));
+    DSX_CUDA(cudaEventRecord(e1, lab->nstream));
+    DSX_CUDA(cudaEventSynchronize(e1));
+    DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  std::sort(ts.begin(), ts.end());
+  *ms = ts[reps / 2];
+  return invalidate_prefetch(lab);
 }
 
 dsx_status dsx_lab_last_step_times(dsx_lab* lab, float* out3) {

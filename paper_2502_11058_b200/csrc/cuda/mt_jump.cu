@@ -1010,30 +1010,42 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
 }
 
 // Walks generations from a checkpoint until the target pair; writes the new
-// rng state.  Also serves the (rare) overflow continuation.
+// rng state.  Also serves the (rare) overflow continuation.  One CTA per
+// (worker, step of the batch): step t ends with pair (t+1)*M - 1; the last
+// step's CTA publishes the segment prefix (and the overflow extent).
 __global__ void __launch_bounds__(kThreads)
 mt_finish_kernel(uint64_t* mt, const int* pnorm, int P, int gens, int ck_every, int nck,
-                 unsigned long long pairs_needed, double stddev, double* slots, long long cap,
+                 unsigned long long pairs_per_step, double stddev, double* slots, long long cap,
                  const unsigned long long* cnt, unsigned long long* pfx, const uint64_t* ck,
                  const uint64_t* tail, int* status) {
   __shared__ Smem sm;
   __shared__ unsigned long long s_pfx_target[3];
-  const int w = blockIdx.x, tid = threadIdx.x;
+  const int w = blockIdx.x, tid = threadIdx.x, t = blockIdx.y;
+  const bool publish = t == (int)gridDim.y - 1;
+  const unsigned long long pairs_needed = pairs_per_step * (unsigned long long)(t + 1);
+  mt += (long long)t * gridDim.x * (kMtN + 1);
+  status += (long long)t * gridDim.x;
   const int p = pnorm[w];
   unsigned long long* pf = pfx + (long long)w * (P + 2);
   if (tid == 0) {
-    unsigned long long run = 0;
+    unsigned long long run = 0, at = 0;
     int star = -1;
     for (int s = 0; s < P; ++s) {
-      pf[s] = run;
+      if (publish) pf[s] = run;
       const unsigned long long c = cnt[(long long)w * P + s];
-      if (star < 0 && run + c >= pairs_needed) star = s;
+      if (star < 0 && run + c >= pairs_needed) {
+        star = s;
+        at = run;
+      }
       run += c;
     }
-    pf[P] = run;
-    pf[P + 1] = run;
+    if (publish) {
+      pf[P] = run;
+      pf[P + 1] = run;
+    }
     s_pfx_target[0] = (unsigned long long)(star < 0 ? P : star);
     s_pfx_target[1] = run;
+    s_pfx_target[2] = at;
   }
   __syncthreads();
   const int star = (int)s_pfx_target[0];
@@ -1044,7 +1056,7 @@ mt_finish_kernel(uint64_t* mt, const int* pnorm, int P, int gens, int ck_every, 
   double* out = nullptr;
   bool overflow = star >= P;
   if (!overflow) {
-    target = pairs_needed - 1 - pf[star];
+    target = pairs_needed - 1 - s_pfx_target[2];
     // last checkpoint at or before the target pair
     const uint64_t* base = ck + ((long long)w * P + star) * (long long)nck * kCkWords;
     int c = 0;
@@ -1108,7 +1120,7 @@ mt_finish_kernel(uint64_t* mt, const int* pnorm, int P, int gens, int ck_every, 
       if (tid == 0) {
         st[kMtN] = (uint64_t)sm.misc[0];
         if (overflow) {
-          pf[P + 1] = total + target + 1;
+          if (publish) pf[P + 1] = total + target + 1;
           status[w] = (2 * (target + 1) <= (unsigned long long)cap) ? 0 : 1;
         } else {
           status[w] = 0;
@@ -1124,16 +1136,15 @@ mt_finish_kernel(uint64_t* mt, const int* pnorm, int P, int gens, int ck_every, 
 }  // namespace
 
 NoiseEngine::~NoiseEngine() {
-  for (void* p : {(void*)ybuf_, (void*)win_, (void*)jidx_, (void*)joff_, (void*)slots_, (void*)cnt_,
-                  (void*)pfx_, (void*)ck_, (void*)tail_, (void*)status_})
+  for (void* p : {(void*)ybuf_, (void*)win_, (void*)cfg_[0].jbits, (void*)cfg_[1].jbits, (void*)joff_,
+                  (void*)slots_, (void*)cnt_, (void*)pfx_, (void*)ck_, (void*)tail_, (void*)status_})
     if (p) cudaFree(p);
 }
 
-bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err) {
-  dim_ = dim;
-  kl_ = kl;
-  // outputs one step needs: 2 per attempt, M / (pi/4) attempts, + 8 sd + slack
-  const double M = (double)((dim + 1) / 2);
+// Segment geometry for a run of `steps` steps, and its jump bitsets.
+bool NoiseEngine::make_cfg(int steps, int nsm, Cfg* c, std::string* err) {
+  // outputs a run needs: 2 per attempt, M / (pi/4) attempts, + 8 sd + slack
+  const double M = (double)((dim_ + 1) / 2) * steps;
   const double pa = 0.78539816339744831;
   const double attempts = M / pa + 8.0 * std::sqrt(M * (1.0 - pa)) / pa + 1024.0;
   const double E = 2.0 * attempts;
@@ -1143,37 +1154,64 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
   // ~1.3 us of whole-GPU time each (T_jump ~ 1.3 us * kl * (P-1)); their sum
   // is minimal at P* = sqrt(1.72e-3 * E / kl).  Capped so segment CTAs fit
   // one wave at 2 per SM; segments no shorter than 64 generations.
-  int P = (int)std::lround(std::sqrt(1.72e-3 * E / kl));
+  int P = (int)std::lround(std::sqrt(1.72e-3 * E / kl_));
   P = std::min(P, (int)std::ceil(E / min_seg));
-  P = std::min(P, std::max(1, 2 * nsm / kl));
+  P = std::min(P, std::max(1, 2 * nsm / kl_));
   P = std::max(1, P);
   long long gens = (long long)std::ceil(E / P / 312.0);
   if (gens < 1) gens = 1;
-  S_ = gens * 312;
-  P_ = (int)std::ceil(E / (double)S_);
-  gens_ = (int)gens;
-  ck_every_ = 16;
-  nck_ = (gens_ + 1 + ck_every_ - 1) / ck_every_ + 1;
-  cap_ = S_ + 16;
-
+  c->steps = steps;
+  c->S = gens * 312;
+  c->P = (int)std::ceil(E / (double)c->S);
+  c->gens = (int)gens;
+  c->nck = (c->gens + 1 + ck_every_ - 1) / ck_every_ + 1;
+  c->cap = c->S + 16;
+  // jump bitsets for s = 1..P-1: c_s = x^(sS-1) mod phi
   const std::vector<uint64_t>& phi = mt_char_poly();
-  if (phi.empty()) {
+  constexpr int kCW = kJumpBits / 32 + 1;
+  std::vector<uint32_t> bits((size_t)std::max(1, c->P - 1) * kCW, 0);
+  if (c->P > 1) {
+    Poly cs = x_pow((unsigned long long)c->S - 1, phi);
+    const Poly step = x_pow((unsigned long long)c->S, phi);
+    for (int s = 1; s < c->P; ++s) {
+      if (s > 1) cs = mulmod(cs, step, phi);
+      uint32_t* dst = bits.data() + (size_t)(s - 1) * kCW;
+      for (int i = 0; i < kDeg; ++i)
+        if (get_bit(cs.data(), (size_t)i)) dst[i >> 5] |= 1u << (i & 31);
+    }
+  }
+  if (cudaMalloc(&c->jbits, bits.size() * 4) != cudaSuccess) {
+    *err = "noise engine: cudaMalloc failed";
+    return false;
+  }
+  cudaMemcpy(c->jbits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice);
+  return true;
+}
+
+bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, int max_steps, std::string* err) {
+  dim_ = dim;
+  kl_ = kl;
+  ck_every_ = 16;
+  if (mt_char_poly().empty()) {
     *err = "MT19937-64 characteristic polynomial: Berlekamp-Massey did not reach degree 19937";
     return false;
   }
-  // jump bitsets for s = 1..P-1: c_s = x^(sS-1) mod phi
-  constexpr int kCW = kJumpBits / 32 + 1;
-  std::vector<uint32_t> bits((size_t)std::max(1, P_ - 1) * kCW, 0);
-  if (P_ > 1) {
-    Poly c = x_pow((unsigned long long)S_ - 1, phi);
-    const Poly step = x_pow((unsigned long long)S_, phi);
-    for (int s = 1; s < P_; ++s) {
-      if (s > 1) c = mulmod(c, step, phi);
-      uint32_t* dst = bits.data() + (size_t)(s - 1) * kCW;
-      for (int i = 0; i < kDeg; ++i)
-        if (get_bit(c.data(), (size_t)i)) dst[i >> 5] |= 1u << (i & 31);
-    }
+  max_steps = std::max(1, max_steps);
+  if (!make_cfg(1, nsm, &cfg_[0], err)) return false;
+  if (max_steps > 1) {
+    if (!make_cfg(max_steps, nsm, &cfg_[1], err)) return false;
+  } else {
+    cfg_[1] = cfg_[0];
+    cfg_[1].jbits = nullptr;  // shared with cfg_[0] (freed once)
   }
+  long long P = 0, kw = 0, ckw = 0;
+  for (const Cfg& c : cfg_) {
+    P = std::max<long long>(P, c.P);
+    slot_stride_ = std::max<long long>(slot_stride_, (long long)kl * (c.P + 1) * c.cap);
+    ckw = std::max<long long>(ckw, (long long)kl * c.P * c.nck * kCkWords);
+    kw = std::max<long long>(kw, (long long)kl * c.P * kMtN);
+  }
+  pfx_stride_ = (long long)kl * (P + 2);
   auto alloc = [&](void** p, size_t bytes) {
     if (cudaMalloc(p, bytes) != cudaSuccess) {
       *err = "noise engine: cudaMalloc failed";
@@ -1181,16 +1219,13 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
     }
     return true;
   };
-  if (!alloc((void**)&ybuf_, 8ull * kPrefixWords * kl) || !alloc((void**)&win_, 8ull * kMtN * P_ * kl) ||
-      !alloc((void**)&jidx_, bits.size() * 4) ||
-      !alloc((void**)&slots_, 2 * 8ull * cap_ * (P_ + 1) * kl) ||
-      !alloc((void**)&cnt_, 2 * 8ull * P_ * kl) || !alloc((void**)&pfx_, 2 * 8ull * (P_ + 2) * kl) ||
-      !alloc((void**)&ck_, 8ull * kCkWords * nck_ * P_ * kl) ||
-      !alloc((void**)&tail_, 8ull * kCkWords * P_ * kl) || !alloc((void**)&status_, 2 * 4ull * kl) ||
-      !alloc((void**)&joff_, 8ull * kl))
+  if (!alloc((void**)&ybuf_, 8ull * kPrefixWords * kl) || !alloc((void**)&win_, 8ull * kw) ||
+      !alloc((void**)&slots_, 2 * 8ull * slot_stride_) || !alloc((void**)&cnt_, 2 * 8ull * P * kl) ||
+      !alloc((void**)&pfx_, 2 * 8ull * pfx_stride_) || !alloc((void**)&ck_, 8ull * ckw) ||
+      !alloc((void**)&tail_, 8ull * kCkWords * P * kl) ||
+      !alloc((void**)&status_, 2 * 4ull * kl * max_steps) || !alloc((void**)&joff_, 2 * 4ull * kl))
     return false;
-  cudaMemcpy(jidx_, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemset(status_, 0, 2 * 4ull * kl);
+  cudaMemset(status_, 0, 2 * 4ull * kl * max_steps);
   if (cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            8 * kPrefixWords) != cudaSuccess) {
     *err = "noise engine: cannot opt in to 162 KB shared memory";
@@ -1199,21 +1234,28 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, std::string* err
   return true;
 }
 
-bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, double stddev,
+bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int steps, double stddev,
                       void* stream_ptr, std::string* err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  const int ci = steps > 1 ? 1 : 0;
+  const Cfg& c = cfg_[ci];
+  if (steps != c.steps) {
+    *err = "noise engine: unsupported batch length";
+    return false;
+  }
+  set_cfg_[set] = ci;
   int* pnorm = joff_;              // [kl] cursor normalized by the prefix kernel
   int* pnorm2 = joff_ + kl_;       // [kl] the same, written by segment 0
-  double* slots = slots_ + (long long)set * (P_ + 1) * cap_ * kl_;
-  unsigned long long* cnt = cnt_ + (long long)set * P_ * kl_;
-  unsigned long long* pfx = pfx_ + (long long)set * (P_ + 2) * kl_;
-  int* status = status_ + set * kl_;
-  if (P_ > 1) {
-    mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt_src, ybuf_, win_, P_, pnorm);
+  double* slots = slots_ + (long long)set * slot_stride_;
+  unsigned long long* cnt = cnt_ + (long long)set * (pfx_stride_ / kl_ - 2) * kl_;
+  unsigned long long* pfx = pfx_ + (long long)set * pfx_stride_;
+  int* status = status_ + (long long)set * kl_ * cfg_[1].steps;
+  const int P = c.P;
+  if (P > 1) {
+    mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt_src, ybuf_, win_, P, pnorm);
     ++launches_;
-    dim3 grid((P_ - 1 + kJumpsPerCta - 1) / kJumpsPerCta, kl_);
-    mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(
-        ybuf_, reinterpret_cast<const uint32_t*>(jidx_), win_, P_);
+    dim3 grid((P - 1 + kJumpsPerCta - 1) / kJumpsPerCta, kl_);
+    mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(ybuf_, c.jbits, win_, P);
     ++launches_;
   }
   // DSX_SEG_WS: 2 (default) v5 kernel, 1 single-twister warp-specialized, 0 v3
@@ -1222,20 +1264,21 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, double 
     return e ? std::atoi(e) : 2;
   }();
   if (ws == 2) {
-    mt_segment_ws2_kernel<<<dim3(P_, kl_), kWs2Threads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
-                                                                     ck_every_, nck_, stddev, slots, cap_,
-                                                                     cnt, ck_, tail_);
-  } else if (ws == 1) {
-    mt_segment_ws_kernel<<<dim3(P_, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
-                                                                    ck_every_, nck_, stddev, slots, cap_,
+    mt_segment_ws2_kernel<<<dim3(P, kl_), kWs2Threads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
+                                                                    ck_every_, c.nck, stddev, slots, c.cap,
                                                                     cnt, ck_, tail_);
+  } else if (ws == 1) {
+    mt_segment_ws_kernel<<<dim3(P, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
+                                                                   ck_every_, c.nck, stddev, slots, c.cap,
+                                                                   cnt, ck_, tail_);
   } else {
-    mt_segment_kernel<<<dim3(P_, kl_), kThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P_, gens_,
-                                                               ck_every_, nck_, stddev, slots, cap_,
-                                                               cnt, ck_, tail_);
+    mt_segment_kernel<<<dim3(P, kl_), kThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
+                                                              ck_every_, c.nck, stddev, slots, c.cap,
+                                                              cnt, ck_, tail_);
   }
-  mt_finish_kernel<<<kl_, kThreads, 0, stream>>>(mt_dst, pnorm2, P_, gens_, ck_every_, nck_, (dim_ + 1) / 2,
-                                                 stddev, slots, cap_, cnt, pfx, ck_, tail_, status);
+  mt_finish_kernel<<<dim3(kl_, steps), kThreads, 0, stream>>>(mt_dst, pnorm2, P, c.gens, ck_every_, c.nck,
+                                                              (dim_ + 1) / 2, stddev, slots, c.cap, cnt, pfx,
+                                                              ck_, tail_, status);
   launches_ += 2;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

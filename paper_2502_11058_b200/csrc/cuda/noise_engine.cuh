@@ -29,42 +29,55 @@ struct NoiseView {
   const unsigned long long* pfx;    // [kl][P+2] exclusive pair prefix per segment
   long long cap;                    // slot capacity (doubles)
   int P;                            // segments (slot P = overflow)
+  unsigned long long base;          // first pair of this step in the run's stream
 };
 
 class NoiseEngine {
  public:
-  // dim: normals per worker per step; kl: local workers; nsm: SM count.
+  // dim: normals per worker per step; kl: local workers; nsm: SM count;
+  // max_steps: the longest batch one run generates (1 or a larger T).
   NoiseEngine() = default;
   ~NoiseEngine();
-  bool init(unsigned long long dim, int kl, int nsm, std::string* err);
-  // Generates one step's noise for all local workers from the states
-  // mt_src[kl][313] into buffer set `set` (0/1, double-buffered so the next
-  // step's noise can be produced while the current update reads the other
-  // set) and writes the advanced states to mt_dst.  stddev = sigma/sqrt(dim).
-  bool run(const uint64_t* mt_src, uint64_t* mt_dst, int set, double stddev, void* stream,
+  bool init(unsigned long long dim, int kl, int nsm, int max_steps, std::string* err);
+  // Generates `steps` (1 or max_steps) consecutive steps' noise for all local
+  // workers from the states mt_src[kl][313] into buffer set `set` (0/1,
+  // double-buffered so the next batch is produced while updates read the
+  // other set) and writes the state after each step t to
+  // mt_dst[t][kl][313].  One run pays the jump-ahead once for all its steps.
+  bool run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int steps, double stddev, void* stream,
            std::string* err);
-  NoiseView view(int set) const {
-    return {slots_ + (long long)set * (P_ + 1) * cap_ * kl_,
-            pfx_ + (long long)set * (P_ + 2) * kl_, cap_, P_};
+  // Noise of step t (< steps of the set's last run).
+  NoiseView view(int set, int t) const {
+    const Cfg& c = cfg_[set_cfg_[set]];
+    return {slots_ + (long long)set * slot_stride_, pfx_ + (long long)set * pfx_stride_, c.cap, c.P,
+            (unsigned long long)t * ((dim_ + 1) / 2)};
   }
-  int segments() const { return P_; }
-  long long segment_outputs() const { return S_; }
+  int max_steps() const { return cfg_[1].steps; }
+  int segments(int steps = 1) const { return cfg_[steps > 1 ? 1 : 0].P; }
+  long long segment_outputs(int steps = 1) const { return cfg_[steps > 1 ? 1 : 0].S; }
   uint64_t launches() const { return launches_; }
 
  private:
+  struct Cfg {
+    int steps = 1, P = 1, gens = 1, nck = 1;
+    long long S = 0, cap = 0;
+    uint32_t* jbits = nullptr;     // [P-1][kJumpBits/32+1] bitsets of c_s = x^(sS-1) mod phi
+  };
+  bool make_cfg(int steps, int nsm, Cfg* c, std::string* err);
   unsigned long long dim_ = 0;
-  int kl_ = 0, P_ = 1, gens_ = 1, ck_every_ = 16, nck_ = 1;
-  long long S_ = 0, cap_ = 0;
+  int kl_ = 0, ck_every_ = 16;
+  Cfg cfg_[2];                     // [0]: one step per run, [1]: max_steps per run
+  int set_cfg_[2] = {0, 0};
+  long long slot_stride_ = 0, pfx_stride_ = 0;
   uint64_t* ybuf_ = nullptr;       // [kl][kPrefixWords]
   uint64_t* win_ = nullptr;        // [kl][P][312]
-  uint16_t* jidx_ = nullptr;       // set-bit indexes of c_s, s = 1..P-1
-  int* joff_ = nullptr;            // [P] offsets into jidx (joff[0] unused)
-  double* slots_ = nullptr;        // [kl][P+1][cap]
-  unsigned long long* cnt_ = nullptr;  // [kl][P]
-  unsigned long long* pfx_ = nullptr;  // [kl][P+2]
+  int* joff_ = nullptr;            // [2][kl] normalized cursors
+  double* slots_ = nullptr;        // [2][kl][P+1][cap]
+  unsigned long long* cnt_ = nullptr;  // [2][kl][P]
+  unsigned long long* pfx_ = nullptr;  // [2][kl][P+2]
   uint64_t* ck_ = nullptr;         // [kl][P][nck][kCkWords]
   uint64_t* tail_ = nullptr;       // [kl][P][kCkWords] segment end states
-  int* status_ = nullptr;          // [kl] 0 ok, else overflow failure
+  int* status_ = nullptr;          // [2][steps][kl] 0 ok, else overflow failure
   uint64_t launches_ = 0;
 };
 

@@ -58,6 +58,7 @@ _SIGS = {
     "dsx_lab_step_host": ([C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "dsx_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], C.c_int),
     "dsx_host_free": ([C.c_void_p], C.c_int),
+    "dsx_lab_engine_time": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_int)], C.c_int),
     "dsx_lab_set_rng": ([C.c_void_p, C.c_int, C.c_void_p, C.c_uint64], C.c_int),
     "dsx_lab_get_rng": ([C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
     "dsx_lab_seed_rng": ([C.c_void_p, C.c_uint64], C.c_int),
