@@ -29,6 +29,7 @@
 #include <random>
 #include <sstream>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "dsx.h"
@@ -313,60 +314,85 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     };
     if (threadIdx.x == 0 && first != t.start) scalar(t.start);
     if (threadIdx.x == 1 && first + 2 * (long long)npairs < end) scalar(end - 1);
-#pragma unroll 2
-    for (int pr = threadIdx.x; pr < npairs; pr += kThreads) {
-      const long long i = first + 2 * (long long)pr;
-      double lam0, opt0, lam1, opt1;
-      quad_coeffs(a.q, i, &lam0, &opt0);
-      quad_coeffs(a.q, i + 1, &lam1, &opt1);
-      T w0[KL], w1[KL];
+    // Main loop, specialised per tile on (stale rows, simple noise
+    // addressing) so that every row load and every noise load of an
+    // iteration is independent and issued back to back: the noise base of
+    // worker k is one of two rebased pointers (a select, no dependent chain),
+    // and noise — read exactly once — is streamed with evict-first loads.
+    auto pairs = [&](auto stale_c, auto simple_c) {
+      constexpr bool STALE = decltype(stale_c)::value;
+      constexpr bool SIMPLE = decltype(simple_c)::value;
+      for (int pr = threadIdx.x; pr < npairs; pr += kThreads) {
+        const long long i = first + 2 * (long long)pr;
+        double lam0, opt0, lam1, opt1;
+        quad_coeffs(a.q, i, &lam0, &opt0);
+        quad_coeffs(a.q, i + 1, &lam1, &opt1);
+        V2 wv[KL];
+        double2 xv[KL];
+        if constexpr (STALE) {
+          const V2 m = *reinterpret_cast<const V2*>(a.mean_in + i);
 #pragma unroll
-      for (int k = 0; k < KL; ++k) {
-        const V2 w = stale ? *reinterpret_cast<const V2*>(a.mean_in + i)
-                           : *reinterpret_cast<const V2*>(a.w + k * a.ld + i);
-        double x0 = 0.0, x1 = 0.0;
+          for (int k = 0; k < KL; ++k) wv[k] = m;
+        } else {
+#pragma unroll
+          for (int k = 0; k < KL; ++k) wv[k] = *reinterpret_cast<const V2*>(a.w + k * a.ld + i);
+        }
         if constexpr (NM == 1) {
-          const double2 xv = *reinterpret_cast<const double2*>(a.noise + k * a.ld + i);
-          x0 = xv.x;
-          x1 = xv.y;
+#pragma unroll
+          for (int k = 0; k < KL; ++k) xv[k] = __ldcs(reinterpret_cast<const double2*>(a.noise + k * a.ld + i));
         }
         if constexpr (NM == 2) {
-          if (s_simple) {
-            const double2 xv = *reinterpret_cast<const double2*>(
-                s_base[k][((unsigned long long)i >> 1) >= s_bound[k]] + i);
-            x0 = xv.x;
-            x1 = xv.y;
+          if constexpr (SIMPLE) {
+            const unsigned long long m = (unsigned long long)i >> 1;
+            const double* np[KL];
+#pragma unroll
+            for (int k = 0; k < KL; ++k) np[k] = s_base[k][m >= s_bound[k] ? 1 : 0];
+#pragma unroll
+            for (int k = 0; k < KL; ++k) xv[k] = __ldcs(reinterpret_cast<const double2*>(np[k] + i));
           } else {
-            x0 = noise_at(k, i);
-            x1 = noise_at(k, i + 1);
+#pragma unroll
+            for (int k = 0; k < KL; ++k) xv[k] = make_double2(noise_at(k, i), noise_at(k, i + 1));
           }
         }
-        const auto g0 = grad_step(w.x, lam0, opt0, x0, a.eta, NOISE, &w0[k]);
-        const auto g1 = grad_step(w.y, lam1, opt1, x1, a.eta, NOISE, &w1[k]);
-        nsq[k] += to_d(g0) * to_d(g0) + to_d(g1) * to_d(g1);
-      }
-      if (avg) {
-        V2 m;
-        m.x = psum<0, KL, T>(w0) / (T)a.k_total;
-        m.y = psum<0, KL, T>(w1) / (T)a.k_total;
-#pragma unroll
-        for (int k = 0; k < KL; ++k) *reinterpret_cast<V2*>(a.w + k * a.ld + i) = m;
-      } else if (part) {
-        // multi-rank synced tile: only this rank's subtree sum leaves the
-        // kernel; the rows are rewritten by the cross-rank average
-        V2 m;
-        m.x = psum<0, KL, T>(w0);
-        m.y = psum<0, KL, T>(w1);
-        *reinterpret_cast<V2*>(a.partial_out + i) = m;
-      } else {
+        T w0[KL], w1[KL];
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
-          V2 o;
-          o.x = w0[k];
-          o.y = w1[k];
-          *reinterpret_cast<V2*>(a.w + k * a.ld + i) = o;
+          const double x0 = NOISE ? xv[k].x : 0.0, x1 = NOISE ? xv[k].y : 0.0;
+          const auto g0 = grad_step(wv[k].x, lam0, opt0, x0, a.eta, NOISE, &w0[k]);
+          const auto g1 = grad_step(wv[k].y, lam1, opt1, x1, a.eta, NOISE, &w1[k]);
+          nsq[k] += to_d(g0) * to_d(g0) + to_d(g1) * to_d(g1);
+        }
+        if (avg) {
+          V2 m;
+          m.x = psum<0, KL, T>(w0) / (T)a.k_total;
+          m.y = psum<0, KL, T>(w1) / (T)a.k_total;
+#pragma unroll
+          for (int k = 0; k < KL; ++k) *reinterpret_cast<V2*>(a.w + k * a.ld + i) = m;
+        } else if (part) {
+          // multi-rank synced tile: only this rank's subtree sum leaves the
+          // kernel; the rows are rewritten by the cross-rank average
+          V2 m;
+          m.x = psum<0, KL, T>(w0);
+          m.y = psum<0, KL, T>(w1);
+          *reinterpret_cast<V2*>(a.partial_out + i) = m;
+        } else {
+#pragma unroll
+          for (int k = 0; k < KL; ++k) {
+            V2 o;
+            o.x = w0[k];
+            o.y = w1[k];
+            *reinterpret_cast<V2*>(a.w + k * a.ld + i) = o;
+          }
         }
       }
+    };
+    using Yes = std::true_type;
+    using No = std::false_type;
+    const bool simple = NM != 2 || s_simple;
+    if (stale) {
+      if (simple) pairs(Yes{}, Yes{}); else pairs(Yes{}, No{});
+    } else {
+      if (simple) pairs(No{}, Yes{}); else pairs(No{}, No{});
     }
   } else {
     // generic worker count: row pass, then the pairwise program for
