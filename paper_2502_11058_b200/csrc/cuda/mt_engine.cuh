@@ -38,10 +38,12 @@ __host__ __device__ __forceinline__ uint64_t mt_temper(uint64_t z) {
 
 // 2 * generate_canonical<double,53>(z) - 1.  (double)z rounds to nearest,
 // the 2^-64 scale is exact, and the >= 1 clamp mirrors random.tcc:3371.
+// Computed as t = 2u directly ((double)z * 2^-63, exact power-of-two
+// scaling, so t == 2 * u bit for bit; the clamp u -> 1 - 2^-53 is t -> 2 - 2^-52).
 __device__ __forceinline__ double mt_polar_coord(uint64_t tempered) {
-  double u = __dmul_rn(__ull2double_rn(tempered), 5.421010862427522170037264e-20);
-  if (u >= 1.0) u = 0x1.fffffffffffffp-1;
-  return __dsub_rn(__dmul_rn(2.0, u), 1.0);
+  double t = __dmul_rn(__ull2double_rn(tempered), 0x1p-63);
+  if (t >= 2.0) t = 0x1.fffffffffffffp0;
+  return __dsub_rn(t, 1.0);
 }
 
 // Polar acceptance: !(r2 > 1 || r2 == 0) with r2 = x*x + y*y (no FMA).

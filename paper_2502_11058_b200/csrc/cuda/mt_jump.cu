@@ -792,7 +792,7 @@ mt_segment_ws_kernel(const uint64_t* win_state, const uint64_t* win, const int* 
 //  * accepted pairs go to a shared FIFO and are transformed in full chunks
 //    of 320 (or 640 with 2-way ILP), the remainder carried to the next round,
 //    so no warp idles at the end of a round with a half-empty transform.
-constexpr int kProdWarps = 2;
+constexpr int kProdWarps = 4;
 constexpr int kProdThreads = 32 * kProdWarps;
 constexpr int kWs2Threads = kProdThreads + kThreads;
 constexpr int kBarProd = 6;
@@ -877,6 +877,7 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
   int hh = 0;                      // a carried half pair enters this round
   unsigned long long local = 0;    // accepted pairs pushed to the FIFO
   unsigned long long head = 0;     // accepted pairs transformed and stored
+  int ck_next = 0, ck_idx = 0;     // next checkpoint generation / its index
   auto transform = [&](unsigned long long g) {
     const double2 xy = fifo[g % kQCap];
     double r2;
@@ -893,8 +894,10 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
     if (k) named_sync(kBarFull + h, kWs2Threads);
     const int rg = min(R, ngen - q);
     const double half_in = s_half[h];
-    if (q % ck_every == 0) {
-      uint64_t* c = ckw + (long long)(q / ck_every) * kCkWords;
+    if (q == ck_next) {  // every ck_every generations (no integer division)
+      uint64_t* c = ckw + (long long)ck_idx * kCkWords;
+      ck_next += ck_every;
+      ++ck_idx;
       if (tid < kMtN) c[tid] = ring[h][tid];
       if (tid == 0) {
         c[kMtN] = (uint64_t)hh;
