@@ -53,6 +53,9 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "measured", "profile"],
+                    help="multi-GPU: schedule from the CUDA-event profile measured on these GPUs "
+                         "(auto for N>1) or from --profile's times")
     return ap.parse_args()
 
 
@@ -175,17 +178,38 @@ def run_ref_tool(args, steps, warmup):
     return json.loads(out.strip().splitlines()[-1])
 
 
-def workload_config(args, world, dim):
+def workload_config(args, world, dim, schedule_src="profile"):
+    sched = ("bubble_fill(schedule_dfs(profile measured on these GPUs by dsx_lab_profile, H))"
+             if schedule_src == "measured" else "bubble_fill(schedule_dfs(profile, H))")
     return {"workload": "resnet18-shaped quadratic lab (61 registered layers), 8 workers, H=5",
             "profile": os.path.relpath(args.profile, REPO), "workers": args.workers,
             "period": args.period, "dim_per_worker": dim, "sigma": args.sigma,
-            "schedule": "bubble_fill(schedule_dfs(profile, H))", "seed": args.seed,
+            "schedule": sched, "seed": args.seed,
             "parallelism": f"dp{world} ({args.workers // world} workers/GPU)",
             "sync_algo": args.sync_algo if world > 1 else "fused in-kernel (single GPU)",
             "l2": "working set > 126 MB L2 (no flush needed)"}
 
 
 # ------------------------------------------------------------------ our arm ---
+
+def measured_schedule(lab, sizes, H, dist, rank):
+    import tempfile
+
+    import numpy as np
+
+    from paper_2502_11058_b200.lab import schedule_from_profile, write_profile
+    t_bp, t_comm = lab.profile(reps=5)
+    t_comm = np.where(t_comm < 0, 0.0, t_comm)
+    if dist is not None:
+        import torch
+        t = torch.tensor(np.concatenate([t_bp, t_comm]), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_bp, t_comm = t.numpy()[: len(sizes)], t.numpy()[len(sizes):]
+    path = os.path.join(tempfile.mkdtemp(prefix=f"dreamddp_r{rank}_"), "measured.profile")
+    write_profile(path, [int(s) * 8 for s in sizes], np.zeros(len(sizes)), t_bp, t_comm,
+                  bandwidth=1.0, latency=0.0)
+    sets, fills, _, text = schedule_from_profile(path, H)
+    return sets, fills, text
 
 def our_arm(args, world, rank, local_rank, dist):
     import ctypes as C
@@ -211,6 +235,14 @@ def our_arm(args, world, rank, local_rank, dist):
     lab.set_overlap(not args.no_overlap)
     lab.seed(args.seed)
     lab.fill(0.0)
+    schedule_src = args.schedule if args.schedule != "auto" else ("measured" if world > 1 else "profile")
+    fixed_masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
+    sched_text = None
+    if schedule_src == "measured":
+        # DreamDDP's loop on this box: CUDA-event profile of every layer's
+        # local step and cross-rank average, identical on all ranks (max),
+        # then the bit-exact DFS + bubble-fill scheduler on it
+        sets, fills, sched_text = measured_schedule(lab, sizes, H, dist, rank)
     masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
 
     def barrier():
@@ -266,6 +298,47 @@ def our_arm(args, world, rank, local_rank, dist):
         N.call("dsx_lab_engine_time", lab.h, nb.value, 3, C.byref(eb), None)
         eng = {"run_1_step_ms": round(e1.value, 4), "batch_steps": nb.value,
                "run_batch_ms": round(eb.value, 4), "per_step_ms": round(eb.value / nb.value, 4)}
+
+    def max_ranks(vals):
+        if dist is None:
+            return vals
+        import torch
+        t = torch.tensor(vals, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t]
+
+    def synced_frac(ms):
+        sz = np.asarray(sizes, dtype=np.float64)
+        return round(float(np.mean([np.dot(m[1:], sz) / dim for m in ms])), 4)
+
+    schedule_info = {"source": schedule_src, "synced_param_frac_per_step": synced_frac(masks)}
+    if schedule_src == "measured":
+        schedule_info["text"] = sched_text
+        # the same workload under the fixed profile's schedule, for comparison
+        lab.sync()
+        barrier()
+        lab.record(0)
+        for _ in range(args.steps):
+            lab.step(learning_rate(r, H), fixed_masks[r % H])
+            r += 1
+        lab.record(1)
+        ms_f = max_ranks([lab.elapsed_ms(0, 1)])[0]
+        lab.sync()
+        lab.set_pipeline(False)
+        lab.set_instrument(True)
+        per_f = []
+        for _ in range(2 * H):
+            lab.step(learning_rate(r, H), fixed_masks[r % H])
+            r += 1
+            per_f.append(lab.last_step_times())
+        lab.set_instrument(False)
+        lab.set_pipeline(True)
+        sf, ef = max_ranks([statistics.mean(p[1] for p in per_f), statistics.mean(p[2] for p in per_f)])
+        schedule_info["fixed_profile_schedule"] = {
+            "schedule": "bubble_fill(schedule_dfs(profile, H))", "value": round(args.steps / (ms_f / 1e3), 3),
+            "synced_param_frac_per_step": synced_frac(fixed_masks),
+            "sync_ms_per_iter": round(sf, 5), "exposed_sync_ms_per_iter": round(ef, 5),
+            "exposed_sync_frac": round(ef / sf, 4) if sf > 0 else None}
     step_ms = [p[0] for p in per]
     sync_ms = [p[1] for p in per]
     exposed_ms = [p[2] for p in per]
@@ -366,10 +439,11 @@ def our_arm(args, world, rank, local_rank, dist):
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_max / args.steps, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
-        "config": workload_config(args, world, dim),
+        "config": workload_config(args, world, dim, schedule_src),
         "exposed_sync_ms_per_iter": round(exposed_mean, 5),
         "sync_ms_per_iter": round(sync_mean, 5),
         "exposed_sync_frac": round(exposed_mean / sync_mean, 4) if sync_mean > 0 else None,
+        "schedule": schedule_info,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks.summary(),
     }

@@ -169,7 +169,10 @@ dsx_status dsx_lab_set_link(dsx_lab* lab, double bandwidth, double latency);
 /* CUDA-event layer profiler: t_bp[l] = device seconds of layer l's local
  * step (state untouched), t_comm[l] = seconds of its cross-rank average
  * (multi-rank), or the throttled link's model, or -1 (not measured).
- * Median of `reps`.  Feeds dsc_write_profile -> schedule_dfs. */
+ * Median of `reps`.  Each layer is timed alone, then the set is rescaled to
+ * the step as it runs (one fused update pass; the grouped whole-model
+ * average), keeping the layers' relative costs.  Feeds dsc_write_profile ->
+ * schedule_dfs. */
 dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm);
 
 /* Timing on the lab's compute stream: CUDA events in slots 0..31. */

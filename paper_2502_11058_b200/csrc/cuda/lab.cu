@@ -714,9 +714,55 @@ struct PeerPtrs {
   void* p[kMaxProg];
 };
 
+// Cross-rank flags in peer memory (replacing 4-byte NCCL all-reduces as
+// barriers).  Every rank owns kFlagWords u64 words, mapped into all peers:
+// [0, kMaxProg) ready epochs by source rank, [kMaxProg, 2 kMaxProg) counts
+// of completed averaging launches by source rank.  Values only grow, so no
+// reset is needed; writers fence at system scope before publishing.
+constexpr int kFlagWords = 2 * kMaxProg;
+struct FlagPtrs {
+  unsigned long long* p[kMaxProg];
+};
+struct Signal {
+  FlagPtrs f;
+  int rank, R;
+  unsigned long long value;  // count published by this launch's last block
+  unsigned int* counter;     // local finished-block counter (nullptr: no signal)
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Thread q < R: optionally publishes `value` into rank q's slot[rank], then
+// waits until this rank's slot[q] reached `value` (every peer published).
+// A peer that never arrives traps after ~30 s instead of hanging the GPU.
+__global__ void flag_wait_kernel(FlagPtrs f, int rank, int R, int slot, unsigned long long value, int publish) {
+  const int q = threadIdx.x;
+  if (q >= R) return;
+  if (publish) {
+    __threadfence_system();
+    st_release_sys(f.p[q] + slot + rank, value);
+  }
+  const unsigned long long* mine = f.p[rank] + slot + q;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_sys(mine) < value) {
+    __nanosleep(64);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 30000000000ull) __trap();
+  }
+}
+
 template <typename T, int W>
 __global__ void __launch_bounds__(256)
-p2p_average_kernel(PeerPtrs peers, long long a, long long b, int k_total, PairProg prog) {
+p2p_average_kernel(PeerPtrs peers, long long a, long long b, int k_total, PairProg prog, Signal sig) {
   using V2 = typename Vec2<T>::type;
   // vector body on even coordinates, scalar head/tail
   const long long first = a + (a & 1);
@@ -762,6 +808,14 @@ p2p_average_kernel(PeerPtrs peers, long long a, long long b, int k_total, PairPr
     }
   }
   __threadfence_system();
+  if (sig.counter) {  // the last block to finish publishes this launch's count to every rank
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(sig.counter, 1u) == gridDim.x - 1) {
+      *sig.counter = 0;
+      __threadfence_system();
+      for (int q = 0; q < sig.R; ++q) st_release_sys(sig.f.p[q] + kMaxProg + sig.rank, sig.value);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -882,6 +936,12 @@ struct dsx_lab {
   PeerPtrs peers{};            // every rank's exchange buffer, mapped here
   std::vector<void*> opened;   // IPC mappings to close
   int* bar = nullptr;          // 4-byte barrier all-reduce scratch
+  // peer-memory flag barriers (DSX_FLAG_BARRIER=0: NCCL all-reduce barriers)
+  bool flag_bar = false;
+  unsigned long long* flags = nullptr;   // this rank's flag block [kFlagWords]
+  FlagPtrs fpeers{};                     // every rank's flag block, mapped here
+  unsigned int* sig_counter = nullptr;   // finished-block counter of the averaging kernel
+  unsigned long long epoch = 0, sig_count = 0;
   int chunks = 4;              // overlap groups per step
   bool lazy = true;            // lazy broadcast of cross-rank means (DSX_LAZY=0: off)
   MaskBits stale_bits{};       // layers whose rows are stale (mean in staging)
@@ -1196,11 +1256,26 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
   // lazy broadcast (fused path): the synced layers' rows stay stale, their
   // mean lives in the exchange buffer and the next update reads it there
   const bool lazy = fused_partial && lab->lazy;
+  const int R = lab->nranks;
+  const bool fb = lab->flag_bar;
   auto barrier = [&]() -> dsx_status {
     DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
     return DSX_OK;
   };
-  const int R = lab->nranks;
+  // "every rank's subtree sums of this group are final"
+  auto ready = [&]() -> dsx_status {
+    if (!fb) return barrier();
+    flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, R, 0, ++lab->epoch, 1);
+    ++lab->launches;
+    return DSX_OK;
+  };
+  // "every rank's averaging writes so far have landed"
+  auto landed = [&]() -> dsx_status {
+    if (!fb) return barrier();
+    flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, R, kMaxProg, lab->sig_count, 0);
+    ++lab->launches;
+    return DSX_OK;
+  };
   bool any = false, started = false;
   std::vector<std::pair<long long, long long>> pending;  // ranges awaiting the row broadcast
   for (int g = 0; g < G; ++g) {
@@ -1222,9 +1297,10 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
     DSX_CUDA(cudaStreamWaitEvent(lab->side, lab->ev_chunk[g % kMaxChunks], 0));
     if (lab->kl > 1 && !fused_partial)
       for (const auto& r : sub) launch_partial<T>(lab, lab->side, r.first, r.second, part + r.first);
-    DSX_TRY(barrier());  // this group's subtree sums final on every rank
+    DSX_TRY(ready());  // this group's subtree sums final on every rank
     started = true;
-    if (!pending.empty() && !lazy) {  // previous group's averages landed (barrier above)
+    if (!pending.empty() && !lazy) {  // previous group's averages must have landed
+      if (fb) DSX_TRY(landed());
       for (const auto& r : pending) {
         broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->side>>>(static_cast<T*>(lab->w), lab->ld,
                                                                        lab->kl, r.first, r.second,
@@ -1237,13 +1313,18 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
       const long long base = r.second / R, extra = r.second % R;
       const long long a = r.first + lab->rank * base + std::min<long long>(lab->rank, extra);
       const long long n = base + (lab->rank < extra ? 1 : 0);
-      if (n <= 0) continue;
-      const int blocks = (int)std::min<long long>(lab->nsm * 4, (n / 2 + 255) / 256 + 1);
+      // with flag barriers every rank launches (possibly empty) so the
+      // published launch counts stay in lockstep
+      if (n <= 0 && !fb) continue;
+      const int blocks = (int)std::min<long long>(lab->nsm * 4, (std::max(n, 0LL) / 2 + 255) / 256 + 1);
+      Signal sig{};
+      if (fb) sig = Signal{lab->fpeers, lab->rank, R, ++lab->sig_count, lab->sig_counter};
+      const long long e = a + std::max(n, 0LL);
       switch (R) {
-        case 2: p2p_average_kernel<T, 2><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks); break;
-        case 4: p2p_average_kernel<T, 4><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks); break;
-        case 8: p2p_average_kernel<T, 8><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks); break;
-        default: p2p_average_kernel<T, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + n, lab->K, lab->prog_ranks);
+        case 2: p2p_average_kernel<T, 2><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig); break;
+        case 4: p2p_average_kernel<T, 4><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig); break;
+        case 8: p2p_average_kernel<T, 8><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig); break;
+        default: p2p_average_kernel<T, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig);
       }
       ++lab->launches;
     }
@@ -1258,7 +1339,7 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
   }
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
   if (any) {
-    DSX_TRY(barrier());  // the last group's peer writes landed everywhere
+    DSX_TRY(landed());  // every group's peer writes landed everywhere
     if (!lazy) {
       for (const auto& r : pending) {
         broadcast_rows_kernel<T><<<lab->nsm * 2, 256, 0, lab->side>>>(static_cast<T*>(lab->w), lab->ld,
@@ -1631,6 +1712,8 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   for (auto& ev : lab->tl_ev)
     if (ev) cudaEventDestroy(ev);
   if (lab->bar) cudaFree(lab->bar);
+  if (lab->flags) cudaFree(lab->flags);
+  if (lab->sig_counter) cudaFree(lab->sig_counter);
   for (auto& ev : lab->ev_chunk)
     if (ev) cudaEventDestroy(ev);
   for (void* p : {lab->w, (void*)lab->curv, (void*)lab->opt, (void*)lab->noise, (void*)lab->mt, (void*)lab->grad_buf,
@@ -2093,36 +2176,47 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   const char* p2p_env = std::getenv("DSX_P2P");
   int ok = (p2p_env && p2p_env[0] == '0') || nranks > kMaxProg ? 0 : 1;
   void* xbuf = lab->kl == 1 ? lab->w : lab->staging;
-  cudaIpcMemHandle_t mine{};
-  if (ok && cudaIpcGetMemHandle(&mine, xbuf) != cudaSuccess) ok = 0;
+  DSX_CUDA(cudaMalloc(&lab->flags, 8 * kFlagWords));
+  DSX_CUDA(cudaMemset(lab->flags, 0, 8 * kFlagWords));
+  DSX_CUDA(cudaMalloc(&lab->sig_counter, 4));
+  DSX_CUDA(cudaMemset(lab->sig_counter, 0, 4));
+  // two handles per rank: the exchange buffer and the flag block
+  constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+  cudaIpcMemHandle_t mine[2]{};
+  if (ok && (cudaIpcGetMemHandle(&mine[0], xbuf) != cudaSuccess ||
+             cudaIpcGetMemHandle(&mine[1], lab->flags) != cudaSuccess))
+    ok = 0;
   char* d_handles = nullptr;
   int* d_ok = nullptr;
-  DSX_CUDA(cudaMalloc(&d_handles, sizeof(cudaIpcMemHandle_t) * nranks));
+  DSX_CUDA(cudaMalloc(&d_handles, 2 * kH * nranks));
   DSX_CUDA(cudaMalloc(&d_ok, 4));
-  DSX_CUDA(cudaMemcpy(d_handles + sizeof(cudaIpcMemHandle_t) * rank, &mine, sizeof mine, cudaMemcpyHostToDevice));
+  DSX_CUDA(cudaMemcpy(d_handles + 2 * kH * rank, mine, 2 * kH, cudaMemcpyHostToDevice));
   DSX_CUDA(cudaMemcpy(d_ok, &ok, 4, cudaMemcpyHostToDevice));
-  DSX_NCCL(ncclAllGather(d_handles + sizeof(cudaIpcMemHandle_t) * rank, d_handles, sizeof(cudaIpcMemHandle_t),
-                         ncclChar, lab->comm, lab->side));
+  DSX_NCCL(ncclAllGather(d_handles + 2 * kH * rank, d_handles, 2 * kH, ncclChar, lab->comm, lab->side));
   DSX_NCCL(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, lab->comm, lab->side));
   DSX_CUDA(cudaStreamSynchronize(lab->side));
-  std::vector<cudaIpcMemHandle_t> handles(nranks);
-  DSX_CUDA(cudaMemcpy(handles.data(), d_handles, sizeof(cudaIpcMemHandle_t) * nranks, cudaMemcpyDeviceToHost));
+  std::vector<cudaIpcMemHandle_t> handles(2 * (size_t)nranks);
+  DSX_CUDA(cudaMemcpy(handles.data(), d_handles, 2 * kH * nranks, cudaMemcpyDeviceToHost));
   DSX_CUDA(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
   int local_ok = ok;
   if (ok) {
-    for (int q = 0; q < nranks; ++q) {
+    for (int q = 0; q < nranks && local_ok; ++q) {
       if (q == rank) {
         lab->peers.p[q] = xbuf;
+        lab->fpeers.p[q] = lab->flags;
         continue;
       }
-      void* ptr = nullptr;
-      if (cudaIpcOpenMemHandle(&ptr, handles[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        cudaGetLastError();
-        local_ok = 0;
-        break;
+      for (int which = 0; which < 2; ++which) {
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, handles[2 * q + which], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          local_ok = 0;
+          break;
+        }
+        lab->opened.push_back(ptr);
+        if (which == 0) lab->peers.p[q] = ptr;
+        else lab->fpeers.p[q] = static_cast<unsigned long long*>(ptr);
       }
-      lab->opened.push_back(ptr);
-      lab->peers.p[q] = ptr;
     }
   }
   DSX_CUDA(cudaMemcpy(d_ok, &local_ok, 4, cudaMemcpyHostToDevice));
@@ -2132,6 +2226,8 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   cudaFree(d_handles);
   cudaFree(d_ok);
   lab->p2p = ok != 0;
+  const char* fb = std::getenv("DSX_FLAG_BARRIER");
+  lab->flag_bar = lab->p2p && !(fb && fb[0] == '0');
   return DSX_OK;
 }
 
@@ -2177,6 +2273,27 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
     t_bp[b] = ts[reps / 2] * 1e-3;
     tb = te;
   }
+  // Layers alone carry one launch each; the real step updates every layer in
+  // one fused pass (except the single-GPU throttled mode, which launches per
+  // layer).  Rescale so the layers sum to the fused pass's time (relative
+  // costs kept), i.e. the profile describes the step as it runs.
+  if (!(lab->nranks == 1 && lab->link_bw > 0.0)) {
+    for (int r = 0; r < reps; ++r) {
+      DSX_CUDA(cudaEventRecord(e0, lab->stream));
+      if (lab->dtype == DSX_F64) launch_update<double>(lab, lab->stream, 0, lab->ntiles, 0, false, none, 0.0);
+      else launch_update<float>(lab, lab->stream, 0, lab->ntiles, 0, false, none, 0.0);
+      DSX_CUDA(cudaEventRecord(e1, lab->stream));
+      DSX_CUDA(cudaEventSynchronize(e1));
+      DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
+    }
+    std::sort(ts.begin(), ts.end());
+    double alone = 0.0;
+    for (int b = 0; b < lab->L; ++b) alone += t_bp[b];
+    if (alone > 0.0) {
+      const double scale = ts[reps / 2] * 1e-3 / alone;
+      for (int b = 0; b < lab->L; ++b) t_bp[b] *= scale;
+    }
+  }
   if (t_comm) {
     std::vector<unsigned char> one(lab->L + 1, 0);
     for (int b = 0; b < lab->L; ++b) {
@@ -2195,29 +2312,88 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
       const size_t bytes = es * (size_t)lab->ld * lab->kl;
       DSX_CUDA(cudaMalloc(&backup, bytes));
       DSX_CUDA(cudaMemcpyAsync(backup, lab->w, bytes, cudaMemcpyDeviceToDevice, lab->side));
+      // the step's own barriers: peer-memory flags (or NCCL all-reduces)
+      const bool fb = lab->flag_bar;
+      auto bar_ready = [&]() -> dsx_status {
+        if (fb) {
+          flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, lab->nranks, 0, ++lab->epoch, 1);
+        } else {
+          DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+        }
+        return DSX_OK;
+      };
+      auto bar_landed = [&]() -> dsx_status {
+        if (fb) {
+          flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, lab->nranks, kMaxProg, lab->sig_count, 0);
+        } else {
+          DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+        }
+        return DSX_OK;
+      };
+      auto sig = [&]() { return fb ? Signal{lab->fpeers, lab->rank, lab->nranks, ++lab->sig_count, lab->sig_counter} : Signal{}; };
       for (int b = 0; b < lab->L; ++b) {
         const long long lo = (long long)lab->offs[b], n = (long long)(lab->offs[b + 1] - lab->offs[b]);
         for (int r = 0; r < reps; ++r) {
-          DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+          DSX_TRY(bar_landed());
           DSX_CUDA(cudaEventRecord(e0, lab->side));
+          DSX_TRY(bar_ready());
           const int R = lab->nranks;
           const long long base = n / R, extra = n % R;
           const long long a = lo + lab->rank * base + std::min<long long>(lab->rank, extra);
           const long long m = base + (lab->rank < extra ? 1 : 0);
-          if (m > 0) {
-            const int blocks = (int)std::min<long long>(lab->nsm * 4, (m / 2 + 255) / 256 + 1);
+          {
+            const int blocks = (int)std::min<long long>(lab->nsm * 4, (std::max(m, 0LL) / 2 + 255) / 256 + 1);
+            const long long e = a + std::max(m, 0LL);
             if (lab->dtype == DSX_F64)
-              p2p_average_kernel<double, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + m, lab->K, lab->prog_ranks);
+              p2p_average_kernel<double, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig());
             else
-              p2p_average_kernel<float, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, a + m, lab->K, lab->prog_ranks);
+              p2p_average_kernel<float, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig());
           }
-          DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+          DSX_TRY(bar_landed());
           DSX_CUDA(cudaEventRecord(e1, lab->side));
           DSX_CUDA(cudaEventSynchronize(e1));
           DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
         }
         std::sort(ts.begin(), ts.end());
         t_comm[b] = ts[reps / 2] * 1e-3;
+      }
+      // the step averages in `chunks` groups (two barriers each), not per
+      // layer: rescale to the grouped whole-model average
+      const int G = lab->overlap ? std::max(1, std::min(lab->chunks, lab->ntiles)) : 1;
+      for (int r = 0; r < reps; ++r) {
+        DSX_TRY(bar_landed());
+        DSX_CUDA(cudaEventRecord(e0, lab->side));
+        for (int g = 0; g < G; ++g) {
+          const int te = lab->ntiles - (int)((long long)lab->ntiles * g / G);
+          const int tb = lab->ntiles - (int)((long long)lab->ntiles * (g + 1) / G);
+          if (te <= tb) continue;
+          const long long lo = lab->h_tiles[tb].start;
+          const long long n = lab->h_tiles[te - 1].start + lab->h_tiles[te - 1].len - lo;
+          const int R = lab->nranks;
+          const long long base = n / R, extra = n % R;
+          const long long a = lo + lab->rank * base + std::min<long long>(lab->rank, extra);
+          const long long m = base + (lab->rank < extra ? 1 : 0);
+          DSX_TRY(bar_ready());
+          {
+            const int blocks = (int)std::min<long long>(lab->nsm * 4, (std::max(m, 0LL) / 2 + 255) / 256 + 1);
+            const long long e = a + std::max(m, 0LL);
+            if (lab->dtype == DSX_F64)
+              p2p_average_kernel<double, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig());
+            else
+              p2p_average_kernel<float, 0><<<blocks, 256, 0, lab->side>>>(lab->peers, a, e, lab->K, lab->prog_ranks, sig());
+          }
+        }
+        DSX_TRY(bar_landed());
+        DSX_CUDA(cudaEventRecord(e1, lab->side));
+        DSX_CUDA(cudaEventSynchronize(e1));
+        DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
+      }
+      std::sort(ts.begin(), ts.end());
+      double alone = 0.0;
+      for (int b = 0; b < lab->L; ++b) alone += t_comm[b];
+      if (alone > 0.0) {
+        const double scale = ts[reps / 2] * 1e-3 / alone;
+        for (int b = 0; b < lab->L; ++b) t_comm[b] *= scale;
       }
       DSX_CUDA(cudaMemcpyAsync(lab->w, backup, bytes, cudaMemcpyDeviceToDevice, lab->side));
       DSX_CUDA(cudaStreamSynchronize(lab->side));
