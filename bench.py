@@ -240,9 +240,14 @@ def our_arm(args, world, rank, local_rank, dist):
     sched_text = None
     if schedule_src == "measured":
         # DreamDDP's loop on this box: CUDA-event profile of every layer's
-        # local step and cross-rank average, identical on all ranks (max),
-        # then the bit-exact DFS + bubble-fill scheduler on it
+        # local step (with its noise read: one step runs first) and cross-rank
+        # average under load, identical on all ranks (max), then the bit-exact
+        # DFS + bubble-fill scheduler on it
+        lab.step(learning_rate(0, H), fixed_masks[0])
+        lab.sync()
         sets, fills, sched_text = measured_schedule(lab, sizes, H, dist, rank)
+        lab.seed(args.seed)
+        lab.fill(0.0)
     masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
 
     def barrier():

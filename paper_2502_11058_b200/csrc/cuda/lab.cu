@@ -2257,14 +2257,17 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
   DSX_CUDA(cudaEventCreate(&e0));
   DSX_CUDA(cudaEventCreate(&e1));
   std::vector<float> ts(reps);
+  // with an engine run available, the local step reads its noise like the
+  // real step does (reading leaves every state untouched)
+  const int pnoise = (lab->engine && lab->batch_set >= 0) ? 2 : 0;
   int tb = 0;
   for (int b = 0; b < lab->L; ++b) {
     int te = tb;
     while (te < lab->ntiles && lab->h_tiles[te].block == b) ++te;
     for (int r = 0; r < reps; ++r) {
       DSX_CUDA(cudaEventRecord(e0, lab->stream));
-      if (lab->dtype == DSX_F64) launch_update<double>(lab, lab->stream, tb, te - tb, 0, false, none, 0.0);
-      else launch_update<float>(lab, lab->stream, tb, te - tb, 0, false, none, 0.0);
+      if (lab->dtype == DSX_F64) launch_update<double>(lab, lab->stream, tb, te - tb, pnoise, false, none, 0.0);
+      else launch_update<float>(lab, lab->stream, tb, te - tb, pnoise, false, none, 0.0);
       DSX_CUDA(cudaEventRecord(e1, lab->stream));
       DSX_CUDA(cudaEventSynchronize(e1));
       DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
@@ -2280,8 +2283,8 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
   if (!(lab->nranks == 1 && lab->link_bw > 0.0)) {
     for (int r = 0; r < reps; ++r) {
       DSX_CUDA(cudaEventRecord(e0, lab->stream));
-      if (lab->dtype == DSX_F64) launch_update<double>(lab, lab->stream, 0, lab->ntiles, 0, false, none, 0.0);
-      else launch_update<float>(lab, lab->stream, 0, lab->ntiles, 0, false, none, 0.0);
+      if (lab->dtype == DSX_F64) launch_update<double>(lab, lab->stream, 0, lab->ntiles, pnoise, false, none, 0.0);
+      else launch_update<float>(lab, lab->stream, 0, lab->ntiles, pnoise, false, none, 0.0);
       DSX_CUDA(cudaEventRecord(e1, lab->stream));
       DSX_CUDA(cudaEventSynchronize(e1));
       DSX_CUDA(cudaEventElapsedTime(&ts[r], e0, e1));
@@ -2358,10 +2361,16 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
         t_comm[b] = ts[reps / 2] * 1e-3;
       }
       // the step averages in `chunks` groups (two barriers each), not per
-      // layer: rescale to the grouped whole-model average
+      // layer, and while the local step runs: rescale to the grouped
+      // whole-model average timed under a concurrent fused update
       const int G = lab->overlap ? std::max(1, std::min(lab->chunks, lab->ntiles)) : 1;
       for (int r = 0; r < reps; ++r) {
         DSX_TRY(bar_landed());
+        DSX_CUDA(cudaStreamSynchronize(lab->side));
+        if (lab->overlap) {
+          if (lab->dtype == DSX_F64) launch_update<double>(lab, lab->stream, 0, lab->ntiles, pnoise, false, none, 0.0);
+          else launch_update<float>(lab, lab->stream, 0, lab->ntiles, pnoise, false, none, 0.0);
+        }
         DSX_CUDA(cudaEventRecord(e0, lab->side));
         for (int g = 0; g < G; ++g) {
           const int te = lab->ntiles - (int)((long long)lab->ntiles * g / G);
@@ -2395,6 +2404,7 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
         const double scale = ts[reps / 2] * 1e-3 / alone;
         for (int b = 0; b < lab->L; ++b) t_comm[b] *= scale;
       }
+      DSX_CUDA(cudaStreamSynchronize(lab->stream));
       DSX_CUDA(cudaMemcpyAsync(lab->w, backup, bytes, cudaMemcpyDeviceToDevice, lab->side));
       DSX_CUDA(cudaStreamSynchronize(lab->side));
       cudaFree(backup);
