@@ -1681,7 +1681,11 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
   cudaEventCreateWithFlags(&lab->ev_split, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&lab->ev_synced, cudaEventDisableTiming);
   if (lab->engine) {
-    if (cudaStreamCreateWithPriority(&lab->nstream, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
+    // DSX_NOISE_PRIO=0: the engine stream at the compute stream's priority
+    // (batched runs have several steps of slack), else high priority
+    const char* np = std::getenv("DSX_NOISE_PRIO");
+    const int nprio = (np && np[0] == '0') ? lo_prio : hi_prio;
+    if (cudaStreamCreateWithPriority(&lab->nstream, cudaStreamNonBlocking, nprio) != cudaSuccess)
       return cleanup(fail(DSX_ERR_CUDA, "noise stream creation failed"));
     for (int b = 0; b < 2; ++b) {
       cudaEventCreateWithFlags(&lab->ev_noise[b], cudaEventDisableTiming);
