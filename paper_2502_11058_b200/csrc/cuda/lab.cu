@@ -1637,8 +1637,12 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
     lab->q.opt = lab->opt;
   }
   if (lab->sigma > 0.0) {
+    // steps per engine run: the jump-ahead count per run is ~P*kl (P capped
+    // so the segment CTAs fill the GPU), so fewer local workers need longer
+    // runs to amortise it: 4 steps at 8 workers, up to 16 at 1-2
     const char* nb = std::getenv("DSX_NOISE_BATCH");
-    lab->tmax = std::max(1, std::min(16, nb ? std::atoi(nb) : kNoiseBatch));
+    const int def = std::max(kNoiseBatch, std::min(16, 32 / std::max(1, lab->kl)));
+    lab->tmax = std::max(1, std::min(16, nb ? std::atoi(nb) : def));
   }
   if (cudaMalloc(&lab->mt, (1 + 2 * (size_t)lab->tmax) * 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
     return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(mt) failed"));

@@ -25,7 +25,7 @@ namespace {
 
 constexpr int kDeg = 19937;               // deg phi
 constexpr int kPolyWords = 312;            // ceil(19938 / 64)
-constexpr int kPrefixWords = 65 * kMtN;    // Y[0 .. 20280): >= 1 + 19940 + 311 + 10
+constexpr int kPrefixWords = 66 * kMtN;    // Y[0 .. 20592): >= 1 + 19968 + 311 + 16 (jump2 reads)
 constexpr int kJumpBits = 19952;           // c padded to a multiple of 16
 constexpr int kCkWords = kMtN + 4;         // x[312], carry flag, carry bits, local count, pad
 constexpr int kThreads = 320;
@@ -412,6 +412,83 @@ mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 
 #pragma unroll
     for (int q = 0; q < kJA; ++q)
       if (j0 + q < kMtN) out[j0 + q] = acc[q];
+  }
+}
+
+// Jump kernel v2 (the default).  The polynomial c_s is split into kJ2Parts
+// bit ranges, one warp each; a warp covers all 312 window words (lane l owns
+// words 11l .. 11l+10, an odd stride so the 64-bit shared loads are
+// conflict-free), so each set bit costs 11 XOR64 per lane against one
+// shared load per bit for the sliding window — 2.4x fewer instructions per
+// jump than one warp per quarter window.  The parts' partial windows are
+// XOR-reduced through shared memory.  kJ2PerCta jumps of one worker share
+// the CTA's copy of the stream prefix.
+constexpr int kJ2PerCta = 2;
+constexpr int kJ2A = 11;                              // words per lane
+constexpr int kJ2Q = 16;                              // ring (= kJ2A + 5 prefetch)
+constexpr int kJ2Lanes = (kMtN + kJ2A - 1) / kJ2A;    // 29
+constexpr int kJ2Span = 19968;                        // bits over all parts (c padded)
+static_assert(kJ2Span >= kDeg && kJ2Span <= 32 * (kJumpBits / 32 + 1), "parts");
+static_assert(1 + kJ2Span + kJ2Lanes * kJ2A + kJ2Q <= kPrefixWords + kJ2A, "prefix");
+
+template <int kJ2Parts>
+__global__ void __launch_bounds__(kJ2PerCta * kJ2Parts * 32)
+mt_jump2_kernel(const uint64_t* ybuf, const uint32_t* cbits, uint64_t* win, int P) {
+  constexpr int kJ2Bits = kJ2Span / kJ2Parts;  // bits per part, a multiple of 16
+  static_assert(kJ2Bits % 32 == 0 || kJ2Bits % 16 == 0, "16-bit words");
+  extern __shared__ uint64_t ys[];                    // [kPrefixWords] then partials
+  uint64_t* part = ys + kPrefixWords;                 // [kJ2PerCta][kJ2Parts][kMtN]
+  const int w = blockIdx.y;
+  const uint64_t* y = ybuf + (long long)w * kPrefixWords;
+  for (int i = threadIdx.x; i < kPrefixWords; i += blockDim.x) ys[i] = y[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jl = warp / kJ2Parts, pt = warp % kJ2Parts;
+  const int s = 1 + blockIdx.x * kJ2PerCta + jl;
+  constexpr int kCW = kJumpBits / 32 + 1;
+  uint64_t acc[kJ2A];
+#pragma unroll
+  for (int q = 0; q < kJ2A; ++q) acc[q] = 0;
+  if (s < P) {
+    const uint32_t* c = cbits + (long long)(s - 1) * kCW;
+    const int i_begin = pt * kJ2Bits;
+    const int j0 = lane < kJ2Lanes ? kJ2A * lane : 0;
+    // lanes past the window read (harmless) words near the start; their
+    // accumulators are never stored.  Reads stay inside the prefix: the
+    // last part's bits beyond deg(phi) are zero but the ring still loads.
+    const uint64_t* yb = ys + 1 + j0 + i_begin;
+    uint64_t ring[kJ2Q];
+#pragma unroll
+    for (int q = 0; q < kJ2Q; ++q) ring[q] = yb[q];
+    for (int i0 = 0; i0 < kJ2Bits; i0 += kJ2Q) {
+      const uint32_t cw = c[(i_begin + i0) >> 5] >> ((i_begin + i0) & 31);  // 16 bits
+#pragma unroll
+      for (int u = 0; u < kJ2Q; ++u) {
+        if ((cw >> u) & 1u) {
+#pragma unroll
+          for (int q = 0; q < kJ2A; ++q) acc[q] ^= ring[(u + q) % kJ2Q];
+        }
+        const int nxt = i0 + u + kJ2Q;
+        ring[u] = nxt < kJ2Bits + kJ2Q ? yb[nxt] : 0;
+      }
+    }
+  }
+  uint64_t* mine = part + ((long long)jl * kJ2Parts + pt) * kMtN;
+  if (lane < kJ2Lanes) {
+#pragma unroll
+    for (int q = 0; q < kJ2A; ++q)
+      if (kJ2A * lane + q < kMtN) mine[kJ2A * lane + q] = acc[q];
+  }
+  __syncthreads();
+  // XOR the parts: the CTA's threads cover both jumps' 312 words
+  for (int t = threadIdx.x; t < kJ2PerCta * kMtN; t += blockDim.x) {
+    const int j = t / kMtN, m = t % kMtN;
+    const int sj = 1 + blockIdx.x * kJ2PerCta + j;
+    if (sj >= P) continue;
+    uint64_t v = 0;
+#pragma unroll
+    for (int q = 0; q < kJ2Parts; ++q) v ^= part[((long long)j * kJ2Parts + q) * kMtN + m];
+    win[((long long)w * P + sj) * kMtN + m] = v;
   }
 }
 
@@ -1230,8 +1307,12 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, int max_steps, s
     return false;
   cudaMemset(status_, 0, 2 * 4ull * kl * max_steps);
   if (cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           8 * kPrefixWords) != cudaSuccess) {
-    *err = "noise engine: cannot opt in to 162 KB shared memory";
+                           8 * kPrefixWords) != cudaSuccess ||
+      cudaFuncSetAttribute(mt_jump2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8 * (kPrefixWords + kJ2PerCta * 4 * kMtN)) != cudaSuccess ||
+      cudaFuncSetAttribute(mt_jump2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8 * (kPrefixWords + kJ2PerCta * 8 * kMtN)) != cudaSuccess) {
+    *err = "noise engine: cannot opt in to 205 KB shared memory";
     return false;
   }
   return true;
@@ -1257,8 +1338,27 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int ste
   if (P > 1) {
     mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt_src, ybuf_, win_, P, pnorm);
     ++launches_;
-    dim3 grid((P - 1 + kJumpsPerCta - 1) / kJumpsPerCta, kl_);
-    mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(ybuf_, c.jbits, win_, P);
+    static const bool jump_v1 = [] {
+      const char* e = std::getenv("DSX_JUMP");
+      return e && e[0] == '1';
+    }();
+    if (jump_v1) {
+      dim3 grid((P - 1 + kJumpsPerCta - 1) / kJumpsPerCta, kl_);
+      mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(ybuf_, c.jbits, win_, P);
+    } else {
+      // DSX_JUMP_PARTS: 4 (default) or 8 warps per jump
+      static const int parts = [] {
+        const char* e = std::getenv("DSX_JUMP_PARTS");
+        return e && std::atoi(e) == 8 ? 8 : 4;
+      }();
+      dim3 grid((P - 1 + kJ2PerCta - 1) / kJ2PerCta, kl_);
+      if (parts == 8)
+        mt_jump2_kernel<8><<<grid, kJ2PerCta * 8 * 32, 8 * (kPrefixWords + kJ2PerCta * 8 * kMtN), stream>>>(
+            ybuf_, c.jbits, win_, P);
+      else
+        mt_jump2_kernel<4><<<grid, kJ2PerCta * 4 * 32, 8 * (kPrefixWords + kJ2PerCta * 4 * kMtN), stream>>>(
+            ybuf_, c.jbits, win_, P);
+    }
     ++launches_;
   }
   // DSX_SEG_WS: 2 (default) v5 kernel, 1 single-twister warp-specialized, 0 v3
