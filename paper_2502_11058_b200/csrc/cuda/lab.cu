@@ -226,12 +226,17 @@ __device__ __forceinline__ int seg_search(const unsigned long long* pf, int P, u
 __device__ __forceinline__ double seg_noise(const NoiseView& nv, int k, int seg, long long i) {
   const unsigned long long* pf = nv.pfx + (long long)k * (nv.P + 2);
   const unsigned long long m = nv.base + ((unsigned long long)i >> 1);
-  return nv.slots[((long long)k * (nv.P + 1) + seg) * nv.cap + 2 * (long long)(m - pf[seg]) + (i & 1)];
+  const double* at = nv.slots + ((long long)k * (nv.P + 1) + seg) * nv.cap + 2 * (long long)(m - pf[seg]);
+  if (nv.raw) {  // the accepted attempt (x, y) of pair m -> its two normals
+    const double2 n = mt_polar_normals(at[0], at[1], nv.stddev);
+    return (i & 1) ? n.y : n.x;
+  }
+  return at[i & 1];
 }
 
 // NM: 0 no noise, 1 flat noise buffer, 2 segmented engine output.
 template <typename T, int KL, int NM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   constexpr int KMAX = KL > 0 ? KL : kMaxProg;
   constexpr bool NOISE = NM != 0;
@@ -287,7 +292,12 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     auto noise_at = [&](int k, long long i) -> double {
       if constexpr (NM == 1) return a.noise[k * a.ld + i];
       if constexpr (NM == 2) {
-        if (s_simple) return s_base[k][((unsigned long long)i >> 1) >= s_bound[k]][i];
+        if (s_simple) {
+          const double* at = s_base[k][((unsigned long long)i >> 1) >= s_bound[k]];
+          if (!a.nv.raw) return at[i];
+          const double2 n = mt_polar_normals(at[i & ~1LL], at[(i & ~1LL) + 1], a.nv.stddev);
+          return (i & 1) ? n.y : n.x;
+        }
         const int sg = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
                                   a.nv.base + ((unsigned long long)i >> 1));
         return seg_noise(a.nv, k, sg, i);
@@ -349,6 +359,12 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
             for (int k = 0; k < KL; ++k) np[k] = s_base[k][m >= s_bound[k] ? 1 : 0];
 #pragma unroll
             for (int k = 0; k < KL; ++k) xv[k] = __ldcs(reinterpret_cast<const double2*>(np[k] + i));
+            if (a.nv.raw) {
+              // the polar transform of the engine's raw attempts, here where
+              // the issue slots idle on HBM latency anyway
+#pragma unroll
+              for (int k = 0; k < KL; ++k) xv[k] = mt_polar_normals(xv[k].x, xv[k].y, a.nv.stddev);
+            }
           } else {
 #pragma unroll
             for (int k = 0; k < KL; ++k) xv[k] = make_double2(noise_at(k, i), noise_at(k, i + 1));

@@ -63,4 +63,15 @@ __device__ __forceinline__ double mt_scale(double v, double mult, double stddev)
   return __dadd_rn(__dmul_rn(__dmul_rn(v, mult), stddev), 0.0);
 }
 
+// An accepted attempt (x, y) -> its two normals in the order
+// normal_distribution hands them out: (y * mult, x * mult), scaled
+// (random.tcc:1836-1840).  The same arithmetic wherever it runs, so the
+// engine may store raw attempts and let the consumer transform them.
+__device__ __forceinline__ double2 mt_polar_normals(double x, double y, double stddev) {
+  double r2;
+  mt_polar_accept(x, y, &r2);
+  const double m = mt_polar_mult(r2);
+  return make_double2(mt_scale(y, m, stddev), mt_scale(x, m, stddev));
+}
+
 }  // namespace dsx

@@ -875,6 +875,10 @@ constexpr int kWs2Threads = kProdThreads + kThreads;
 constexpr int kBarProd = 6;
 constexpr int kQCap = 1024;  // FIFO capacity: < 320 carried + 624 new per round
 
+// RAW (the default): the accepted attempts (x, y) are stored as they are and
+// the consumer applies the polar transform (mt_polar_normals) — the update
+// kernel has idle issue slots while it waits on HBM, the engine does not.
+template <bool RAW>
 __global__ void __launch_bounds__(kWs2Threads, 2)
 mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
                       int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
@@ -1063,10 +1067,15 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
     for (int u = 0; u < kPairSlots; ++u) {
       const int idx = u * (kThreads / 32) + cw;
       const int excl = __shfl_sync(0xffffffffu, incl - c, idx);
-      if (acc[u]) fifo[(local + (unsigned long long)(excl + before[u])) % kQCap] = make_double2(px[u], py[u]);
+      const unsigned long long g = local + (unsigned long long)(excl + before[u]);
+      if (acc[u]) {
+        if constexpr (RAW) *reinterpret_cast<double2*>(out + 2 * g) = make_double2(px[u], py[u]);
+        else fifo[g % kQCap] = make_double2(px[u], py[u]);
+      }
     }
     local += (unsigned long long)total;
     hh = hh_next;
+    if constexpr (RAW) continue;     // wcnt[h] is rewritten only two rounds on
     named_sync(kBarCons, kThreads);  // FIFO entries visible
     while (local - head >= 2 * kThreads) {
       const unsigned long long g = head + (unsigned long long)tid;
@@ -1079,7 +1088,8 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
       head += kThreads;
     }
   }
-  for (unsigned long long g = head + (unsigned long long)tid; g < local; g += kThreads) transform(g);
+  if constexpr (!RAW)
+    for (unsigned long long g = head + (unsigned long long)tid; g < local; g += kThreads) transform(g);
   if (tid == 0) {
     cnt[(long long)w * P + s] = local;
     uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
@@ -1097,7 +1107,7 @@ __global__ void __launch_bounds__(kThreads)
 mt_finish_kernel(uint64_t* mt, const int* pnorm, int P, int gens, int ck_every, int nck,
                  unsigned long long pairs_per_step, double stddev, double* slots, long long cap,
                  const unsigned long long* cnt, unsigned long long* pfx, const uint64_t* ck,
-                 const uint64_t* tail, int* status) {
+                 const uint64_t* tail, int* status, int raw) {
   __shared__ Smem sm;
   __shared__ unsigned long long s_pfx_target[3];
   const int w = blockIdx.x, tid = threadIdx.x, t = blockIdx.y;
@@ -1183,9 +1193,14 @@ mt_finish_kernel(uint64_t* mt, const int* pnorm, int P, int gens, int ck_every, 
     if (overflow && e.acc) {
       const unsigned long long m = local + (unsigned long long)e.rank;
       if (2 * m + 1 < (unsigned long long)cap) {
-        const double mult = mt_polar_mult(e.r2);
-        out[2 * m] = mt_scale(e.py, mult, stddev);
-        out[2 * m + 1] = mt_scale(e.px, mult, stddev);
+        if (raw) {
+          out[2 * m] = e.px;
+          out[2 * m + 1] = e.py;
+        } else {
+          const double mult = mt_polar_mult(e.r2);
+          out[2 * m] = mt_scale(e.py, mult, stddev);
+          out[2 * m + 1] = mt_scale(e.px, mult, stddev);
+        }
       }
     }
     if (local + (unsigned long long)e.total > target) {
@@ -1361,15 +1376,25 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int ste
     }
     ++launches_;
   }
-  // DSX_SEG_WS: 2 (default) v5 kernel, 1 single-twister warp-specialized, 0 v3
+  // DSX_SEG_WS: 2 (default) v5 kernel, 1 single-twister warp-specialized, 0 v3;
+  // DSX_NOISE_RAW=0: v5 stores finished normals instead of raw attempts
   static const int ws = [] {
     const char* e = std::getenv("DSX_SEG_WS");
     return e ? std::atoi(e) : 2;
   }();
-  if (ws == 2) {
-    mt_segment_ws2_kernel<<<dim3(P, kl_), kWs2Threads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
-                                                                    ck_every_, c.nck, stddev, slots, c.cap,
-                                                                    cnt, ck_, tail_);
+  static const bool raw_ok = [] {
+    const char* e = std::getenv("DSX_NOISE_RAW");
+    return !(e && e[0] == '0');
+  }();
+  const int raw = ws == 2 && raw_ok ? 1 : 0;
+  raw_[set] = raw;
+  stddev_[set] = stddev;
+  if (ws == 2 && raw) {
+    mt_segment_ws2_kernel<true><<<dim3(P, kl_), kWs2Threads, 0, stream>>>(
+        mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_, c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
+  } else if (ws == 2) {
+    mt_segment_ws2_kernel<false><<<dim3(P, kl_), kWs2Threads, 0, stream>>>(
+        mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_, c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
   } else if (ws == 1) {
     mt_segment_ws_kernel<<<dim3(P, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
                                                                    ck_every_, c.nck, stddev, slots, c.cap,
@@ -1381,7 +1406,7 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int ste
   }
   mt_finish_kernel<<<dim3(kl_, steps), kThreads, 0, stream>>>(mt_dst, pnorm2, P, c.gens, ck_every_, c.nck,
                                                               (dim_ + 1) / 2, stddev, slots, c.cap, cnt, pfx,
-                                                              ck_, tail_, status);
+                                                              ck_, tail_, status, raw);
   launches_ += 2;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -30,6 +30,8 @@ struct NoiseView {
   long long cap;                    // slot capacity (doubles)
   int P;                            // segments (slot P = overflow)
   unsigned long long base;          // first pair of this step in the run's stream
+  int raw;                          // slots hold accepted attempts (x, y), not normals
+  double stddev;                    // for the consumer-side transform (raw)
 };
 
 class NoiseEngine {
@@ -50,7 +52,7 @@ class NoiseEngine {
   NoiseView view(int set, int t) const {
     const Cfg& c = cfg_[set_cfg_[set]];
     return {slots_ + (long long)set * slot_stride_, pfx_ + (long long)set * pfx_stride_, c.cap, c.P,
-            (unsigned long long)t * ((dim_ + 1) / 2)};
+            (unsigned long long)t * ((dim_ + 1) / 2), raw_[set], stddev_[set]};
   }
   int max_steps() const { return cfg_[1].steps; }
   int segments(int steps = 1) const { return cfg_[steps > 1 ? 1 : 0].P; }
@@ -68,6 +70,8 @@ class NoiseEngine {
   int kl_ = 0, ck_every_ = 16;
   Cfg cfg_[2];                     // [0]: one step per run, [1]: max_steps per run
   int set_cfg_[2] = {0, 0};
+  int raw_[2] = {0, 0};            // per set: the last run stored raw attempts
+  double stddev_[2] = {0.0, 0.0};
   long long slot_stride_ = 0, pfx_stride_ = 0;
   uint64_t* ybuf_ = nullptr;       // [kl][kPrefixWords]
   uint64_t* win_ = nullptr;        // [kl][P][312]
