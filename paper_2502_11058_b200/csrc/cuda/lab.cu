@@ -223,11 +223,12 @@ __device__ __forceinline__ int seg_search(const unsigned long long* pf, int P, u
   return lo;
 }
 
+template <bool RAW>
 __device__ __forceinline__ double seg_noise(const NoiseView& nv, int k, int seg, long long i) {
   const unsigned long long* pf = nv.pfx + (long long)k * (nv.P + 2);
   const unsigned long long m = nv.base + ((unsigned long long)i >> 1);
   const double* at = nv.slots + ((long long)k * (nv.P + 1) + seg) * nv.cap + 2 * (long long)(m - pf[seg]);
-  if (nv.raw) {  // the accepted attempt (x, y) of pair m -> its two normals
+  if constexpr (RAW) {  // the accepted attempt (x, y) of pair m -> its two normals
     const double2 n = mt_polar_normals(at[0], at[1], nv.stddev);
     return (i & 1) ? n.y : n.x;
   }
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   constexpr int KMAX = KL > 0 ? KL : kMaxProg;
   constexpr bool NOISE = NM != 0;
+  constexpr bool SEG = NM >= 2;   // engine segments: 2 finished normals, 3 raw attempts
   const int tile_id = a.tile_base + blockIdx.x;
   const Tile t = a.tiles[tile_id];
   const int kl = KL > 0 ? KL : a.kl;
@@ -259,7 +261,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   __shared__ const double* s_base[KL > 0 ? KL : 1][2];
   __shared__ unsigned long long s_bound[KL > 0 ? KL : 1];
   __shared__ int s_simple;
-  if constexpr (NM == 2 && KL > 0) {
+  if constexpr (SEG && KL > 0) {
     if (threadIdx.x == 0) s_simple = 1;
     __syncthreads();
     if (threadIdx.x < KL) {
@@ -291,16 +293,19 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     const int npairs = (int)((end - first) >> 1);
     auto noise_at = [&](int k, long long i) -> double {
       if constexpr (NM == 1) return a.noise[k * a.ld + i];
-      if constexpr (NM == 2) {
+      if constexpr (SEG) {
         if (s_simple) {
           const double* at = s_base[k][((unsigned long long)i >> 1) >= s_bound[k]];
-          if (!a.nv.raw) return at[i];
-          const double2 n = mt_polar_normals(at[i & ~1LL], at[(i & ~1LL) + 1], a.nv.stddev);
-          return (i & 1) ? n.y : n.x;
+          if constexpr (NM == 2) {
+            return at[i];
+          } else {
+            const double2 n = mt_polar_normals(at[i & ~1LL], at[(i & ~1LL) + 1], a.nv.stddev);
+            return (i & 1) ? n.y : n.x;
+          }
         }
         const int sg = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
                                   a.nv.base + ((unsigned long long)i >> 1));
-        return seg_noise(a.nv, k, sg, i);
+        return seg_noise<NM == 3>(a.nv, k, sg, i);
       }
       return 0.0;
     };
@@ -351,7 +356,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
 #pragma unroll
           for (int k = 0; k < KL; ++k) xv[k] = __ldcs(reinterpret_cast<const double2*>(a.noise + k * a.ld + i));
         }
-        if constexpr (NM == 2) {
+        if constexpr (SEG) {
           if constexpr (SIMPLE) {
             const unsigned long long m = (unsigned long long)i >> 1;
             const double* np[KL];
@@ -359,7 +364,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
             for (int k = 0; k < KL; ++k) np[k] = s_base[k][m >= s_bound[k] ? 1 : 0];
 #pragma unroll
             for (int k = 0; k < KL; ++k) xv[k] = __ldcs(reinterpret_cast<const double2*>(np[k] + i));
-            if (a.nv.raw) {
+            if constexpr (NM == 3) {
               // the polar transform of the engine's raw attempts, here where
               // the issue slots idle on HBM latency anyway
 #pragma unroll
@@ -422,10 +427,10 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
         const T w = a.w[k * a.ld + i];
         double xi = 0.0;
         if constexpr (NM == 1) xi = a.noise[k * a.ld + i];
-        if constexpr (NM == 2) {
+        if constexpr (SEG) {
           const int s = seg_search(a.nv.pfx + (long long)k * (a.nv.P + 2), a.nv.P,
                                    a.nv.base + ((unsigned long long)i >> 1));
-          xi = seg_noise(a.nv, k, s, i);
+          xi = seg_noise<NM == 3>(a.nv, k, s, i);
         }
         T wn;
         const auto g = grad_step(w, lam, opt, xi, a.eta, NOISE, &wn);
@@ -445,6 +450,199 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     for (int k = 0; k < kl; ++k) {
       const double s = block_sum(nsq[k], red);
       if (threadIdx.x == 0) a.norm_part[(long long)k * a.ntiles + tile_id] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Async-staged update kernel (fp64, 2..8 local rows; opt-in, DSX_UPD_ASYNC=1).
+// The loads of chunk c+2 are in flight (cp.async, 16-B per row and pair,
+// straight into shared memory) while chunk c is computed, so memory-level
+// parallelism no longer costs registers and the polar transform of the
+// engine's raw attempts hides under HBM time.  512 threads: each pair of
+// coordinates is owned by two threads of one warp (lanes l, l^16), each
+// updating half of the rows; the pairwise worker sum splits at KL/2 exactly
+// like pairwise_coord_sum, so the halves combine with one shuffle.
+// ---------------------------------------------------------------------------
+constexpr int kAThreads = 512;
+constexpr int kAPairs = 256;   // pairs per chunk
+constexpr int kAStages = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int KL, int NM>
+__global__ void __launch_bounds__(kAThreads, 1)
+lab_update_async_kernel(UpdateArgs<double> a) {
+  static_assert(KL >= 2 && KL % 2 == 0, "rows split over two threads");
+  constexpr int KH = KL / 2;
+  constexpr bool NOISE = NM != 0;
+  extern __shared__ __align__(16) double2 stage[];  // [kAStages][2 (w, x)][KL][kAPairs]
+  const int tile_id = a.tile_base + blockIdx.x;
+  const Tile t = a.tiles[tile_id];
+  const bool avg = a.average && mask_has(a.mask, t.block);
+  const bool part = a.partial_out != nullptr && mask_has(a.mask, t.block);
+  const bool stale = a.mean_in != nullptr && mask_has(a.stale, t.block);
+  const int tid = threadIdx.x;
+  const int pl = (tid >> 5) * 16 + (tid & 15);  // pair lane 0..255
+  const int h = (tid >> 4) & 1;                 // row half
+  const int k0 = h * KH;
+  __shared__ const double* s_base[KL][2];
+  __shared__ unsigned long long s_bound[KL];
+  __shared__ int s_simple;
+  if constexpr (NM == 2) {
+    if (tid == 0) s_simple = 1;
+    __syncthreads();
+    if (tid < KL) {
+      const int k = tid;
+      const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
+      const unsigned long long m0 = a.nv.base + ((unsigned long long)t.start >> 1);
+      const unsigned long long m1 = a.nv.base + ((unsigned long long)(t.start + t.len - 1) >> 1);
+      const int s0 = seg_search(pf, a.nv.P, m0);
+      const int s1 = s0 < a.nv.P ? s0 + 1 : s0;
+      const double* slot0 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s0) * a.nv.cap;
+      const double* slot1 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s1) * a.nv.cap;
+      s_base[k][0] = slot0 - 2 * (long long)pf[s0] + 2 * (long long)a.nv.base;
+      s_base[k][1] = slot1 - 2 * (long long)pf[s1] + 2 * (long long)a.nv.base;
+      s_bound[k] = s0 < a.nv.P ? pf[s0 + 1] - a.nv.base : ~0ull;
+      if (s1 < a.nv.P && m1 >= pf[s1 + 1]) s_simple = 0;
+    }
+    __syncthreads();
+  }
+  // 16-byte address of coordinate pair (i, i+1)'s noise for worker k
+  auto noise_pair = [&](int k, long long i) -> const double* {
+    const unsigned long long m = (unsigned long long)i >> 1;
+    if (s_simple) return s_base[k][m >= s_bound[k] ? 1 : 0] + i;
+    const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
+    const int sg = seg_search(pf, a.nv.P, a.nv.base + m);
+    return a.nv.slots + ((long long)k * (a.nv.P + 1) + sg) * a.nv.cap + 2 * (long long)(a.nv.base + m - pf[sg]);
+  };
+  auto noise_of = [&](int k, long long i) -> double {  // one coordinate (scalar head / tail)
+    const double* at = noise_pair(k, i & ~1LL);
+    if (!a.nv.raw) return at[i & 1];
+    const double2 n = mt_polar_normals(at[0], at[1], a.nv.stddev);
+    return (i & 1) ? n.y : n.x;
+  };
+  double nsq[KL];  // scalar head / tail (threads 0, 1): every row
+  double nh[KH];   // main loop: this thread's rows k0 + q
+#pragma unroll
+  for (int k = 0; k < KL; ++k) nsq[k] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) nh[q] = 0.0;
+  const long long first = t.start + (t.start & 1);
+  const long long end = t.start + t.len;
+  const int npairs = (int)((end - first) >> 1);
+  // odd head / tail: one scalar coordinate each, all rows by one thread
+  if ((tid == 0 && first != t.start) || (tid == 1 && first + 2 * (long long)npairs < end)) {
+    const long long i = tid == 0 ? t.start : end - 1;
+    double lam, opt;
+    quad_coeffs(a.q, i, &lam, &opt);
+    double wn[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+      const double x = NOISE ? noise_of(k, i) : 0.0;
+      const double g = grad_step(stale ? a.mean_in[i] : a.w[k * a.ld + i], lam, opt, x, a.eta, NOISE, &wn[k]);
+      nsq[k] += g * g;
+    }
+    if (part) {
+      a.partial_out[i] = psum<0, KL, double>(wn);
+    } else {
+      const double m = avg ? psum<0, KL, double>(wn) / (double)a.k_total : 0.0;
+#pragma unroll
+      for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = avg ? m : wn[k];
+    }
+  }
+  const int nchunks = (npairs + kAPairs - 1) / kAPairs;
+  auto slot = [&](int st, int which, int k) -> double2* {
+    return stage + (((long long)st * 2 + which) * KL + k) * kAPairs + pl;
+  };
+  auto issue = [&](int c) {
+    if (c < nchunks) {
+      const int pr = c * kAPairs + pl;
+      if (pr < npairs) {
+        const long long i = first + 2 * (long long)pr;
+        const int st = c % kAStages;
+#pragma unroll
+        for (int q = 0; q < KH; ++q) {
+          const int k = k0 + q;
+          if (stale) {
+            if (q == 0) cp_async16(slot(st, 0, k), a.mean_in + i);
+          } else {
+            cp_async16(slot(st, 0, k), a.w + k * a.ld + i);
+          }
+          if constexpr (NM == 2) cp_async16(slot(st, 1, k), noise_pair(k, i));
+        }
+      }
+    }
+    cp_async_commit();  // (possibly empty) group per chunk keeps the counting uniform
+  };
+  issue(0);
+  issue(1);
+  for (int c = 0; c < nchunks; ++c) {
+    issue(c + 2);
+    cp_async_wait<2>();  // this thread's copies of chunk c have landed
+    const int pr = c * kAPairs + pl;
+    const bool live = pr < npairs;
+    const int st = c % kAStages;
+    const long long i = first + 2 * (long long)(live ? pr : 0);
+    double w0[KH], w1[KH];
+    if (live) {
+      double lam0, opt0, lam1, opt1;
+      quad_coeffs(a.q, i, &lam0, &opt0);
+      quad_coeffs(a.q, i + 1, &lam1, &opt1);
+#pragma unroll
+      for (int q = 0; q < KH; ++q) {
+        const int k = k0 + q;
+        const double2 wv = *slot(st, 0, stale ? k0 : k);
+        double2 xv = make_double2(0.0, 0.0);
+        if constexpr (NM == 2) {
+          xv = *slot(st, 1, k);
+          if (a.nv.raw) xv = mt_polar_normals(xv.x, xv.y, a.nv.stddev);
+        }
+        const double g0 = grad_step(wv.x, lam0, opt0, xv.x, a.eta, NOISE, &w0[q]);
+        const double g1 = grad_step(wv.y, lam1, opt1, xv.y, a.eta, NOISE, &w1[q]);
+        nh[q] += g0 * g0 + g1 * g1;
+      }
+    }
+    // pairwise sum over all KL rows: this half's subtree, then the other
+    // half's from lane ^ 16 (psum<0,KL> = psum<0,KH> + psum<KH,KL>)
+    double s0 = 0.0, s1 = 0.0;
+    if (avg || part) {
+      const double m0 = psum<0, KH, double>(w0), m1 = psum<0, KH, double>(w1);
+      const double o0 = __shfl_xor_sync(0xffffffffu, m0, 16), o1 = __shfl_xor_sync(0xffffffffu, m1, 16);
+      s0 = h == 0 ? m0 + o0 : o0 + m0;
+      s1 = h == 0 ? m1 + o1 : o1 + m1;
+    }
+    if (live) {
+      if (avg) {
+        const double2 m = make_double2(s0 / (double)a.k_total, s1 / (double)a.k_total);
+#pragma unroll
+        for (int q = 0; q < KH; ++q) *reinterpret_cast<double2*>(a.w + (k0 + q) * a.ld + i) = m;
+      } else if (part) {
+        if (h == 0) *reinterpret_cast<double2*>(a.partial_out + i) = make_double2(s0, s1);
+      } else {
+#pragma unroll
+        for (int q = 0; q < KH; ++q)
+          *reinterpret_cast<double2*>(a.w + (k0 + q) * a.ld + i) = make_double2(w0[q], w1[q]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  {
+    __shared__ double red[kAThreads / 32];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+      double v = nsq[k];
+#pragma unroll
+      for (int q = 0; q < KH; ++q)
+        if (k0 + q == k) v += nh[q];
+      const double sk = block_sum(v, red);
+      if (tid == 0) a.norm_part[(long long)k * a.ntiles + tile_id] = sk;
     }
   }
 }
@@ -667,7 +865,7 @@ __global__ void gradient_kernel(const T* w, unsigned long long dim, QuadParams q
     if (nm == 1) gi = __dadd_rn(gi, flat[i]);
     if (nm == 2) {
       const int s = seg_search(nv.pfx + (long long)k * (nv.P + 2), nv.P, nv.base + ((unsigned long long)i >> 1));
-      gi = __dadd_rn(gi, seg_noise(nv, k, s, i));
+      gi = __dadd_rn(gi, nv.raw ? seg_noise<true>(nv, k, s, i) : seg_noise<false>(nv, k, s, i));
     }
     g[i] = gi;
   }
@@ -1031,7 +1229,30 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.mean_in = lab->stale_any ? static_cast<const T*>(lab->staging) : nullptr;
   a.stale = lab->stale_bits;
   if (lab->engine) a.nv = lab->engine->view(lab->cur_set, lab->cur_t);
-  if (nm == 2) {
+  if constexpr (std::is_same_v<T, double> && KL >= 2 && KL % 2 == 0) {
+    // async-staged kernel, opt-in (DSX_UPD_ASYNC=1): measured no faster
+    // than the register-staged one (0.42 ms at sigma=1, 8 workers)
+    static const bool use_async = [] {
+      const char* e = std::getenv("DSX_UPD_ASYNC");
+      return e && e[0] == '1';
+    }();
+    if (use_async && nm != 1) {
+      constexpr size_t smem = sizeof(double2) * kAStages * 2 * KL * kAPairs;
+      static const bool attr = [] {
+        cudaFuncSetAttribute(lab_update_async_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lab_update_async_kernel<KL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+      }();
+      (void)attr;
+      if (nm == 2) lab_update_async_kernel<KL, 2><<<count, kAThreads, smem, s>>>(a);
+      else lab_update_async_kernel<KL, 0><<<count, kAThreads, smem, s>>>(a);
+      ++lab->launches;
+      return;
+    }
+  }
+  if (nm == 2 && a.nv.raw) {
+    lab_update_kernel<T, KL, 3><<<count, kThreads, 0, s>>>(a, lab->prog_local);
+  } else if (nm == 2) {
     lab_update_kernel<T, KL, 2><<<count, kThreads, 0, s>>>(a, lab->prog_local);
   } else if (nm == 1) {
     lab_update_kernel<T, KL, 1><<<count, kThreads, 0, s>>>(a, lab->prog_local);

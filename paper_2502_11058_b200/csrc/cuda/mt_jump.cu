@@ -875,7 +875,7 @@ constexpr int kWs2Threads = kProdThreads + kThreads;
 constexpr int kBarProd = 6;
 constexpr int kQCap = 1024;  // FIFO capacity: < 320 carried + 624 new per round
 
-// RAW (the default): the accepted attempts (x, y) are stored as they are and
+// RAW (opt-in): the accepted attempts (x, y) are stored as they are and
 // the consumer applies the polar transform (mt_polar_normals) — the update
 // kernel has idle issue slots while it waits on HBM, the engine does not.
 template <bool RAW>
@@ -1377,14 +1377,16 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int ste
     ++launches_;
   }
   // DSX_SEG_WS: 2 (default) v5 kernel, 1 single-twister warp-specialized, 0 v3;
-  // DSX_NOISE_RAW=0: v5 stores finished normals instead of raw attempts
+  // DSX_NOISE_RAW=1: v5 stores the raw accepted attempts and the update
+  // kernel applies the polar transform (+3-7 % it/s, but the update kernel
+  // then runs at ~0.64 of HBM instead of ~0.83; off by default)
   static const int ws = [] {
     const char* e = std::getenv("DSX_SEG_WS");
     return e ? std::atoi(e) : 2;
   }();
   static const bool raw_ok = [] {
     const char* e = std::getenv("DSX_NOISE_RAW");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   const int raw = ws == 2 && raw_ok ? 1 : 0;
   raw_[set] = raw;
