@@ -12,6 +12,8 @@
  *                          per-layer times (the CUDA-event profiler's output).
  *   dsc_compare_modes / dsc_simulate_trace — the simulator's predictions,
  *                          set beside the measured GPU timeline.
+ *   dsc_synth_profile    — synth_profile (profile.cpp:188-228) saved as a
+ *                          profile v1 file (the schedule sweep's inputs).
  */
 #ifndef DREAMDDP_DREAMSCHED_C_H_
 #define DREAMDDP_DREAMSCHED_C_H_
@@ -43,6 +45,9 @@ int dsc_compare_modes(const char* profile_path, int period, long long iters, cha
  * schedule) -> trace-event JSON text and the makespan. */
 int dsc_simulate_trace(const char* profile_path, const char* mode, int period, long long iters,
                        char* out, size_t cap, double* makespan);
+/* synth_profile(layers, seed, regime "balanced" | "comm-heavy" |
+ * "compute-heavy") -> save_profile(path). */
+int dsc_synth_profile(const char* path, int layers, uint64_t seed, const char* regime);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,14 @@ int dsc_write_profile(const char* path, int layers, const char* const* names,
   });
 }
 
+int dsc_synth_profile(const char* path, int layers, uint64_t seed, const char* regime) {
+  return guarded([&] {
+    const dreamsched::ModelProfile p =
+        dreamsched::synth_profile(layers, seed, dreamsched::parse_regime(regime ? regime : "balanced"));
+    dreamsched::save_profile(p, path);
+  });
+}
+
 namespace {
 void copy_out(const std::string& t, char* out, size_t cap) {
   if (t.size() + 1 > cap) throw dreamsched::ArgumentError("output buffer too small");

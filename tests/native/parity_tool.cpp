@@ -151,6 +151,21 @@ int cmd_trace(const std::string& path, const std::string& mode, int period, long
   return 0;
 }
 
+// synth_profile (profile.cpp:188-228) for every regime, then its DFS + fill
+// schedule: the schedule sweep's inputs.
+int cmd_synth(int l_count, unsigned long long seed) {
+  for (const char* regime : {"balanced", "comm-heavy", "compute-heavy"}) {
+    const ModelProfile p = synth_profile(l_count, seed, parse_regime(regime));
+    write_profile(p, std::cout);
+    for (int h : {2, 4, 8}) {
+      if (h > l_count) continue;
+      const Schedule s = bubble_fill(schedule_dfs(p, h).best, p);
+      write_schedule(s, std::cout);
+    }
+  }
+  return 0;
+}
+
 // Builds the lab problem: either make_quadratic(dim, blocks, ...) or, when
 // `profile` is non-empty, one block per profile layer sized param_bytes/4
 // (min 1) with make_quadratic's evenly spread curvature.
@@ -355,6 +370,7 @@ int main(int argc, char** argv) {
     if (cmd == "profile" && argc >= 4) return cmd_profile(argv[2], std::atoi(argv[3]));
     if (cmd == "trace" && argc >= 6) return cmd_trace(argv[2], argv[3], std::atoi(argv[4]), std::atoll(argv[5]));
     if (cmd == "steps") return cmd_steps(argc, argv);
+    if (cmd == "synth" && argc >= 4) return cmd_synth(std::atoi(argv[2]), std::strtoull(argv[3], nullptr, 10));
     if (cmd == "train" && argc >= 3) return cmd_train(argv[2]);
     if (cmd == "bench") return cmd_bench(argc, argv);
     if (cmd == "apibench") return cmd_apibench();

@@ -77,6 +77,28 @@ def test_trace_json_byte_identical():
     assert out == G.read("trace_three_layer_plsgd.txt")
 
 
+@pytest.mark.skipif(not os.path.exists(REF_TOOL), reason="reference build absent")
+@pytest.mark.parametrize("L,seed", [(12, 1), (24, 7), (36, 3), (48, 11)])
+def test_synth_profile_sweep_inputs_match_reference(L, seed):
+    """synth_profile (the schedule sweep's generator) and its DFS + fill
+    schedules, byte-identical to the reference for every regime."""
+    ref = subprocess.run([REF_TOOL, "synth", str(L), str(seed)], check=True, capture_output=True,
+                         text=True).stdout
+    assert run_tool("synth", str(L), str(seed)) == ref
+
+
+def test_c_abi_synth_profile(tmp_path):
+    import ctypes as C
+
+    from paper_2502_11058_b200 import native
+    from paper_2502_11058_b200.lab import _dsc
+    native.load_dsx()
+    path = str(tmp_path / "s.profile")
+    assert _dsc().dsc_synth_profile(path.encode(), C.c_int(12), C.c_uint64(1), b"balanced") == 0
+    assert open(path).read() == run_tool("synth", "12", "1").split("dreamsched-schedule")[0]
+    assert _dsc().dsc_synth_profile(path.encode(), C.c_int(12), C.c_uint64(1), b"bogus") == 1
+
+
 def test_c_abi_simulator_matches_trace_fixture():
     """dsc_simulate_trace + dsc_compare_modes (the C-ABI the four-mode GPU
     runner uses) reproduce the reference's trace + mode report byte for byte."""
