@@ -192,7 +192,7 @@ def workload_config(args, world, dim, schedule_src="profile"):
 
 # ------------------------------------------------------------------ our arm ---
 
-def measured_schedule(lab, sizes, H, dist, rank):
+def measured_schedule(lab, sizes, H, dist, rank, fill=True):
     import tempfile
 
     import numpy as np
@@ -208,7 +208,7 @@ def measured_schedule(lab, sizes, H, dist, rank):
     path = os.path.join(tempfile.mkdtemp(prefix=f"dreamddp_r{rank}_"), "measured.profile")
     write_profile(path, [int(s) * 8 for s in sizes], np.zeros(len(sizes)), t_bp, t_comm,
                   bandwidth=1.0, latency=0.0)
-    sets, fills, _, text = schedule_from_profile(path, H)
+    sets, fills, _, text = schedule_from_profile(path, H, fill=fill)
     return sets, fills, text
 
 def our_arm(args, world, rank, local_rank, dist):
@@ -317,18 +317,6 @@ def our_arm(args, world, rank, local_rank, dist):
         return round(float(np.mean([np.dot(m[1:], sz) / dim for m in ms])), 4)
 
     schedule_info = {"source": schedule_src, "synced_param_frac_per_step": synced_frac(masks)}
-    averaging = None
-    if world > 1 and sync_mean > 0:
-        # cross-rank average of the synced layers: ring-convention bytes
-        # 2(W-1)/W x S per rank over NVLink, S = synced bytes of the exchange row
-        esz_b = 8 if args.dtype == "f64" else 4
-        S = synced_frac(masks) * dim * esz_b
-        ach = 2 * (world - 1) / world * S / (sync_mean * 1e-3) / 1e9
-        averaging = {"bound": "nvlink", "kernel": "p2p_average (peer-memory reduce + broadcast)",
-                     "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
-                     "frac": round(ach / 900.0, 4), "peak_kind": "nominal NVLink5 per direction",
-                     "synced_bytes_per_step": int(S), "sync_ms_per_iter": round(sync_mean, 5),
-                     "note": "sync span includes the flag barriers and runs under the concurrent update"}
     if schedule_src == "measured":
         schedule_info["text"] = sched_text
         # the same workload under the fixed profile's schedule, for comparison
@@ -368,6 +356,18 @@ def our_arm(args, world, rank, local_rank, dist):
         sync_mean, exposed_mean = float(t[0]), float(t[1])
     else:
         sync_mean, exposed_mean = 0.0, 0.0
+    averaging = None
+    if world > 1 and sync_mean > 0:
+        # cross-rank average of the synced layers: ring-convention bytes
+        # 2(W-1)/W x S per rank over NVLink, S = synced bytes of the exchange row
+        esz_b = 8 if args.dtype == "f64" else 4
+        S = synced_frac(masks) * dim * esz_b
+        ach = 2 * (world - 1) / world * S / (sync_mean * 1e-3) / 1e9
+        averaging = {"bound": "nvlink", "kernel": "p2p_average (peer-memory reduce + broadcast)",
+                     "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
+                     "frac": round(ach / 900.0, 4), "peak_kind": "nominal NVLink5 per direction",
+                     "synced_bytes_per_step": int(S), "sync_ms_per_iter": round(sync_mean, 5),
+                     "note": "sync span includes the flag barriers and runs under the concurrent update"}
 
     # roofline: the dominant kernel on the path
     esz = 8 if args.dtype == "f64" else 4

@@ -11,7 +11,8 @@ reference's generator, profile.cpp:188-228) scaled to --dim parameters per
 worker; K = 8 workers over the N ranks; sigma = 1.  The plsgd schedule is
 DFS + bubble fill on the profile measured on these GPUs (dsx_lab_profile),
 FLSGD averages every layer every H-th step.  Reports iterations/s and the
-exposed / total sync time per iteration of both.
+exposed / total sync time per iteration of each (and of plsgd without
+the bubble fill, whose extra averages are free only in the cost model).
 """
 import argparse
 import ctypes as C
@@ -113,16 +114,19 @@ def main():
             lab.sync()
             sets, fills, text = bench.measured_schedule(lab, sizes, H, dist, rank)
             masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
+            masks_nf = [sync_mask("partial", H, r, L, sets, None) for r in range(H)]
             nothing = np.zeros(L + 1, dtype=np.uint8)
             steps = max(8 * H, 24)
             plsgd = run_mode(lab, lambda r: masks[r % H], H, steps, dist)
+            plsgd_nf = run_mode(lab, lambda r: masks_nf[r % H], H, steps, dist)
             flsgd = run_mode(lab, lambda r: everything if (r + 1) % H == 0 else nothing, H, steps, dist)
             lab.close()
             row = {"H": H, "L": L, "dim_per_worker": dim, "gpus": world, "workers": K,
                    "synced_param_frac_per_step": round(float(np.mean(
                        [np.dot(m[1:], sizes) / dim for m in masks])), 4),
-                   "plsgd": plsgd, "flsgd": flsgd,
-                   "speedup_vs_flsgd": round(plsgd["it_per_s"] / flsgd["it_per_s"], 4)}
+                   "plsgd": plsgd, "plsgd_no_fill": plsgd_nf, "flsgd": flsgd,
+                   "speedup_vs_flsgd": round(plsgd["it_per_s"] / flsgd["it_per_s"], 4),
+                   "speedup_no_fill_vs_flsgd": round(plsgd_nf["it_per_s"] / flsgd["it_per_s"], 4)}
             rows.append(row)
             if rank == 0:
                 print(json.dumps(row), flush=True)
