@@ -87,6 +87,9 @@ def main():
     ap.add_argument("--regime", default="balanced")
     ap.add_argument("--H", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--L", type=int, nargs="+", default=[12, 24, 36, 48])
+    ap.add_argument("--link-ratio", type=float, default=None,
+                    help="throttle the sync link (dsx_lab_set_link) so the whole model's transfer "
+                         "takes this multiple of the measured local step: the paper's slow-network regime")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -112,6 +115,14 @@ def main():
             everything = np.ones(L + 1, dtype=np.uint8)
             lab.step(bench.learning_rate(0, H), everything)
             lab.sync()
+            bw = None
+            if a.link_ratio:
+                t_bp, _ = lab.profile(reps=3)
+                import torch
+                t = torch.tensor([float(np.sum(t_bp))], dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                bw = dim * 8 / (a.link_ratio * float(t[0]))
+                lab.set_link(bw, 0.0)
             sets, fills, text = bench.measured_schedule(lab, sizes, H, dist, rank)
             masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
             masks_nf = [sync_mask("partial", H, r, L, sets, None) for r in range(H)]
@@ -119,9 +130,14 @@ def main():
             steps = max(8 * H, 24)
             plsgd = run_mode(lab, lambda r: masks[r % H], H, steps, dist)
             plsgd_nf = run_mode(lab, lambda r: masks_nf[r % H], H, steps, dist)
+            # FLSGD as the paper runs it: the full average after the local step
+            # (simulator.cpp:117-120), not overlapped with it
+            lab.set_overlap(False)
             flsgd = run_mode(lab, lambda r: everything if (r + 1) % H == 0 else nothing, H, steps, dist)
+            lab.set_overlap(True)
             lab.close()
             row = {"H": H, "L": L, "dim_per_worker": dim, "gpus": world, "workers": K,
+                   "link_Bps": bw,
                    "synced_param_frac_per_step": round(float(np.mean(
                        [np.dot(m[1:], sizes) / dim for m in masks])), 4),
                    "plsgd": plsgd, "plsgd_no_fill": plsgd_nf, "flsgd": flsgd,
