@@ -317,6 +317,21 @@ def our_arm(args, world, rank, local_rank, dist):
         return round(float(np.mean([np.dot(m[1:], sz) / dim for m in ms])), 4)
 
     schedule_info = {"source": schedule_src, "synced_param_frac_per_step": synced_frac(masks)}
+    nosync = None
+    if world > 1:
+        # the same steps with nothing to average: what the sync adds to an
+        # iteration once every overlap (update, pipelined noise engine) counts
+        none = np.zeros(L + 1, dtype=np.uint8)
+        lab.sync()
+        barrier()
+        lab.record(0)
+        for _ in range(args.steps):
+            lab.step(learning_rate(r, H), none)
+            r += 1
+        lab.record(1)
+        ms_n = max_ranks([lab.elapsed_ms(0, 1)])[0]
+        lab.sync()
+        nosync = ms_n / args.steps
     if schedule_src == "measured":
         schedule_info["text"] = sched_text
         # the same workload under the fixed profile's schedule, for comparison
@@ -460,6 +475,10 @@ def our_arm(args, world, rank, local_rank, dist):
         "exposed_sync_ms_per_iter": round(exposed_mean, 5),
         "sync_ms_per_iter": round(sync_mean, 5),
         "exposed_sync_frac": round(exposed_mean / sync_mean, 4) if sync_mean > 0 else None,
+        "ms_per_step_without_sync": round(nosync, 5) if nosync else None,
+        "sync_added_ms_per_iter": round(ms_max / args.steps - nosync, 5) if nosync else None,
+        "sync_added_frac": (round((ms_max / args.steps - nosync) / sync_mean, 4)
+                            if nosync and sync_mean > 0 else None),
         "schedule": schedule_info, "averaging": averaging,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks.summary(),
