@@ -448,7 +448,9 @@ def our_arm(args, world, rank, local_rank, dist):
         e2e = {"value": args.e2e_steps / el, "unit": "iterations/s",
                "h2d_bytes_per_step": kl * dim * 8 + rng_bytes,
                "d2h_bytes_per_step": kl * dim * 8 + rng_bytes,
-               "path": "dsx_lab_step_host: host worker rows + rng states in/out every step, chunked H2D/update/D2H overlap"}
+               "path": ("dsx_lab_step_host: host worker rows + rng states in/out every step, " +
+                        ("chunked H2D/update/D2H overlap" if world == 1 else
+                         "rows in overlapping the noise engine, multi-rank step, rows out"))}
 
     if rank != 0:
         lab.close()

@@ -2136,12 +2136,20 @@ dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask
   } guard{lab, lab->pipeline};
   lab->pipeline = false;
   const long long D = (long long)lab->dim;
+  bool contiguous = true;  // rows packed as one [kl][dim] buffer
+  for (int k = 1; k < lab->kl; ++k)
+    if (rows[k] != rows[0] + (long long)k * D) contiguous = false;
   if (lab->dtype != DSX_F64 || lab->nranks != 1 || lab->link_bw > 0.0 || lab->use_chain) {
-    // the staged path: whole rows in, one step, whole rows out
-    for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, rows[k]));
+    // the staged path: whole rows in (one async copy, overlapping the noise
+    // engine), one step, whole rows out
     DSX_CUDA(cudaMemcpy(mt_state(lab, lab->mt_commit), rng, 8ull * (kMtN + 1) * lab->kl, cudaMemcpyHostToDevice));
+    if (contiguous) DSX_TRY(dsx_lab_set_all_params(lab, rows[0]));
+    else
+      for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, rows[k]));
     DSX_TRY(dsx_lab_step(lab, eta, mask));
-    for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, rows[k]));
+    if (contiguous) DSX_TRY(dsx_lab_get_all_params(lab, rows[0]));
+    else
+      for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, rows[k]));
     return dsx_lab_get_state(lab, nullptr, rng);
   }
   if (!lab->h2d) {
