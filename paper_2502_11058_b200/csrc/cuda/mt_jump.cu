@@ -1391,11 +1391,22 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int ste
   const int raw = ws == 2 && raw_ok ? 1 : 0;
   raw_[set] = raw;
   stddev_[set] = stddev;
+  // DSX_SEG_PAD: extra (unused) shared memory per segment CTA, bytes — caps
+  // the engine at fewer CTAs per SM so update CTAs can share its SMs
+  static const int pad = [] {
+    const char* e = std::getenv("DSX_SEG_PAD");
+    const int v = e ? std::atoi(e) : 0;
+    if (v > 0) {
+      cudaFuncSetAttribute(mt_segment_ws2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+      cudaFuncSetAttribute(mt_segment_ws2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+    }
+    return v > 0 ? v : 0;
+  }();
   if (ws == 2 && raw) {
-    mt_segment_ws2_kernel<true><<<dim3(P, kl_), kWs2Threads, 0, stream>>>(
+    mt_segment_ws2_kernel<true><<<dim3(P, kl_), kWs2Threads, pad, stream>>>(
         mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_, c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
   } else if (ws == 2) {
-    mt_segment_ws2_kernel<false><<<dim3(P, kl_), kWs2Threads, 0, stream>>>(
+    mt_segment_ws2_kernel<false><<<dim3(P, kl_), kWs2Threads, pad, stream>>>(
         mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_, c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
   } else if (ws == 1) {
     mt_segment_ws_kernel<<<dim3(P, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,

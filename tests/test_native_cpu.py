@@ -164,3 +164,23 @@ def test_mt_jump_ahead_matches_recurrence(jump):
     ok = C.c_int(0)
     native.call("dsx_mt_jump_selftest", jump, C.byref(ok))
     assert ok.value == 1
+
+
+def test_sweep_layer_sizes_follow_synth_profile():
+    """tools/sweep.py scales synth_profile's layer bytes to the requested
+    per-worker dimension (even sizes, every layer >= 2 coordinates)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("sweep", os.path.join(REPO, "tools", "sweep.py"))
+    sweep = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sweep)
+    from paper_2502_11058_b200.lab import profile_layers
+    sizes = sweep.synth_sizes(24, 1, "balanced", 1_000_000, 0)
+    assert len(sizes) == 24 and all(s >= 2 and s % 2 == 0 for s in sizes)
+    assert abs(sum(sizes) - 1_000_000) <= 2 * 24
+    # proportional to the profile's bytes
+    import subprocess as sp
+    text = sp.run([TOOL, "synth", "24", "1"], check=True, capture_output=True, text=True).stdout
+    pb = [int(ln.split("\t")[2]) for ln in text.split("dreamsched-schedule")[0].splitlines()[1:25]]
+    big = max(range(24), key=lambda i: pb[i])
+    assert sizes[big] == max(sizes)
+    del profile_layers
