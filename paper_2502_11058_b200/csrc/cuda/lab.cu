@@ -1171,6 +1171,10 @@ struct dsx_lab {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
   int host_chunks = 24;
+  // the rng states the last host-state step returned: a caller passing them
+  // back unchanged finds that step's successor noise already generated
+  std::vector<uint64_t> host_rng;
+  bool host_rng_valid = false;
   size_t staging_elems = 0;
   int nsm = 148;
 };
@@ -1768,6 +1772,7 @@ dsx_status launch_engine(dsx_lab* lab, int set, int steps, int src) {
 // Drops generated-but-unconsumed noise (the rest of the current run and a
 // prefetched run): the committed rng state is about to change.
 dsx_status invalidate_prefetch(dsx_lab* lab) {
+  lab->host_rng_valid = false;
   if (lab->nstream) DSX_CUDA(cudaStreamSynchronize(lab->nstream));
   lab->pf_set = -1;
   lab->batch_set = -1;
@@ -2127,8 +2132,15 @@ dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
   DSX_CUDA(cudaStreamSynchronize(lab->side));
   drop_stale(lab);
-  DSX_TRY(invalidate_prefetch(lab));
-  // every call brings its own rng state: one-step engine runs, no prefetch
+  const size_t rng_words = (size_t)(kMtN + 1) * lab->kl;
+  // the caller handing back the states this lab returned last time (a
+  // training loop) keeps the noise generated ahead for them; any other
+  // state drops it
+  const bool rng_hit = lab->host_rng_valid && lab->engine && lab->host_rng.size() == rng_words &&
+                       std::memcmp(lab->host_rng.data(), rng, 8 * rng_words) == 0;
+  if (!rng_hit) DSX_TRY(invalidate_prefetch(lab));
+  lab->host_rng_valid = false;
+  // fresh engine runs here are one step; runs generated ahead use the batch
   struct PipelineOff {
     dsx_lab* l;
     bool on;
@@ -2166,8 +2178,9 @@ dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask
     lab->ev_out.push_back(b);
   }
   // engine states first (small), then the noise engine overlaps the first
-  // parameter chunks' transfer
-  DSX_CUDA(cudaMemcpy(mt_state(lab, lab->mt_commit), rng, 8ull * (kMtN + 1) * lab->kl, cudaMemcpyHostToDevice));
+  // parameter chunks' transfer (or its output is already there: rng_hit)
+  if (!rng_hit)
+    DSX_CUDA(cudaMemcpy(mt_state(lab, lab->mt_commit), rng, 8ull * (kMtN + 1) * lab->kl, cudaMemcpyHostToDevice));
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[0], lab->stream));
   int noise = 0;
   DSX_TRY(run_noise(lab, &noise));
@@ -2219,11 +2232,23 @@ dsx_status dsx_lab_step_host(dsx_lab* lab, double eta, const unsigned char* mask
   ++lab->launches;
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[4], lab->stream));
   DSX_TRY(after_update(lab, noise));
+  // generate the next engine run now, from the state this call returns,
+  // while the parameters stream back (and the caller does its host work)
+  if (noise == 2 && lab->pf_set < 0 && lab->batch_set >= 0 && lab->batch_t >= lab->batch_n) {
+    const int set = 1 - lab->batch_set;
+    DSX_TRY(launch_engine(lab, set, lab->tmax, boundary_slot(lab, lab->batch_set, lab->batch_n - 1)));
+    lab->pf_set = set;
+    lab->pf_n = lab->tmax;
+  }
   DSX_CUDA(cudaMemcpyAsync(rng, mt_state(lab, lab->mt_commit), 8ull * (kMtN + 1) * lab->kl,
                            cudaMemcpyDeviceToHost, lab->stream));
   DSX_CUDA(cudaStreamSynchronize(lab->d2h));
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
   DSX_CUDA(cudaGetLastError());
+  if (noise == 2) {
+    lab->host_rng.assign(rng, rng + rng_words);
+    lab->host_rng_valid = true;
+  }
   return DSX_OK;
 }
 
