@@ -1305,15 +1305,19 @@ int update_blocks_per_sm(int kl, int nm) {
 }
 
 // Overlap groups of the multi-rank step, from the top layer down: cuts[0] =
-// ntiles > cuts[1] > ... > cuts[G] = 0.  Every group but the last holds a
-// whole number of update waves, so each group launch ends on a full wave
-// instead of leaving SMs idle in a partial one.
+// ntiles > cuts[1] > ... > cuts[G] = 0.  When the step has at least G waves
+// of update CTAs, every group but the last holds whole waves, so its launch
+// ends on a full wave instead of leaving SMs idle in a partial one.
 std::vector<int> overlap_groups(const dsx_lab* lab, int want) {
   const int wave = std::max(1, lab->wave);
-  const int G = std::max(1, std::min(want, lab->ntiles / wave));
-  const int per = std::max(1, lab->ntiles / G / wave) * wave;
+  const int G = std::max(1, std::min(want, lab->ntiles));
   std::vector<int> cuts{lab->ntiles};
-  for (int g = 1; g < G; ++g) cuts.push_back(std::max(0, lab->ntiles - g * per));
+  if (lab->ntiles >= G * wave) {  // whole waves per group
+    const int per = (lab->ntiles / G / wave) * wave;
+    for (int g = 1; g < G; ++g) cuts.push_back(lab->ntiles - g * per);
+  } else {  // fewer tiles than G waves: equal groups (measured better than fewer groups)
+    for (int g = 1; g < G; ++g) cuts.push_back(lab->ntiles - (int)((long long)lab->ntiles * g / G));
+  }
   cuts.push_back(0);
   return cuts;
 }
@@ -1527,6 +1531,8 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
                           int noise) {
   const auto ranges = masked_ranges(lab, mask);
   lab->has_ranges = !ranges.empty();
+  // (one group per layer on the throttled link was measured: the per-layer
+  // cross-rank barriers cost far more than the finer overlap gains)
   const std::vector<int> cuts = overlap_groups(lab, lab->overlap ? lab->chunks : 1);
   const int G = (int)cuts.size() - 1;
   T* part = lab->kl > 1 ? static_cast<T*>(lab->staging) : nullptr;
