@@ -477,13 +477,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int KL, int NM>
-__global__ void __launch_bounds__(kAThreads, 1)
-lab_update_async_kernel(UpdateArgs<double> a) {
+__device__ __forceinline__ void async_update_tile(const UpdateArgs<double>& a, int tile_id, double2* stage) {
   static_assert(KL >= 2 && KL % 2 == 0, "rows split over two threads");
   constexpr int KH = KL / 2;
   constexpr bool NOISE = NM != 0;
-  extern __shared__ __align__(16) double2 stage[];  // [kAStages][2 (w, x)][KL][kAPairs]
-  const int tile_id = a.tile_base + blockIdx.x;
   const Tile t = a.tiles[tile_id];
   const bool avg = a.average && mask_has(a.mask, t.block);
   const bool part = a.partial_out != nullptr && mask_has(a.mask, t.block);
@@ -645,6 +642,15 @@ lab_update_async_kernel(UpdateArgs<double> a) {
       if (tid == 0) a.norm_part[(long long)k * a.ntiles + tile_id] = sk;
     }
   }
+  __syncthreads();  // the stage and the tile's shared lookups are reused by the next tile
+}
+
+// Persistent: a CTA walks tiles tile_base + blockIdx.x, + gridDim.x, ...
+template <int KL, int NM>
+__global__ void __launch_bounds__(kAThreads, 1)
+lab_update_async_kernel(UpdateArgs<double> a, int count) {
+  extern __shared__ __align__(16) double2 stage[];  // [kAStages][2 (w, x)][KL][kAPairs]
+  for (int i = blockIdx.x; i < count; i += gridDim.x) async_update_tile<KL, NM>(a, a.tile_base + i, stage);
 }
 
 // ||g_k||^2 = fixed-order sum of the tile partials (one CTA per worker row),
@@ -1249,8 +1255,14 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
         return true;
       }();
       (void)attr;
-      if (nm == 2) lab_update_async_kernel<KL, 2><<<count, kAThreads, smem, s>>>(a);
-      else lab_update_async_kernel<KL, 0><<<count, kAThreads, smem, s>>>(a);
+      // DSX_UPD_ASYNC_CTAS: persistent CTA count (default: one per tile)
+      static const int ctas = [] {
+        const char* e = std::getenv("DSX_UPD_ASYNC_CTAS");
+        return e ? std::atoi(e) : 0;
+      }();
+      const int grid = ctas > 0 ? std::min(ctas, count) : count;
+      if (nm == 2) lab_update_async_kernel<KL, 2><<<grid, kAThreads, smem, s>>>(a, count);
+      else lab_update_async_kernel<KL, 0><<<grid, kAThreads, smem, s>>>(a, count);
       ++lab->launches;
       return;
     }
