@@ -989,7 +989,38 @@ p2p_average_kernel(PeerPtrs peers, long long a, long long b, int k_total, PairPr
   const long long npairs = (b - first) >> 1;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long j = tid; j < npairs; j += stride) {
+  long long j0 = tid;
+  if constexpr (W > 0) {
+    // two pairs per thread per iteration: all 2W peer loads in flight at once
+    for (; j0 + stride < npairs; j0 += 2 * stride) {
+      const long long i0 = first + 2 * j0, i1 = first + 2 * (j0 + stride);
+      V2 v0[W], v1[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        v0[q] = *reinterpret_cast<const V2*>(static_cast<const T*>(peers.p[q]) + i0);
+        v1[q] = *reinterpret_cast<const V2*>(static_cast<const T*>(peers.p[q]) + i1);
+      }
+      T ax[W], ay[W], bx[W], by[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        ax[q] = v0[q].x;
+        ay[q] = v0[q].y;
+        bx[q] = v1[q].x;
+        by[q] = v1[q].y;
+      }
+      V2 m0, m1;
+      m0.x = psum<0, W, T>(ax) / (T)k_total;
+      m0.y = psum<0, W, T>(ay) / (T)k_total;
+      m1.x = psum<0, W, T>(bx) / (T)k_total;
+      m1.y = psum<0, W, T>(by) / (T)k_total;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        *reinterpret_cast<V2*>(static_cast<T*>(peers.p[q]) + i0) = m0;
+        *reinterpret_cast<V2*>(static_cast<T*>(peers.p[q]) + i1) = m1;
+      }
+    }
+  }
+  for (long long j = j0; j < npairs; j += stride) {
     const long long i = first + 2 * j;
     T vx[W > 0 ? W : kMaxProg], vy[W > 0 ? W : kMaxProg];
     const int nr = W > 0 ? W : prog.n + 1;
