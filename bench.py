@@ -288,7 +288,26 @@ def our_arm(args, world, rank, local_rank, dist):
     lab.set_pipeline(False)
     lab.set_instrument(True)
     per = []
+    esz = 8 if args.dtype == "f64" else 4
+    sz = np.asarray(sizes, dtype=np.float64)
+    lazy = world > 1 and 1 < kl <= 8
+
+    def update_bytes_of(m_cur, m_prev):
+        """Algorithmic bytes of one step's update kernels.  Single GPU: every
+        row read and written (+ noise).  Several ranks with >1 local row
+        (lazy broadcast): a layer averaged last step is read once (its mean),
+        a layer averaged this step writes only its subtree sum."""
+        noise = kl * 8 if args.sigma > 0 else 0
+        if not lazy:
+            return float(dim) * (kl * 2 * esz + noise)
+        cur, prev = np.asarray(m_cur[1:], bool), np.asarray(m_prev[1:], bool)
+        reads = np.where(prev, 1, kl) * esz + noise
+        writes = np.where(cur, 1, kl) * esz
+        return float(np.dot(sz, reads + writes))
+
+    step_bytes = []
     for _ in range(2 * H):
+        step_bytes.append(update_bytes_of(masks[r % H], masks[(r - 1) % H]))
         lab.step(learning_rate(r, H), masks[r % H])
         r += 1
         per.append(lab.last_step_times())
@@ -385,9 +404,8 @@ def our_arm(args, world, rank, local_rank, dist):
                      "note": "sync span includes the flag barriers and runs under the concurrent update"}
 
     # roofline: the dominant kernel on the path
-    esz = 8 if args.dtype == "f64" else 4
     peak, peak_kind = measured_peaks()
-    update_bytes = kl * dim * (2 * esz + (8 if args.sigma > 0 else 0))
+    update_bytes = int(round(statistics.mean(step_bytes)))
     upd = statistics.mean(update_ms)
     noi = statistics.mean(noise_ms)
     # The HBM roofline belongs to the update (+ in-kernel averaging) kernel;
