@@ -62,34 +62,66 @@ def parse_args():
 # ---------------------------------------------------------------- helpers ---
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML
+    every 5 ms (nvidia-smi every 100 ms when NVML is unavailable)."""
 
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(device))
+        except Exception:
+            self._nvml = None
 
     def sample_once(self):
+        if self._nvml:
+            nv, h = self._nvml
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, bit in self.REASONS.items():
+                    if bits & bit:
+                        self.reasons.add(name)
+                return
+            except Exception:
+                self._nvml = None
         try:
             out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.QUERY,
                                   "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                  timeout=5).stdout.strip()
-            if out:
-                self.rows.append([x.strip() for x in out.split(",")])
+            r = [x.strip() for x in out.split(",")] if out else []
+            if len(r) >= 9:
+                if r[1].replace(".", "").isdigit():
+                    self.sm.append(float(r[1]))
+                if r[2].replace(".", "").isdigit():
+                    self.mx.append(float(r[2]))
+                for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                    "sw_power_cap"], r[5:9]):
+                    if v.lower() in ("active", "1"):
+                        self.reasons.add(name)
         except Exception:
             pass
 
     def _loop(self):
         while not self._stop.is_set():
             self.sample_once()
-            self._stop.wait(0.1)
+            self._stop.wait(0.005 if self._nvml else 0.1)
 
     def start(self):
+        self.sample_once()  # one sample at the start of the timed region
         self._t = threading.Thread(target=self._loop, daemon=True)
         self._t.start()
 
@@ -97,21 +129,14 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        if not self.rows:
+        if not self.sm:
             self.sample_once()
 
     def summary(self):
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for name, v in zip(names, r[5:9]):
-                if v.strip().lower() in ("active", "1"):
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def measured_peaks():
