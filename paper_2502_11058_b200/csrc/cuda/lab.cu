@@ -107,6 +107,18 @@ struct QuadParams {
   const double* opt;
 };
 
+// Fused cross-rank average (multi-rank, pairwise, <= 8 ranks): a synced
+// tile's CTA publishes its subtree sums, waits for every rank's CTA of the
+// same tile, then averages in the reference's pairwise rank order — the
+// update and the collective in one kernel, tile by tile, over NVLink.
+constexpr int kMaxFuse = 8;
+struct FusedArgs {
+  int R = 0, rank = 0;                       // R == 0: off
+  unsigned long long epoch = 0;              // this step's flag value
+  const void* xs[kMaxFuse] = {};             // every rank's subtree sums (this step's parity)
+  unsigned long long* tf[kMaxFuse] = {};     // every rank's tile flags (this parity) [R][ntiles]
+};
+
 template <typename T>
 struct UpdateArgs {
   T* w;
@@ -126,7 +138,42 @@ struct UpdateArgs {
   T* partial_out;     // multi-rank: subtree sums of synced tiles (else null)
   const T* mean_in;   // multi-rank: cross-rank means of the layers in `stale`
   MaskBits stale;     // layers whose rows are stale: every row equals mean_in
+  FusedArgs fz;       // fused average (multi-rank); mean_out = where the means go
+  T* mean_out;
 };
+
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Publishes this CTA's tile to every rank, then waits (thread 0) until every
+// rank published it; traps after ~30 s instead of hanging.
+__device__ __forceinline__ void fused_tile_barrier(const FusedArgs& f, int ntiles, int tile) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < f.R; ++q) st_release_sys_u64(f.tf[q] + (long long)f.rank * ntiles + tile, f.epoch);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int q = 0; q < f.R; ++q) {
+      const unsigned long long* mine = f.tf[f.rank] + (long long)q * ntiles + tile;
+      while (ld_acquire_sys_u64(mine) < f.epoch) {
+        __nanosleep(32);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 30000000000ull) __trap();
+      }
+    }
+  }
+  __syncthreads();
+}
+
+
 
 // lambda_i and w*_i.  The analytic form is make_quadratic's
 // mu + (beta - mu) * i / (dim - 1) (trainer.cpp:117-120), evaluated with the
@@ -155,6 +202,21 @@ __device__ __forceinline__ T psum(const T* v) {
   } else {
     constexpr int MID = LO + N / 2;
     return psum<LO, MID, T>(v) + psum<MID, HI, T>(v);
+  }
+}
+
+// Pairwise sum over the R ranks' values (split at R/2, like the in-process tree)
+template <typename T>
+__device__ __forceinline__ T rank_psum(const T* v, int R) {
+  switch (R) {
+    case 2: return psum<0, 2, T>(v);
+    case 4: return psum<0, 4, T>(v);
+    case 8: return psum<0, 8, T>(v);
+    case 3: return psum<0, 3, T>(v);
+    case 5: return psum<0, 5, T>(v);
+    case 6: return psum<0, 6, T>(v);
+    case 7: return psum<0, 7, T>(v);
+    default: return v[0];
   }
 }
 
@@ -246,7 +308,11 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   const Tile t = a.tiles[tile_id];
   const int kl = KL > 0 ? KL : a.kl;
   const bool avg = a.average && mask_has(a.mask, t.block);
-  const bool part = KL > 1 && a.partial_out != nullptr && mask_has(a.mask, t.block);
+  // fused cross-rank average of a synced tile (multi-rank): phase 1 writes
+  // this rank's subtree sums into its published buffer (like `part`)
+  const bool fused_tile = KL > 0 && a.fz.R > 0 && mask_has(a.mask, t.block);
+  const bool part = (KL > 1 && a.partial_out != nullptr && mask_has(a.mask, t.block)) || fused_tile;
+  T* const part_dst = fused_tile ? static_cast<T*>(const_cast<void*>(a.fz.xs[a.fz.rank])) : a.partial_out;
   // lazy broadcast: after a cross-rank average the mean lives once in the
   // exchange buffer; all kl rows are logically equal to it, so it is read
   // once instead of kl times (and the rows are never written back while the
@@ -320,7 +386,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
         nsq[k] += to_d(g) * to_d(g);
       }
       if (part) {
-        a.partial_out[i] = psum<0, KL, T>(wn);
+        part_dst[i] = psum<0, KL, T>(wn);
         return;
       }
       const T m = avg ? psum<0, KL, T>(wn) / (T)a.k_total : T(0);
@@ -395,7 +461,7 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
           V2 m;
           m.x = psum<0, KL, T>(w0);
           m.y = psum<0, KL, T>(w1);
-          *reinterpret_cast<V2*>(a.partial_out + i) = m;
+          *reinterpret_cast<V2*>(part_dst + i) = m;
         } else {
 #pragma unroll
           for (int k = 0; k < KL; ++k) {
@@ -409,11 +475,43 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     };
     using Yes = std::true_type;
     using No = std::false_type;
-    const bool simple = NM != 2 || s_simple;
+    const bool simple = !SEG || s_simple;
     if (stale) {
       if (simple) pairs(Yes{}, Yes{}); else pairs(Yes{}, No{});
     } else {
       if (simple) pairs(No{}, Yes{}); else pairs(No{}, No{});
+    }
+    if (fused_tile) {
+      // phase 2: every rank's sums of this tile are published; phase 3: the
+      // cross-rank mean, pairwise over ranks / K, straight from peer memory
+      fused_tile_barrier(a.fz, a.ntiles, tile_id);
+      const int R = a.fz.R;
+      auto mean_at = [&](long long i) -> T {
+        T v[kMaxFuse];
+#pragma unroll
+        for (int q = 0; q < kMaxFuse; ++q) v[q] = q < R ? static_cast<const T*>(a.fz.xs[q])[i] : T(0);
+        return rank_psum<T>(v, R) / (T)a.k_total;
+      };
+      for (int pr = threadIdx.x; pr < npairs; pr += kThreads) {
+        const long long i = first + 2 * (long long)pr;
+        T vx[kMaxFuse], vy[kMaxFuse];
+#pragma unroll
+        for (int q = 0; q < kMaxFuse; ++q) {
+          if (q < R) {
+            const V2 v = *reinterpret_cast<const V2*>(static_cast<const T*>(a.fz.xs[q]) + i);
+            vx[q] = v.x;
+            vy[q] = v.y;
+          } else {
+            vx[q] = vy[q] = T(0);
+          }
+        }
+        V2 m;
+        m.x = rank_psum<T>(vx, R) / (T)a.k_total;
+        m.y = rank_psum<T>(vy, R) / (T)a.k_total;
+        *reinterpret_cast<V2*>(a.mean_out + i) = m;
+      }
+      if (threadIdx.x == 0 && first != t.start) a.mean_out[t.start] = mean_at(t.start);
+      if (threadIdx.x == 1 && first + 2 * (long long)npairs < end) a.mean_out[end - 1] = mean_at(end - 1);
     }
   } else {
     // generic worker count: row pass, then the pairwise program for
@@ -1193,6 +1291,15 @@ struct dsx_lab {
   FlagPtrs fpeers{};                     // every rank's flag block, mapped here
   unsigned int* sig_counter = nullptr;   // finished-block counter of the averaging kernel
   unsigned long long epoch = 0, sig_count = 0;
+  // fused update + average (DSX_FUSED=0: separate averaging kernel): the
+  // published subtree sums [2][dim] and tile flags [2][R][ntiles] of every
+  // rank, mapped into every peer
+  bool fused = false;
+  void* xsum = nullptr;
+  unsigned long long* tflags = nullptr;
+  void* xpeer[kMaxFuse] = {};
+  unsigned long long* tpeer[kMaxFuse] = {};
+  unsigned long long fepoch = 0;
   int chunks = 4;              // overlap groups per step (at most)
   int wave = 296;              // update CTAs resident at once (blocks/SM x SMs)
   bool lazy = true;            // lazy broadcast of cross-rank means (DSX_LAZY=0: off)
@@ -1252,7 +1359,7 @@ dsx_status check_row(dsx_lab* lab, int local) {
 
 template <typename T, int KL>
 void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int nm, bool average,
-                     const MaskBits& mask, double eta, T* partial_out) {
+                     const MaskBits& mask, double eta, T* partial_out, const FusedArgs* fz, T* mean_out) {
   UpdateArgs<T> a{};
   a.w = static_cast<T*>(lab->w);
   a.ld = lab->ld;
@@ -1271,6 +1378,10 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.mean_in = lab->stale_any ? static_cast<const T*>(lab->staging) : nullptr;
   a.stale = lab->stale_bits;
   if (lab->engine) a.nv = lab->engine->view(lab->cur_set, lab->cur_t);
+  if (fz) {
+    a.fz = *fz;
+    a.mean_out = mean_out;
+  }
   if constexpr (std::is_same_v<T, double> && KL >= 2 && KL % 2 == 0) {
     // async-staged kernel, opt-in (DSX_UPD_ASYNC=1): measured no faster
     // than the register-staged one (0.42 ms at sigma=1, 8 workers)
@@ -1278,7 +1389,7 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
       const char* e = std::getenv("DSX_UPD_ASYNC");
       return e && e[0] == '1';
     }();
-    if (use_async && nm != 1) {
+    if (use_async && nm != 1 && !fz) {
       constexpr size_t smem = sizeof(double2) * kAStages * 2 * KL * kAPairs;
       static const bool attr = [] {
         cudaFuncSetAttribute(lab_update_async_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1312,17 +1423,18 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
 
 template <typename T>
 void launch_update(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int noise, bool average,
-                   const MaskBits& mask, double eta, T* partial_out = nullptr) {
+                   const MaskBits& mask, double eta, T* partial_out = nullptr, const FusedArgs* fz = nullptr,
+                   T* mean_out = nullptr) {
   switch (lab->kl) {
-    case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    case 2: return launch_update_t<T, 2>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    case 3: return launch_update_t<T, 3>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    case 4: return launch_update_t<T, 4>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    case 5: return launch_update_t<T, 5>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    case 6: return launch_update_t<T, 6>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    case 7: return launch_update_t<T, 7>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    case 8: return launch_update_t<T, 8>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
-    default: return launch_update_t<T, 0>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 2: return launch_update_t<T, 2>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 3: return launch_update_t<T, 3>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 4: return launch_update_t<T, 4>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 5: return launch_update_t<T, 5>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 6: return launch_update_t<T, 6>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 7: return launch_update_t<T, 7>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 8: return launch_update_t<T, 8>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    default: return launch_update_t<T, 0>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
   }
 }
 
@@ -1688,6 +1800,47 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
   return DSX_OK;
 }
 
+// Multi-rank step with the average fused into the update kernel: one launch
+// over every tile; a synced tile's CTA publishes its subtree sums, waits for
+// the same tile on every rank (peer-memory flags) and writes the pairwise
+// cross-rank mean — into the exchange buffer, read lazily by the next step,
+// or (one worker per GPU) straight into the row.  No separate averaging
+// kernel, barrier or launch; the transfer overlaps other tiles' updates.
+template <typename T>
+dsx_status step_multi_fused(dsx_lab* lab, double eta, const unsigned char* mask, const MaskBits& bits,
+                            int noise) {
+  const auto ranges = masked_ranges(lab, mask);
+  lab->has_ranges = !ranges.empty();
+  // buffers alternate per SYNCED step: a rank writing the sums of synced
+  // step e+2 has waited on some tile of step e+1 of every peer, which each
+  // peer publishes only after its step-e kernel (all of its reads of the
+  // e-buffer) completed
+  const int parity = lab->has_ranges ? (int)(++lab->fepoch & 1) : 0;
+  FusedArgs fz;
+  fz.R = lab->nranks;
+  fz.rank = lab->rank;
+  fz.epoch = lab->fepoch;
+  const size_t es = elem_size(lab);
+  for (int q = 0; q < lab->nranks; ++q) {
+    fz.xs[q] = static_cast<const char*>(lab->xpeer[q]) + es * (size_t)parity * lab->ld;
+    fz.tf[q] = lab->tpeer[q] + (size_t)parity * lab->nranks * lab->ntiles;
+  }
+  T* mean_out = lab->kl > 1 ? static_cast<T*>(lab->staging) : static_cast<T*>(lab->w);
+  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[1], lab->stream));
+  launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, false, bits, eta, nullptr,
+                   lab->has_ranges ? &fz : nullptr, mean_out);
+  if (lab->instrument) {
+    DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
+    DSX_CUDA(cudaEventRecord(lab->iev[2], lab->stream));
+  }
+  DSX_CUDA(cudaEventRecord(lab->ev_synced, lab->stream));
+  if (lab->kl > 1) {  // the synced layers' rows are stale now (mean in the exchange buffer)
+    lab->stale_bits = bits;
+    lab->stale_any = lab->has_ranges;
+  }
+  return DSX_OK;
+}
+
 template <typename T>
 dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int noise) {
   MaskBits bits{};
@@ -1700,7 +1853,8 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int no
   } else if (single) {
     launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, lab->K > 1, bits, eta);
   } else if (lab->p2p && lab->sync_algo == DSX_SYNC_PAIRWISE) {
-    DSX_TRY(step_multi_p2p<T>(lab, eta, mask, bits, noise));
+    if (lab->fused && lab->link_bw <= 0.0) DSX_TRY(step_multi_fused<T>(lab, eta, mask, bits, noise));
+    else DSX_TRY(step_multi_p2p<T>(lab, eta, mask, bits, noise));
   } else {
     const auto ranges = masked_ranges(lab, mask);
     lab->has_ranges = !ranges.empty();
@@ -2048,6 +2202,8 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
     if (ev) cudaEventDestroy(ev);
   if (lab->bar) cudaFree(lab->bar);
   if (lab->flags) cudaFree(lab->flags);
+  if (lab->xsum) cudaFree(lab->xsum);
+  if (lab->tflags) cudaFree(lab->tflags);
   if (lab->sig_counter) cudaFree(lab->sig_counter);
   for (auto& ev : lab->ev_chunk)
     if (ev) cudaEventDestroy(ev);
@@ -2554,42 +2710,52 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   DSX_CUDA(cudaMemset(lab->flags, 0, 8 * kFlagWords));
   DSX_CUDA(cudaMalloc(&lab->sig_counter, 4));
   DSX_CUDA(cudaMemset(lab->sig_counter, 0, 4));
-  // two handles per rank: the exchange buffer and the flag block
+  DSX_CUDA(cudaMalloc(&lab->xsum, es * 2 * lab->ld));  // [2][ld]: 16-B aligned halves
+  DSX_CUDA(cudaMalloc(&lab->tflags, 8ull * 2 * nranks * std::max(1, lab->ntiles)));
+  DSX_CUDA(cudaMemset(lab->tflags, 0, 8ull * 2 * nranks * std::max(1, lab->ntiles)));
+  // four handles per rank: exchange buffer, flag block, published sums, tile flags
+  constexpr int kNB = 4;
   constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
-  cudaIpcMemHandle_t mine[2]{};
-  if (ok && (cudaIpcGetMemHandle(&mine[0], xbuf) != cudaSuccess ||
-             cudaIpcGetMemHandle(&mine[1], lab->flags) != cudaSuccess))
-    ok = 0;
+  void* const bufs[kNB] = {xbuf, lab->flags, lab->xsum, lab->tflags};
+  cudaIpcMemHandle_t mine[kNB]{};
+  for (int b = 0; b < kNB && ok; ++b)
+    if (cudaIpcGetMemHandle(&mine[b], bufs[b]) != cudaSuccess) ok = 0;
   char* d_handles = nullptr;
   int* d_ok = nullptr;
-  DSX_CUDA(cudaMalloc(&d_handles, 2 * kH * nranks));
+  DSX_CUDA(cudaMalloc(&d_handles, kNB * kH * nranks));
   DSX_CUDA(cudaMalloc(&d_ok, 4));
-  DSX_CUDA(cudaMemcpy(d_handles + 2 * kH * rank, mine, 2 * kH, cudaMemcpyHostToDevice));
+  DSX_CUDA(cudaMemcpy(d_handles + kNB * kH * rank, mine, kNB * kH, cudaMemcpyHostToDevice));
   DSX_CUDA(cudaMemcpy(d_ok, &ok, 4, cudaMemcpyHostToDevice));
-  DSX_NCCL(ncclAllGather(d_handles + 2 * kH * rank, d_handles, 2 * kH, ncclChar, lab->comm, lab->side));
+  DSX_NCCL(ncclAllGather(d_handles + kNB * kH * rank, d_handles, kNB * kH, ncclChar, lab->comm, lab->side));
   DSX_NCCL(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, lab->comm, lab->side));
   DSX_CUDA(cudaStreamSynchronize(lab->side));
-  std::vector<cudaIpcMemHandle_t> handles(2 * (size_t)nranks);
-  DSX_CUDA(cudaMemcpy(handles.data(), d_handles, 2 * kH * nranks, cudaMemcpyDeviceToHost));
+  std::vector<cudaIpcMemHandle_t> handles(kNB * (size_t)nranks);
+  DSX_CUDA(cudaMemcpy(handles.data(), d_handles, kNB * kH * nranks, cudaMemcpyDeviceToHost));
   DSX_CUDA(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
   int local_ok = ok;
   if (ok) {
     for (int q = 0; q < nranks && local_ok; ++q) {
-      if (q == rank) {
-        lab->peers.p[q] = xbuf;
-        lab->fpeers.p[q] = lab->flags;
-        continue;
-      }
-      for (int which = 0; which < 2; ++which) {
+      void* got[kNB];
+      for (int b = 0; b < kNB; ++b) {
+        if (q == rank) {
+          got[b] = bufs[b];
+          continue;
+        }
         void* ptr = nullptr;
-        if (cudaIpcOpenMemHandle(&ptr, handles[2 * q + which], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        if (cudaIpcOpenMemHandle(&ptr, handles[kNB * q + b], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
           cudaGetLastError();
           local_ok = 0;
           break;
         }
         lab->opened.push_back(ptr);
-        if (which == 0) lab->peers.p[q] = ptr;
-        else lab->fpeers.p[q] = static_cast<unsigned long long*>(ptr);
+        got[b] = ptr;
+      }
+      if (!local_ok) break;
+      lab->peers.p[q] = got[0];
+      lab->fpeers.p[q] = static_cast<unsigned long long*>(got[1]);
+      if (q < kMaxFuse) {
+        lab->xpeer[q] = got[2];
+        lab->tpeer[q] = static_cast<unsigned long long*>(got[3]);
       }
     }
   }
@@ -2602,6 +2768,12 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   lab->p2p = ok != 0;
   const char* fb = std::getenv("DSX_FLAG_BARRIER");
   lab->flag_bar = lab->p2p && !(fb && fb[0] == '0');
+  // opt-in (DSX_FUSED=1): measured slower than the separate averaging
+  // kernel (2 GPUs, sigma=1: 1210 vs 1500 it/s) — a synced tile's CTA idles
+  // on the peer's same tile while holding its SM slot
+  const char* fz = std::getenv("DSX_FUSED");
+  lab->fused = lab->p2p && sync_algo == DSX_SYNC_PAIRWISE && nranks <= kMaxFuse && lab->kl <= 8 &&
+               fz && fz[0] == '1';
   return DSX_OK;
 }
 
