@@ -751,6 +751,223 @@ lab_update_async_kernel(UpdateArgs<double> a, int count) {
   for (int i = blockIdx.x; i < count; i += gridDim.x) async_update_tile<KL, NM>(a, a.tile_base + i, stage);
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA 1-D) update kernel, single GPU, fp64 (default with engine noise).
+// Persistent CTAs, each walking whole tiles in 512-coordinate chunks: one
+// producer lane moves a chunk's 8 row slices and 8 noise slices into shared
+// memory with cp.async.bulk (completion counted on an mbarrier), 8 consumer
+// warps update and average it in place, and the rows go back with bulk
+// stores — the memory pipeline costs no registers, so fewer SMs can carry
+// the full HBM stream and the rest stay free for the noise engine.
+// ---------------------------------------------------------------------------
+constexpr int kBChunk = 512;                 // coordinates per chunk
+constexpr int kBStages = 3;
+constexpr int kBConsumers = 256;             // one pair per consumer thread
+constexpr int kBThreads = kBConsumers + 32;  // + producer warp
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
+struct BulkChunk {  // producer -> consumers, per stage
+  int tile;
+  long long a0, a1;  // coordinate window [a0, a1), even-aligned
+  int simple;        // noise staged (else consumers look it up)
+  int last;          // last chunk of its tile
+};
+
+template <int KL, int NM>
+__global__ void __launch_bounds__(kBThreads, 1)
+lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
+  constexpr bool NOISE = NM != 0;
+  extern __shared__ __align__(128) double bsm[];  // [stage][2: w, x][KL][kBChunk]
+  __shared__ __align__(8) uint64_t full[kBStages], empty[kBStages];
+  __shared__ BulkChunk info[kBStages];
+  __shared__ double red[kBConsumers / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto wbuf = [&](int st, int k) { return bsm + ((long long)(st * 2 + 0) * KL + k) * kBChunk; };
+  auto xbuf = [&](int st, int k) { return bsm + ((long long)(st * 2 + 1) * KL + k) * kBChunk; };
+  if (tid == 0) {
+    for (int st = 0; st < kBStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kBConsumers / 32) {
+    // ------------------------------- producer -------------------------------
+    int j = 0;  // chunk counter (ring position)
+    for (int ti = blockIdx.x; ti < count; ti += gridDim.x) {
+      const int tile_id = a.tile_base + ti;
+      const Tile t = a.tiles[tile_id];
+      // per-worker noise split of this tile (lane k)
+      const double* nb0 = nullptr;
+      const double* nb1 = nullptr;
+      long long ibound = 0;
+      int simple = 1;
+      if constexpr (NM == 2) {
+        if (lane < KL) {
+          const int k = lane;
+          const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
+          const unsigned long long m0 = a.nv.base + ((unsigned long long)t.start >> 1);
+          const unsigned long long m1 = a.nv.base + ((unsigned long long)(t.start + t.len - 1) >> 1);
+          const int s0 = seg_search(pf, a.nv.P, m0);
+          const int s1 = s0 < a.nv.P ? s0 + 1 : s0;
+          nb0 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s0) * a.nv.cap - 2 * (long long)pf[s0] + 2 * (long long)a.nv.base;
+          nb1 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s1) * a.nv.cap - 2 * (long long)pf[s1] + 2 * (long long)a.nv.base;
+          ibound = s0 < a.nv.P ? 2 * (long long)(pf[s0 + 1] - a.nv.base) : (1LL << 62);
+          if (s1 < a.nv.P && m1 >= pf[s1 + 1]) simple = 0;
+        }
+        simple = __all_sync(0xffffffffu, simple);
+      }
+      const long long lo = t.start & ~1LL, hi = (t.start + t.len + 1) & ~1LL;
+      for (long long a0 = lo; a0 < hi; a0 += kBChunk, ++j) {
+        const long long a1 = a0 + kBChunk < hi ? a0 + kBChunk : hi;
+        const int st = j % kBStages, u = j / kBStages;
+        if (u > 0) mbar_wait(&empty[st], (u - 1) & 1);
+        if (lane == 0) {
+          info[st] = BulkChunk{tile_id, a0, a1, simple, a1 >= hi ? 1 : 0};
+          const unsigned row = 8u * (unsigned)(a1 - a0);
+          const unsigned bytes = row * KL * ((NM == 2 && simple) ? 2u : 1u);
+          mbar_expect_tx(&full[st], bytes);
+          for (int k = 0; k < KL; ++k) bulk_g2s(wbuf(st, k), a.w + k * a.ld + a0, row, &full[st]);
+        }
+        if constexpr (NM == 2) {
+          if (simple && lane < KL) {
+            const int k = lane;
+            const long long cut = min(max(ibound, (long long)a0), (long long)a1);
+            if (cut > a0) bulk_g2s(xbuf(st, k), nb0 + a0, 8u * (unsigned)(cut - a0), &full[st]);
+            if (a1 > cut) bulk_g2s(xbuf(st, k) + (cut - a0), nb1 + cut, 8u * (unsigned)(a1 - cut), &full[st]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+  // -------------------------------- consumers --------------------------------
+  double nsq[KL];
+#pragma unroll
+  for (int k = 0; k < KL; ++k) nsq[k] = 0.0;
+  int j = 0;
+  for (int ti = blockIdx.x; ti < count; ti += gridDim.x) {
+    const int tile_id = a.tile_base + ti;
+    const Tile t = a.tiles[tile_id];
+    const bool avg = a.average && mask_has(a.mask, t.block);
+    const long long lo = t.start & ~1LL, hi = (t.start + t.len + 1) & ~1LL;
+    for (long long a0 = lo; a0 < hi; a0 += kBChunk, ++j) {
+      const int st = j % kBStages, u = j / kBStages;
+      mbar_wait(&full[st], u & 1);
+      const BulkChunk ci = info[st];
+      const long long a1 = ci.a1;
+      const int p = tid;  // pair of the chunk
+      const long long i = a0 + 2 * (long long)p;
+      const bool in0 = i < a1 && i >= t.start && i < t.start + t.len;
+      const bool in1 = i + 1 < a1 && i + 1 >= t.start && i + 1 < t.start + t.len;
+      if (in0 || in1) {
+        double lam0, opt0, lam1, opt1;
+        quad_coeffs(a.q, i, &lam0, &opt0);
+        quad_coeffs(a.q, i + 1, &lam1, &opt1);
+        double w0[KL], w1[KL];
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+          const double2 wv = *reinterpret_cast<const double2*>(wbuf(st, k) + 2 * p);
+          double2 xv = make_double2(0.0, 0.0);
+          if constexpr (NM == 2) {
+            if (ci.simple) {
+              xv = *reinterpret_cast<const double2*>(xbuf(st, k) + 2 * p);
+            } else {
+              const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
+              const int sg = seg_search(pf, a.nv.P, a.nv.base + ((unsigned long long)i >> 1));
+              xv = *reinterpret_cast<const double2*>(a.nv.slots + ((long long)k * (a.nv.P + 1) + sg) * a.nv.cap +
+                                                     2 * (long long)(a.nv.base + ((unsigned long long)i >> 1) - pf[sg]));
+            }
+          }
+          const double g0 = grad_step(wv.x, lam0, opt0, xv.x, a.eta, NOISE, &w0[k]);
+          const double g1 = grad_step(wv.y, lam1, opt1, xv.y, a.eta, NOISE, &w1[k]);
+          if (in0) nsq[k] += g0 * g0;
+          if (in1) nsq[k] += g1 * g1;
+        }
+        if (avg) {
+          const double m0 = psum<0, KL, double>(w0) / (double)a.k_total;
+          const double m1 = psum<0, KL, double>(w1) / (double)a.k_total;
+#pragma unroll
+          for (int k = 0; k < KL; ++k) {
+            w0[k] = m0;
+            w1[k] = m1;
+          }
+        }
+        const bool full_pair = in0 && in1;
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+          if (full_pair) {
+            *reinterpret_cast<double2*>(wbuf(st, k) + 2 * p) = make_double2(w0[k], w1[k]);
+          } else {  // a tile edge: write the in-tile coordinate directly
+            if (in0) a.w[k * a.ld + i] = w0[k];
+            if (in1) a.w[k * a.ld + i + 1] = w1[k];
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kBConsumers) : "memory");
+      if (tid == 0) {
+        // rows back with bulk stores, full pairs inside the tile only
+        const long long e0 = (t.start + 1) & ~1LL, e1 = (t.start + t.len) & ~1LL;
+        const long long s0 = a0 > e0 ? a0 : e0, s1 = a1 < e1 ? a1 : e1;
+        if (s1 > s0)
+          for (int k = 0; k < KL; ++k)
+            bulk_s2g(a.w + k * a.ld + s0, wbuf(st, k) + (s0 - a0), 8u * (unsigned)(s1 - s0));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&empty[st]);
+      }
+      if (ci.last) {
+        // the tile's gradient-norm partials (fixed order within the CTA)
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+          double x = nsq[k];
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          asm volatile("bar.sync 1, %0;" ::"n"(kBConsumers) : "memory");
+          if (lane == 0) red[warp] = x;
+          asm volatile("bar.sync 1, %0;" ::"n"(kBConsumers) : "memory");
+          if (tid == 0) {
+            double sk = 0.0;
+            for (int q = 0; q < kBConsumers / 32; ++q) sk += red[q];
+            a.norm_part[(long long)k * a.ntiles + tile_id] = sk;
+          }
+          nsq[k] = 0.0;
+        }
+      }
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ||g_k||^2 = fixed-order sum of the tile partials (one CTA per worker row),
 // then the max over rows (atomicMax on the bit pattern: non-negative doubles
 // order like their uint64 images, so the result is order-independent).
@@ -1381,6 +1598,30 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   if (fz) {
     a.fz = *fz;
     a.mean_out = mean_out;
+  }
+  if constexpr (std::is_same_v<T, double> && (KL == 2 || KL == 4 || KL == 8)) {
+    // bulk-copy kernel: the default with engine noise (0.91 vs 0.84 of HBM at
+    // sigma=1); the register-staged kernel stays faster without noise (0.83
+    // vs 0.80).  DSX_UPD_BULK=0 off, =1 on (one CTA per SM), =n n CTAs.
+    static const int bulk_env = [] {
+      const char* e = std::getenv("DSX_UPD_BULK");
+      return e ? std::atoi(e) : -1;
+    }();
+    const int bulk_ctas = bulk_env >= 0 ? bulk_env : (nm == 2 ? 1 : 0);
+    if (bulk_ctas > 0 && (nm == 0 || nm == 2) && !fz && !partial_out && a.mean_in == nullptr) {
+      constexpr size_t smem = sizeof(double) * kBStages * 2 * KL * kBChunk;
+      static const bool attr = [] {
+        cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+      }();
+      (void)attr;
+      const int grid = std::min(count, bulk_ctas == 1 ? lab->nsm : bulk_ctas);
+      if (nm == 2) lab_update_bulk_kernel<KL, 2><<<grid, kBThreads, smem, s>>>(a, count);
+      else lab_update_bulk_kernel<KL, 0><<<grid, kBThreads, smem, s>>>(a, count);
+      ++lab->launches;
+      return;
+    }
   }
   if constexpr (std::is_same_v<T, double> && KL >= 2 && KL % 2 == 0) {
     // async-staged kernel, opt-in (DSX_UPD_ASYNC=1): measured no faster
