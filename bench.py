@@ -436,7 +436,12 @@ def our_arm(args, world, rank, local_rank, dist):
     # The HBM roofline belongs to the update (+ in-kernel averaging) kernel;
     # the noise engine is integer/fp64-ALU bound (no HBM or tensor roofline)
     # and is reported beside it.
-    dom = {"kernel": "lab_update (fused gradient+update+average)", "ms": upd,
+    # which update kernel ran (mirrors libdsx's choice): the bulk-copy kernel
+    # on one GPU with engine noise, the register-staged one otherwise
+    bulk = (world == 1 and args.sigma > 0 and args.dtype == "f64" and kl in (2, 4, 8)
+            and os.environ.get("DSX_UPD_BULK", "") != "0")
+    dom = {"kernel": ("lab_update_bulk (fused gradient+update+average, cp.async.bulk data path)" if bulk
+                      else "lab_update (fused gradient+update+average)"), "ms": upd,
            "bytes": update_bytes}
     achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
     traffic = None
