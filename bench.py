@@ -438,7 +438,7 @@ def our_arm(args, world, rank, local_rank, dist):
     # and is reported beside it.
     # which update kernel ran (mirrors libdsx's choice): the bulk-copy kernel
     # on one GPU with engine noise, the register-staged one otherwise
-    bulk = (world == 1 and args.sigma > 0 and args.dtype == "f64" and kl in (2, 4, 8)
+    bulk = (args.sigma > 0 and args.dtype == "f64" and kl == 8
             and os.environ.get("DSX_UPD_BULK", "") != "0")
     dom = {"kernel": ("lab_update_bulk (fused gradient+update+average, cp.async.bulk data path)" if bulk
                       else "lab_update (fused gradient+update+average)"), "ms": upd,

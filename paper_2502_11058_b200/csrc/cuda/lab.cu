@@ -845,6 +845,8 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
         }
         simple = __all_sync(0xffffffffu, simple);
       }
+      // lazy multi-rank rows: a layer averaged last step is read once (its mean)
+      const bool stale = a.mean_in != nullptr && mask_has(a.stale, t.block);
       const long long lo = t.start & ~1LL, hi = (t.start + t.len + 1) & ~1LL;
       for (long long a0 = lo; a0 < hi; a0 += kBChunk, ++j) {
         const long long a1 = a0 + kBChunk < hi ? a0 + kBChunk : hi;
@@ -853,9 +855,11 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
         if (lane == 0) {
           info[st] = BulkChunk{tile_id, a0, a1, simple, a1 >= hi ? 1 : 0};
           const unsigned row = 8u * (unsigned)(a1 - a0);
-          const unsigned bytes = row * KL * ((NM == 2 && simple) ? 2u : 1u);
+          const unsigned bytes = row * ((stale ? 1u : (unsigned)KL) + ((NM == 2 && simple) ? (unsigned)KL : 0u));
           mbar_expect_tx(&full[st], bytes);
-          for (int k = 0; k < KL; ++k) bulk_g2s(wbuf(st, k), a.w + k * a.ld + a0, row, &full[st]);
+          if (stale) bulk_g2s(wbuf(st, 0), a.mean_in + a0, row, &full[st]);
+          else
+            for (int k = 0; k < KL; ++k) bulk_g2s(wbuf(st, k), a.w + k * a.ld + a0, row, &full[st]);
         }
         if constexpr (NM == 2) {
           if (simple && lane < KL) {
@@ -879,6 +883,8 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
     const int tile_id = a.tile_base + ti;
     const Tile t = a.tiles[tile_id];
     const bool avg = a.average && mask_has(a.mask, t.block);
+    const bool part = a.partial_out != nullptr && mask_has(a.mask, t.block);
+    const bool stale = a.mean_in != nullptr && mask_has(a.stale, t.block);
     const long long lo = t.start & ~1LL, hi = (t.start + t.len + 1) & ~1LL;
     for (long long a0 = lo; a0 < hi; a0 += kBChunk, ++j) {
       const int st = j % kBStages, u = j / kBStages;
@@ -896,7 +902,7 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
         double w0[KL], w1[KL];
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
-          const double2 wv = *reinterpret_cast<const double2*>(wbuf(st, k) + 2 * p);
+          const double2 wv = *reinterpret_cast<const double2*>(wbuf(st, stale ? 0 : k) + 2 * p);
           double2 xv = make_double2(0.0, 0.0);
           if constexpr (NM == 2) {
             if (ci.simple) {
@@ -923,6 +929,16 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
           }
         }
         const bool full_pair = in0 && in1;
+        if (part) {
+          // multi-rank synced tile: only this rank's subtree sum leaves
+          const double m0 = psum<0, KL, double>(w0), m1 = psum<0, KL, double>(w1);
+          if (full_pair) {
+            *reinterpret_cast<double2*>(a.partial_out + i) = make_double2(m0, m1);
+          } else {
+            if (in0) a.partial_out[i] = m0;
+            if (in1) a.partial_out[i + 1] = m1;
+          }
+        } else
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
           if (full_pair) {
@@ -939,7 +955,7 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
         // rows back with bulk stores, full pairs inside the tile only
         const long long e0 = (t.start + 1) & ~1LL, e1 = (t.start + t.len) & ~1LL;
         const long long s0 = a0 > e0 ? a0 : e0, s1 = a1 < e1 ? a1 : e1;
-        if (s1 > s0)
+        if (s1 > s0 && !part)
           for (int k = 0; k < KL; ++k)
             bulk_s2g(a.w + k * a.ld + s0, wbuf(st, k) + (s0 - a0), 8u * (unsigned)(s1 - s0));
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -1607,8 +1623,10 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
       const char* e = std::getenv("DSX_UPD_BULK");
       return e ? std::atoi(e) : -1;
     }();
-    const int bulk_ctas = bulk_env >= 0 ? bulk_env : (nm == 2 ? 1 : 0);
-    if (bulk_ctas > 0 && (nm == 0 || nm == 2) && !fz && !partial_out && a.mean_in == nullptr) {
+    // (with 2-4 local rows a 512-coordinate chunk carries too little per
+    // mbarrier round trip: 4 GPUs 0.29 vs 0.17 ms, so 8 rows only by default)
+    const int bulk_ctas = bulk_env >= 0 ? bulk_env : (nm == 2 && KL == 8 ? 1 : 0);
+    if (bulk_ctas > 0 && (nm == 0 || nm == 2) && !fz) {
       constexpr size_t smem = sizeof(double) * kBStages * 2 * KL * kBChunk;
       static const bool attr = [] {
         cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
