@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for b in 0 -1 0 -1; do
-  DSX_UPD_BULK=$b timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 2978${b#-} bench.py --gpus 4 --steps 100 --warmup 5 --no-e2e > gpurun_out/n4r.log 2>&1; echo bulk$b=$?
-  tail -1 gpurun_out/n4r.log | python3 -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['ms_per_step_without_sync'], d['sync_added_frac'], d['roofline']['kernel'][:20])"
+for i in 1 2 3; do
+  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 2978$i bench.py --gpus 4 --steps 100 --warmup 5 --no-e2e > gpurun_out/n4r.log 2>&1; echo run$i=$?
+  tail -1 gpurun_out/n4r.log | python3 -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['ms_per_step_without_sync'], d['sync_added_frac'], d['schedule']['synced_param_frac_per_step'])"
 done
