@@ -2954,8 +2954,8 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   // engine already keep the GPU busy while the average runs on the sync
   // stream, and splitting the update only adds launch tails (measured at
   // 2 GPUs: 1610 vs 1500 it/s); with fewer local workers the backward-order
-  // groups pay off (4 GPUs: 2615 vs 2370 it/s).
-  lab->chunks = lab->kl >= 4 ? 1 : 4;
+  // groups pay off (4 GPUs: 2615 vs 2370 it/s, one group vs four).
+  lab->chunks = lab->kl >= 4 ? 1 : 6;  // 4 GPUs: 6 groups 2510, 4 groups 2370, 2 groups 2470 it/s
   if (const char* c = std::getenv("DSX_SYNC_CHUNKS")) lab->chunks = std::max(1, std::min(kMaxChunks, std::atoi(c)));
   {
     const int nm = lab->sigma > 0.0 ? 2 : 0;
