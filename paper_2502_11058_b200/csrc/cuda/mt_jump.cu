@@ -878,20 +878,31 @@ constexpr int kQCap = 1024;  // FIFO capacity: < 320 carried + 624 new per round
 // RAW (opt-in): the accepted attempts (x, y) are stored as they are and
 // the consumer applies the polar transform (mt_polar_normals) — the update
 // kernel has idle issue slots while it waits on HBM, the engine does not.
-template <bool RAW>
+// Shared memory of the v5 segment kernel with R generations per round.
+template <int R>
+struct Ws2Smem {
+  static constexpr int kQ = (kThreads + R * kMtN / 2) <= 1024 ? 1024 : 2048;  // FIFO entries
+  static constexpr size_t kRing = sizeof(uint64_t) * 2 * R * kMtN;
+  static constexpr size_t kV = sizeof(double) * (R * kMtN + 2);
+  static constexpr size_t kBytes = kRing + kV + sizeof(double2) * kQ;
+};
+
+template <bool RAW, int R>
 __global__ void __launch_bounds__(kWs2Threads, 2)
 mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
                       int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
                       double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
                       uint64_t* tail) {
-  constexpr int R = kWsR;
-  constexpr int kPairSlots = 2;  // 624 pairs of an interior round over 320 threads
+  constexpr int kPairSlots = (R * kMtN / 2 + kThreads - 1) / kThreads;  // pairs per consumer per round
   constexpr int kCounts = kPairSlots * (kThreads / 32);
-  static_assert(R * kMtN / 2 <= kPairSlots * kThreads, "pair slots");
+  constexpr int kQCap = Ws2Smem<R>::kQ;
   static_assert(kCounts <= 32, "scan fits one warp");
-  __shared__ __align__(16) uint64_t ring[2][R * kMtN];
-  __shared__ __align__(16) double v[R * kMtN + 2];  // boundary rounds only (and the boot state)
-  __shared__ __align__(16) double2 fifo[kQCap];
+  static_assert(kThreads + R * kMtN / 2 <= kQCap, "FIFO holds the carry plus one round");
+  extern __shared__ __align__(16) unsigned char ws2_dsm[];
+  // ring[2][R*312] | v[R*312+2] (boundary rounds + boot) | fifo[kQCap]
+  auto ring_half = [&](int h) { return reinterpret_cast<uint64_t*>(ws2_dsm) + (long long)h * R * kMtN; };
+  double* v = reinterpret_cast<double*>(ws2_dsm + Ws2Smem<R>::kRing);
+  double2* fifo = reinterpret_cast<double2*>(ws2_dsm + Ws2Smem<R>::kRing + Ws2Smem<R>::kV);
   __shared__ int wcnt[2][kCounts];
   __shared__ double s_half[2];
   __shared__ int s_p;
@@ -909,17 +920,17 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
       p = (int)st[kMtN];
       named_sync(kBarProd, kProdThreads);
       if (p >= kMtN) {
-        for (int k = pt; k < kMtM; k += kProdThreads) ring[0][k] = mt_next_word(boot[k], boot[k + 1], boot[k + kMtM]);
+        for (int k = pt; k < kMtM; k += kProdThreads) ring_half(0)[k] = mt_next_word(boot[k], boot[k + 1], boot[k + kMtM]);
         named_sync(kBarProd, kProdThreads);
         for (int k = kMtM + pt; k < kMtN; k += kProdThreads)
-          ring[0][k] = mt_next_word(boot[k], (k + 1 < kMtN) ? boot[k + 1] : ring[0][0], ring[0][k - kMtM]);
+          ring_half(0)[k] = mt_next_word(boot[k], (k + 1 < kMtN) ? boot[k + 1] : ring_half(0)[0], ring_half(0)[k - kMtM]);
         p = 0;
       } else {
-        for (int k = pt; k < kMtN; k += kProdThreads) ring[0][k] = boot[k];
+        for (int k = pt; k < kMtN; k += kProdThreads) ring_half(0)[k] = boot[k];
       }
       if (pt == 0) pnorm_out[w] = p;
     } else {
-      for (int k = pt; k < kMtN; k += kProdThreads) ring[0][k] = win[((long long)w * P + s) * kMtN + k];
+      for (int k = pt; k < kMtN; k += kProdThreads) ring_half(0)[k] = win[((long long)w * P + s) * kMtN + k];
       p = pnorm_in[w];
     }
     if (pt == 0) s_p = p;
@@ -932,8 +943,8 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
       const int rg = min(R, ngen - k * R);
       for (int g = 0; g < rg; ++g) {
         if (k == 0 && g == 0) continue;  // gen 0 already in place
-        const uint64_t* src = g ? &ring[h][(g - 1) * kMtN] : &ring[1 - h][(R - 1) * kMtN];
-        uint64_t* dst = &ring[h][g * kMtN];
+        const uint64_t* src = g ? ring_half(h) + (g - 1) * kMtN : ring_half(1 - h) + (R - 1) * kMtN;
+        uint64_t* dst = ring_half(h) + g * kMtN;
         for (int i = pt; i < kMtM; i += kProdThreads) dst[i] = mt_next_word(src[i], src[i + 1], src[i + kMtM]);
         named_sync(kBarProd, kProdThreads);
         for (int i = kMtM + pt; i < kMtN; i += kProdThreads)
@@ -979,7 +990,7 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
       uint64_t* c = ckw + (long long)ck_idx * kCkWords;
       ck_next += ck_every;
       ++ck_idx;
-      if (tid < kMtN) c[tid] = ring[h][tid];
+      if (tid < kMtN) c[tid] = ring_half(h)[tid];
       if (tid == 0) {
         c[kMtN] = (uint64_t)hh;
         c[kMtN + 1] = (uint64_t)__double_as_longlong(half_in);
@@ -988,14 +999,14 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
     }
     if (k == rounds - 1) {  // end state for an overflow continuation
       uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
-      if (tid < kMtN) c[tid] = ring[h][(rg - 1) * kMtN + tid];
+      if (tid < kMtN) c[tid] = ring_half(h)[(rg - 1) * kMtN + tid];
     }
     bool acc[kPairSlots];
     double px[kPairSlots], py[kPairSlots];
     int npairs, hh_next;
     if (q > 0 && q + R <= gens) {
       // interior: R complete generations; round output n is ring word n
-      const uint64_t* rw = ring[h];
+      const uint64_t* rw = ring_half(h);
       npairs = (hh + R * kMtN) >> 1;
       hh_next = (hh + R * kMtN) & 1;
 #pragma unroll
@@ -1022,7 +1033,7 @@ mt_segment_ws2_kernel(const uint64_t* win_state, const uint64_t* win, const int*
           const int gen = q + g;
           const int lo = gen == 0 ? p : 0;
           const int hi = (gen == gens) ? p : kMtN;
-          if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(ring[h][g * kMtN + tid]));
+          if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(ring_half(h)[g * kMtN + tid]));
           nvals += hi - lo;
         }
       }
@@ -1286,7 +1297,12 @@ bool NoiseEngine::make_cfg(int steps, int nsm, Cfg* c, std::string* err) {
 bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, int max_steps, std::string* err) {
   dim_ = dim;
   kl_ = kl;
-  ck_every_ = 16;
+  {
+    // 6 generations per round (default; engine 0.77 -> 0.74 ms/step) or 4
+    const char* e = std::getenv("DSX_SEG_R");
+    seg_r_ = (e && std::atoi(e) == 4) ? 4 : 6;
+  }
+  ck_every_ = seg_r_ == 6 ? 12 : 16;  // a checkpoint every few whole rounds
   if (mt_char_poly().empty()) {
     *err = "MT19937-64 characteristic polynomial: Berlekamp-Massey did not reach degree 19937";
     return false;
@@ -1396,18 +1412,26 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int ste
   static const int pad = [] {
     const char* e = std::getenv("DSX_SEG_PAD");
     const int v = e ? std::atoi(e) : 0;
-    if (v > 0) {
-      cudaFuncSetAttribute(mt_segment_ws2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
-      cudaFuncSetAttribute(mt_segment_ws2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
-    }
+    const int p4 = (int)Ws2Smem<4>::kBytes + std::max(0, v), p6 = (int)Ws2Smem<6>::kBytes + std::max(0, v);
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p4);
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p4);
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, p6);
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, p6);
     return v > 0 ? v : 0;
   }();
-  if (ws == 2 && raw) {
-    mt_segment_ws2_kernel<true><<<dim3(P, kl_), kWs2Threads, pad, stream>>>(
-        mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_, c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
-  } else if (ws == 2) {
-    mt_segment_ws2_kernel<false><<<dim3(P, kl_), kWs2Threads, pad, stream>>>(
-        mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_, c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
+  if (ws == 2) {
+    // generations per round (DSX_SEG_R: 4 or 6; checkpoints every 16 / 12)
+    auto go = [&](auto kern, size_t smem) {
+      kern<<<dim3(P, kl_), kWs2Threads, smem + pad, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_,
+                                                               c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
+    };
+    if (seg_r_ == 6) {
+      if (raw) go(mt_segment_ws2_kernel<true, 6>, Ws2Smem<6>::kBytes);
+      else go(mt_segment_ws2_kernel<false, 6>, Ws2Smem<6>::kBytes);
+    } else {
+      if (raw) go(mt_segment_ws2_kernel<true, 4>, Ws2Smem<4>::kBytes);
+      else go(mt_segment_ws2_kernel<false, 4>, Ws2Smem<4>::kBytes);
+    }
   } else if (ws == 1) {
     mt_segment_ws_kernel<<<dim3(P, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
                                                                    ck_every_, c.nck, stddev, slots, c.cap,

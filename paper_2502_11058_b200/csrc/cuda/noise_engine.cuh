@@ -67,7 +67,7 @@ class NoiseEngine {
   };
   bool make_cfg(int steps, int nsm, Cfg* c, std::string* err);
   unsigned long long dim_ = 0;
-  int kl_ = 0, ck_every_ = 16;
+  int kl_ = 0, ck_every_ = 16, seg_r_ = 4;
   Cfg cfg_[2];                     // [0]: one step per run, [1]: max_steps per run
   int set_cfg_[2] = {0, 0};
   int raw_[2] = {0, 0};            // per set: the last run stored raw attempts
