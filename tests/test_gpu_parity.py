@@ -269,3 +269,40 @@ def test_step_host_matches_device_resident_steps(pinned, chunks, monkeypatch):
     assert torch.equal(rng, want)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("batch,K", [("1", 8), ("3", 8), ("8", 8), ("16", 2)])
+def test_batched_engine_run_boundaries(batch, K, monkeypatch):
+    """Pipelined multi-step engine runs (T steps of noise per run, the next
+    run prefetched): the committed rng state after any step equals libstdc++'s,
+    reading it mid-run is exact, and a host write of the state mid-run drops
+    the prefetched noise (trainer.cpp:191-199 draws each step's noise where the
+    previous step stopped)."""
+    from paper_2502_11058_b200 import Lab, LabDesc
+    from paper_2502_11058_b200.lab import sync_mask
+    monkeypatch.setenv("DSX_NOISE_BATCH", batch)
+    dim, L, H, seed = 30011, 5, 3, 123
+    curv, sizes = O.make_quadratic(dim, L)
+    sets = O.enp(L, H)
+    lab = Lab(LabDesc(dim=dim, block_sizes=list(sizes), workers_total=K, sigma=1.0))
+    lab.seed(seed)
+    rngs = [O.worker_rng(seed, k) for k in range(K)]
+    w = np.zeros((K, dim))
+    lab.set_params(w)
+    T = int(batch)
+    steps = 2 * T + 3
+    for r in range(steps):
+        eta = O.learning_rate(r, 1.0, 2.0, H)
+        mask = sync_mask("partial", H, r, L, sets)
+        lab.step(eta, mask)
+        O.plsgd_step(w, rngs, curv, np.ones(dim), 1.0, sizes, eta, mask)
+        if r == T // 2 + 1:  # mid-run read of the committed state
+            assert lab.rng_text(K - 1) == O.mt_state_text(rngs[K - 1])
+        if r == T + 1:  # mid-run host write: advance worker 0 by 5 draws
+            for _ in range(5):
+                O.lib().orc_mt_next(O.C.byref(rngs[0]))
+            lab.set_rng(0, np.array(list(rngs[0].x), dtype=np.uint64), int(rngs[0].p))
+    assert rel_err(lab.get_params(), w) <= 1e-12
+    for k in range(K):
+        assert lab.rng_text(k) == O.mt_state_text(rngs[k])
+    lab.close()
