@@ -31,7 +31,8 @@ STEP_CASES = [
 ]
 TRAIN_CASES = ["lab_partial.train", "lab_full.train", "lab_ssgd_const.train"]
 PROFILE_CASES = [("resnet18_like.profile", 5), ("three_layer.profile", 2),
-                 ("three_layer_light.profile", 2), ("totals_123.profile", 1)]
+                 ("three_layer_light.profile", 2), ("totals_123.profile", 1),
+                 ("mlp8_w1024.profile", 4)]  # BASELINE configs[0]: 8-layer MLP, H=4
 
 
 def run(args):

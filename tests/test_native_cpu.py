@@ -66,7 +66,8 @@ def test_sched_fuzz_golden_byte_identical():
 
 
 @pytest.mark.parametrize("name,h", [("resnet18_like", 5), ("three_layer", 2),
-                                    ("three_layer_light", 2), ("totals_123", 1)])
+                                    ("three_layer_light", 2), ("totals_123", 1),
+                                    ("mlp8_w1024", 4)])
 def test_profile_fixture_schedules_byte_identical(name, h):
     out = run_tool("profile", os.path.join(G.DATA, name + ".profile"), str(h))
     assert out.replace(G.DATA + "/", "") == G.read("profile_%s_h%d.txt" % (name, h))
