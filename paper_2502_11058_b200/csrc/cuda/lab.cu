@@ -1464,6 +1464,7 @@ struct dsx_lab {
   double sigma = 0.0, stddev = 0.0;
 
   void* w = nullptr;
+  double* stage64 = nullptr;  // fp32 labs: dense fp64 rows for host transfers (lazy)
   double* curv = nullptr;
   double* opt = nullptr;
   double* noise = nullptr;
@@ -2295,6 +2296,52 @@ dsx_status after_update(dsx_lab* lab, int mode) {
   return DSX_OK;
 }
 
+// fp32 labs keep the fp64 host interface: whole-state transfers go through a
+// dense fp64 staging buffer in HBM and one narrowing / widening pass on the
+// lab stream (round-to-nearest, the same rounding as a host double->float
+// conversion), instead of a host conversion and one pageable copy per row.
+__global__ void narrow_rows_kernel(const double* __restrict__ src, float* __restrict__ dst, long long ld,
+                                   long long dim, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[(i / dim) * ld + i % dim] = __double2float_rn(src[i]);
+}
+
+__global__ void widen_rows_kernel(const float* __restrict__ src, double* __restrict__ dst, long long ld,
+                                  long long dim, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = (double)src[(i / dim) * ld + i % dim];
+}
+
+dsx_status ensure_stage64(dsx_lab* lab) {
+  if (lab->stage64) return DSX_OK;
+  DSX_CUDA(cudaMalloc(&lab->stage64, 8 * (size_t)lab->dim * lab->kl));
+  return DSX_OK;
+}
+
+// host fp64 [kl][dim] -> fp32 rows (async on the lab stream)
+dsx_status set_all_f32(dsx_lab* lab, const double* w) {
+  DSX_TRY(ensure_stage64(lab));
+  const long long n = (long long)lab->dim * lab->kl;
+  DSX_CUDA(cudaMemcpyAsync(lab->stage64, w, 8 * (size_t)n, cudaMemcpyHostToDevice, lab->stream));
+  narrow_rows_kernel<<<4 * lab->nsm, 256, 0, lab->stream>>>(lab->stage64, static_cast<float*>(lab->w), lab->ld,
+                                                           lab->dim, n);
+  DSX_CUDA(cudaGetLastError());
+  ++lab->launches;
+  return DSX_OK;
+}
+
+// fp32 rows -> host fp64 [kl][dim] (async on the lab stream)
+dsx_status get_all_f32(dsx_lab* lab, double* w) {
+  DSX_TRY(ensure_stage64(lab));
+  const long long n = (long long)lab->dim * lab->kl;
+  widen_rows_kernel<<<4 * lab->nsm, 256, 0, lab->stream>>>(static_cast<const float*>(lab->w), lab->stage64, lab->ld,
+                                                          lab->dim, n);
+  DSX_CUDA(cudaGetLastError());
+  ++lab->launches;
+  DSX_CUDA(cudaMemcpyAsync(w, lab->stage64, 8 * (size_t)n, cudaMemcpyDeviceToHost, lab->stream));
+  return DSX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2464,6 +2511,7 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : lab->tl_ev)
     if (ev) cudaEventDestroy(ev);
+  if (lab->stage64) cudaFree(lab->stage64);
   if (lab->bar) cudaFree(lab->bar);
   if (lab->flags) cudaFree(lab->flags);
   if (lab->xsum) cudaFree(lab->xsum);
@@ -2541,8 +2589,7 @@ dsx_status dsx_lab_set_all_params(dsx_lab* lab, const double* w) {
                                cudaMemcpyHostToDevice, lab->stream));
     return DSX_OK;
   }
-  for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, w + (long long)k * lab->dim));
-  return DSX_OK;
+  return set_all_f32(lab, w);
 }
 
 dsx_status dsx_lab_set_state(dsx_lab* lab, const double* w, const uint64_t* rng) {
@@ -2556,7 +2603,7 @@ dsx_status dsx_lab_set_state(dsx_lab* lab, const double* w, const uint64_t* rng)
       DSX_CUDA(cudaMemcpy2DAsync(lab->w, 8 * lab->ld, w, 8 * lab->dim, 8 * lab->dim, lab->kl,
                                  cudaMemcpyHostToDevice, lab->stream));
     } else {
-      for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_set_params(lab, k, w + (long long)k * lab->dim));
+      DSX_TRY(set_all_f32(lab, w));
     }
   }
   if (rng) {
@@ -2579,7 +2626,7 @@ dsx_status dsx_lab_get_state(dsx_lab* lab, double* w, uint64_t* rng) {
       DSX_CUDA(cudaMemcpy2DAsync(w, 8 * lab->dim, lab->w, 8 * lab->ld, 8 * lab->dim, lab->kl,
                                  cudaMemcpyDeviceToHost, lab->stream));
     } else {
-      for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, w + (long long)k * lab->dim));
+      DSX_TRY(get_all_f32(lab, w));
     }
   }
   if (rng) {
@@ -2744,7 +2791,9 @@ dsx_status dsx_lab_get_all_params(dsx_lab* lab, double* w) {
     DSX_CUDA(cudaStreamSynchronize(lab->stream));
     return DSX_OK;
   }
-  for (int k = 0; k < lab->kl; ++k) DSX_TRY(dsx_lab_get_params(lab, k, w + (long long)k * lab->dim));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  DSX_TRY(get_all_f32(lab, w));
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
   return DSX_OK;
 }
 

@@ -306,3 +306,20 @@ def test_batched_engine_run_boundaries(batch, K, monkeypatch):
     for k in range(K):
         assert lab.rng_text(k) == O.mt_state_text(rngs[k])
     lab.close()
+
+
+@pytest.mark.parametrize("K,dim", [(1, 1), (3, 999), (8, 70001)])
+def test_f32_host_transfer_round_trip(K, dim):
+    """fp32 labs: whole-state set/get through the HBM fp64 staging buffer and
+    the narrowing/widening kernels give exactly the host double->float
+    rounding (row pitch ld != dim for these sizes), per row and whole-state."""
+    from paper_2502_11058_b200 import Lab, LabDesc
+    rng = np.random.default_rng(dim)
+    lab = Lab(LabDesc(dim=dim, block_sizes=[dim], workers_total=K, sigma=0.0, dtype="f32"))
+    w = rng.normal(size=(K, dim)) * 1e3
+    lab.set_params(w)
+    want = w.astype(np.float32).astype(np.float64)
+    assert np.array_equal(lab.get_params(), want)
+    lab.step(0.0, np.zeros(2, dtype=np.uint8))
+    assert np.array_equal(lab.get_params(), want)
+    lab.close()
