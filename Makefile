@@ -25,7 +25,7 @@ CUDA_HDRS := $(wildcard $(SRC)/cuda/*.cuh)
 API_HDRS  := $(wildcard include/dreamsched/*.hpp) include/dsx.h
 
 .PHONY: all clean acceptance
-all: $(LIB)/libdsx.so $(LIB)/libdreamsched.so build/parity_tool $(if $(wildcard $(REF)),acceptance)
+all: $(LIB)/libdsx.so $(LIB)/libdreamsched.so build/parity_tool $(if $(wildcard $(REF)),acceptance build/unit_tests)
 
 $(LIB)/libdsx.so: $(CUDA_SRCS) $(CUDA_HDRS) include/dsx.h
 	@mkdir -p $(LIB) build
@@ -43,6 +43,18 @@ acceptance: build/acceptance
 build/acceptance: $(REF)/tests/acceptance/acceptance_main.cpp tests/native/eager_init.cpp $(LIB)/libdreamsched.so
 	@mkdir -p build
 	$(CXX) -std=c++20 -O2 -Iinclude -I$(REF)/tests/support $< tests/native/eager_init.cpp -L$(LIB) -ldreamsched -ldsx \
+	    -Wl,-rpath,'$$ORIGIN/../$(LIB)' -o $@
+
+# The reference's own unit suite (proj/tests/unit/*.cpp, doctest) compiled
+# unchanged against this library through tests/native/doctest_shim; the
+# trainer cases run on the GPU path (tests/test_unit_suite.py).
+UNIT_SRCS := $(wildcard $(REF)/tests/unit/*.cpp)
+# simulator_test.cpp reads trace JSON with nlohmann/json (the local 3.11.3 header)
+JSON_DIR ?= $(shell python3 -c "import os,site;c=[os.path.join(p,'include/cudnn_frontend/thirdparty/nlohmann') for p in site.getsitepackages()];print(next((x for x in c if os.path.exists(os.path.join(x,'json.hpp'))),''))")
+build/unit_tests: $(UNIT_SRCS) tests/native/doctest_shim/doctest.h $(LIB)/libdreamsched.so
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Iinclude -I$(REF)/tests/support -Itests/native/doctest_shim -I$(JSON_DIR) \
+	    -DDREAMSCHED_TEST_DATA_DIR='"/root/repo/tests/golden/data"' $(UNIT_SRCS) -L$(LIB) -ldreamsched -ldsx \
 	    -Wl,-rpath,'$$ORIGIN/../$(LIB)' -o $@
 
 clean:

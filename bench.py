@@ -32,31 +32,54 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 PROFILE = os.path.join(REPO, "tests", "golden", "data", "resnet18_like.profile")
+GPT2_PROFILE = os.path.join(REPO, "tests", "golden", "data", "gpt2_small.profile")
 METRIC = "iterations/sec at 1/2/4/8 B200 vs CPU ref; exposed sync time per iteration"
 REF_TOOL = os.path.join(REPO, "oracle", "_ref", "parity_tool_ref")
 
 
-def parse_args():
+CONFIGS = {
+    # BASELINE.json configs[1]: the headline workload
+    "resnet18": {"profile": PROFILE, "workers": 8, "period": 5, "parity_steps": 10,
+                 "workload": "resnet18-shaped quadratic lab (61 registered layers), 8 workers, H=5"},
+    # BASELINE.json configs[2] at its parameter scale (GPT-2 small: 124,439,808
+    # parameters per worker registered as embeddings + 12 blocks + ln_f)
+    "gpt2": {"profile": GPT2_PROFILE, "workers": 8, "period": 4, "parity_steps": 2,
+             "workload": "gpt2-small-shaped quadratic lab (14 registered layers, 124,439,808 "
+                         "params/worker), 8 workers, H=4"},
+}
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=48)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workers", type=int, default=8)
-    ap.add_argument("--period", type=int, default=5)
+    ap.add_argument("--config", default="resnet18", choices=sorted(CONFIGS))
+    ap.add_argument("--workers", type=int, default=None)
+    ap.add_argument("--period", type=int, default=None)
     ap.add_argument("--sigma", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--profile", default=PROFILE)
+    ap.add_argument("--profile", default=None)
     ap.add_argument("--sync-algo", default="pairwise", choices=["pairwise", "nccl_avg"])
     ap.add_argument("--no-overlap", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parity-steps", type=int, default=None,
+                    help="steps of the full-size parity pass vs the reference (default per config)")
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="also skips the parity pass")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="auto", choices=["auto", "measured", "profile"],
                     help="multi-GPU: schedule from the CUDA-event profile measured on these GPUs "
                          "(auto for N>1) or from --profile's times")
-    return ap.parse_args()
+    a = ap.parse_args(argv)
+    c = CONFIGS[a.config]
+    a.profile = a.profile or c["profile"]
+    a.workers = a.workers or c["workers"]
+    a.period = a.period or c["period"]
+    a.parity_steps = c["parity_steps"] if a.parity_steps is None else a.parity_steps
+    a.workload = c["workload"]
+    return a
 
 
 # ---------------------------------------------------------------- helpers ---
@@ -167,16 +190,16 @@ def learning_rate(r: int, period: int) -> float:
 def reference_arm(args, world, rank):
     if rank != 0:
         return None
-    sizes_note = "resnet18_like.profile blocks"
     steps = max(1, args.steps)
     warm = max(0, args.warmup)
-    # Bound the run: the full-size reference step takes seconds (4.3 s at
-    # sigma=1 in the survey); time one step first and cap the sample.
+    # Bound the run: the full-size reference step takes seconds (2 s at
+    # sigma=1 for resnet18, ~1 min for gpt2); time one step first and cap
+    # the sample at ~150 s of CPU work.
     probe = run_ref_tool(args, 1, 0)
     per_step = probe["seconds"]
     budget_s = 150.0
     steps = int(max(1, min(steps, budget_s // max(per_step, 1e-9))))
-    warm = int(min(warm, 1))
+    warm = int(min(warm, 1)) if per_step < 20 else 0
     res = run_ref_tool(args, steps, warm)
     it_s = res["it_per_s"]
     line = {
@@ -187,7 +210,8 @@ def reference_arm(args, world, rank):
         "config": workload_config(args, world, res["dim"]),
         "cpu_baseline": {"value": it_s, "unit": "iterations/s", "cores": 1, "kind": "reference",
                          "sample": f"{steps} timed plsgd_step calls ({warm} warm-up) of the full "
-                                   f"workload ({sizes_note}), reference trainer.cpp single thread"},
+                                   f"workload ({os.path.basename(args.profile)} blocks), reference "
+                                   "trainer.cpp single thread"},
         "e2e": {"value": it_s, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -195,6 +219,9 @@ def reference_arm(args, world, rank):
 
 
 def run_ref_tool(args, steps, warmup):
+    """The reference's trainer.cpp (compiled from /root/reference into
+    oracle/_ref) running plsgd_step on the same workload; returns its JSON
+    line, including the per-worker parity digest after warmup + steps."""
     if not os.path.exists(REF_TOOL):
         raise RuntimeError("oracle/_ref/parity_tool_ref missing (built by __graft_entry__.build())")
     cmd = [REF_TOOL, "bench", "0", "0", str(args.workers), str(args.period), repr(args.sigma),
@@ -206,13 +233,50 @@ def run_ref_tool(args, steps, warmup):
 def workload_config(args, world, dim, schedule_src="profile"):
     sched = ("bubble_fill(schedule_dfs(profile measured on these GPUs by dsx_lab_profile, H))"
              if schedule_src == "measured" else "bubble_fill(schedule_dfs(profile, H))")
-    return {"workload": "resnet18-shaped quadratic lab (61 registered layers), 8 workers, H=5",
+    return {"workload": args.workload, "config": args.config,
             "profile": os.path.relpath(args.profile, REPO), "workers": args.workers,
             "period": args.period, "dim_per_worker": dim, "sigma": args.sigma,
             "schedule": sched, "seed": args.seed,
             "parallelism": f"dp{world} ({args.workers // world} workers/GPU)",
             "sync_algo": args.sync_algo if world > 1 else "fused in-kernel (single GPU)",
             "l2": "working set > 126 MB L2 (no flush needed)"}
+
+
+# ------------------------------------------------------------------ digest ---
+
+def fnv1a64(text: str) -> str:
+    h = 1469598103934665603
+    for ch in text.encode():
+        h ^= ch
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+def row_digest(w, rng_text):
+    """The parity_tool's per-worker digest (tests/native/parity_tool.cpp
+    cmd_bench): sequential sum and sum of squares, 64 strided samples, FNV-1a
+    of the rng state's text."""
+    import numpy as np
+    w = np.asarray(w, dtype=np.float64)
+    idx = (np.arange(64, dtype=np.int64) * (len(w) - 1)) // 63
+    return {"sum": float(np.cumsum(w)[-1]), "sumsq": float(np.cumsum(w * w)[-1]),
+            "rng_fnv": fnv1a64(rng_text), "samples": [float(x) for x in w[idx]]}
+
+
+def compare_digests(got, want, tol):
+    def rel(a, b):
+        return abs(a - b) / max(abs(b), 1e-300)
+    worst = {"sum": 0.0, "sumsq": 0.0, "samples": 0.0}
+    rng_ok = len(got) == len(want)
+    for g, w in zip(got, want):
+        worst["sum"] = max(worst["sum"], rel(g["sum"], w["sum"]))
+        worst["sumsq"] = max(worst["sumsq"], rel(g["sumsq"], w["sumsq"]))
+        worst["samples"] = max([worst["samples"]] + [rel(a, b) for a, b in zip(g["samples"], w["samples"])])
+        rng_ok = rng_ok and g["rng_fnv"] == w["rng_fnv"]
+    ok = rng_ok and max(worst.values()) <= tol
+    return {"ok": ok, "tolerance_rel": tol, "max_rel_row_sum": worst["sum"],
+            "max_rel_row_sumsq": worst["sumsq"], "max_rel_samples": worst["samples"],
+            "rng_states_exact": rng_ok}
 
 
 # ------------------------------------------------------------------ our arm ---
@@ -235,6 +299,7 @@ def measured_schedule(lab, sizes, H, dist, rank, fill=True):
                   bandwidth=1.0, latency=0.0)
     sets, fills, _, text = schedule_from_profile(path, H, fill=fill)
     return sets, fills, text
+
 
 def our_arm(args, world, rank, local_rank, dist):
     import ctypes as C
@@ -279,32 +344,46 @@ def our_arm(args, world, rank, local_rank, dist):
         if dist is not None:
             dist.barrier()
 
+    def max_ranks(vals):
+        if dist is None:
+            return vals
+        import torch
+        t = torch.tensor(vals, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t]
+
+    def timed_window(nsteps, mask_list):
+        """Exactly nsteps steps between two events on the lab stream.  The
+        noise engine is drained before the window and may only generate noise
+        for these nsteps steps, so the window holds exactly its own engine
+        work (no batch generated before record(0), none after record(1))."""
+        nonlocal r
+        lab.sync()
+        lab.set_noise_horizon(nsteps)
+        barrier()
+        lab.record(0)
+        for _ in range(nsteps):
+            lab.step(learning_rate(r, H), mask_list[r % H])
+            r += 1
+        lab.record(1)
+        ms = lab.elapsed_ms(0, 1)  # waits for the last event
+        lab.sync()
+        lab.set_noise_horizon(-1)
+        return max_ranks([ms])[0]
+
     r = 0
     for _ in range(max(3, args.warmup)):
         lab.step(learning_rate(r, H), masks[r % H])
         r += 1
     lab.sync()
     barrier()
-    lab.sync()
     clocks = ClockSampler(local_rank)
     clocks.start()
     launches0 = lab.launches()
-    lab.record(0)
-    for _ in range(args.steps):
-        lab.step(learning_rate(r, H), masks[r % H])
-        r += 1
-    lab.record(1)
-    ms = lab.elapsed_ms(0, 1)  # waits for the last event
-    lab.sync()
+    ms_max = timed_window(args.steps, masks)
     clocks.stop()
     launches = lab.launches() - launches0
     barrier()
-    ms_max = ms
-    if dist is not None:
-        import torch
-        t = torch.tensor([ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
     value = args.steps / (ms_max / 1e3)
 
     # per-step breakdown with instrumentation (separate pass; not the timed
@@ -348,16 +427,7 @@ def our_arm(args, world, rank, local_rank, dist):
         eng = {"run_1_step_ms": round(e1.value, 4), "batch_steps": nb.value,
                "run_batch_ms": round(eb.value, 4), "per_step_ms": round(eb.value / nb.value, 4)}
 
-    def max_ranks(vals):
-        if dist is None:
-            return vals
-        import torch
-        t = torch.tensor(vals, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return [float(x) for x in t]
-
     def synced_frac(ms):
-        sz = np.asarray(sizes, dtype=np.float64)
         return round(float(np.mean([np.dot(m[1:], sz) / dim for m in ms])), 4)
 
     schedule_info = {"source": schedule_src, "synced_param_frac_per_step": synced_frac(masks)}
@@ -366,28 +436,11 @@ def our_arm(args, world, rank, local_rank, dist):
         # the same steps with nothing to average: what the sync adds to an
         # iteration once every overlap (update, pipelined noise engine) counts
         none = np.zeros(L + 1, dtype=np.uint8)
-        lab.sync()
-        barrier()
-        lab.record(0)
-        for _ in range(args.steps):
-            lab.step(learning_rate(r, H), none)
-            r += 1
-        lab.record(1)
-        ms_n = max_ranks([lab.elapsed_ms(0, 1)])[0]
-        lab.sync()
-        nosync = ms_n / args.steps
+        nosync = timed_window(args.steps, [none] * H) / args.steps
     if schedule_src == "measured":
         schedule_info["text"] = sched_text
         # the same workload under the fixed profile's schedule, for comparison
-        lab.sync()
-        barrier()
-        lab.record(0)
-        for _ in range(args.steps):
-            lab.step(learning_rate(r, H), fixed_masks[r % H])
-            r += 1
-        lab.record(1)
-        ms_f = max_ranks([lab.elapsed_ms(0, 1)])[0]
-        lab.sync()
+        ms_f = timed_window(args.steps, fixed_masks)
         lab.set_pipeline(False)
         lab.set_instrument(True)
         per_f = []
@@ -409,61 +462,122 @@ def our_arm(args, world, rank, local_rank, dist):
     noise_ms = [p[3] for p in per]
     update_ms = [p[4] for p in per]
     if dist is not None:
-        import torch
-        t = torch.tensor([statistics.mean(sync_ms), statistics.mean(exposed_ms)], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sync_mean, exposed_mean = float(t[0]), float(t[1])
+        sync_mean, exposed_mean = max_ranks([statistics.mean(sync_ms), statistics.mean(exposed_ms)])
     else:
         sync_mean, exposed_mean = 0.0, 0.0
+
+    peak, peak_kind = measured_peaks()
     averaging = None
+    link_peak = None
+    if world > 1:
+        # NVLink roofline measured now, on these GPUs: a copy with the
+        # averaging kernel's access pattern (dsx_lab_link_probe)
+        link_peak = lab.link_probe(5) if args.sync_algo == "pairwise" else None
     if world > 1 and sync_mean > 0:
         # cross-rank average of the synced layers: ring-convention bytes
         # 2(W-1)/W x S per rank over NVLink, S = synced bytes of the exchange row
-        esz_b = 8 if args.dtype == "f64" else 4
-        S = synced_frac(masks) * dim * esz_b
+        S = synced_frac(masks) * dim * esz
         ach = 2 * (world - 1) / world * S / (sync_mean * 1e-3) / 1e9
+        lp = link_peak or None
         averaging = {"bound": "nvlink", "kernel": "p2p_average (peer-memory reduce + broadcast)",
-                     "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
-                     "frac": round(ach / 900.0, 4), "peak_kind": "nominal NVLink5 per direction",
+                     "achieved": round(ach, 1), "peak": round(lp, 1) if lp else None, "unit": "GB/s",
+                     "frac": round(ach / lp, 4) if lp else None,
+                     "peak_kind": "measured in this run: copy kernel with the averaging access pattern "
+                                  "(dsx_lab_link_probe)",
                      "synced_bytes_per_step": int(S), "sync_ms_per_iter": round(sync_mean, 5),
                      "note": "sync span includes the flag barriers and runs under the concurrent update"}
 
     # roofline: the dominant kernel on the path
-    peak, peak_kind = measured_peaks()
     update_bytes = int(round(statistics.mean(step_bytes)))
     upd = statistics.mean(update_ms)
     noi = statistics.mean(noise_ms)
-    # The HBM roofline belongs to the update (+ in-kernel averaging) kernel;
-    # the noise engine is integer/fp64-ALU bound (no HBM or tensor roofline)
-    # and is reported beside it.
     # which update kernel ran (mirrors libdsx's choice): the bulk-copy kernel
     # on one GPU with engine noise, the register-staged one otherwise
     bulk = (args.sigma > 0 and args.dtype == "f64" and kl == 8
             and os.environ.get("DSX_UPD_BULK", "") != "0")
-    dom = {"kernel": ("lab_update_bulk (fused gradient+update+average, cp.async.bulk data path)" if bulk
-                      else "lab_update (fused gradient+update+average)"), "ms": upd,
-           "bytes": update_bytes}
+    kname = "lab_update_bulk" if bulk else "lab_update"
+    dom = {"kernel": (kname + (" (fused gradient+update+average, cp.async.bulk data path)" if bulk
+                               else " (fused gradient+update+average)")), "ms": upd, "bytes": update_bytes}
     achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            # dram bytes per launch from the committed ncu capture
-            # (profiles/r01_ncu_summary.md), for this kernel and noise mode;
-            # the capture is single-GPU with all 8 workers, so it applies at N=1
-            rec = json.load(open(tpath)).get(dom["kernel"].split(" ")[0], {})
-            traffic = rec.get("sigma1" if args.sigma > 0 else "sigma0") if world == 1 else None
-        except Exception:
-            traffic = None
+    if os.path.exists(tpath) and world == 1 and args.config == "resnet18" and K == 8:
+        # dram bytes per launch from the committed ncu capture of this kernel,
+        # dtype and noise mode (single GPU, 8 workers, resnet18 workload)
+        key = f"{kname}:{args.dtype}:sigma{1 if args.sigma > 0 else 0}"
+        traffic = json.load(open(tpath)).get(key)
+    # step-level roofline: the step's HBM bytes (update kernels
+    # + the engine's normal writes) at the measured HBM peak; with several
+    # ranks the average's NVLink bytes at the link peak measured above are
+    # assumed perfectly overlapped (max).  achieved/roof = t_roof / ms_per_step.
+    engine_write = float(kl * dim * 8) if args.sigma > 0 else 0.0
+    t_hbm = (update_bytes + engine_write) / (peak * 1e9) * 1e3
+    t_link = 0.0
+    if world > 1 and link_peak:
+        t_link = 2 * (world - 1) / world * synced_frac(masks) * dim * esz / (link_peak * 1e9) * 1e3
+    t_roof = max(t_hbm, t_link)
+    ms_step = ms_max / args.steps
+    step_roof = {"t_roof_ms": round(t_roof, 5), "ms_per_step": round(ms_step, 5),
+                 "frac": round(t_roof / ms_step, 4),
+                 "hbm_bytes_per_step": int(update_bytes + engine_write), "t_hbm_ms": round(t_hbm, 5),
+                 "t_nvlink_ms": round(t_link, 5),
+                 "definition": "t_roof = max(HBM bytes of the step (update reads/writes + noise-engine "
+                               "normal writes) / HBM peak, NVLink bus bytes of the average / measured "
+                               "link peak); the noise engine's ALU work is not in the bound"}
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": dom["kernel"], "kernel_ms": round(dom["ms"], 4),
                 "algorithmic_bytes_per_launch": dom["bytes"], "peak_kind": peak_kind,
+                "step": step_roof,
                 "step_breakdown_ms": {"step_serialized": round(statistics.mean(step_ms), 4),
                                       "noise_engine": round(noi, 4), "update": round(upd, 4)},
                 "noise_engine": {"bound": "alu (int64 twist/temper + fp64 polar)",
                                  "ms_one_step_run": round(noi, 4), "normals_per_step": kl * dim,
                                  "batched": eng, "overlapped_with_update": True}}
+
+    # full-size parity against the reference (its trainer.cpp compiled from
+    # /root/reference): the same seed, schedule and step count from zeros;
+    # per-worker digests of every worker's parameters and rng state.  Rank 0
+    # runs the reference (also the CPU baseline at N=1) while the GPUs step.
+    parity = None
+    cpu = None
+    ref_res = None
+    if not args.no_cpu_baseline and args.parity_steps > 0:
+        import threading as th
+        ref_box = {}
+        ref_thread = None
+        if rank == 0:
+            def _ref():
+                try:
+                    ref_box["res"] = run_ref_tool(args, max(1, args.parity_steps - 1),
+                                                  1 if args.parity_steps > 1 else 0)
+                except Exception as e:  # noqa: BLE001
+                    ref_box["err"] = str(e)
+            ref_thread = th.Thread(target=_ref, daemon=True)
+            ref_thread.start()
+        lab.seed(args.seed)
+        lab.fill(0.0)
+        for rr in range(args.parity_steps):
+            lab.step(learning_rate(rr, H), fixed_masks[rr % H])
+        lab.sync()
+        mine = [row_digest(lab.get_row(k), lab.rng_text(k)) for k in range(kl)]
+        if dist is not None:
+            allv = [None] * world
+            dist.all_gather_object(allv, mine)
+            mine = [d for part in allv for d in part]
+        if rank == 0:
+            ref_thread.join()
+            ref_res = ref_box.get("res")
+            if ref_res is None:
+                parity = {"ok": None, "error": ref_box.get("err", "reference run failed")}
+            else:
+                tol = 1e-12 if args.dtype == "f64" else 1e-5
+                parity = compare_digests(mine, ref_res["digest"], tol)
+                parity.update({"steps": args.parity_steps, "workers": len(mine),
+                               "schedule": "bubble_fill(schedule_dfs(profile, H))",
+                               "reference": "oracle/_ref/parity_tool_ref bench (trainer.cpp compiled "
+                                            "from /root/reference), same seed/schedule/steps",
+                               "pipelined_engine_batches": eng["batch_steps"] if eng else None})
 
     # e2e through the C-ABI with HOST buffers (plsgd_step semantics: worker
     # params + rng states in and out every step)
@@ -487,11 +601,7 @@ def our_arm(args, world, rank, local_rank, dist):
             N.call("dsx_lab_step_host", lab.h, learning_rate(r, H), masks_c[r % H].ctypes.data, rows, rp)
             r += 1
         lab.sync()
-        el = time.perf_counter() - t0
-        if dist is not None:
-            t = torch.tensor([el], dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = max_ranks([time.perf_counter() - t0])[0]
         rng_bytes = kl * 313 * 8
         e2e = {"value": args.e2e_steps / el, "unit": "iterations/s",
                "h2d_bytes_per_step": kl * dim * 8 + rng_bytes,
@@ -504,21 +614,16 @@ def our_arm(args, world, rank, local_rank, dist):
         lab.close()
         return None
 
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            res = run_ref_tool(args, 2, 1)
-            cpu = {"value": res["it_per_s"], "unit": "iterations/s", "cores": 1,
-                   "kind": "reference",
-                   "sample": "2 timed plsgd_step calls (1 warm-up) of the full workload, "
-                             "reference trainer.cpp compiled from /root/reference, 1 thread"}
-        except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "unit": "iterations/s", "cores": 1, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+    if world == 1 and ref_res is not None:
+        n_timed = max(1, args.parity_steps - 1)
+        cpu = {"value": ref_res["it_per_s"], "unit": "iterations/s", "cores": 1, "kind": "reference",
+               "sample": f"{n_timed} timed plsgd_step calls (after {args.parity_steps - n_timed} warm-up) of "
+                         "the full workload, reference trainer.cpp compiled from /root/reference, 1 thread "
+                         "(the same run is the parity reference)"}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "iterations/s", "n_gpus": world,
-        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_max / args.steps, 5),
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
         "config": workload_config(args, world, dim, schedule_src),
@@ -526,20 +631,41 @@ def our_arm(args, world, rank, local_rank, dist):
         "sync_ms_per_iter": round(sync_mean, 5),
         "exposed_sync_frac": round(exposed_mean / sync_mean, 4) if sync_mean > 0 else None,
         "ms_per_step_without_sync": round(nosync, 5) if nosync else None,
-        "sync_added_ms_per_iter": round(ms_max / args.steps - nosync, 5) if nosync else None,
-        "sync_added_frac": (round((ms_max / args.steps - nosync) / sync_mean, 4)
+        "sync_added_ms_per_iter": round(ms_step - nosync, 5) if nosync else None,
+        "sync_added_frac": (round((ms_step - nosync) / sync_mean, 4)
                             if nosync and sync_mean > 0 else None),
         "schedule": schedule_info, "averaging": averaging,
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks.summary(),
+        "timing": "exactly `steps` steps between CUDA events on the lab stream; the noise engine is "
+                  "drained before the window and bounded to the window's steps (dsx_lab_set_noise_horizon)",
     }
     lab.close()
     return line
 
 
+def spawn_ranks(args_argv, n):
+    """`python bench.py --gpus N` without torchrun: launch N ranks on this
+    node (torch.distributed.run, 127.0.0.1) and relay rank 0's line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + args_argv
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
+    world = int(env_world or "1")
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+              "(torchrun --nproc-per-node N) or pass a matching --gpus", file=sys.stderr)
+        sys.exit(2)
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None

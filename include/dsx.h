@@ -160,6 +160,20 @@ dsx_status dsx_lab_set_overlap(dsx_lab* lab, int enabled);
  * serializes noise and update (used to time each alone). */
 dsx_status dsx_lab_set_pipeline(dsx_lab* lab, int enabled);
 
+/* Bounded noise look-ahead (timing windows): drains the noise stream, drops
+ * noise generated ahead of the committed rng state, and lets the engine
+ * generate noise only for the next `steps` dsx_lab_step calls (runs are cut
+ * to one step when a whole batch would reach past the horizon).  A window of
+ * exactly `steps` steps then contains exactly its own engine work.  steps < 0
+ * restores unbounded pipelining.  Results are unchanged either way. */
+dsx_status dsx_lab_set_noise_horizon(dsx_lab* lab, long long steps);
+
+/* NVLink roofline for the averaging kernel, measured now (collective: every
+ * rank calls it between steps): a copy kernel with the averaging kernel's
+ * access pattern over every rank's peer-mapped scratch buffer; *gbs = bus
+ * bytes 2(W-1)/W x S per rank / median time.  0 on a single rank. */
+dsx_status dsx_lab_link_probe(dsx_lab* lab, int reps, double* gbs);
+
 /* Bandwidth-throttled sync (the paper's low-bandwidth regime): every synced
  * layer additionally occupies the FIFO sync stream for latency +
  * layer_bytes/bandwidth seconds (comm_time, profile.cpp:103-110), issued

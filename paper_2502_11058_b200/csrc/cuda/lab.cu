@@ -166,7 +166,7 @@ __device__ __forceinline__ void fused_tile_barrier(const FusedArgs& f, int ntile
         __nanosleep(32);
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 30000000000ull) __trap();
+        if (t - t0 > 600000000000ull) __trap();
       }
     }
   }
@@ -1292,8 +1292,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 // Thread q < R: optionally publishes `value` into rank q's slot[rank], then
 // waits until this rank's slot[q] reached `value` (every peer published).
-// A peer that never arrives traps after ~30 s instead of hanging the GPU.
-__global__ void flag_wait_kernel(FlagPtrs f, int rank, int R, int slot, unsigned long long value, int publish) {
+// A peer that never arrives traps after `timeout_ns` (DSX_FLAG_TIMEOUT_S,
+// default 600 s: a slow host thread on a peer is not a failure) instead of
+// hanging the GPU forever; the trap message names the rank and epoch.
+__global__ void flag_wait_kernel(FlagPtrs f, int rank, int R, int slot, unsigned long long value, int publish,
+                                 unsigned long long timeout_ns) {
   const int q = threadIdx.x;
   if (q >= R) return;
   if (publish) {
@@ -1307,7 +1310,10 @@ __global__ void flag_wait_kernel(FlagPtrs f, int rank, int R, int slot, unsigned
     __nanosleep(64);
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 30000000000ull) __trap();
+    if (t - t0 > timeout_ns) {
+      printf("dsx: rank %d timed out waiting for rank %d (flag slot %d, epoch %llu)\n", rank, q, slot, value);
+      __trap();
+    }
   }
 }
 
@@ -1397,6 +1403,36 @@ p2p_average_kernel(PeerPtrs peers, long long a, long long b, int k_total, PairPr
       __threadfence_system();
       for (int q = 0; q < sig.R; ++q) st_release_sys(sig.f.p[q] + kMaxProg + sig.rank, sig.value);
     }
+  }
+}
+
+// NVLink roofline probe: the averaging kernel's exact access pattern (this
+// rank's slice read from every rank's buffer, written back to every rank's
+// buffer: 2(W-1)/W x S bytes over NVLink per rank) as a plain copy — 16-B
+// vectors, four slices in flight per thread, no reduction.  What p2p_average
+// achieves is reported against this, measured in the same run.
+template <int W>
+__global__ void __launch_bounds__(256) p2p_probe_kernel(PeerPtrs peers, long long a, long long b) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = a + tid;
+  for (; i + 3 * stride < b; i += 4 * stride) {
+    double2 v[4][W];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < W; ++q) v[u][q] = static_cast<const double2*>(peers.p[q])[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < W; ++q) static_cast<double2*>(peers.p[(q + 1) % W])[i + u * stride] = v[u][q];
+  }
+  for (; i < b; i += stride) {
+    double2 v[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) v[q] = static_cast<const double2*>(peers.p[q])[i];
+#pragma unroll
+    for (int q = 0; q < W; ++q) static_cast<double2*>(peers.p[(q + 1) % W])[i] = v[q];
   }
 }
 
@@ -1503,6 +1539,7 @@ struct dsx_lab {
   int batch_set = -1, batch_t = 0, batch_n = 0;  // current run: set, next step, steps
   int pf_set = -1, pf_n = 0;               // run prefetched into the other set
   bool pipeline = true;
+  long long horizon = -1;                  // steps the engine may generate ahead (-1: unbounded)
   bool has_ranges = false, synced_last = false;
   bool overlap = true;
   uint64_t launches = 0;
@@ -1525,6 +1562,7 @@ struct dsx_lab {
   FlagPtrs fpeers{};                     // every rank's flag block, mapped here
   unsigned int* sig_counter = nullptr;   // finished-block counter of the averaging kernel
   unsigned long long epoch = 0, sig_count = 0;
+  unsigned long long flag_timeout_ns = 600ull * 1000000000ull;  // DSX_FLAG_TIMEOUT_S
   // fused update + average (DSX_FUSED=0: separate averaging kernel): the
   // published subtree sums [2][dim] and tile flags [2][R][ntiles] of every
   // rank, mapped into every peer
@@ -1964,14 +2002,14 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
   // "every rank's subtree sums of this group are final"
   auto ready = [&]() -> dsx_status {
     if (!fb) return barrier();
-    flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, R, 0, ++lab->epoch, 1);
+    flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, R, 0, ++lab->epoch, 1, lab->flag_timeout_ns);
     ++lab->launches;
     return DSX_OK;
   };
   // "every rank's averaging writes so far have landed"
   auto landed = [&]() -> dsx_status {
     if (!fb) return barrier();
-    flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, R, kMaxProg, lab->sig_count, 0);
+    flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, R, kMaxProg, lab->sig_count, 0, lab->flag_timeout_ns);
     ++lab->launches;
     return DSX_OK;
   };
@@ -2266,7 +2304,7 @@ dsx_status run_noise(dsx_lab* lab, int* mode) {
     } else {
       const int commit_set = lab->mt_commit == 0 ? -1 : (lab->mt_commit - 1) / lab->tmax;
       const int set = commit_set == 0 ? 1 : 0;
-      const int steps = lab->pipeline ? lab->tmax : 1;
+      const int steps = (lab->pipeline && (lab->horizon < 0 || lab->horizon >= lab->tmax)) ? lab->tmax : 1;
       DSX_TRY(launch_engine(lab, set, steps, lab->mt_commit));
       lab->batch_set = set;
       lab->batch_n = steps;
@@ -2289,6 +2327,9 @@ dsx_status after_update(dsx_lab* lab, int mode) {
   if (mode != 2) return DSX_OK;
   DSX_CUDA(cudaEventRecord(lab->ev_upd[lab->cur_set], lab->stream));
   if (!lab->pipeline || lab->pf_set >= 0 || lab->batch_set < 0) return DSX_OK;
+  // a bounded horizon: never generate noise for steps beyond it (the whole
+  // next run must be consumed within the horizon)
+  if (lab->horizon >= 0 && lab->horizon - (lab->batch_n - lab->batch_t) < lab->tmax) return DSX_OK;
   const int set = 1 - lab->batch_set;
   DSX_TRY(launch_engine(lab, set, lab->tmax, boundary_slot(lab, lab->batch_set, lab->batch_n - 1)));
   lab->pf_set = set;
@@ -2430,6 +2471,25 @@ dsx_status dsx_lab_create(const dsx_lab_desc* d, dsx_lab** out) {
     const char* nb = std::getenv("DSX_NOISE_BATCH");
     const int def = std::max(kNoiseBatch, std::min(16, 32 / std::max(1, lab->kl)));
     lab->tmax = std::max(1, std::min(16, nb ? std::atoi(nb) : def));
+    // The engine's normals buffers hold two runs (double-buffered) of tmax
+    // steps: ~2 x 8 B x kl x 2.55 x dim x tmax / 2 plus checkpoints.  At
+    // GPT-2 size (dim 124M, 8 workers) 8-step runs would need ~170 GB, so
+    // the run length is cut until the engine fits the free HBM (keeping a
+    // reserve for the caller).
+    size_t freeb = 0, totb = 0;
+    if (cudaMemGetInfo(&freeb, &totb) == cudaSuccess) {
+      const double reserve = 3.0 * (1ull << 30);
+      const double avail = 0.9 * ((double)freeb - reserve);
+      auto engine_bytes = [&](int T) {
+        const double E = 2.0 * ((double)((lab->dim + 1) / 2) * T / 0.78539816339744831) + 4096.0;
+        return 8.0 * lab->kl * E * 2.10 + 256.0 * (1 << 20);
+      };
+      while (lab->tmax > 1 && engine_bytes(lab->tmax) > avail) --lab->tmax;
+      if (engine_bytes(lab->tmax) > avail)
+        return cleanup(fail(DSX_ERR_CUDA, "noise engine does not fit in free HBM (" +
+                                              std::to_string((long long)(engine_bytes(1) / 1e9)) +
+                                              " GB needed for one-step runs); use fewer workers per GPU"));
+    }
   }
   if (cudaMalloc(&lab->mt, (1 + 2 * (size_t)lab->tmax) * 8 * (size_t)(kMtN + 1) * lab->kl) != cudaSuccess)
     return cleanup(fail(DSX_ERR_CUDA, "cudaMalloc(mt) failed"));
@@ -2856,6 +2916,7 @@ dsx_status dsx_lab_step(dsx_lab* lab, double eta, const unsigned char* mask) {
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[0], lab->stream));
   int noise = 0;
   DSX_TRY(run_noise(lab, &noise));
+  if (lab->horizon > 0) --lab->horizon;
   if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[5], lab->stream));
   DSX_TRY(lab->dtype == DSX_F64 ? step_impl<double>(lab, eta, mask, noise)
                                 : step_impl<float>(lab, eta, mask, noise));
@@ -2882,6 +2943,12 @@ dsx_status dsx_lab_step_with_noise(dsx_lab* lab, double eta, const unsigned char
 dsx_status dsx_lab_last_max_grad_norm_sq(dsx_lab* lab, double* out) {
   DSX_TRY(check_lab(lab));
   if (!out) return fail(DSX_ERR_ARGUMENT, "null out");
+  if (lab->nranks > 1 && lab->comm) {
+    // the reference's max runs over all K workers (trainer.cpp:190-200):
+    // every rank holds a max over its own rows, so reduce across ranks
+    // (a collective: every rank calls this after the same step)
+    DSX_NCCL(ncclAllReduce(lab->maxnorm, lab->maxnorm, 1, ncclDouble, ncclMax, lab->comm, lab->stream));
+  }
   DSX_CUDA(cudaStreamSynchronize(lab->stream));
   DSX_CUDA(cudaMemcpy(out, lab->maxnorm, 8, cudaMemcpyDeviceToHost));
   return DSX_OK;
@@ -3079,6 +3146,8 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   cudaFree(d_handles);
   cudaFree(d_ok);
   lab->p2p = ok != 0;
+  if (const char* t = std::getenv("DSX_FLAG_TIMEOUT_S"))
+    lab->flag_timeout_ns = (unsigned long long)std::max(1.0, std::atof(t)) * 1000000000ull;
   const char* fb = std::getenv("DSX_FLAG_BARRIER");
   lab->flag_bar = lab->p2p && !(fb && fb[0] == '0');
   // Several ranks: size the noise engine's segment wave for two thirds of the
@@ -3103,6 +3172,62 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   const char* fz = std::getenv("DSX_FUSED");
   lab->fused = lab->p2p && sync_algo == DSX_SYNC_PAIRWISE && nranks <= kMaxFuse && lab->kl <= 8 &&
                fz && fz[0] == '1';
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_link_probe(dsx_lab* lab, int reps, double* gbs) {
+  DSX_TRY(check_lab(lab));
+  if (!gbs) return fail(DSX_ERR_ARGUMENT, "null out");
+  *gbs = 0.0;
+  if (lab->nranks < 2) return DSX_OK;
+  if (!lab->p2p) return fail(DSX_ERR_STATE, "link probe needs the NVLink peer-memory exchange");
+  const int W = lab->nranks;
+  // scratch: every rank's fused-path sums buffer [2][ld] (mapped into all
+  // peers at comm init, idle between steps) as 16-B units
+  const long long units = (long long)(elem_size(lab) * 2 * lab->ld / 16);
+  const long long per = units / W;
+  const long long a = per * lab->rank, b = a + per;
+  PeerPtrs pp{};
+  for (int q = 0; q < W; ++q) pp.p[q] = lab->xpeer[q];
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
+  DSX_CUDA(cudaStreamSynchronize(lab->side));
+  auto barrier = [&]() -> dsx_status {
+    DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
+    DSX_CUDA(cudaStreamSynchronize(lab->side));
+    return DSX_OK;
+  };
+  auto launch = [&]() {
+    const int grid = lab->nsm * 4;
+    switch (W) {
+      case 2: p2p_probe_kernel<2><<<grid, 256, 0, lab->side>>>(pp, a, b); break;
+      case 4: p2p_probe_kernel<4><<<grid, 256, 0, lab->side>>>(pp, a, b); break;
+      case 8: p2p_probe_kernel<8><<<grid, 256, 0, lab->side>>>(pp, a, b); break;
+      default: break;
+    }
+  };
+  if (W != 2 && W != 4 && W != 8) return fail(DSX_ERR_STATE, "link probe: 2, 4 or 8 ranks");
+  std::vector<float> ms;
+  cudaEvent_t e0, e1;
+  DSX_CUDA(cudaEventCreate(&e0));
+  DSX_CUDA(cudaEventCreate(&e1));
+  for (int r = 0; r < std::max(1, reps) + 1; ++r) {  // first launch warms up
+    DSX_TRY(barrier());
+    DSX_CUDA(cudaEventRecord(e0, lab->side));
+    launch();
+    DSX_CUDA(cudaEventRecord(e1, lab->side));
+    DSX_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    DSX_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    if (r > 0) ms.push_back(t);
+  }
+  DSX_TRY(barrier());
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  std::sort(ms.begin(), ms.end());
+  const double med = ms[ms.size() / 2];
+  // ring convention: 2(W-1)/W x S per rank, S = W x slice bytes
+  const double bus = 2.0 * (W - 1) * (double)per * 16.0;
+  *gbs = bus / (med * 1e-3) / 1e9;
   return DSX_OK;
 }
 
@@ -3194,7 +3319,7 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
       const bool fb = lab->flag_bar;
       auto bar_ready = [&]() -> dsx_status {
         if (fb) {
-          flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, lab->nranks, 0, ++lab->epoch, 1);
+          flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, lab->nranks, 0, ++lab->epoch, 1, lab->flag_timeout_ns);
         } else {
           DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
         }
@@ -3202,7 +3327,7 @@ dsx_status dsx_lab_profile(dsx_lab* lab, int reps, double* t_bp, double* t_comm)
       };
       auto bar_landed = [&]() -> dsx_status {
         if (fb) {
-          flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, lab->nranks, kMaxProg, lab->sig_count, 0);
+          flag_wait_kernel<<<1, 64, 0, lab->side>>>(lab->fpeers, lab->rank, lab->nranks, kMaxProg, lab->sig_count, 0, lab->flag_timeout_ns);
         } else {
           DSX_NCCL(ncclAllReduce(lab->bar, lab->bar, 1, ncclInt32, ncclSum, lab->comm, lab->side));
         }
@@ -3294,6 +3419,16 @@ dsx_status dsx_lab_set_pipeline(dsx_lab* lab, int enabled) {
   DSX_TRY(check_lab(lab));
   if (!enabled) DSX_TRY(invalidate_prefetch(lab));
   lab->pipeline = enabled != 0;
+  return DSX_OK;
+}
+
+dsx_status dsx_lab_set_noise_horizon(dsx_lab* lab, long long steps) {
+  DSX_TRY(check_lab(lab));
+  if (steps >= 0) {
+    DSX_CUDA(cudaStreamSynchronize(lab->stream));
+    DSX_TRY(invalidate_prefetch(lab));
+  }
+  lab->horizon = steps < 0 ? -1 : steps;
   return DSX_OK;
 }
 

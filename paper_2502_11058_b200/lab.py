@@ -88,6 +88,11 @@ class Lab:
         N.call("dsx_lab_get_all_params", self.h, w.ctypes.data)
         return w
 
+    def get_row(self, local: int) -> np.ndarray:
+        w = np.empty(self.dim, dtype=np.float64)
+        N.call("dsx_lab_get_params", self.h, local, w.ctypes.data)
+        return w
+
     def fill(self, value: float) -> None:
         N.call("dsx_lab_fill_params", self.h, value)
 
@@ -147,6 +152,18 @@ class Lab:
 
     def set_pipeline(self, on: bool) -> None:
         N.call("dsx_lab_set_pipeline", self.h, int(on))
+
+    def set_noise_horizon(self, steps: int) -> None:
+        """Drain the noise engine and bound its look-ahead to `steps` steps
+        (-1: unbounded), so a timing window holds exactly its own engine work."""
+        N.call("dsx_lab_set_noise_horizon", self.h, int(steps))
+
+    def link_probe(self, reps: int = 5) -> float:
+        """Collective: NVLink bus GB/s of a copy with the averaging kernel's
+        access pattern (0 on one rank)."""
+        out = C.c_double()
+        N.call("dsx_lab_link_probe", self.h, reps, C.byref(out))
+        return out.value
 
     def set_overlap(self, on: bool) -> None:
         N.call("dsx_lab_set_overlap", self.h, int(on))

@@ -73,6 +73,8 @@ _SIGS = {
     "dsx_lab_comm_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
     "dsx_lab_set_overlap": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_lab_set_pipeline": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_lab_set_noise_horizon": ([C.c_void_p, C.c_longlong], C.c_int),
+    "dsx_lab_link_probe": ([C.c_void_p, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "dsx_lab_set_link": ([C.c_void_p, C.c_double, C.c_double], C.c_int),
     "dsx_lab_profile": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "dsx_lab_last_timeline": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),

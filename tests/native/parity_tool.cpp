@@ -350,9 +350,43 @@ int cmd_bench(int argc, char** argv) {
   const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   double checksum = 0.0;
   for (const auto& w : workers) for (double v : w.w) checksum += v;
+  // Parity digest of the state after warmup + steps iterations, per worker:
+  // sequential sum and sum of squares of w, 64 strided samples of w, and the
+  // FNV-1a 64 hash of the rng state's text form (operator<<: 312 words + p).
+  std::string digest = "[";
+  for (int k = 0; k < K; ++k) {
+    const auto& w = workers[static_cast<std::size_t>(k)].w;
+    double s1 = 0.0, s2 = 0.0;
+    for (double v : w) {
+      s1 += v;
+      s2 += v * v;
+    }
+    std::ostringstream ss;
+    ss << workers[static_cast<std::size_t>(k)].rng;
+    const std::string text = ss.str();
+    std::uint64_t h = 1469598103934665603ull;
+    for (unsigned char ch : text) {
+      h ^= ch;
+      h *= 1099511628211ull;
+    }
+    char buf[128];
+    digest += (k ? ", " : "");
+    std::snprintf(buf, sizeof buf, "{\"sum\": %.17g, \"sumsq\": %.17g, \"rng_fnv\": \"%016llx\", \"samples\": [",
+                  s1, s2, static_cast<unsigned long long>(h));
+    digest += buf;
+    for (int j = 0; j < 64; ++j) {
+      const std::size_t i = static_cast<std::size_t>(j) * (w.size() - 1) / 63;
+      std::snprintf(buf, sizeof buf, "%s%.17g", j ? ", " : "", w[i]);
+      digest += buf;
+    }
+    digest += "]}";
+  }
+  digest += "]";
   std::printf("{\"steps\": %d, \"seconds\": %.6f, \"it_per_s\": %.6f, \"dim\": %zu, \"workers\": %d, "
-              "\"blocks\": %d, \"period\": %d, \"sigma\": %g, \"checksum\": %.17g}\n",
-              steps, sec, steps / sec, problem.dim, K, problem.layer_count(), H, sigma, checksum);
+              "\"blocks\": %d, \"period\": %d, \"sigma\": %g, \"checksum\": %.17g, \"total_steps\": %lld, "
+              "\"digest\": %s}\n",
+              steps, sec, steps / sec, problem.dim, K, problem.layer_count(), H, sigma, checksum, r,
+              digest.c_str());
   return 0;
 }
 
