@@ -27,9 +27,17 @@ API_HDRS  := $(wildcard include/dreamsched/*.hpp) include/dsx.h
 .PHONY: all clean acceptance
 all: $(LIB)/libdsx.so $(LIB)/libdreamsched.so build/parity_tool $(if $(wildcard $(REF)),acceptance build/unit_tests)
 
-$(LIB)/libdsx.so: $(CUDA_SRCS) $(CUDA_HDRS) include/dsx.h
-	@mkdir -p $(LIB) build
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CUDA_SRCS) $(NCCL_LINK) 2> build/ptxas.log || (cat build/ptxas.log; false)
+# one object per .cu so `make -j` compiles them in parallel; ptxas -v output
+# per object in build/ptxas_<name>.log
+CUDA_OBJS := $(patsubst $(SRC)/cuda/%.cu,build/obj/%.o,$(CUDA_SRCS))
+build/obj/%.o: $(SRC)/cuda/%.cu
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -MMD -MP -c -o $@ $< 2> build/ptxas_$*.log || (cat build/ptxas_$*.log; false)
+-include $(CUDA_OBJS:.o=.d)
+
+$(LIB)/libdsx.so: $(CUDA_OBJS)
+	@mkdir -p $(LIB)
+	$(NVCC) $(ARCH) -shared -o $@ $(CUDA_OBJS) $(NCCL_LINK)
 
 $(LIB)/libdreamsched.so: $(HOST_SRCS) $(API_HDRS) $(LIB)/libdsx.so
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIB) -ldsx -Wl,-rpath,'$$ORIGIN'

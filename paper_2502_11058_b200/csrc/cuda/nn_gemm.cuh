@@ -1,0 +1,346 @@
+// nn_gemm.cuh — the dense-layer GEMMs of the NN local step (north_star (1)):
+//
+//   gemm_tc_kernel   bf16 x bf16 -> fp32 on the 5th-gen tensor cores:
+//                    TMA (cp.async.bulk.tensor, 128-B swizzle) stages A/B
+//                    tiles through a multi-stage mbarrier ring, one elected
+//                    thread issues tcgen05.mma (kind::f16, M=128, N=BN, K=16)
+//                    into a TMEM accumulator, four epilogue warps drain it
+//                    with tcgen05.ld and apply the layer epilogue.
+//   gemm_f32_kernel  fp32 SIMT FFMA GEMM for the 1e-5 parity runs (TF32 or
+//                    bf16 tensor cores cannot meet 1e-5; SURVEY §7 "fp32
+//                    GEMM parity").
+//
+// One GEMM, C[m][n] = sum_k A(m,k) B(n,k), batched over local workers
+// (blockIdx.z), covers the three GEMMs of a Linear layer y = x W^T with
+// row-major tensors x[B][in], W[out][in], y[B][out]:
+//   forward  y  = x  W^T : A = x  (K-major),  B = W  (K-major)
+//   dgrad    dx = dy W   : A = dy (K-major),  B = W  (N-major: W[k=out][n=in])
+//   wgrad    dW = dy^T x : A = dy (M-major),  B = x  (N-major)
+// MN-major operands are read by TMA in 64-element-wide boxes and described
+// to the MMA as MN-major canonical layouts, so no transposed copies exist.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dsx.h"
+
+namespace dsx_nn {
+
+// epilogue kinds
+enum : int {
+  kEpiF32 = 0,       // C fp32 = acc (+ C if accumulate)
+  kEpiBiasAct = 1,   // C = act(acc + bias[n])   (act: none / relu), T out
+  kEpiDRelu = 2,     // C = acc * (mask(m,n) > 0), T out (dgrad through relu)
+};
+
+struct GemmArgs {
+  int M, N, K, batch;
+  int epi, relu, accumulate;
+  void* C;
+  long long ldc, strideC;        // elements
+  const float* bias;             // [batch][...] fp32, indexed bias[b*strideBias + n]
+  long long strideBias;
+  const void* mask;              // relu' source, same element type as C
+  long long ldmask, strideMask;
+};
+
+// One GEMM call: operands (element pointers, leading dims, per-batch
+// strides), majors, tile width (0: auto) and the epilogue.  gemm() (gemm.cu)
+// launches the tcgen05 kernel for bf16 and the SIMT kernel for fp32.
+struct GemmCall {
+  bool bf16;
+  bool a_mn, b_mn;
+  const void* A;
+  long long lda, sA;
+  const void* B;
+  long long ldb, sB;
+  bool out_bf16;
+  int bn;
+  GemmArgs g;
+};
+dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm);
+
+constexpr int kBM = 128, kBK = 64, kUmmaK = 16;
+
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void nn_mbar_init(uint64_t* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nn_mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void nn_mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n NN_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra NN_WAIT_%=;\n}\n" ::"r"(
+          su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor (sm_100 UMMA): start address, leading /
+// stride byte offsets (16-B units), version 1, 128-B swizzle.
+__device__ __forceinline__ uint64_t smem_desc(unsigned addr, unsigned lbo_bytes, unsigned sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Epilogue of one output element (m, n) of batch b.
+template <typename TOut>
+__device__ __forceinline__ void epi_store(const GemmArgs& g, int b, int m, int n, float acc) {
+  if (g.epi == kEpiF32) {
+    float* c = static_cast<float*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+    *c = g.accumulate ? *c + acc : acc;
+    return;
+  }
+  TOut* c = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+  if (g.epi == kEpiBiasAct) {
+    float v = acc + (g.bias ? g.bias[(long long)b * g.strideBias + n] : 0.f);
+    if (g.relu) v = fmaxf(v, 0.f);
+    *c = from_f<TOut>(v);
+  } else {  // kEpiDRelu
+    const TOut mk = static_cast<const TOut*>(g.mask)[(long long)b * g.strideMask + (long long)m * g.ldmask + n];
+    *c = from_f<TOut>(to_f<TOut>(mk) > 0.f ? acc : 0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 GEMM: one 128 x BN output tile per CTA; warp 0 = TMA producer,
+// warp 1 = TMEM owner + MMA issuer, warps 2..5 = epilogue (TMEM lanes
+// 32*(warp%4) .. +31, i.e. rows of the tile).
+// ---------------------------------------------------------------------------
+template <int BN>
+struct TcCfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStages = BN >= 256 ? 4 : 6;
+  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+};
+
+template <int BN, bool A_MN, bool B_MN, typename TOut>
+__global__ void __launch_bounds__(192, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g) {
+  using Cfg = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tmem_full = empty + Cfg::kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM, b = blockIdx.z;
+  const int nk = (g.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&ta) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tb) : "memory");
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      nn_mbar_init(&full[s], 1);
+      nn_mbar_init(&empty[s], 1);
+    }
+    nn_mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(Cfg::kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int k = 0; k < nk; ++k) {
+        const int s = k % Cfg::kStages;
+        const unsigned ph = (unsigned)(k / Cfg::kStages) & 1u;
+        nn_mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* sa = smem + s * Cfg::kStage;
+        uint8_t* sb = sa + Cfg::kABytes;
+        nn_mbar_expect_tx(&full[s], Cfg::kStage);
+        if constexpr (!A_MN) {
+          tma_load_3d(sa, &ta, &full[s], k * kBK, m0, b);
+        } else {
+#pragma unroll
+          for (int i = 0; i < kBM / 64; ++i) tma_load_3d(sa + i * 64 * kBK * 2, &ta, &full[s], m0 + 64 * i, k * kBK, b);
+        }
+        if constexpr (!B_MN) {
+          tma_load_3d(sb, &tb, &full[s], k * kBK, n0, b);
+        } else {
+#pragma unroll
+          for (int i = 0; i < BN / 64; ++i) tma_load_3d(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, k * kBK, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      // instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                             ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+      for (int k = 0; k < nk; ++k) {
+        const int s = k % Cfg::kStages;
+        const unsigned ph = (unsigned)(k / Cfg::kStages) & 1u;
+        nn_mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const unsigned sa = su32(smem + s * Cfg::kStage);
+        const unsigned sb = sa + Cfg::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
+          // K-major: the 16-element K slice is 32 B into each 128-B swizzled
+          // row (8-row atoms 1024 B apart); MN-major: 16 K rows of 128 B
+          // further, 64-element MN chunks kBK*128 B apart.
+          const uint64_t ad = A_MN ? smem_desc(sa + kk * kUmmaK * 128, kBK * 128, 1024)
+                                   : smem_desc(sa + kk * kUmmaK * 2, 16, 1024);
+          const uint64_t bd = B_MN ? smem_desc(sb + kk * kUmmaK * 128, kBK * 128, 1024)
+                                   : smem_desc(sb + kk * kUmmaK * 2, 16, 1024);
+          tc_mma(tmem, ad, bd, idesc, (k | kk) != 0 ? 1u : 0u);
+        }
+        tc_commit(&empty[s]);  // frees the stage once these MMAs have read it
+      }
+      tc_commit(tmem_full);
+    }
+  } else {  // epilogue warps 2..5
+    nn_mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int m = m0 + 32 * q + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+          "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+            "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+            "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (m < g.M) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + c + j;
+          if (n < g.N) epi_store<TOut>(g, b, m, n, __uint_as_float(r[j]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 SIMT GEMM (parity path): 64x64 tile, 256 threads, 4x4 per thread,
+// K staged 16 at a time through shared memory; same operand majors and
+// epilogues as the tensor-core kernel.
+// ---------------------------------------------------------------------------
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, long long lda, long long sA,
+                                                       const float* __restrict__ B, long long ldb, long long sB,
+                                                       GemmArgs g) {
+  constexpr int T = 64, TK = 16;
+  __shared__ float as[TK][T + 4];
+  __shared__ float bs[TK][T + 4];
+  const int b = blockIdx.z;
+  const int m0 = blockIdx.y * T, n0 = blockIdx.x * T;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const float* Ab = A + (long long)b * sA;
+  const float* Bb = B + (long long)b * sB;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < g.K; k0 += TK) {
+    // 64x16 elements of each operand, 4 per thread
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = threadIdx.x + 256 * i;
+      int mm, kk;
+      if (A_MN) { kk = e >> 6; mm = e & 63; } else { mm = e >> 4; kk = e & 15; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      float v = 0.f;
+      if (gm < g.M && gk < g.K) v = A_MN ? Ab[(long long)gk * lda + gm] : Ab[(long long)gm * lda + gk];
+      as[kk][mm] = v;
+      int nn;
+      if (B_MN) { kk = e >> 6; nn = e & 63; } else { nn = e >> 4; kk = e & 15; }
+      const int gn = n0 + nn, gk2 = k0 + kk;
+      float w = 0.f;
+      if (gn < g.N && gk2 < g.K) w = B_MN ? Bb[(long long)gk2 * ldb + gn] : Bb[(long long)gn * ldb + gk2];
+      bs[kk][nn] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        av[i] = as[kk][ty + 16 * i];
+        bv[i] = bs[kk][tx + 16 * i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      if (m < g.M && n < g.N) epi_store<float>(g, b, m, n, acc[i][j]);
+    }
+}
+
+}  // namespace dsx_nn

@@ -14,7 +14,9 @@ DSX_PATH = os.path.join(LIB_DIR, "libdsx.so")
 DREAMSCHED_PATH = os.path.join(LIB_DIR, "libdreamsched.so")
 
 DSX_OK, DSX_ERR_ARGUMENT, DSX_ERR_STATE, DSX_ERR_CUDA, DSX_ERR_NCCL = range(5)
-DSX_F64, DSX_F32 = 0, 1
+DSX_F64, DSX_F32, DSX_BF16 = 0, 1, 2
+DSX_OPT_SGD, DSX_OPT_MOMENTUM, DSX_OPT_ADAM = 0, 1, 2
+DSX_EPI_F32, DSX_EPI_BIAS_ACT, DSX_EPI_DRELU = 0, 1, 2
 DSX_SYNC_PAIRWISE, DSX_SYNC_NCCL_AVG = 0, 1
 
 
@@ -37,6 +39,29 @@ class LabDescC(C.Structure):
         ("curvature", C.POINTER(C.c_double)),
         ("optimum", C.POINTER(C.c_double)),
         ("noise_sigma", C.c_double),
+    ]
+
+
+class GemmDescC(C.Structure):
+    _fields_ = [
+        ("dtype", C.c_int), ("M", C.c_int), ("N", C.c_int), ("K", C.c_int), ("batch", C.c_int),
+        ("a_mn", C.c_int), ("b_mn", C.c_int),
+        ("A", C.c_void_p), ("lda", C.c_longlong), ("strideA", C.c_longlong),
+        ("B", C.c_void_p), ("ldb", C.c_longlong), ("strideB", C.c_longlong),
+        ("C", C.c_void_p), ("ldc", C.c_longlong), ("strideC", C.c_longlong),
+        ("out_dtype", C.c_int), ("epi", C.c_int), ("relu", C.c_int), ("accumulate", C.c_int),
+        ("bias", C.c_void_p), ("strideBias", C.c_longlong),
+        ("mask", C.c_void_p), ("ldmask", C.c_longlong), ("strideMask", C.c_longlong),
+        ("bn", C.c_int), ("stream", C.c_void_p),
+    ]
+
+
+class MlpDescC(C.Structure):
+    _fields_ = [
+        ("device", C.c_int), ("dtype", C.c_int), ("workers_total", C.c_int), ("worker_begin", C.c_int),
+        ("workers_local", C.c_int), ("layers", C.c_int), ("widths", C.POINTER(C.c_int)),
+        ("batch", C.c_int), ("optimizer", C.c_int), ("momentum", C.c_double), ("beta1", C.c_double),
+        ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double),
     ]
 
 
@@ -88,9 +113,34 @@ _SIGS = {
 }
 
 
-def exported_symbols():
-    """Every entry point include/dsx.h declares (checked by the CPU tests)."""
-    return sorted(_SIGS)
+# include/dsx_nn.h: the NN local step
+_NN_SIGS = {
+    "dsx_gemm": ([C.POINTER(GemmDescC)], C.c_int),
+    "dsx_mlp_create": ([C.POINTER(MlpDescC), C.POINTER(C.c_void_p)], C.c_int),
+    "dsx_mlp_destroy": ([C.c_void_p], C.c_int),
+    "dsx_mlp_param_layout": ([C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p], C.c_int),
+    "dsx_mlp_set_params": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "dsx_mlp_get_params": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "dsx_mlp_get_state": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_mlp_set_batch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int], C.c_int),
+    "dsx_mlp_step": ([C.c_void_p, C.c_double, C.c_longlong, C.c_void_p], C.c_int),
+    "dsx_mlp_last_loss": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_mlp_sync": ([C.c_void_p], C.c_int),
+    "dsx_mlp_comm_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
+    "dsx_mlp_set_instrument": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_mlp_last_step_times": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_mlp_profile": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_mlp_event_record": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_mlp_event_elapsed": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
+    "dsx_mlp_launch_count": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "dsx_mlp_set_graphs": ([C.c_void_p, C.c_int], C.c_int),
+}
+_SIGS.update(_NN_SIGS)
+
+
+def exported_symbols(header: str = "dsx.h"):
+    """Every entry point include/<header> declares (checked by the CPU tests)."""
+    return sorted(_NN_SIGS) if header == "dsx_nn.h" else sorted(k for k in _SIGS if k not in _NN_SIGS)
 
 
 def load_dsx():

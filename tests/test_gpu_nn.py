@@ -1,0 +1,164 @@
+"""NN local step on the GPU (north_star (1), BASELINE configs[0]):
+
+* the layer GEMMs — tcgen05/TMA bf16 kernel in the three operand-major
+  combinations a Linear layer needs (forward K/K, dgrad K/N, wgrad M/N),
+  every tile width, ragged M/N/K, batched over workers — against a torch
+  fp32 matmul of the same bf16 operands; the fp32 SIMT kernel against fp64;
+* the K-worker MLP (fp32 SIMT path) against the float64 CPU restatement
+  oracle/mlp_oracle.py after 2H steps of scheduled partial sync, for SGD
+  with momentum and Adam (optimizer states local): relative L2 error of
+  every worker's parameters <= 1e-5 (north_star: fp32 parameters within
+  1e-5), synced layers bit-identical across workers;
+* the bf16 tensor-core MLP trains (loss falls) and tracks the fp32 run.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle.mlp_oracle import MlpOracle  # noqa: E402  (checker only)
+from paper_2502_11058_b200 import native as N  # noqa: E402
+from paper_2502_11058_b200.lab import enp, sync_mask  # noqa: E402
+from paper_2502_11058_b200.nn import Mlp, batch, gemm, init_params, teacher  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _rel(a, b):
+    return float((a - b).norm() / max(float(b.norm()), 1e-30))
+
+
+@pytest.mark.parametrize("M,N_,K,batchn", [(256, 1024, 1024, 4), (200, 136, 72, 2), (128, 64, 64, 1),
+                                           (384, 512, 320, 3)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_tc_gemm_forward_kk(M, N_, K, batchn, bn):
+    torch.manual_seed(0)
+    A = torch.randn(batchn, M, K, device=DEV).bfloat16()
+    B = torch.randn(batchn, N_, K, device=DEV).bfloat16()
+    bias = torch.randn(batchn, N_, device=DEV)
+    Cb = torch.zeros(batchn, M, N_, device=DEV, dtype=torch.bfloat16)
+    Cf = torch.zeros(batchn, M, N_, device=DEV)
+    ref = torch.bmm(A.float(), B.float().transpose(1, 2))
+    gemm(A, B, Cf, M=M, N_=N_, K=K, batch=batchn, lda=K, sA=M * K, ldb=K, sB=N_ * K, ldc=N_, sC=M * N_, bn=bn)
+    torch.cuda.synchronize()
+    assert _rel(Cf, ref) < 1e-5
+    gemm(A, B, Cb, M=M, N_=N_, K=K, batch=batchn, lda=K, sA=M * K, ldb=K, sB=N_ * K, ldc=N_, sC=M * N_,
+         epi=N.DSX_EPI_BIAS_ACT, relu=True, bias=bias, s_bias=N_, bn=bn)
+    torch.cuda.synchronize()
+    want = torch.relu(ref + bias[:, None, :]).bfloat16()
+    assert _rel(Cb.float(), want.float()) < 1e-2
+
+
+@pytest.mark.parametrize("M,N_,K,batchn", [(256, 1024, 1024, 4), (200, 136, 72, 2), (256, 1024, 16, 1)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_tc_gemm_dgrad_kn(M, N_, K, batchn, bn):
+    """dx = dy W: A = dy[M][K] K-major, B(n,k) = W[k][n] N-major, relu' mask epilogue."""
+    torch.manual_seed(1)
+    dy = torch.randn(batchn, M, K, device=DEV).bfloat16()
+    W = torch.randn(batchn, K, N_, device=DEV).bfloat16()
+    xin = torch.randn(batchn, M, N_, device=DEV).bfloat16()
+    C = torch.zeros(batchn, M, N_, device=DEV, dtype=torch.bfloat16)
+    gemm(dy, W, C, M=M, N_=N_, K=K, batch=batchn, b_mn=True, lda=K, sA=M * K, ldb=N_, sB=K * N_, ldc=N_,
+         sC=M * N_, epi=N.DSX_EPI_DRELU, mask=xin, ldmask=N_, s_mask=M * N_, bn=bn)
+    torch.cuda.synchronize()
+    ref = torch.bmm(dy.float(), W.float()) * (xin.float() > 0)
+    assert _rel(C.float(), ref.bfloat16().float()) < 1e-2
+
+
+@pytest.mark.parametrize("M,N_,K,batchn", [(1024, 1024, 256, 4), (10, 1024, 256, 2), (136, 200, 72, 1)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_tc_gemm_wgrad_mn(M, N_, K, batchn, bn):
+    """dW = dy^T x: A(m,k) = dy[k][m] M-major, B(n,k) = x[k][n] N-major, fp32 out."""
+    torch.manual_seed(2)
+    ld_a = (M + 7) // 8 * 8  # 16-B rows (the class dimension is padded like the MLP's)
+    dy = torch.randn(batchn, K, ld_a, device=DEV).bfloat16()
+    x = torch.randn(batchn, K, N_, device=DEV).bfloat16()
+    C = torch.zeros(batchn, M, N_, device=DEV)
+    gemm(dy, x, C, M=M, N_=N_, K=K, batch=batchn, a_mn=True, b_mn=True, lda=ld_a, sA=K * ld_a, ldb=N_,
+         sB=K * N_, ldc=N_, sC=M * N_, bn=bn)
+    torch.cuda.synchronize()
+    ref = torch.bmm(dy.float()[:, :, :M].transpose(1, 2), x.float())
+    assert _rel(C, ref) < 1e-5
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True), (True, False)])
+def test_f32_gemm_against_fp64(a_mn, b_mn):
+    torch.manual_seed(3)
+    M, N_, K, bt = 130, 77, 65, 2
+    A = torch.randn(bt, K, M, device=DEV) if a_mn else torch.randn(bt, M, K, device=DEV)
+    B = torch.randn(bt, K, N_, device=DEV) if b_mn else torch.randn(bt, N_, K, device=DEV)
+    C = torch.zeros(bt, M, N_, device=DEV)
+    gemm(A, B, C, M=M, N_=N_, K=K, batch=bt, a_mn=a_mn, b_mn=b_mn, lda=M if a_mn else K, sA=M * K,
+         ldb=N_ if b_mn else K, sB=N_ * K, ldc=N_, sC=M * N_, dtype="f32")
+    torch.cuda.synchronize()
+    Ad = A.double().transpose(1, 2) if a_mn else A.double()
+    Bd = B.double() if b_mn else B.double().transpose(1, 2)
+    assert _rel(C.double(), torch.bmm(Ad, Bd)) < 1e-6
+
+
+def _run_pair(widths, K, H, steps, optimizer, lr, dtype="f32", bsz=64, seed=1):
+    L = len(widths) - 1
+    t = teacher(seed, widths[0], widths[-1])
+    init = init_params(seed, widths)
+    m = Mlp(widths, bsz, K, dtype=dtype, optimizer=optimizer)
+    for k in range(K):
+        m.set_params(k, init)
+    orc = MlpOracle(widths, init, K, optimizer=optimizer)
+    sets = enp(L, H)
+    losses = []
+    for r in range(steps):
+        bs = [batch(seed, k, r, bsz, widths[0], t) for k in range(K)]
+        mask = sync_mask("partial", H, r, L, sets)
+        m.set_batch(np.stack([b[0] for b in bs]), np.stack([b[1] for b in bs]))
+        m.step(lr, r, mask)
+        orc.step(bs, lr, r, mask)
+        losses.append((m.last_loss().copy(), orc.loss.copy()))
+    got = [m.get_params(k) for k in range(K)]
+    m.close()
+    return got, orc, losses
+
+
+@pytest.mark.parametrize("optimizer,lr", [("momentum", 0.05), ("adam", 1e-3), ("sgd", 0.1)])
+def test_mlp_fp32_matches_cpu_restatement(optimizer, lr):
+    widths = [256, 256, 256, 256, 256, 256, 256, 256, 10]  # 8 registered layers
+    K, H = 4, 4
+    got, orc, losses = _run_pair(widths, K, H, 2 * H, optimizer, lr)
+    for k in range(K):
+        err = np.linalg.norm(got[k] - orc.w[k]) / np.linalg.norm(orc.w[k])
+        assert err <= 1e-5, (optimizer, k, err)
+    for gl, ol in losses:
+        np.testing.assert_allclose(gl, ol, rtol=1e-4)
+    # layers averaged at the last step are identical across workers
+    last_mask = sync_mask("partial", H, 2 * H - 1, len(widths) - 1, enp(len(widths) - 1, H))
+    for l in range(1, len(widths)):
+        if last_mask[l]:
+            lo, hi = orc.offsets[l - 1], orc.offsets[l]
+            for k in range(1, K):
+                assert np.array_equal(got[k][lo:hi], got[0][lo:hi])
+
+
+def test_mlp_fp32_config0_shape_matches_cpu_restatement():
+    """BASELINE configs[0] at full width (fc1..fc7 1024x1024, fc8 -> 10),
+    K = 4, H = 4, 2H steps, SGD with momentum, batch 256."""
+    widths = [1024] * 8 + [10]
+    got, orc, _ = _run_pair(widths, 4, 4, 8, "momentum", 0.05, bsz=256)
+    for k in range(4):
+        err = np.linalg.norm(got[k] - orc.w[k]) / np.linalg.norm(orc.w[k])
+        assert err <= 1e-5, (k, err)
+
+
+def test_mlp_bf16_tensor_cores_train_and_track_fp32():
+    widths = [1024] * 8 + [10]
+    K, H, steps = 4, 4, 40
+    got16, orc, losses16 = _run_pair(widths, K, H, steps, "momentum", 0.05, dtype="bf16", bsz=256)
+    first = float(np.mean(losses16[0][0]))
+    last = float(np.mean([np.mean(l[0]) for l in losses16[-5:]]))
+    assert last < 0.8 * first, (first, last)
+    # same trajectory as the float64 restatement up to bf16 operand rounding
+    for k in range(K):
+        err = np.linalg.norm(got16[k] - orc.w[k]) / np.linalg.norm(orc.w[k])
+        assert err < 2e-2, (k, err)

@@ -33,14 +33,24 @@ def _exports(lib):
     return {ln.split()[-1] for ln in out.splitlines() if ln.strip()}
 
 
-def test_dsx_exports_every_declared_symbol():
+@pytest.mark.parametrize("header", ["dsx.h", "dsx_nn.h"])
+def test_dsx_exports_every_declared_symbol(header):
     from paper_2502_11058_b200 import native
-    declared = _declared("dsx.h", "dsx")
-    assert declared == native.exported_symbols()
+    declared = _declared(header, "dsx")
+    assert declared == native.exported_symbols(header)
     exported = _exports(native.DSX_PATH)
     missing = [s for s in declared if s not in exported]
     assert not missing, missing
     native.load_dsx()  # resolves every signature
+
+
+def test_dense_gemm_uses_tcgen05_and_tma():
+    """The NN layer GEMMs are tcgen05 (UTCHMMA, TMEM loads) fed by TMA
+    (UTMALDG) — checked in the SASS of the shipped library."""
+    from paper_2502_11058_b200 import native
+    out = subprocess.run(["cuobjdump", "-sass", native.DSX_PATH], capture_output=True, text=True).stdout
+    for op in ("UTCHMMA", "UTMALDG", "LDTM"):
+        assert op in out, op
 
 
 def test_dreamsched_c_exports():
