@@ -47,12 +47,13 @@ def split(flat, widths):
 
 class MlpOracle:
     def __init__(self, widths, init, workers, optimizer="momentum", momentum=0.9, beta1=0.9, beta2=0.999,
-                 eps=1e-8, weight_decay=0.0):
+                 eps=1e-8, weight_decay=0.0, dtype=np.float64):
+        self.dtype = dtype  # float64 (the checker); float32 only to measure rounding sensitivity
         self.widths = list(widths)
         self.K = workers
         self.opt = optimizer
         self.mu, self.b1, self.b2, self.eps, self.wd = momentum, beta1, beta2, eps, weight_decay
-        self.w = [np.asarray(init, dtype=np.float64).copy() for _ in range(workers)]
+        self.w = [np.asarray(init, dtype=dtype).copy() for _ in range(workers)]
         self.m = [np.zeros_like(self.w[0]) for _ in range(workers)]
         self.v = [np.zeros_like(self.w[0]) for _ in range(workers)]
         self.offsets = [0]
@@ -78,7 +79,7 @@ class MlpOracle:
     def local_step(self, k, x, y, lr, t):
         L = len(self.widths) - 1
         layers = split(self.w[k], self.widths)
-        acts = [np.asarray(x, dtype=np.float64)]
+        acts = [np.asarray(x, dtype=self.dtype)]
         for l, (W, b) in enumerate(layers):
             z = acts[-1] @ W.T + b
             acts.append(np.maximum(z, 0.0) if l < L - 1 else z)

@@ -92,7 +92,8 @@ dsx_status launch_tc_bn(bool am, bool bm, bool ob, const CUtensorMap& ta, const 
                         cudaStream_t s) {
   if (!am && !bm) return ob ? launch_tc_t<BN, false, false, __nv_bfloat16>(ta, tb, g, s)
                             : launch_tc_t<BN, false, false, float>(ta, tb, g, s);
-  if (!am && bm && ob) return launch_tc_t<BN, false, true, __nv_bfloat16>(ta, tb, g, s);
+  if (!am && bm) return ob ? launch_tc_t<BN, false, true, __nv_bfloat16>(ta, tb, g, s)
+                           : launch_tc_t<BN, false, true, float>(ta, tb, g, s);
   if (am && bm && !ob) return launch_tc_t<BN, true, true, float>(ta, tb, g, s);
   return nfail(DSX_ERR_ARGUMENT, "gemm: unsupported operand-major / output combination for the tensor-core path");
 }

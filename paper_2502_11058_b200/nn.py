@@ -35,15 +35,15 @@ def batch(seed: int, worker: int, step: int, size: int, in_dim: int, t: np.ndarr
 
 
 def init_params(seed: int, widths) -> np.ndarray:
-    """Packed per-worker parameters (layer l: W[out][in] then b[out]),
-    torch.nn.Linear's default U(-1/sqrt(in), 1/sqrt(in)); every worker starts
-    from the same point (data-parallel initialisation)."""
+    """Packed per-worker parameters (layer l: W[out][in] then b[out]): He
+    initialisation W ~ N(0, 2/in) (keeps the 8-layer ReLU stack's signal
+    alive), b = 0; every worker starts from the same point (data-parallel
+    initialisation)."""
     rng = np.random.default_rng([seed, 0x1a17])
     parts = []
     for i, o in zip(widths[:-1], widths[1:]):
-        bound = 1.0 / np.sqrt(i)
-        parts.append(rng.uniform(-bound, bound, size=o * i).astype(np.float32))
-        parts.append(rng.uniform(-bound, bound, size=o).astype(np.float32))
+        parts.append((rng.standard_normal(o * i) * np.sqrt(2.0 / i)).astype(np.float32))
+        parts.append(np.zeros(o, dtype=np.float32))
     return np.concatenate(parts)
 
 
