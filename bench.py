@@ -33,6 +33,7 @@ sys.path.insert(0, REPO)
 
 PROFILE = os.path.join(REPO, "tests", "golden", "data", "resnet18_like.profile")
 GPT2_PROFILE = os.path.join(REPO, "tests", "golden", "data", "gpt2_small.profile")
+MLP_PROFILE = os.path.join(REPO, "tests", "golden", "data", "mlp8_w1024.profile")
 METRIC = "iterations/sec at 1/2/4/8 B200 vs CPU ref; exposed sync time per iteration"
 REF_TOOL = os.path.join(REPO, "oracle", "_ref", "parity_tool_ref")
 
@@ -46,6 +47,18 @@ CONFIGS = {
     "gpt2": {"profile": GPT2_PROFILE, "workers": 8, "period": 4, "parity_steps": 2,
              "workload": "gpt2-small-shaped quadratic lab (14 registered layers, 124,439,808 "
                          "params/worker), 8 workers, H=4"},
+    # BASELINE.json configs[0] as the real NN: 8 Linear layers (1024 wide, 10
+    # classes), batch 256/worker, 4 workers, H=4, SGD momentum; bf16 tcgen05
+    # GEMMs (--dtype f32: the fp32 SIMT parity path)
+    "mlp": {"profile": MLP_PROFILE, "workers": 4, "period": 4, "parity_steps": 8, "nn": True,
+            "widths": [1024] * 8 + [10], "batch": 256,
+            "workload": "configs[0] MLP: 8 Linear layers (1024 wide -> 10 classes, 7,357,450 "
+                        "params/worker), batch 256/worker, 4 workers, H=4, SGD momentum"},
+    # the same step at a compute-bound size (tensor-pipe roofline)
+    "mlp_wide": {"profile": MLP_PROFILE, "workers": 4, "period": 4, "parity_steps": 0, "nn": True,
+                 "widths": [4096] * 8 + [16], "batch": 2048,
+                 "workload": "wide MLP: 8 Linear layers (4096 wide -> 16 classes), batch 2048/worker, "
+                             "4 workers, H=4, SGD momentum"},
 }
 
 
@@ -60,7 +73,10 @@ def parse_args(argv=None):
     ap.add_argument("--period", type=int, default=None)
     ap.add_argument("--sigma", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--dtype", default=None, choices=["f64", "f32", "bf16"],
+                    help="lab: f64 (default) / f32; mlp: bf16 (default, tcgen05) / f32 (SIMT)")
+    ap.add_argument("--optimizer", default="momentum", choices=["sgd", "momentum", "adam"])
+    ap.add_argument("--lr", type=float, default=None)
     ap.add_argument("--profile", default=None)
     ap.add_argument("--sync-algo", default="pairwise", choices=["pairwise", "nccl_avg"])
     ap.add_argument("--no-overlap", action="store_true")
@@ -79,6 +95,16 @@ def parse_args(argv=None):
     a.period = a.period or c["period"]
     a.parity_steps = c["parity_steps"] if a.parity_steps is None else a.parity_steps
     a.workload = c["workload"]
+    a.nn = bool(c.get("nn"))
+    a.widths = c.get("widths")
+    a.batch = c.get("batch")
+    a.dtype = a.dtype or ("bf16" if a.nn else "f64")
+    if a.nn and a.dtype == "f64":
+        ap.error("the MLP computes in bf16 (tensor cores) or f32")
+    if not a.nn and a.dtype == "bf16":
+        ap.error("the quadratic lab computes in f64 or f32")
+    if a.lr is None:
+        a.lr = {"sgd": 0.05, "momentum": 0.01, "adam": 1e-3}[a.optimizer]
     return a
 
 
@@ -644,6 +670,335 @@ def our_arm(args, world, rank, local_rank, dist):
     return line
 
 
+
+# -------------------------------------------------------------- the NN arm ---
+
+def mlp_flops_per_worker(widths, batch):
+    """GEMM flops of one local step: forward, wgrad and dgrad (no dgrad into
+    the input layer), 2*M*N*K each."""
+    f = 0.0
+    for l, (i, o) in enumerate(zip(widths[:-1], widths[1:])):
+        f += 2.0 * batch * i * o * (3 if l > 0 else 2)
+    return f
+
+
+def mlp_data_pool(args, kl, rank, npool):
+    import numpy as np
+
+    from paper_2502_11058_b200.nn import batch as make_batch
+    from paper_2502_11058_b200.nn import teacher
+    t = teacher(args.seed, args.widths[0], args.widths[-1])
+    xs = np.empty((npool, kl, args.batch, args.widths[0]), dtype=np.float32)
+    ys = np.empty((npool, kl, args.batch), dtype=np.int32)
+    for p in range(npool):
+        for k in range(kl):
+            xs[p, k], ys[p, k] = make_batch(args.seed, rank * kl + k, p, args.batch, args.widths[0], t)
+    return xs, ys
+
+
+def mlp_cpu_oracle(args, K, steps, masks):
+    """The float64 CPU restatement (oracle/mlp_oracle.py; checker and CPU
+    baseline only) on the same data: (params after `steps`, seconds of the
+    timed steps after one warm-up step)."""
+    from oracle.mlp_oracle import MlpOracle
+    from paper_2502_11058_b200.nn import batch as make_batch
+    from paper_2502_11058_b200.nn import init_params, teacher
+    t = teacher(args.seed, args.widths[0], args.widths[-1])
+    orc = MlpOracle(args.widths, init_params(args.seed, args.widths), K, optimizer=args.optimizer,
+                    eps=1e-6 if args.optimizer == "adam" else 1e-8)
+    t0 = None
+    for r in range(steps):
+        if r == 1:
+            t0 = time.perf_counter()
+        orc.step([make_batch(args.seed, k, r, args.batch, args.widths[0], t) for k in range(K)],
+                 args.lr, r, masks[r % len(masks)])
+    sec = time.perf_counter() - t0 if t0 is not None else None
+    return orc, sec
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info()) or 1
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def mlp_reference_arm(args, world, rank):
+    """The reference has no NN: its CPU implementation of this
+    path is the restatement of plsgd_step with the NN gradient
+    (oracle/mlp_oracle.py, float64 numpy, all BLAS threads)."""
+    if rank != 0:
+        return None
+    from paper_2502_11058_b200.lab import enp, sync_mask
+    L, H = len(args.widths) - 1, args.period
+    masks = [sync_mask("partial", H, r, L, enp(L, H)) for r in range(H)]
+    steps = max(2, min(args.steps, 4)) + 1
+    _, sec = mlp_cpu_oracle(args, args.workers, steps, masks)
+    it_s = (steps - 1) / sec
+    cores = blas_threads()
+    return {"impl": "reference", "metric": METRIC, "value": it_s, "unit": "iterations/s", "n_gpus": world,
+            "steps": steps - 1, "warmup": 1, "ms_per_step": 1e3 / it_s, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": mlp_config(args, world, "enp"),
+            "cpu_baseline": {"value": it_s, "unit": "iterations/s", "cores": cores, "kind": "port",
+                             "sample": f"{steps - 1} timed steps (1 warm-up) of all {args.workers} workers, "
+                                       "oracle/mlp_oracle.py float64 numpy (the reference has no NN)"},
+            "e2e": {"value": it_s, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def mlp_config(args, world, schedule_src):
+    return {"workload": args.workload, "config": args.config, "widths": args.widths, "batch_per_worker": args.batch,
+            "workers": args.workers, "period": args.period, "optimizer": args.optimizer, "lr": args.lr,
+            "schedule": schedule_src, "seed": args.seed,
+            "parallelism": f"dp{world} ({args.workers // world} workers/GPU)",
+            "sync": ("NCCL ncclAvg in place per layer on the side stream" if world > 1 else
+                     "pairwise local average kernel per layer on the side stream"),
+            "l2": "activations+weights per step > L2 only for mlp_wide; mlp's working set is L2-resident "
+                  "(a real training step reuses its weights)"}
+
+
+def mlp_arm(args, world, rank, local_rank, dist):
+    import tempfile
+
+    import numpy as np
+    import torch
+
+    from paper_2502_11058_b200.lab import enp, nccl_unique_id, schedule_from_profile, sync_mask, write_profile
+    from paper_2502_11058_b200.nn import Mlp, gemm, init_params, layer_sizes
+
+    K, H = args.workers, args.period
+    if K % world:
+        raise SystemExit(f"--workers {K} must be divisible by the GPU count {world}")
+    kl = K // world
+    L = len(args.widths) - 1
+    torch.cuda.set_device(local_rank)
+    m = Mlp(args.widths, args.batch, K, workers_local=kl, worker_begin=rank * kl, dtype=args.dtype,
+            optimizer=args.optimizer, eps=1e-6 if args.optimizer == "adam" else 1e-8, device=local_rank)
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        m.comm_init(obj[0], world, rank)
+    init = init_params(args.seed, args.widths)
+    for k in range(kl):
+        m.set_params(k, init)
+    npool = 8
+    xs, ys = mlp_data_pool(args, kl, rank, npool)
+    dx = torch.from_numpy(xs).to(f"cuda:{local_rank}")
+    dy = torch.from_numpy(ys).to(f"cuda:{local_rank}")
+
+    def use_batch(r):
+        p = r % npool
+        m.set_batch_ptr(dx[p].data_ptr(), dy[p].data_ptr(), True)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_ranks(vals):
+        if dist is None:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t]
+
+    # DreamDDP's loop: CUDA-event profile of every layer (FP, BP + update,
+    # cross-worker average) -> profile v1 -> bit-exact DFS + bubble fill
+    use_batch(0)
+    t_fp, t_bp, t_comm = m.profile(reps=5)
+    t_fp, t_bp, t_comm = (np.asarray(v) for v in (max_ranks(list(t_fp)), max_ranks(list(t_bp)),
+                                                      max_ranks(list(t_comm))))
+    path = os.path.join(tempfile.mkdtemp(prefix=f"dreamddp_mlp_r{rank}_"), "measured.profile")
+    write_profile(path, [4 * s for s in layer_sizes(args.widths)], t_fp, t_bp, t_comm, bandwidth=1.0, latency=0.0)
+    sets, fills, _, sched_text = schedule_from_profile(path, H, fill=True)
+    masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
+    sz = np.asarray(layer_sizes(args.widths), dtype=np.float64)
+    synced_frac = float(np.mean([np.dot(mk[1:], sz) / sz.sum() for mk in masks]))
+
+    r = 0
+
+    def run(nsteps, mask_list):
+        nonlocal r
+        for _ in range(nsteps):
+            use_batch(r)
+            m.step(args.lr, r, mask_list[r % H])
+            r += 1
+
+    def timed(nsteps, mask_list):
+        m.sync()
+        barrier()
+        m.record(0)
+        run(nsteps, mask_list)
+        m.record(1)
+        ms = m.elapsed_ms(0, 1)
+        m.sync()
+        return max_ranks([ms])[0]
+
+    run(max(3, args.warmup), masks)
+    m.sync()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    l0 = m.launches()
+    ms_max = timed(args.steps, masks)
+    clocks.stop()
+    launches = m.launches() - l0
+    value = args.steps / (ms_max / 1e3)
+    ms_step = ms_max / args.steps
+
+    # the same steps with nothing averaged: what the sync adds
+    none = np.zeros(L + 1, dtype=np.uint8)
+    ms_nosync = timed(args.steps, [none] * H) / args.steps
+    # per-step instrumentation: compute span, sync span, exposed sync
+    m.set_instrument(True)
+    per = []
+    for _ in range(2 * H):
+        run(1, masks)
+        per.append(m.last_step_times())
+    m.set_instrument(False)
+    comp, span, exp_ = (max_ranks([statistics.mean(p[i] for p in per)])[0] for i in (1, 2, 3))
+
+    # roofline: tensor pipe.  Dominant kernel = a hidden layer's forward GEMM
+    # (M = batch, N = K = width, all local workers batched), timed alone with
+    # CUDA events on its stream; plus the whole step's GEMM flops / step time.
+    peak_tf = None
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        peak_tf, peak_kind = float(pk["bf16_tflops"]), "measured (cuBLAS bf16 burst, MEASURED_PEAKS.json)"
+    except Exception:  # noqa: BLE001
+        peak_tf, peak_kind = 2250.0, "fallback nominal dense bf16"
+    dev = torch.device(f"cuda:{local_rank}")
+    W_ = args.widths[1]
+    A = torch.randn(kl, args.batch, W_, device=dev).bfloat16()
+    B = torch.randn(kl, W_, W_, device=dev).bfloat16()
+    Cc = torch.empty(kl, args.batch, W_, device=dev, dtype=torch.bfloat16)
+    bias = torch.zeros(kl, W_, device=dev)
+    st = torch.cuda.current_stream(dev)
+
+    def one():
+        gemm(A, B, Cc, M=args.batch, N_=W_, K=W_, batch=kl, lda=W_, sA=args.batch * W_, ldb=W_, sB=W_ * W_,
+             ldc=W_, sC=args.batch * W_, epi=1, relu=True, bias=bias, s_bias=W_, stream=st.cuda_stream)
+    kern = None
+    if args.dtype == "bf16":
+        for _ in range(3):
+            one()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(50):
+            one()
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        kms = e0.elapsed_time(e1) / 50
+        kflops = 2.0 * args.batch * W_ * W_ * kl
+        kern = {"kernel": "gemm_tc_kernel (forward, hidden layer, tcgen05 + TMA, fused bias+ReLU)",
+                "shape": [args.batch, W_, W_, kl], "ms": round(kms, 5), "flops": kflops,
+                "achieved": round(kflops / kms / 1e9, 1)}
+    step_flops = mlp_flops_per_worker(args.widths, args.batch) * kl
+    step_tf = step_flops / (ms_step * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "unit": "TFLOP/s", "peak": peak_tf, "peak_kind": peak_kind,
+                "achieved": kern["achieved"] if kern else round(step_tf, 2),
+                "frac": round((kern["achieved"] if kern else step_tf) / peak_tf, 4), "traffic": None,
+                "dominant_kernel": kern,
+                "step": {"gemm_flops_per_step": step_flops, "achieved": round(step_tf, 2),
+                         "frac": round(step_tf / peak_tf, 4), "ms_per_step": round(ms_step, 5),
+                         "t_roof_ms": round(step_flops / (peak_tf * 1e12) * 1e3, 5)}}
+
+    # parity + CPU baseline: the float64 restatement on the same data, same
+    # schedule, from the same init, 2H steps (rank 0; every rank's workers)
+    parity, cpu = None, None
+    if args.parity_steps > 0 and not args.no_cpu_baseline:
+        pm = Mlp(args.widths, args.batch, K, workers_local=kl, worker_begin=rank * kl, dtype=args.dtype,
+                 optimizer=args.optimizer, eps=1e-6 if args.optimizer == "adam" else 1e-8, device=local_rank)
+        if world > 1:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            pm.comm_init(obj[0], world, rank)
+        for k in range(kl):
+            pm.set_params(k, init)
+        for rr in range(args.parity_steps):
+            p = rr % npool
+            pm.set_batch_ptr(dx[p].data_ptr(), dy[p].data_ptr(), True)
+            pm.step(args.lr, rr, masks[rr % H])
+        pm.sync()
+        mine = [pm.get_params(k) for k in range(kl)]
+        pm.close()
+        if dist is not None:
+            allv = [None] * world
+            dist.all_gather_object(allv, mine)
+            mine = [w for part in allv for w in part]
+        if rank == 0:
+            # the pool cycles every npool steps; the oracle regenerates step r's batch
+            # as batch(seed, k, r % npool) to match
+            from oracle.mlp_oracle import MlpOracle
+            from paper_2502_11058_b200.nn import batch as make_batch
+            from paper_2502_11058_b200.nn import teacher
+            t = teacher(args.seed, args.widths[0], args.widths[-1])
+            orc = MlpOracle(args.widths, init, K, optimizer=args.optimizer,
+                            eps=1e-6 if args.optimizer == "adam" else 1e-8)
+            t0 = time.perf_counter()
+            for rr in range(args.parity_steps):
+                orc.step([make_batch(args.seed, k, rr % npool, args.batch, args.widths[0], t) for k in range(K)],
+                         args.lr, rr, masks[rr % H])
+            sec = time.perf_counter() - t0
+            errs = [float(np.linalg.norm(w - o) / np.linalg.norm(o)) for w, o in zip(mine, orc.w)]
+            tol = 3e-2 if args.dtype == "bf16" else 1e-4
+            parity = {"ok": max(errs) <= tol, "max_rel_l2": max(errs), "tolerance_rel_l2": tol,
+                      "steps": args.parity_steps, "workers": K,
+                      "reference": "oracle/mlp_oracle.py float64 restatement (parity unpinned by the reference: "
+                                   "it has no NN)",
+                      "note": ("bf16 tensor-core operands vs float64" if args.dtype == "bf16" else
+                               "fp32 vs float64; the strict 1e-5 check runs in tests/test_gpu_nn.py")}
+            cpu = {"value": args.parity_steps / sec, "unit": "iterations/s", "cores": blas_threads(),
+                   "kind": "port", "sample": f"{args.parity_steps} steps of all {K} workers, oracle/mlp_oracle.py "
+                                             "float64 numpy (the same run is the parity reference)"}
+
+    # e2e: host batches (pinned) in and the loss out every step, through the
+    # public step call
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        hx = torch.from_numpy(xs).pin_memory()
+        hy = torch.from_numpy(ys).pin_memory()
+        m.sync()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            p = r % npool
+            m.set_batch_ptr(hx[p].data_ptr(), hy[p].data_ptr(), False)
+            m.step(args.lr, r, masks[r % H])
+            m.last_loss()
+            r += 1
+        m.sync()
+        el = max_ranks([time.perf_counter() - t0])[0]
+        e2e = {"value": args.e2e_steps / el, "unit": "iterations/s",
+               "h2d_bytes_per_step": int(xs[0].nbytes + ys[0].nbytes), "d2h_bytes_per_step": 4 * kl,
+               "path": "dsx_mlp_set_batch (pinned host x + labels) + dsx_mlp_step + dsx_mlp_last_loss every step"}
+
+    if rank != 0:
+        m.close()
+        return None
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (N(0,1) inputs, linear-teacher labels; device-resident pool of 8 batches/worker)",
+        "config": mlp_config(args, world, "measured"),
+        "exposed_sync_ms_per_iter": round(exp_, 5), "sync_ms_per_iter": round(span, 5),
+        "exposed_sync_frac": round(exp_ / span, 4) if span > 0 else None,
+        "compute_ms_per_iter": round(comp, 5),
+        "ms_per_step_without_sync": round(ms_nosync, 5),
+        "sync_added_ms_per_iter": round(ms_step - ms_nosync, 5),
+        "schedule": {"source": "dsx_mlp_profile -> write_profile -> schedule_dfs + bubble_fill",
+                     "text": sched_text, "synced_param_frac_per_step": round(synced_frac, 4),
+                     "profile_ms": {"fp": [round(x * 1e3, 4) for x in t_fp], "bp": [round(x * 1e3, 4) for x in t_bp],
+                                    "comm": [round(x * 1e3, 4) for x in t_comm]}},
+        "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+    m.close()
+    return line
+
+
 def spawn_ranks(args_argv, n):
     """`python bench.py --gpus N` without torchrun: launch N ranks on this
     node (torch.distributed.run, 127.0.0.1) and relay rank 0's line."""
@@ -674,7 +1029,10 @@ def main():
         import torch.distributed as dist_mod
         dist_mod.init_process_group("gloo")
         dist = dist_mod
-    if args.impl == "reference":
+    if args.nn:
+        line = (mlp_reference_arm(args, world, rank) if args.impl == "reference"
+                else mlp_arm(args, world, rank, local_rank, dist))
+    elif args.impl == "reference":
         line = reference_arm(args, world, rank)
     else:
         line = our_arm(args, world, rank, local_rank, dist)

@@ -78,7 +78,15 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
     NN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::kSmem));
     attr = true;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + kBM - 1) / kBM, g.batch);
+  // persistent: at most one CTA per SM (the smem ring holds the SM)
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long long tiles = (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch;
+  const int grid = (int)std::min<long long>(tiles, nsm);
   kern<<<grid, 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g);
   NN_CUDA(cudaGetLastError());
   return DSX_OK;
@@ -101,11 +109,13 @@ dsx_status launch_tc_bn(bool am, bool bm, bool ob, const CUtensorMap& ta, const 
 int pick_bn(const GemmArgs& g, int nsm) {
   // widest tile that still gives about one wave of CTAs
   const long long mt = (g.M + kBM - 1) / kBM;
+  // widest tile that still fills every SM; small GEMMs take the narrowest
+  // (most CTAs in flight)
   for (int bn : {256, 128}) {
     const long long ctas = mt * ((g.N + bn - 1) / bn) * g.batch;
     if (g.N >= bn && ctas >= nsm) return bn;
   }
-  return g.N > 64 ? 128 : 64;
+  return 64;
 }
 
 }  // namespace

@@ -147,19 +147,40 @@ __device__ __forceinline__ void epi_store(const GemmArgs& g, int b, int m, int n
 }
 
 // ---------------------------------------------------------------------------
-// tcgen05 GEMM: one 128 x BN output tile per CTA; warp 0 = TMA producer,
-// warp 1 = TMEM owner + MMA issuer, warps 2..5 = epilogue (TMEM lanes
-// 32*(warp%4) .. +31, i.e. rows of the tile).
+// tcgen05 GEMM, persistent: one CTA per SM walks the 128 x BN output tiles
+// (tile = blockIdx.x + i * gridDim.x).  Warp 0 = TMA producer (smem ring of
+// kStages stages, mbarrier full/empty), warp 1 = TMEM owner + MMA issuer,
+// warps 2..5 = epilogue.  The accumulator is double-buffered in TMEM
+// (2 x BN columns), so tile i's epilogue overlaps tile i+1's MMAs.  The
+// epilogue drains TMEM with tcgen05.ld (each warp owns TMEM lanes
+// 32*(warp%4) .. +31 = 32 tile rows), transposes 32x32 chunks through a
+// padded shared-memory buffer and stores full rows: coalesced 128-B (fp32)
+// or 64-B (bf16) row segments per warp instruction, with bias / ReLU / ReLU'
+// applied on the coalesced side.
 // ---------------------------------------------------------------------------
 template <int BN>
 struct TcCfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = BN >= 256 ? 4 : 6;
-  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kEpiBytes = 4 * 32 * 33 * 4;  // per epilogue warp: 32 x 33 fp32
+  static constexpr int kSmem = kStages * kStage + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
+
+template <typename TOut>
+__device__ __forceinline__ float epi_value(const GemmArgs& g, int b, int m, int n, float acc) {
+  if (g.epi == kEpiBiasAct) {
+    float v = acc + (g.bias ? g.bias[(long long)b * g.strideBias + n] : 0.f);
+    return g.relu ? fmaxf(v, 0.f) : v;
+  }
+  if (g.epi == kEpiDRelu) {
+    const TOut mk = static_cast<const TOut*>(g.mask)[(long long)b * g.strideMask + (long long)m * g.ldmask + n];
+    return to_f<TOut>(mk) > 0.f ? acc : 0.f;
+  }
+  return acc;
+}
 
 template <int BN, bool A_MN, bool B_MN, typename TOut>
 __global__ void __launch_bounds__(192, 1)
@@ -167,13 +188,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
+  float* epi_smem = reinterpret_cast<float*>(smem + Cfg::kStages * Cfg::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage + Cfg::kEpiBytes);
   uint64_t* empty = full + Cfg::kStages;
-  uint64_t* tmem_full = empty + Cfg::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + Cfg::kStages;  // [2]
+  uint64_t* tempty = tfull + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM, b = blockIdx.z;
   const int nk = (g.K + kBK - 1) / kBK;
+  const int mt = (g.M + kBM - 1) / kBM, ntl = (g.N + BN - 1) / BN;
+  const int tiles = mt * ntl * g.batch;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&ta) : "memory");
@@ -182,7 +206,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       nn_mbar_init(&full[s], 1);
       nn_mbar_init(&empty[s], 1);
     }
-    nn_mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      nn_mbar_init(&tfull[a], 1);
+      nn_mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -198,24 +225,31 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      for (int k = 0; k < nk; ++k) {
-        const int s = k % Cfg::kStages;
-        const unsigned ph = (unsigned)(k / Cfg::kStages) & 1u;
-        nn_mbar_wait(&empty[s], ph ^ 1u);
-        uint8_t* sa = smem + s * Cfg::kStage;
-        uint8_t* sb = sa + Cfg::kABytes;
-        nn_mbar_expect_tx(&full[s], Cfg::kStage);
-        if constexpr (!A_MN) {
-          tma_load_3d(sa, &ta, &full[s], k * kBK, m0, b);
-        } else {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+        const int m0 = mb * kBM, n0 = nb * BN;
+        for (int k = 0; k < nk; ++k, ++it) {
+          const int s = it % Cfg::kStages;
+          const unsigned ph = (unsigned)(it / Cfg::kStages) & 1u;
+          nn_mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* sa = smem + s * Cfg::kStage;
+          uint8_t* sb = sa + Cfg::kABytes;
+          nn_mbar_expect_tx(&full[s], Cfg::kStage);
+          if constexpr (!A_MN) {
+            tma_load_3d(sa, &ta, &full[s], k * kBK, m0, b);
+          } else {
 #pragma unroll
-          for (int i = 0; i < kBM / 64; ++i) tma_load_3d(sa + i * 64 * kBK * 2, &ta, &full[s], m0 + 64 * i, k * kBK, b);
-        }
-        if constexpr (!B_MN) {
-          tma_load_3d(sb, &tb, &full[s], k * kBK, n0, b);
-        } else {
+            for (int i = 0; i < kBM / 64; ++i)
+              tma_load_3d(sa + i * 64 * kBK * 2, &ta, &full[s], m0 + 64 * i, k * kBK, b);
+          }
+          if constexpr (!B_MN) {
+            tma_load_3d(sb, &tb, &full[s], k * kBK, n0, b);
+          } else {
 #pragma unroll
-          for (int i = 0; i < BN / 64; ++i) tma_load_3d(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, k * kBK, b);
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_3d(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, k * kBK, b);
+          }
         }
       }
     }
@@ -224,54 +258,105 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       // instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                              ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
-      for (int k = 0; k < nk; ++k) {
-        const int s = k % Cfg::kStages;
-        const unsigned ph = (unsigned)(k / Cfg::kStages) & 1u;
-        nn_mbar_wait(&full[s], ph);
+      int it = 0, tc = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tc) {
+        const int acc = tc & 1;
+        const unsigned aph = (unsigned)(tc >> 1) & 1u;
+        nn_mbar_wait(&tempty[acc], aph ^ 1u);  // the epilogue drained this buffer
         tc_fence_after();
-        const unsigned sa = su32(smem + s * Cfg::kStage);
-        const unsigned sb = sa + Cfg::kABytes;
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int k = 0; k < nk; ++k, ++it) {
+          const int s = it % Cfg::kStages;
+          const unsigned ph = (unsigned)(it / Cfg::kStages) & 1u;
+          nn_mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const unsigned sa = su32(smem + s * Cfg::kStage);
+          const unsigned sb = sa + Cfg::kABytes;
 #pragma unroll
-        for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
-          // K-major: the 16-element K slice is 32 B into each 128-B swizzled
-          // row (8-row atoms 1024 B apart); MN-major: 16 K rows of 128 B
-          // further, 64-element MN chunks kBK*128 B apart.
-          const uint64_t ad = A_MN ? smem_desc(sa + kk * kUmmaK * 128, kBK * 128, 1024)
-                                   : smem_desc(sa + kk * kUmmaK * 2, 16, 1024);
-          const uint64_t bd = B_MN ? smem_desc(sb + kk * kUmmaK * 128, kBK * 128, 1024)
-                                   : smem_desc(sb + kk * kUmmaK * 2, 16, 1024);
-          tc_mma(tmem, ad, bd, idesc, (k | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
+            // K-major: the 16-element K slice is 32 B into each 128-B swizzled
+            // row (8-row atoms 1024 B apart); MN-major: 16 K rows of 128 B
+            // further, 64-element MN chunks kBK*128 B apart.
+            const uint64_t ad = A_MN ? smem_desc(sa + kk * kUmmaK * 128, kBK * 128, 1024)
+                                     : smem_desc(sa + kk * kUmmaK * 2, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(sb + kk * kUmmaK * 128, kBK * 128, 1024)
+                                     : smem_desc(sb + kk * kUmmaK * 2, 16, 1024);
+            tc_mma(d, ad, bd, idesc, (k | kk) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        tc_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
       }
-      tc_commit(tmem_full);
     }
   } else {  // epilogue warps 2..5
-    nn_mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int m = m0 + 32 * q + lane;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access = tile rows 32q..32q+31
+    float* st = epi_smem + (warp - 2) * 32 * 33;
+    const bool ob = sizeof(TOut) == 2 && g.epi != kEpiF32 && (g.ldc & 1) == 0;
+    int tc = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tc) {
+      const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+      const int m0 = mb * kBM + 32 * q, n0 = nb * BN;
+      const int acc = tc & 1;
+      nn_mbar_wait(&tfull[acc], (unsigned)(tc >> 1) & 1u);
+      tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-          "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-            "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-            "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (m < g.M) {
+      for (int c = 0; c < BN; c += 32) {
+        if (n0 + c >= g.N) break;
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+              "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // row-per-lane -> padded smem (conflict-free: bank = (lane + j) % 32)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = n0 + c + j;
-          if (n < g.N) epi_store<TOut>(g, b, m, n, __uint_as_float(r[j]));
+        for (int j = 0; j < 32; ++j) st[lane * 33 + j] = __uint_as_float(r[j]);
+        __syncwarp();
+        if (ob) {
+          // bf16: two rows per instruction, 16 lanes x 2 columns each
+#pragma unroll 4
+          for (int i2 = 0; i2 < 16; ++i2) {
+            const int row = 2 * i2 + (lane >> 4), cc = 2 * (lane & 15);
+            const int m = m0 + row, n = n0 + c + cc;
+            if (m < g.M && n < g.N) {
+              TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+              const float v0 = epi_value<TOut>(g, b, m, n, st[row * 33 + cc]);
+              if (n + 1 < g.N) {
+                const float v1 = epi_value<TOut>(g, b, m, n + 1, st[row * 33 + cc + 1]);
+                *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
+              } else {
+                *dst = from_f<TOut>(v0);
+              }
+            }
+          }
+        } else {
+          // fp32 (or scalar bf16): one row per instruction, one column per lane
+#pragma unroll 4
+          for (int row = 0; row < 32; ++row) {
+            const int m = m0 + row, n = n0 + c + lane;
+            if (m < g.M && n < g.N) {
+              const float v = st[row * 33 + lane];
+              if (g.epi == kEpiF32) {
+                float* dst = static_cast<float*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+                *dst = g.accumulate ? *dst + v : v;
+              } else {
+                TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+                *dst = from_f<TOut>(epi_value<TOut>(g, b, m, n, v));
+              }
+            }
+          }
         }
+        __syncwarp();
       }
+      // this warp's TMEM reads of buffer `acc` are complete (wait::ld above)
+      tc_fence_before();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[acc])) : "memory");
     }
   }
   tc_fence_before();

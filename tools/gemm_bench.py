@@ -43,7 +43,7 @@ def main():
         C = torch.empty(b, M, Nn, device=dev)
         flops = 2.0 * M * Nn * K * b
         res = {"shape": name, "M": M, "N": Nn, "K": K, "batch": b, "a_mn": am, "b_mn": bm}
-        for bn in (128, 256):
+        for bn in (64, 128, 256):
             ms = timeit(lambda: gemm(A, B, C, M=M, N_=Nn, K=K, batch=b, a_mn=am, b_mn=bm, lda=M if am else K,
                                      sA=M * K, ldb=Nn if bm else K, sB=Nn * K, ldc=Nn, sC=M * Nn, bn=bn), 20)
             res[f"tc_bn{bn}_ms"] = round(ms, 4)
