@@ -24,7 +24,7 @@ def main():
     dist.init_process_group("gloo")
     world, rank = dist.get_world_size(), dist.get_rank()
     dev = int(os.environ.get("LOCAL_RANK", 0))
-    widths, K, H, steps, bsz, seed, lr = [256] * 8 + [10], 4, 4, 8, 64, 3, 0.01
+    widths, K, H, steps, bsz, seed, lr = [256] * 8 + [10], 4, 4, 8, 64, 3, 1e-3
     L = len(widths) - 1
     kl = K // world
     t = teacher(seed, widths[0], widths[-1])
