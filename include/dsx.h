@@ -148,6 +148,14 @@ dsx_status dsx_nccl_unique_id(unsigned char id[128]);
 dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nranks, int rank,
                              int sync_algo);
 
+/* Multi-GPU inside ONE process (the drop-in C++ API's DREAMSCHED_GPUS):
+ * labs[r] is rank r's lab (distinct devices, equal contiguous worker
+ * ranges in rank order).  Creates the communicators with ncclCommInitAll and
+ * maps the peers' exchange buffers directly (peer access, no IPC).  After
+ * this, every multi-rank call must be issued for all labs concurrently, one
+ * host thread per lab (the calls contain cross-GPU barriers). */
+dsx_status dsx_lab_comm_init_local(dsx_lab* const* labs, int n, int sync_algo);
+
 /* Overlapped sync: when enabled (default), the local step runs in two
  * launches — layers above the lowest synced layer first — and the cross-rank
  * averaging of the synced blocks starts on a high-priority side stream as soon

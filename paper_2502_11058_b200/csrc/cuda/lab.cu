@@ -3037,18 +3037,11 @@ dsx_status dsx_nccl_unique_id(unsigned char id[128]) {
   return DSX_OK;
 }
 
-dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nranks, int rank,
-                             int sync_algo) {
-  DSX_TRY(check_lab(lab));
-  if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(DSX_ERR_ARGUMENT, "bad comm args");
-  if (sync_algo != DSX_SYNC_PAIRWISE && sync_algo != DSX_SYNC_NCCL_AVG)
-    return fail(DSX_ERR_ARGUMENT, "bad sync algorithm");
-  if (lab->comm) return fail(DSX_ERR_STATE, "comm already initialised");
-  if (lab->K % nranks != 0 || lab->kl != lab->K / nranks || lab->kbegin != rank * lab->kl)
-    return fail(DSX_ERR_ARGUMENT, "ranks must hold equal contiguous worker ranges");
-  ncclUniqueId u;
-  std::memcpy(u.internal, id, 128);
-  DSX_NCCL(ncclCommInitRank(&lab->comm, nranks, u, rank));
+namespace {
+
+// Communicator-independent part of joining a multi-rank run: rank layout,
+// exactness check, exchange buffers, overlap groups.
+dsx_status comm_prepare(dsx_lab* lab, int nranks, int rank, int sync_algo) {
   lab->nranks = nranks;
   lab->rank = rank;
   lab->sync_algo = sync_algo;
@@ -3080,12 +3073,6 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   }
   if (const char* z = std::getenv("DSX_LAZY")) lab->lazy = z[0] != '0';
 
-  // NVLink peer-memory exchange: map every rank's exchange buffer (its only
-  // worker row, or its subtree-sum staging) through CUDA IPC.  All ranks must
-  // agree on using it, so the per-rank outcome is min-reduced.
-  const char* p2p_env = std::getenv("DSX_P2P");
-  int ok = (p2p_env && p2p_env[0] == '0') || nranks > kMaxProg ? 0 : 1;
-  void* xbuf = lab->kl == 1 ? lab->w : lab->staging;
   DSX_CUDA(cudaMalloc(&lab->flags, 8 * kFlagWords));
   DSX_CUDA(cudaMemset(lab->flags, 0, 8 * kFlagWords));
   DSX_CUDA(cudaMalloc(&lab->sig_counter, 4));
@@ -3093,10 +3080,84 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   DSX_CUDA(cudaMalloc(&lab->xsum, es * 2 * lab->ld));  // [2][ld]: 16-B aligned halves
   DSX_CUDA(cudaMalloc(&lab->tflags, 8ull * 2 * nranks * std::max(1, lab->ntiles)));
   DSX_CUDA(cudaMemset(lab->tflags, 0, 8ull * 2 * nranks * std::max(1, lab->ntiles)));
+  return DSX_OK;
+}
+
+// The exchange buffers of one rank, in the order the peers map them.
+constexpr int kNB = 4;
+void exchange_buffers(dsx_lab* lab, void* out[kNB]) {
+  out[0] = lab->kl == 1 ? lab->w : lab->staging;
+  out[1] = lab->flags;
+  out[2] = lab->xsum;
+  out[3] = lab->tflags;
+}
+
+void set_peer(dsx_lab* lab, int q, void* const got[kNB]) {
+  lab->peers.p[q] = got[0];
+  lab->fpeers.p[q] = static_cast<unsigned long long*>(got[1]);
+  if (q < kMaxFuse) {
+    lab->xpeer[q] = got[2];
+    lab->tpeer[q] = static_cast<unsigned long long*>(got[3]);
+  }
+}
+
+// After the peers are mapped (or not): barrier flavour, engine SM budget,
+// fused-path opt-in.
+dsx_status comm_finish(dsx_lab* lab, int ok, int nranks, int sync_algo) {
+  lab->p2p = ok != 0;
+  if (const char* t = std::getenv("DSX_FLAG_TIMEOUT_S"))
+    lab->flag_timeout_ns = (unsigned long long)std::max(1.0, std::atof(t)) * 1000000000ull;
+  const char* fb = std::getenv("DSX_FLAG_BARRIER");
+  lab->flag_bar = lab->p2p && !(fb && fb[0] == '0');
+  // Several ranks: size the noise engine's segment wave for two thirds of the
+  // SMs.  A resident engine run then never blocks the update and the average
+  // (2 GPUs: 1510 -> 1710 it/s, 4 GPUs: 2260 -> 2590); one GPU keeps every
+  // SM for its engine-bound step.  DSX_ENGINE_SMS overrides.
+  if (lab->engine && nranks > 1 && !std::getenv("DSX_ENGINE_SMS")) {
+    DSX_TRY(invalidate_prefetch(lab));
+    DSX_CUDA(cudaStreamSynchronize(lab->stream));
+    auto* e = new dsx::NoiseEngine();
+    std::string err;
+    if (!e->init(lab->dim, lab->kl, std::max(1, lab->nsm * 2 / 3), lab->tmax, &err)) {
+      delete e;
+      return fail(DSX_ERR_CUDA, err);
+    }
+    delete lab->engine;
+    lab->engine = e;
+  }
+  // opt-in (DSX_FUSED=1): measured slower than the separate averaging
+  // kernel (2 GPUs, sigma=1: 1210 vs 1500 it/s) — a synced tile's CTA idles
+  // on the peer's same tile while holding its SM slot
+  const char* fz = std::getenv("DSX_FUSED");
+  lab->fused = lab->p2p && sync_algo == DSX_SYNC_PAIRWISE && nranks <= kMaxFuse && lab->kl <= 8 &&
+               fz && fz[0] == '1';
+  return DSX_OK;
+}
+
+}  // namespace
+
+dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nranks, int rank,
+                             int sync_algo) {
+  DSX_TRY(check_lab(lab));
+  if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(DSX_ERR_ARGUMENT, "bad comm args");
+  if (sync_algo != DSX_SYNC_PAIRWISE && sync_algo != DSX_SYNC_NCCL_AVG)
+    return fail(DSX_ERR_ARGUMENT, "bad sync algorithm");
+  if (lab->comm) return fail(DSX_ERR_STATE, "comm already initialised");
+  if (lab->K % nranks != 0 || lab->kl != lab->K / nranks || lab->kbegin != rank * lab->kl)
+    return fail(DSX_ERR_ARGUMENT, "ranks must hold equal contiguous worker ranges");
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, 128);
+  DSX_NCCL(ncclCommInitRank(&lab->comm, nranks, u, rank));
+  DSX_TRY(comm_prepare(lab, nranks, rank, sync_algo));
+  // NVLink peer-memory exchange: map every rank's exchange buffer (its only
+  // worker row, or its subtree-sum staging) through CUDA IPC.  All ranks must
+  // agree on using it, so the per-rank outcome is min-reduced.
+  const char* p2p_env = std::getenv("DSX_P2P");
+  int ok = (p2p_env && p2p_env[0] == '0') || nranks > kMaxProg ? 0 : 1;
   // four handles per rank: exchange buffer, flag block, published sums, tile flags
-  constexpr int kNB = 4;
   constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
-  void* const bufs[kNB] = {xbuf, lab->flags, lab->xsum, lab->tflags};
+  void* bufs[kNB];
+  exchange_buffers(lab, bufs);
   cudaIpcMemHandle_t mine[kNB]{};
   for (int b = 0; b < kNB && ok; ++b)
     if (cudaIpcGetMemHandle(&mine[b], bufs[b]) != cudaSuccess) ok = 0;
@@ -3131,12 +3192,7 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
         got[b] = ptr;
       }
       if (!local_ok) break;
-      lab->peers.p[q] = got[0];
-      lab->fpeers.p[q] = static_cast<unsigned long long*>(got[1]);
-      if (q < kMaxFuse) {
-        lab->xpeer[q] = got[2];
-        lab->tpeer[q] = static_cast<unsigned long long*>(got[3]);
-      }
+      set_peer(lab, q, got);
     }
   }
   DSX_CUDA(cudaMemcpy(d_ok, &local_ok, 4, cudaMemcpyHostToDevice));
@@ -3145,33 +3201,63 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   DSX_CUDA(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
   cudaFree(d_handles);
   cudaFree(d_ok);
-  lab->p2p = ok != 0;
-  if (const char* t = std::getenv("DSX_FLAG_TIMEOUT_S"))
-    lab->flag_timeout_ns = (unsigned long long)std::max(1.0, std::atof(t)) * 1000000000ull;
-  const char* fb = std::getenv("DSX_FLAG_BARRIER");
-  lab->flag_bar = lab->p2p && !(fb && fb[0] == '0');
-  // Several ranks: size the noise engine's segment wave for two thirds of the
-  // SMs.  A resident engine run then never blocks the update and the average
-  // (2 GPUs: 1510 -> 1710 it/s, 4 GPUs: 2260 -> 2590); one GPU keeps every
-  // SM for its engine-bound step.  DSX_ENGINE_SMS overrides.
-  if (lab->engine && nranks > 1 && !std::getenv("DSX_ENGINE_SMS")) {
-    DSX_TRY(invalidate_prefetch(lab));
-    DSX_CUDA(cudaStreamSynchronize(lab->stream));
-    auto* e = new dsx::NoiseEngine();
-    std::string err;
-    if (!e->init(lab->dim, lab->kl, std::max(1, lab->nsm * 2 / 3), lab->tmax, &err)) {
-      delete e;
-      return fail(DSX_ERR_CUDA, err);
-    }
-    delete lab->engine;
-    lab->engine = e;
+  return comm_finish(lab, ok, nranks, sync_algo);
+}
+
+dsx_status dsx_lab_comm_init_local(dsx_lab* const* labs, int n, int sync_algo) {
+  if (!labs || n < 1 || n > kMaxProg) return fail(DSX_ERR_ARGUMENT, "bad lab group");
+  if (sync_algo != DSX_SYNC_PAIRWISE && sync_algo != DSX_SYNC_NCCL_AVG)
+    return fail(DSX_ERR_ARGUMENT, "bad sync algorithm");
+  std::vector<int> devs(n);
+  for (int r = 0; r < n; ++r) {
+    DSX_TRY(check_lab(labs[r]));
+    if (labs[r]->comm) return fail(DSX_ERR_STATE, "comm already initialised");
+    if (labs[r]->K % n != 0 || labs[r]->kl != labs[r]->K / n || labs[r]->kbegin != r * labs[r]->kl)
+      return fail(DSX_ERR_ARGUMENT, "labs must hold equal contiguous worker ranges in rank order");
+    devs[r] = labs[r]->device;
+    for (int q = 0; q < r; ++q)
+      if (devs[q] == devs[r]) return fail(DSX_ERR_ARGUMENT, "one lab per device");
   }
-  // opt-in (DSX_FUSED=1): measured slower than the separate averaging
-  // kernel (2 GPUs, sigma=1: 1210 vs 1500 it/s) — a synced tile's CTA idles
-  // on the peer's same tile while holding its SM slot
-  const char* fz = std::getenv("DSX_FUSED");
-  lab->fused = lab->p2p && sync_algo == DSX_SYNC_PAIRWISE && nranks <= kMaxFuse && lab->kl <= 8 &&
-               fz && fz[0] == '1';
+  // one process, one communicator per device (NCCL's single-thread init)
+  std::vector<ncclComm_t> comms(n);
+  DSX_NCCL(ncclCommInitAll(comms.data(), n, devs.data()));
+  for (int r = 0; r < n; ++r) {
+    DSX_CUDA(cudaSetDevice(devs[r]));
+    labs[r]->comm = comms[r];
+    DSX_TRY(comm_prepare(labs[r], n, r, sync_algo));
+  }
+  // peer buffers are plain device pointers here (unified addressing + peer
+  // access), not IPC mappings
+  const char* p2p_env = std::getenv("DSX_P2P");
+  int ok = (p2p_env && p2p_env[0] == '0') ? 0 : 1;
+  for (int r = 0; r < n && ok; ++r) {
+    DSX_CUDA(cudaSetDevice(devs[r]));
+    for (int q = 0; q < n && ok; ++q) {
+      if (q == r) continue;
+      int can = 0;
+      DSX_CUDA(cudaDeviceCanAccessPeer(&can, devs[r], devs[q]));
+      if (!can) {
+        ok = 0;
+        break;
+      }
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devs[q], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ok = 0;
+      cudaGetLastError();
+    }
+  }
+  if (ok) {
+    for (int r = 0; r < n; ++r) {
+      for (int q = 0; q < n; ++q) {
+        void* got[kNB];
+        exchange_buffers(labs[q], got);
+        set_peer(labs[r], q, got);
+      }
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    DSX_CUDA(cudaSetDevice(devs[r]));
+    DSX_TRY(comm_finish(labs[r], ok, n, sync_algo));
+  }
   return DSX_OK;
 }
 

@@ -96,6 +96,7 @@ _SIGS = {
     "dsx_lab_log": ([C.c_void_p, C.c_double, C.c_void_p, C.c_void_p], C.c_int),
     "dsx_nccl_unique_id": ([C.c_void_p], C.c_int),
     "dsx_lab_comm_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
+    "dsx_lab_comm_init_local": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
     "dsx_lab_set_overlap": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_lab_set_pipeline": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_lab_set_noise_horizon": ([C.c_void_p, C.c_longlong], C.c_int),

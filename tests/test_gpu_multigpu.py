@@ -42,3 +42,36 @@ def test_multirank_fused_update_average_bit_exact():
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert '"pass": true' in out.stdout
+
+
+# ---- the drop-in C++ API on several GPUs in one process (DREAMSCHED_GPUS) ----
+# plsgd_step / run_training split the K workers over N labs (one per GPU,
+# one host thread each, dsx_lab_comm_init_local): the reference's goldens
+# must still match (trainer.hpp:94,112; trainer.cpp:237-307).
+
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_cpp_api_plsgd_step_on_several_gpus(gpus, monkeypatch):
+    if _gpus() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    from tests import test_gpu_parity as P
+    monkeypatch.setenv("DREAMSCHED_GPUS", str(gpus))
+    for fname in P.STEP_FILES:
+        P.test_cpp_api_steps_match_reference(fname)
+
+
+@pytest.mark.parametrize("gpus", [2, 4])
+@pytest.mark.parametrize("cfg", ["lab_partial", "lab_full"])
+def test_cpp_api_run_training_on_several_gpus(gpus, cfg, monkeypatch):
+    if _gpus() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    from tests import test_gpu_parity as P
+    monkeypatch.setenv("DREAMSCHED_GPUS", str(gpus))
+    P.test_cpp_api_run_training_matches_reference(cfg)
+
+
+def test_reference_unit_suite_trainer_cases_on_two_gpus(monkeypatch):
+    if _gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    from tests import test_unit_suite as U
+    monkeypatch.setenv("DREAMSCHED_GPUS", "2")
+    U.test_reference_unit_suite_trainer_cases_on_gpu()
