@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <string>
 
+#include "device_once.cuh"
 #include "dsx.h"
 #include "dsx_nn.h"
 #include "nn_gemm.cuh"
@@ -72,19 +73,15 @@ dsx_status make_map(CUtensorMap* map, const void* base, long long inner, long lo
 
 template <int BN, bool AM, bool BM_, typename TOut>
 dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
-  static bool attr = false;
+  static std::atomic<unsigned long long> attr{0};
   auto kern = gemm_tc_kernel<BN, AM, BM_, TOut>;
-  if (!attr) {
-    NN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::kSmem));
-    attr = true;
-  }
+  dsx::once_per_device(attr, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::kSmem);
+  });
   // persistent: at most one CTA per SM (the smem ring holds the SM)
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch;
   const int grid = (int)std::min<long long>(tiles, nsm);
   kern<<<grid, 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g);

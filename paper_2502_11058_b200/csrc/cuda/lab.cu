@@ -32,6 +32,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "device_once.cuh"
 #include "dsx.h"
 #include "mt_engine.cuh"
 #include "noise_engine.cuh"
@@ -107,17 +108,8 @@ struct QuadParams {
   const double* opt;
 };
 
-// Fused cross-rank average (multi-rank, pairwise, <= 8 ranks): a synced
-// tile's CTA publishes its subtree sums, waits for every rank's CTA of the
-// same tile, then averages in the reference's pairwise rank order — the
-// update and the collective in one kernel, tile by tile, over NVLink.
+// ranks whose scratch buffer (the NVLink probe's) is mapped into every peer
 constexpr int kMaxFuse = 8;
-struct FusedArgs {
-  int R = 0, rank = 0;                       // R == 0: off
-  unsigned long long epoch = 0;              // this step's flag value
-  const void* xs[kMaxFuse] = {};             // every rank's subtree sums (this step's parity)
-  unsigned long long* tf[kMaxFuse] = {};     // every rank's tile flags (this parity) [R][ntiles]
-};
 
 template <typename T>
 struct UpdateArgs {
@@ -138,42 +130,7 @@ struct UpdateArgs {
   T* partial_out;     // multi-rank: subtree sums of synced tiles (else null)
   const T* mean_in;   // multi-rank: cross-rank means of the layers in `stale`
   MaskBits stale;     // layers whose rows are stale: every row equals mean_in
-  FusedArgs fz;       // fused average (multi-rank); mean_out = where the means go
-  T* mean_out;
 };
-
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Publishes this CTA's tile to every rank, then waits (thread 0) until every
-// rank published it; traps after ~30 s instead of hanging.
-__device__ __forceinline__ void fused_tile_barrier(const FusedArgs& f, int ntiles, int tile) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int q = 0; q < f.R; ++q) st_release_sys_u64(f.tf[q] + (long long)f.rank * ntiles + tile, f.epoch);
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (int q = 0; q < f.R; ++q) {
-      const unsigned long long* mine = f.tf[f.rank] + (long long)q * ntiles + tile;
-      while (ld_acquire_sys_u64(mine) < f.epoch) {
-        __nanosleep(32);
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 600000000000ull) __trap();
-      }
-    }
-  }
-  __syncthreads();
-}
-
-
 
 // lambda_i and w*_i.  The analytic form is make_quadratic's
 // mu + (beta - mu) * i / (dim - 1) (trainer.cpp:117-120), evaluated with the
@@ -308,11 +265,8 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
   const Tile t = a.tiles[tile_id];
   const int kl = KL > 0 ? KL : a.kl;
   const bool avg = a.average && mask_has(a.mask, t.block);
-  // fused cross-rank average of a synced tile (multi-rank): phase 1 writes
-  // this rank's subtree sums into its published buffer (like `part`)
-  const bool fused_tile = KL > 0 && a.fz.R > 0 && mask_has(a.mask, t.block);
-  const bool part = (KL > 1 && a.partial_out != nullptr && mask_has(a.mask, t.block)) || fused_tile;
-  T* const part_dst = fused_tile ? static_cast<T*>(const_cast<void*>(a.fz.xs[a.fz.rank])) : a.partial_out;
+  const bool part = KL > 1 && a.partial_out != nullptr && mask_has(a.mask, t.block);
+  T* const part_dst = a.partial_out;
   // lazy broadcast: after a cross-rank average the mean lives once in the
   // exchange buffer; all kl rows are logically equal to it, so it is read
   // once instead of kl times (and the rows are never written back while the
@@ -481,38 +435,6 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     } else {
       if (simple) pairs(No{}, Yes{}); else pairs(No{}, No{});
     }
-    if (fused_tile) {
-      // phase 2: every rank's sums of this tile are published; phase 3: the
-      // cross-rank mean, pairwise over ranks / K, straight from peer memory
-      fused_tile_barrier(a.fz, a.ntiles, tile_id);
-      const int R = a.fz.R;
-      auto mean_at = [&](long long i) -> T {
-        T v[kMaxFuse];
-#pragma unroll
-        for (int q = 0; q < kMaxFuse; ++q) v[q] = q < R ? static_cast<const T*>(a.fz.xs[q])[i] : T(0);
-        return rank_psum<T>(v, R) / (T)a.k_total;
-      };
-      for (int pr = threadIdx.x; pr < npairs; pr += kThreads) {
-        const long long i = first + 2 * (long long)pr;
-        T vx[kMaxFuse], vy[kMaxFuse];
-#pragma unroll
-        for (int q = 0; q < kMaxFuse; ++q) {
-          if (q < R) {
-            const V2 v = *reinterpret_cast<const V2*>(static_cast<const T*>(a.fz.xs[q]) + i);
-            vx[q] = v.x;
-            vy[q] = v.y;
-          } else {
-            vx[q] = vy[q] = T(0);
-          }
-        }
-        V2 m;
-        m.x = rank_psum<T>(vx, R) / (T)a.k_total;
-        m.y = rank_psum<T>(vy, R) / (T)a.k_total;
-        *reinterpret_cast<V2*>(a.mean_out + i) = m;
-      }
-      if (threadIdx.x == 0 && first != t.start) a.mean_out[t.start] = mean_at(t.start);
-      if (threadIdx.x == 1 && first + 2 * (long long)npairs < end) a.mean_out[end - 1] = mean_at(end - 1);
-    }
   } else {
     // generic worker count: row pass, then the pairwise program for
     // averaged coordinates.
@@ -550,205 +472,6 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
       if (threadIdx.x == 0) a.norm_part[(long long)k * a.ntiles + tile_id] = s;
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// Async-staged update kernel (fp64, 2..8 local rows; opt-in, DSX_UPD_ASYNC=1).
-// The loads of chunk c+2 are in flight (cp.async, 16-B per row and pair,
-// straight into shared memory) while chunk c is computed, so memory-level
-// parallelism no longer costs registers and the polar transform of the
-// engine's raw attempts hides under HBM time.  512 threads: each pair of
-// coordinates is owned by two threads of one warp (lanes l, l^16), each
-// updating half of the rows; the pairwise worker sum splits at KL/2 exactly
-// like pairwise_coord_sum, so the halves combine with one shuffle.
-// ---------------------------------------------------------------------------
-constexpr int kAThreads = 512;
-constexpr int kAPairs = 256;   // pairs per chunk
-constexpr int kAStages = 3;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int KL, int NM>
-__device__ __forceinline__ void async_update_tile(const UpdateArgs<double>& a, int tile_id, double2* stage) {
-  static_assert(KL >= 2 && KL % 2 == 0, "rows split over two threads");
-  constexpr int KH = KL / 2;
-  constexpr bool NOISE = NM != 0;
-  const Tile t = a.tiles[tile_id];
-  const bool avg = a.average && mask_has(a.mask, t.block);
-  const bool part = a.partial_out != nullptr && mask_has(a.mask, t.block);
-  const bool stale = a.mean_in != nullptr && mask_has(a.stale, t.block);
-  const int tid = threadIdx.x;
-  const int pl = (tid >> 5) * 16 + (tid & 15);  // pair lane 0..255
-  const int h = (tid >> 4) & 1;                 // row half
-  const int k0 = h * KH;
-  __shared__ const double* s_base[KL][2];
-  __shared__ unsigned long long s_bound[KL];
-  __shared__ int s_simple;
-  if constexpr (NM == 2) {
-    if (tid == 0) s_simple = 1;
-    __syncthreads();
-    if (tid < KL) {
-      const int k = tid;
-      const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
-      const unsigned long long m0 = a.nv.base + ((unsigned long long)t.start >> 1);
-      const unsigned long long m1 = a.nv.base + ((unsigned long long)(t.start + t.len - 1) >> 1);
-      const int s0 = seg_search(pf, a.nv.P, m0);
-      const int s1 = s0 < a.nv.P ? s0 + 1 : s0;
-      const double* slot0 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s0) * a.nv.cap;
-      const double* slot1 = a.nv.slots + ((long long)k * (a.nv.P + 1) + s1) * a.nv.cap;
-      s_base[k][0] = slot0 - 2 * (long long)pf[s0] + 2 * (long long)a.nv.base;
-      s_base[k][1] = slot1 - 2 * (long long)pf[s1] + 2 * (long long)a.nv.base;
-      s_bound[k] = s0 < a.nv.P ? pf[s0 + 1] - a.nv.base : ~0ull;
-      if (s1 < a.nv.P && m1 >= pf[s1 + 1]) s_simple = 0;
-    }
-    __syncthreads();
-  }
-  // 16-byte address of coordinate pair (i, i+1)'s noise for worker k
-  auto noise_pair = [&](int k, long long i) -> const double* {
-    const unsigned long long m = (unsigned long long)i >> 1;
-    if (s_simple) return s_base[k][m >= s_bound[k] ? 1 : 0] + i;
-    const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
-    const int sg = seg_search(pf, a.nv.P, a.nv.base + m);
-    return a.nv.slots + ((long long)k * (a.nv.P + 1) + sg) * a.nv.cap + 2 * (long long)(a.nv.base + m - pf[sg]);
-  };
-  auto noise_of = [&](int k, long long i) -> double {  // one coordinate (scalar head / tail)
-    const double* at = noise_pair(k, i & ~1LL);
-    if (!a.nv.raw) return at[i & 1];
-    const double2 n = mt_polar_normals(at[0], at[1], a.nv.stddev);
-    return (i & 1) ? n.y : n.x;
-  };
-  double nsq[KL];  // scalar head / tail (threads 0, 1): every row
-  double nh[KH];   // main loop: this thread's rows k0 + q
-#pragma unroll
-  for (int k = 0; k < KL; ++k) nsq[k] = 0.0;
-#pragma unroll
-  for (int q = 0; q < KH; ++q) nh[q] = 0.0;
-  const long long first = t.start + (t.start & 1);
-  const long long end = t.start + t.len;
-  const int npairs = (int)((end - first) >> 1);
-  // odd head / tail: one scalar coordinate each, all rows by one thread
-  if ((tid == 0 && first != t.start) || (tid == 1 && first + 2 * (long long)npairs < end)) {
-    const long long i = tid == 0 ? t.start : end - 1;
-    double lam, opt;
-    quad_coeffs(a.q, i, &lam, &opt);
-    double wn[KL];
-#pragma unroll
-    for (int k = 0; k < KL; ++k) {
-      const double x = NOISE ? noise_of(k, i) : 0.0;
-      const double g = grad_step(stale ? a.mean_in[i] : a.w[k * a.ld + i], lam, opt, x, a.eta, NOISE, &wn[k]);
-      nsq[k] += g * g;
-    }
-    if (part) {
-      a.partial_out[i] = psum<0, KL, double>(wn);
-    } else {
-      const double m = avg ? psum<0, KL, double>(wn) / (double)a.k_total : 0.0;
-#pragma unroll
-      for (int k = 0; k < KL; ++k) a.w[k * a.ld + i] = avg ? m : wn[k];
-    }
-  }
-  const int nchunks = (npairs + kAPairs - 1) / kAPairs;
-  auto slot = [&](int st, int which, int k) -> double2* {
-    return stage + (((long long)st * 2 + which) * KL + k) * kAPairs + pl;
-  };
-  auto issue = [&](int c) {
-    if (c < nchunks) {
-      const int pr = c * kAPairs + pl;
-      if (pr < npairs) {
-        const long long i = first + 2 * (long long)pr;
-        const int st = c % kAStages;
-#pragma unroll
-        for (int q = 0; q < KH; ++q) {
-          const int k = k0 + q;
-          if (stale) {
-            if (q == 0) cp_async16(slot(st, 0, k), a.mean_in + i);
-          } else {
-            cp_async16(slot(st, 0, k), a.w + k * a.ld + i);
-          }
-          if constexpr (NM == 2) cp_async16(slot(st, 1, k), noise_pair(k, i));
-        }
-      }
-    }
-    cp_async_commit();  // (possibly empty) group per chunk keeps the counting uniform
-  };
-  issue(0);
-  issue(1);
-  for (int c = 0; c < nchunks; ++c) {
-    issue(c + 2);
-    cp_async_wait<2>();  // this thread's copies of chunk c have landed
-    const int pr = c * kAPairs + pl;
-    const bool live = pr < npairs;
-    const int st = c % kAStages;
-    const long long i = first + 2 * (long long)(live ? pr : 0);
-    double w0[KH], w1[KH];
-    if (live) {
-      double lam0, opt0, lam1, opt1;
-      quad_coeffs(a.q, i, &lam0, &opt0);
-      quad_coeffs(a.q, i + 1, &lam1, &opt1);
-#pragma unroll
-      for (int q = 0; q < KH; ++q) {
-        const int k = k0 + q;
-        const double2 wv = *slot(st, 0, stale ? k0 : k);
-        double2 xv = make_double2(0.0, 0.0);
-        if constexpr (NM == 2) {
-          xv = *slot(st, 1, k);
-          if (a.nv.raw) xv = mt_polar_normals(xv.x, xv.y, a.nv.stddev);
-        }
-        const double g0 = grad_step(wv.x, lam0, opt0, xv.x, a.eta, NOISE, &w0[q]);
-        const double g1 = grad_step(wv.y, lam1, opt1, xv.y, a.eta, NOISE, &w1[q]);
-        nh[q] += g0 * g0 + g1 * g1;
-      }
-    }
-    // pairwise sum over all KL rows: this half's subtree, then the other
-    // half's from lane ^ 16 (psum<0,KL> = psum<0,KH> + psum<KH,KL>)
-    double s0 = 0.0, s1 = 0.0;
-    if (avg || part) {
-      const double m0 = psum<0, KH, double>(w0), m1 = psum<0, KH, double>(w1);
-      const double o0 = __shfl_xor_sync(0xffffffffu, m0, 16), o1 = __shfl_xor_sync(0xffffffffu, m1, 16);
-      s0 = h == 0 ? m0 + o0 : o0 + m0;
-      s1 = h == 0 ? m1 + o1 : o1 + m1;
-    }
-    if (live) {
-      if (avg) {
-        const double2 m = make_double2(s0 / (double)a.k_total, s1 / (double)a.k_total);
-#pragma unroll
-        for (int q = 0; q < KH; ++q) *reinterpret_cast<double2*>(a.w + (k0 + q) * a.ld + i) = m;
-      } else if (part) {
-        if (h == 0) *reinterpret_cast<double2*>(a.partial_out + i) = make_double2(s0, s1);
-      } else {
-#pragma unroll
-        for (int q = 0; q < KH; ++q)
-          *reinterpret_cast<double2*>(a.w + (k0 + q) * a.ld + i) = make_double2(w0[q], w1[q]);
-      }
-    }
-  }
-  cp_async_wait<0>();
-  {
-    __shared__ double red[kAThreads / 32];
-#pragma unroll
-    for (int k = 0; k < KL; ++k) {
-      double v = nsq[k];
-#pragma unroll
-      for (int q = 0; q < KH; ++q)
-        if (k0 + q == k) v += nh[q];
-      const double sk = block_sum(v, red);
-      if (tid == 0) a.norm_part[(long long)k * a.ntiles + tile_id] = sk;
-    }
-  }
-  __syncthreads();  // the stage and the tile's shared lookups are reused by the next tile
-}
-
-// Persistent: a CTA walks tiles tile_base + blockIdx.x, + gridDim.x, ...
-template <int KL, int NM>
-__global__ void __launch_bounds__(kAThreads, 1)
-lab_update_async_kernel(UpdateArgs<double> a, int count) {
-  extern __shared__ __align__(16) double2 stage[];  // [kAStages][2 (w, x)][KL][kAPairs]
-  for (int i = blockIdx.x; i < count; i += gridDim.x) async_update_tile<KL, NM>(a, a.tile_base + i, stage);
 }
 
 // ---------------------------------------------------------------------------
@@ -1563,15 +1286,10 @@ struct dsx_lab {
   unsigned int* sig_counter = nullptr;   // finished-block counter of the averaging kernel
   unsigned long long epoch = 0, sig_count = 0;
   unsigned long long flag_timeout_ns = 600ull * 1000000000ull;  // DSX_FLAG_TIMEOUT_S
-  // fused update + average (DSX_FUSED=0: separate averaging kernel): the
-  // published subtree sums [2][dim] and tile flags [2][R][ntiles] of every
-  // rank, mapped into every peer
-  bool fused = false;
+  // scratch [2][ld] of every rank, mapped into every peer: the NVLink
+  // roofline probe's buffer (dsx_lab_link_probe)
   void* xsum = nullptr;
-  unsigned long long* tflags = nullptr;
   void* xpeer[kMaxFuse] = {};
-  unsigned long long* tpeer[kMaxFuse] = {};
-  unsigned long long fepoch = 0;
   int chunks = 4;              // overlap groups per step (at most)
   int wave = 296;              // update CTAs resident at once (blocks/SM x SMs)
   bool lazy = true;            // lazy broadcast of cross-rank means (DSX_LAZY=0: off)
@@ -1631,7 +1349,7 @@ dsx_status check_row(dsx_lab* lab, int local) {
 
 template <typename T, int KL>
 void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int nm, bool average,
-                     const MaskBits& mask, double eta, T* partial_out, const FusedArgs* fz, T* mean_out) {
+                     const MaskBits& mask, double eta, T* partial_out) {
   UpdateArgs<T> a{};
   a.w = static_cast<T*>(lab->w);
   a.ld = lab->ld;
@@ -1650,10 +1368,6 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.mean_in = lab->stale_any ? static_cast<const T*>(lab->staging) : nullptr;
   a.stale = lab->stale_bits;
   if (lab->engine) a.nv = lab->engine->view(lab->cur_set, lab->cur_t);
-  if (fz) {
-    a.fz = *fz;
-    a.mean_out = mean_out;
-  }
   if constexpr (std::is_same_v<T, double> && (KL == 2 || KL == 4 || KL == 8)) {
     // bulk-copy kernel: the default with engine noise (0.91 vs 0.84 of HBM at
     // sigma=1); the register-staged kernel stays faster without noise (0.83
@@ -1665,44 +1379,16 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
     // (with 2-4 local rows a 512-coordinate chunk carries too little per
     // mbarrier round trip: 4 GPUs 0.29 vs 0.17 ms, so 8 rows only by default)
     const int bulk_ctas = bulk_env >= 0 ? bulk_env : (nm == 2 && KL == 8 ? 1 : 0);
-    if (bulk_ctas > 0 && (nm == 0 || nm == 2) && !fz) {
+    if (bulk_ctas > 0 && (nm == 0 || nm == 2)) {
       constexpr size_t smem = sizeof(double) * kBStages * 2 * KL * kBChunk;
-      static const bool attr = [] {
+      static std::atomic<unsigned long long> attr{0};
+      dsx::once_per_device(attr, [] {
         cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-      }();
-      (void)attr;
+      });
       const int grid = std::min(count, bulk_ctas == 1 ? lab->nsm : bulk_ctas);
       if (nm == 2) lab_update_bulk_kernel<KL, 2><<<grid, kBThreads, smem, s>>>(a, count);
       else lab_update_bulk_kernel<KL, 0><<<grid, kBThreads, smem, s>>>(a, count);
-      ++lab->launches;
-      return;
-    }
-  }
-  if constexpr (std::is_same_v<T, double> && KL >= 2 && KL % 2 == 0) {
-    // async-staged kernel, opt-in (DSX_UPD_ASYNC=1): measured no faster
-    // than the register-staged one (0.42 ms at sigma=1, 8 workers)
-    static const bool use_async = [] {
-      const char* e = std::getenv("DSX_UPD_ASYNC");
-      return e && e[0] == '1';
-    }();
-    if (use_async && nm != 1 && !fz) {
-      constexpr size_t smem = sizeof(double2) * kAStages * 2 * KL * kAPairs;
-      static const bool attr = [] {
-        cudaFuncSetAttribute(lab_update_async_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(lab_update_async_kernel<KL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-      }();
-      (void)attr;
-      // DSX_UPD_ASYNC_CTAS: persistent CTA count (default: one per tile)
-      static const int ctas = [] {
-        const char* e = std::getenv("DSX_UPD_ASYNC_CTAS");
-        return e ? std::atoi(e) : 0;
-      }();
-      const int grid = ctas > 0 ? std::min(ctas, count) : count;
-      if (nm == 2) lab_update_async_kernel<KL, 2><<<grid, kAThreads, smem, s>>>(a, count);
-      else lab_update_async_kernel<KL, 0><<<grid, kAThreads, smem, s>>>(a, count);
       ++lab->launches;
       return;
     }
@@ -1721,18 +1407,17 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
 
 template <typename T>
 void launch_update(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int noise, bool average,
-                   const MaskBits& mask, double eta, T* partial_out = nullptr, const FusedArgs* fz = nullptr,
-                   T* mean_out = nullptr) {
+                   const MaskBits& mask, double eta, T* partial_out = nullptr) {
   switch (lab->kl) {
-    case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    case 2: return launch_update_t<T, 2>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    case 3: return launch_update_t<T, 3>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    case 4: return launch_update_t<T, 4>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    case 5: return launch_update_t<T, 5>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    case 6: return launch_update_t<T, 6>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    case 7: return launch_update_t<T, 7>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    case 8: return launch_update_t<T, 8>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
-    default: return launch_update_t<T, 0>(lab, s, tile_base, count, noise, average, mask, eta, partial_out, fz, mean_out);
+    case 1: return launch_update_t<T, 1>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 2: return launch_update_t<T, 2>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 3: return launch_update_t<T, 3>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 4: return launch_update_t<T, 4>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 5: return launch_update_t<T, 5>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 6: return launch_update_t<T, 6>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 7: return launch_update_t<T, 7>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    case 8: return launch_update_t<T, 8>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
+    default: return launch_update_t<T, 0>(lab, s, tile_base, count, noise, average, mask, eta, partial_out);
   }
 }
 
@@ -2098,47 +1783,6 @@ dsx_status step_multi_p2p(dsx_lab* lab, double eta, const unsigned char* mask, c
   return DSX_OK;
 }
 
-// Multi-rank step with the average fused into the update kernel: one launch
-// over every tile; a synced tile's CTA publishes its subtree sums, waits for
-// the same tile on every rank (peer-memory flags) and writes the pairwise
-// cross-rank mean — into the exchange buffer, read lazily by the next step,
-// or (one worker per GPU) straight into the row.  No separate averaging
-// kernel, barrier or launch; the transfer overlaps other tiles' updates.
-template <typename T>
-dsx_status step_multi_fused(dsx_lab* lab, double eta, const unsigned char* mask, const MaskBits& bits,
-                            int noise) {
-  const auto ranges = masked_ranges(lab, mask);
-  lab->has_ranges = !ranges.empty();
-  // buffers alternate per SYNCED step: a rank writing the sums of synced
-  // step e+2 has waited on some tile of step e+1 of every peer, which each
-  // peer publishes only after its step-e kernel (all of its reads of the
-  // e-buffer) completed
-  const int parity = lab->has_ranges ? (int)(++lab->fepoch & 1) : 0;
-  FusedArgs fz;
-  fz.R = lab->nranks;
-  fz.rank = lab->rank;
-  fz.epoch = lab->fepoch;
-  const size_t es = elem_size(lab);
-  for (int q = 0; q < lab->nranks; ++q) {
-    fz.xs[q] = static_cast<const char*>(lab->xpeer[q]) + es * (size_t)parity * lab->ld;
-    fz.tf[q] = lab->tpeer[q] + (size_t)parity * lab->nranks * lab->ntiles;
-  }
-  T* mean_out = lab->kl > 1 ? static_cast<T*>(lab->staging) : static_cast<T*>(lab->w);
-  if (lab->instrument) DSX_CUDA(cudaEventRecord(lab->iev[1], lab->stream));
-  launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, false, bits, eta, nullptr,
-                   lab->has_ranges ? &fz : nullptr, mean_out);
-  if (lab->instrument) {
-    DSX_CUDA(cudaEventRecord(lab->iev[3], lab->stream));
-    DSX_CUDA(cudaEventRecord(lab->iev[2], lab->stream));
-  }
-  DSX_CUDA(cudaEventRecord(lab->ev_synced, lab->stream));
-  if (lab->kl > 1) {  // the synced layers' rows are stale now (mean in the exchange buffer)
-    lab->stale_bits = bits;
-    lab->stale_any = lab->has_ranges;
-  }
-  return DSX_OK;
-}
-
 template <typename T>
 dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int noise) {
   MaskBits bits{};
@@ -2151,8 +1795,7 @@ dsx_status step_impl(dsx_lab* lab, double eta, const unsigned char* mask, int no
   } else if (single) {
     launch_update<T>(lab, lab->stream, 0, lab->ntiles, noise, lab->K > 1, bits, eta);
   } else if (lab->p2p && lab->sync_algo == DSX_SYNC_PAIRWISE) {
-    if (lab->fused && lab->link_bw <= 0.0) DSX_TRY(step_multi_fused<T>(lab, eta, mask, bits, noise));
-    else DSX_TRY(step_multi_p2p<T>(lab, eta, mask, bits, noise));
+    DSX_TRY(step_multi_p2p<T>(lab, eta, mask, bits, noise));
   } else {
     const auto ranges = masked_ranges(lab, mask);
     lab->has_ranges = !ranges.empty();
@@ -2575,7 +2218,6 @@ dsx_status dsx_lab_destroy(dsx_lab* lab) {
   if (lab->bar) cudaFree(lab->bar);
   if (lab->flags) cudaFree(lab->flags);
   if (lab->xsum) cudaFree(lab->xsum);
-  if (lab->tflags) cudaFree(lab->tflags);
   if (lab->sig_counter) cudaFree(lab->sig_counter);
   for (auto& ev : lab->ev_chunk)
     if (ev) cudaEventDestroy(ev);
@@ -3078,32 +2720,26 @@ dsx_status comm_prepare(dsx_lab* lab, int nranks, int rank, int sync_algo) {
   DSX_CUDA(cudaMalloc(&lab->sig_counter, 4));
   DSX_CUDA(cudaMemset(lab->sig_counter, 0, 4));
   DSX_CUDA(cudaMalloc(&lab->xsum, es * 2 * lab->ld));  // [2][ld]: 16-B aligned halves
-  DSX_CUDA(cudaMalloc(&lab->tflags, 8ull * 2 * nranks * std::max(1, lab->ntiles)));
-  DSX_CUDA(cudaMemset(lab->tflags, 0, 8ull * 2 * nranks * std::max(1, lab->ntiles)));
   return DSX_OK;
 }
 
-// The exchange buffers of one rank, in the order the peers map them.
-constexpr int kNB = 4;
+// The exchange buffers of one rank, in the order the peers map them:
+// averaging exchange row, flag block, probe scratch.
+constexpr int kNB = 3;
 void exchange_buffers(dsx_lab* lab, void* out[kNB]) {
   out[0] = lab->kl == 1 ? lab->w : lab->staging;
   out[1] = lab->flags;
   out[2] = lab->xsum;
-  out[3] = lab->tflags;
 }
 
 void set_peer(dsx_lab* lab, int q, void* const got[kNB]) {
   lab->peers.p[q] = got[0];
   lab->fpeers.p[q] = static_cast<unsigned long long*>(got[1]);
-  if (q < kMaxFuse) {
-    lab->xpeer[q] = got[2];
-    lab->tpeer[q] = static_cast<unsigned long long*>(got[3]);
-  }
+  if (q < kMaxFuse) lab->xpeer[q] = got[2];
 }
 
-// After the peers are mapped (or not): barrier flavour, engine SM budget,
-// fused-path opt-in.
-dsx_status comm_finish(dsx_lab* lab, int ok, int nranks, int sync_algo) {
+// After the peers are mapped (or not): barrier flavour, engine SM budget.
+dsx_status comm_finish(dsx_lab* lab, int ok, int nranks) {
   lab->p2p = ok != 0;
   if (const char* t = std::getenv("DSX_FLAG_TIMEOUT_S"))
     lab->flag_timeout_ns = (unsigned long long)std::max(1.0, std::atof(t)) * 1000000000ull;
@@ -3125,12 +2761,6 @@ dsx_status comm_finish(dsx_lab* lab, int ok, int nranks, int sync_algo) {
     delete lab->engine;
     lab->engine = e;
   }
-  // opt-in (DSX_FUSED=1): measured slower than the separate averaging
-  // kernel (2 GPUs, sigma=1: 1210 vs 1500 it/s) — a synced tile's CTA idles
-  // on the peer's same tile while holding its SM slot
-  const char* fz = std::getenv("DSX_FUSED");
-  lab->fused = lab->p2p && sync_algo == DSX_SYNC_PAIRWISE && nranks <= kMaxFuse && lab->kl <= 8 &&
-               fz && fz[0] == '1';
   return DSX_OK;
 }
 
@@ -3154,7 +2784,7 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   // agree on using it, so the per-rank outcome is min-reduced.
   const char* p2p_env = std::getenv("DSX_P2P");
   int ok = (p2p_env && p2p_env[0] == '0') || nranks > kMaxProg ? 0 : 1;
-  // four handles per rank: exchange buffer, flag block, published sums, tile flags
+  // three handles per rank: exchange buffer, flag block, probe scratch
   constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
   void* bufs[kNB];
   exchange_buffers(lab, bufs);
@@ -3201,7 +2831,7 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   DSX_CUDA(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
   cudaFree(d_handles);
   cudaFree(d_ok);
-  return comm_finish(lab, ok, nranks, sync_algo);
+  return comm_finish(lab, ok, nranks);
 }
 
 dsx_status dsx_lab_comm_init_local(dsx_lab* const* labs, int n, int sync_algo) {
@@ -3256,7 +2886,7 @@ dsx_status dsx_lab_comm_init_local(dsx_lab* const* labs, int n, int sync_algo) {
   }
   for (int r = 0; r < n; ++r) {
     DSX_CUDA(cudaSetDevice(devs[r]));
-    DSX_TRY(comm_finish(labs[r], ok, n, sync_algo));
+    DSX_TRY(comm_finish(labs[r], ok, n));
   }
   return DSX_OK;
 }
@@ -3268,7 +2898,7 @@ dsx_status dsx_lab_link_probe(dsx_lab* lab, int reps, double* gbs) {
   if (lab->nranks < 2) return DSX_OK;
   if (!lab->p2p) return fail(DSX_ERR_STATE, "link probe needs the NVLink peer-memory exchange");
   const int W = lab->nranks;
-  // scratch: every rank's fused-path sums buffer [2][ld] (mapped into all
+  // scratch: every rank's probe buffer [2][ld] (mapped into all
   // peers at comm init, idle between steps) as 16-B units
   const long long units = (long long)(elem_size(lab) * 2 * lab->ld / 16);
   const long long per = units / W;

@@ -12,6 +12,7 @@
 #include <random>
 #include <sstream>
 
+#include "device_once.cuh"
 #include "mt_engine.cuh"
 #include "noise_engine.cuh"
 
@@ -354,67 +355,6 @@ mt_prefix_kernel(const uint64_t* mt, uint64_t* ybuf, uint64_t* win, int P, int* 
   if (tid == 0) pnorm[w] = p;
 }
 
-// Segment start windows W_{sS} = sum_i c_s[i] W_{1+i}: one warp per jump,
-// lane l owns window words [10l, 10l+10) with a sliding register window.
-// One warp per jump; lane l (< 29) owns window words [11 l, 11 l + 11): an odd
-// stride, so the 64-bit shared loads of a warp hit distinct banks.  The
-// sliding window lives in a 16-register ring: the word entering the window
-// is loaded 5 iterations before it is first used, hiding the shared-memory
-// latency with only 4 warps per SM (the 162 KB prefix allows one CTA).
-// A jump is split over kWarpsPerJump warps (a quarter of the 312 window
-// words each); lane l (< 26) of a quarter owns 3 consecutive words — an odd
-// stride, so a warp's 64-bit shared loads are bank-conflict free.  The
-// sliding window lives in an 8-register ring: the word entering the window
-// is loaded 5 iterations before it is first used.  kJumpsPerCta jumps of the
-// same worker share the CTA's 162 KB copy of the stream prefix.
-constexpr int kWarpsPerJump = 4;
-constexpr int kJumpsPerCta = 2;
-constexpr int kJumpWarps = kWarpsPerJump * kJumpsPerCta;
-constexpr int kJA = 3;               // accumulator words per lane
-constexpr int kJQ = 8;               // ring size = kJA + prefetch distance
-constexpr int kJWords = kMtN / kWarpsPerJump;    // 78 words per warp
-constexpr int kJLanes = kJWords / kJA;           // 26
-
-__global__ void __launch_bounds__(kJumpWarps * 32)
-mt_jump_kernel(const uint64_t* ybuf, const uint32_t* cbits /*[P-1][kJumpBits/32 + 1]*/, uint64_t* win, int P) {
-  extern __shared__ uint64_t ys[];
-  const int w = blockIdx.y;
-  const uint64_t* y = ybuf + (long long)w * kPrefixWords;
-  for (int i = threadIdx.x; i < kPrefixWords; i += blockDim.x) ys[i] = y[i];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = 1 + blockIdx.x * kJumpsPerCta + warp / kWarpsPerJump;
-  if (s >= P) return;
-  constexpr int kCW = kJumpBits / 32 + 1;
-  const uint32_t* c = cbits + (long long)(s - 1) * kCW;
-  const int j0 = (warp % kWarpsPerJump) * kJWords + (lane < kJLanes ? kJA * lane : 0);
-  const uint64_t* yb = ys + 1 + j0;
-  uint64_t acc[kJA], ring[kJQ];
-#pragma unroll
-  for (int q = 0; q < kJA; ++q) acc[q] = 0;
-#pragma unroll
-  for (int q = 0; q < kJQ; ++q) ring[q] = yb[q];
-  // invariant at iteration i (u = i mod kJQ): ring[(u + q) % kJQ] = Y[1 + j0 + i + q]
-  // for q < kJQ; the window is q < kJA.
-  for (int i0 = 0; i0 < kJumpBits; i0 += kJQ) {
-    const uint32_t cw = c[i0 >> 5] >> (i0 & 31);  // kJQ bits of c, i0 % kJQ == 0
-#pragma unroll
-    for (int u = 0; u < kJQ; ++u) {
-      if ((cw >> u) & 1u) {
-#pragma unroll
-        for (int q = 0; q < kJA; ++q) acc[q] ^= ring[(u + q) % kJQ];
-      }
-      ring[u] = yb[i0 + u + kJQ];  // enters as q = kJQ-1 at iteration i+1
-    }
-  }
-  uint64_t* out = win + ((long long)w * P + s) * kMtN;
-  if (lane < kJLanes) {
-#pragma unroll
-    for (int q = 0; q < kJA; ++q)
-      if (j0 + q < kMtN) out[j0 + q] = acc[q];
-  }
-}
-
 // Jump kernel v2 (the default).  The polynomial c_s is split into kJ2Parts
 // bit ranges, one warp each; a warp covers all 312 window words (lane l owns
 // words 11l .. 11l+10, an odd stride so the 64-bit shared loads are
@@ -503,154 +443,7 @@ __device__ __forceinline__ void store_ck(uint64_t* ck, const uint64_t* x, int ha
   }
 }
 
-// One CTA per (segment, worker): S outputs from relative position sS + p.
-//
-// kRound generations per round.  ring[0..R-1] receive this round's arrays
-// (ring[0] twisted from ring[R], which holds the previous round's last
-// array; chained twists after that, 2 barriers each), all R*312 outputs are
-// tempered and paired at once (2 pair slots per thread), one warp scans the
-// accepted counts, and accepted pairs are transformed and stored as one
-// 16-byte (y*mult, x*mult) pair.  Ring slots are compile-time constants, and
-// interior rounds (every generation complete) take a branch-free path.
-__global__ void __launch_bounds__(kThreads, 2)
-mt_segment_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
-                  int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
-                  double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
-                  uint64_t* tail) {
-  constexpr int R = kRound;
-  constexpr int kSlots = (R * kMtN / 2 + kThreads - 1) / kThreads;  // pair slots per thread
-  constexpr int kCounts = kSlots * (kThreads / 32);
-  static_assert(kCounts <= 32, "scan fits one warp");
-  __shared__ uint64_t ring[R + 1][kMtN];
-  __shared__ double v[R * kMtN + 2];
-  __shared__ int wcnt[kCounts];
-  __shared__ int woff[kCounts + 1];
-  __shared__ short acc_pair[R * kMtN / 2 + 1];
-  __shared__ double acc_r2[R * kMtN / 2 + 1];
-  const int s = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int p;
-  if (s == 0) {
-    // segment 0 starts from the worker's live state (no prefix needed)
-    const uint64_t* st = win_state + (long long)w * (kMtN + 1);
-    if (tid < kMtN) ring[R][tid] = st[tid];
-    p = (int)st[kMtN];
-    __syncthreads();
-    if (p >= kMtN) {
-      twist_into(ring[R], ring[0]);
-      p = 0;
-    } else if (tid < kMtN) {
-      ring[0][tid] = ring[R][tid];
-    }
-    if (tid == 0) pnorm_out[w] = p;
-  } else {
-    if (tid < kMtN) ring[0][tid] = win[((long long)w * P + s) * kMtN + tid];
-    p = pnorm_in[w];
-  }
-  __syncthreads();
-  const int ngen = gens + (p > 0 ? 1 : 0);
-  double* out = slots + ((long long)w * (P + 1) + s) * cap;
-  uint64_t* ckw = ck + ((long long)w * P + s) * (long long)nck * kCkWords;
-  int have_half = 0;
-  double half = 0.0;
-  unsigned long long local = 0;
-  int last = 0;  // ring slot of the last processed generation
-  for (int q = 0; q < ngen; q += R) {
-    const int rg = min(R, ngen - q);
-    if (q) twist_into(ring[R], ring[0]);
-    if (q % ck_every == 0) store_ck(ckw + (long long)(q / ck_every) * kCkWords, ring[0], have_half, half, local);
-#pragma unroll
-    for (int g = 1; g < R; ++g)
-      if (g < rg) twist_into(ring[g - 1], ring[g]);
-    int nvals;
-    if (q > 0 && q + R <= gens) {  // interior: R complete generations
-#pragma unroll
-      for (int g = 0; g < R; ++g)
-        if (tid < kMtN) v[have_half + g * kMtN + tid] = mt_polar_coord(mt_temper(ring[g][tid]));
-      nvals = have_half + R * kMtN;
-    } else {
-      nvals = have_half;
-#pragma unroll
-      for (int g = 0; g < R; ++g) {
-        if (g < rg) {
-          const int gen = q + g;
-          const int lo = gen == 0 ? p : 0;
-          const int hi = (gen == gens) ? p : kMtN;
-          if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(ring[g][tid]));
-          nvals += hi - lo;
-        }
-      }
-    }
-    if (tid == 0 && have_half) v[0] = half;
-    __syncthreads();
-    last = rg - 1;
-    // carry the round's last array to ring[R] for the next round's first twist
-    if (q + R < ngen && tid < kMtN) ring[R][tid] = ring[R - 1][tid];
-    const int npairs = nvals >> 1;
-    bool acc[kSlots];
-    double r2[kSlots];
-    int before[kSlots];
-#pragma unroll
-    for (int u = 0; u < kSlots; ++u) {
-      const int a = tid + u * kThreads;
-      acc[u] = false;
-      r2[u] = 0.0;
-      if (a < npairs) acc[u] = mt_polar_accept(v[2 * a], v[2 * a + 1], &r2[u]);
-      const unsigned bal = __ballot_sync(0xffffffffu, acc[u]);
-      if (lane == 0) wcnt[u * (kThreads / 32) + warp] = __popc(bal);
-      before[u] = __popc(bal & ((1u << lane) - 1u));
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan, slot-major = pair order
-      const int c = lane < kCounts ? wcnt[lane] : 0;
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (lane < kCounts) woff[lane] = incl - c;
-      if (lane == 31) woff[kCounts] = incl;
-    }
-    __syncthreads();
-    const int total = woff[kCounts];
-    // compact the accepted attempts (rank order) so the fp64 polar transform
-    // runs on fully populated warps
-#pragma unroll
-    for (int u = 0; u < kSlots; ++u) {
-      if (acc[u]) {
-        const int j = before[u] + woff[u * (kThreads / 32) + warp];
-        acc_pair[j] = (short)(tid + u * kThreads);
-        acc_r2[j] = r2[u];
-      }
-    }
-    __syncthreads();
-    for (int j = tid; j < total; j += kThreads) {
-      const int a = acc_pair[j];
-      const double mult = mt_polar_mult(acc_r2[j]);
-      double2 o;
-      o.x = mt_scale(v[2 * a + 1], mult, stddev);
-      o.y = mt_scale(v[2 * a], mult, stddev);
-      *reinterpret_cast<double2*>(out + 2 * (local + (unsigned long long)j)) = o;
-    }
-    local += (unsigned long long)total;
-    if (nvals & 1) {
-      half = v[nvals - 1];
-      have_half = 1;
-    } else {
-      have_half = 0;
-    }
-    __syncthreads();
-  }
-  if (tid == 0) cnt[(long long)w * P + s] = local;
-  // end state for an overflow continuation: the last processed array
-  const uint64_t* lastx = ring[0];
-#pragma unroll
-  for (int g = 1; g < R; ++g)
-    if (g == last) lastx = ring[g];
-  store_ck(tail + ((long long)w * P + s) * kCkWords, lastx, have_half, half, local);
-}
-
-// Warp-specialized segment kernel (the default).  Warp 0 is the twister: it
+// Warp-specialized segment kernel helpers.  Warp 0 is the twister: it
 // produces the generation arrays into a double-buffered ring (R arrays per
 // half) with warp-level sync only, one round ahead; warps 1..10 consume a
 // round at a time (temper, polar accept, scan, compaction, fp64 transform)
@@ -674,190 +467,9 @@ __device__ __forceinline__ void warp_twist(const uint64_t* src, uint64_t* dst, i
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kWsThreads, 2)
-mt_segment_ws_kernel(const uint64_t* win_state, const uint64_t* win, const int* pnorm_in,
-                     int* pnorm_out, int P, int gens, int ck_every, int nck, double stddev,
-                     double* slots, long long cap, unsigned long long* cnt, uint64_t* ck,
-                     uint64_t* tail) {
-  constexpr int R = kWsR;
-  constexpr int kSlots = (R * kMtN / 2 + kThreads - 1) / kThreads;  // pair slots per consumer
-  constexpr int kCounts = kSlots * (kThreads / 32);
-  static_assert(kCounts <= 32, "scan fits one warp");
-  __shared__ uint64_t ring[2][R][kMtN];
-  __shared__ uint64_t boot[kMtN];
-  __shared__ double v[R * kMtN + 2];
-  __shared__ int wcnt[kCounts];
-  __shared__ int woff[kCounts + 1];
-  __shared__ short acc_pair[R * kMtN / 2 + 1];
-  __shared__ double acc_r2[R * kMtN / 2 + 1];
-  __shared__ int s_p;
-  const int s = blockIdx.x, w = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (warp == 0) {
-    // ---------------- producer: generations into the ring ----------------
-    int p;
-    if (s == 0) {
-      const uint64_t* st = win_state + (long long)w * (kMtN + 1);
-      for (int k = lane; k < kMtN; k += 32) boot[k] = st[k];
-      p = (int)st[kMtN];
-      __syncwarp();
-      if (p >= kMtN) {
-        warp_twist(boot, ring[0][0], lane);
-        p = 0;
-      } else {
-        for (int k = lane; k < kMtN; k += 32) ring[0][0][k] = boot[k];
-      }
-      if (lane == 0) pnorm_out[w] = p;
-    } else {
-      for (int k = lane; k < kMtN; k += 32) ring[0][0][k] = win[((long long)w * P + s) * kMtN + k];
-      p = pnorm_in[w];
-    }
-    if (lane == 0) s_p = p;
-    __syncwarp();
-    const int ngen = gens + (p > 0 ? 1 : 0);
-    const int rounds = (ngen + R - 1) / R;
-    for (int k = 0; k < rounds; ++k) {
-      const int h = k & 1;
-      if (k >= 2) named_sync(kBarEmpty + h, kWsThreads);  // consumers done with round k-2
-      const int rg = min(R, ngen - k * R);
-      for (int g = 0; g < rg; ++g) {
-        if (k == 0 && g == 0) continue;  // gen 0 already in place
-        const uint64_t* src = g ? ring[h][g - 1] : ring[1 - h][R - 1];
-        warp_twist(src, ring[h][g], lane);
-      }
-      __threadfence_block();
-      named_arrive(kBarFull + h, kWsThreads);
-    }
-    return;
-  }
-
-  // ---------------- consumers (320 threads) ----------------
-  const int tid = threadIdx.x - 32, cw = tid >> 5;
-  named_sync(kBarFull + 0, kWsThreads);  // round 0 ready (also publishes s_p)
-  const int p = s_p;
-  const int ngen = gens + (p > 0 ? 1 : 0);
-  const int rounds = (ngen + R - 1) / R;
-  double* out = slots + ((long long)w * (P + 1) + s) * cap;
-  uint64_t* ckw = ck + ((long long)w * P + s) * (long long)nck * kCkWords;
-  int have_half = 0;
-  double half = 0.0;
-  unsigned long long local = 0;
-  for (int k = 0; k < rounds; ++k) {
-    const int h = k & 1;
-    const int q = k * R;
-    if (k) named_sync(kBarFull + h, kWsThreads);
-    const int rg = min(R, ngen - q);
-    if (q % ck_every == 0) {
-      uint64_t* c = ckw + (long long)(q / ck_every) * kCkWords;
-      if (tid < kMtN) c[tid] = ring[h][0][tid];
-      if (tid == 0) {
-        c[kMtN] = (uint64_t)have_half;
-        c[kMtN + 1] = (uint64_t)__double_as_longlong(half);
-        c[kMtN + 2] = local;
-      }
-    }
-    int nvals;
-    if (q > 0 && q + R <= gens) {  // interior: R complete generations
-#pragma unroll
-      for (int g = 0; g < R; ++g)
-        if (tid < kMtN) v[have_half + g * kMtN + tid] = mt_polar_coord(mt_temper(ring[h][g][tid]));
-      nvals = have_half + R * kMtN;
-    } else {
-      nvals = have_half;
-#pragma unroll
-      for (int g = 0; g < R; ++g) {
-        if (g < rg) {
-          const int gen = q + g;
-          const int lo = gen == 0 ? p : 0;
-          const int hi = (gen == gens) ? p : kMtN;
-          if (tid >= lo && tid < hi) v[nvals + tid - lo] = mt_polar_coord(mt_temper(ring[h][g][tid]));
-          nvals += hi - lo;
-        }
-      }
-    }
-    if (k == rounds - 1) {  // end state for an overflow continuation
-      uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
-      if (tid < kMtN) c[tid] = ring[h][rg - 1][tid];
-    }
-    if (tid == 0 && have_half) v[0] = half;
-    named_arrive(kBarEmpty + h, kWsThreads);  // done reading ring half h
-    named_sync(kBarCons, kThreads);
-    const int npairs = nvals >> 1;
-    bool acc[kSlots];
-    double r2[kSlots];
-    int before[kSlots];
-#pragma unroll
-    for (int u = 0; u < kSlots; ++u) {
-      const int a = tid + u * kThreads;
-      acc[u] = false;
-      r2[u] = 0.0;
-      if (a < npairs) acc[u] = mt_polar_accept(v[2 * a], v[2 * a + 1], &r2[u]);
-      const unsigned bal = __ballot_sync(0xffffffffu, acc[u]);
-      if (lane == 0) wcnt[u * (kThreads / 32) + cw] = __popc(bal);
-      before[u] = __popc(bal & ((1u << lane) - 1u));
-    }
-    named_sync(kBarCons, kThreads);
-    if (cw == 0) {
-      const int c = lane < kCounts ? wcnt[lane] : 0;
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (lane < kCounts) woff[lane] = incl - c;
-      if (lane == 31) woff[kCounts] = incl;
-    }
-    named_sync(kBarCons, kThreads);
-    const int total = woff[kCounts];
-#pragma unroll
-    for (int u = 0; u < kSlots; ++u) {
-      if (acc[u]) {
-        const int j = before[u] + woff[u * (kThreads / 32) + cw];
-        acc_pair[j] = (short)(tid + u * kThreads);
-        acc_r2[j] = r2[u];
-      }
-    }
-    named_sync(kBarCons, kThreads);
-    // two independent polar transforms per iteration (ILP over the fp64 chains)
-    for (int j = tid; j < total; j += 2 * kThreads) {
-      const int j2 = j + kThreads;
-      const bool two = j2 < total;
-      const int a = acc_pair[j];
-      const int a2 = two ? acc_pair[j2] : a;
-      const double m1 = mt_polar_mult(acc_r2[j]);
-      const double m2 = mt_polar_mult(two ? acc_r2[j2] : acc_r2[j]);
-      double2 o;
-      o.x = mt_scale(v[2 * a + 1], m1, stddev);
-      o.y = mt_scale(v[2 * a], m1, stddev);
-      *reinterpret_cast<double2*>(out + 2 * (local + (unsigned long long)j)) = o;
-      if (two) {
-        o.x = mt_scale(v[2 * a2 + 1], m2, stddev);
-        o.y = mt_scale(v[2 * a2], m2, stddev);
-        *reinterpret_cast<double2*>(out + 2 * (local + (unsigned long long)j2)) = o;
-      }
-    }
-    local += (unsigned long long)total;
-    if (nvals & 1) {
-      half = v[nvals - 1];
-      have_half = 1;
-    } else {
-      have_half = 0;
-    }
-    named_sync(kBarCons, kThreads);  // v / acc lists reusable
-  }
-  if (tid == 0) {
-    cnt[(long long)w * P + s] = local;
-    uint64_t* c = tail + ((long long)w * P + s) * kCkWords;
-    c[kMtN] = (uint64_t)have_half;
-    c[kMtN + 1] = (uint64_t)__double_as_longlong(half);
-    c[kMtN + 2] = local;
-  }
-}
-
-// Segment kernel v5 (the default).  Same contract as mt_segment_ws_kernel,
-// rebalanced after ncu showed consumers stalled on the single twister warp
+// Segment kernel v5 (the default; earlier single-twister and block-synchronous
+// versions were measured slower and removed), rebalanced after ncu showed
+// consumers stalled on the single twister warp
 // (~12 % of samples) and on the uneven per-round transform split (~8 %):
 //  * kProdWarps twister warps split every generation's two phases (a 64-
 //    thread named barrier between phases) — half the producer latency;
@@ -1337,12 +949,8 @@ bool NoiseEngine::init(unsigned long long dim, int kl, int nsm, int max_steps, s
       !alloc((void**)&status_, 2 * 4ull * kl * max_steps) || !alloc((void**)&joff_, 2 * 4ull * kl))
     return false;
   cudaMemset(status_, 0, 2 * 4ull * kl * max_steps);
-  if (cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           8 * kPrefixWords) != cudaSuccess ||
-      cudaFuncSetAttribute(mt_jump2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           8 * (kPrefixWords + kJ2PerCta * 4 * kMtN)) != cudaSuccess ||
-      cudaFuncSetAttribute(mt_jump2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           8 * (kPrefixWords + kJ2PerCta * 8 * kMtN)) != cudaSuccess) {
+  if (cudaFuncSetAttribute(mt_jump2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8 * (kPrefixWords + kJ2PerCta * 4 * kMtN)) != cudaSuccess) {
     *err = "noise engine: cannot opt in to 205 KB shared memory";
     return false;
   }
@@ -1369,77 +977,41 @@ bool NoiseEngine::run(const uint64_t* mt_src, uint64_t* mt_dst, int set, int ste
   if (P > 1) {
     mt_prefix_kernel<<<kl_, kThreads, 0, stream>>>(mt_src, ybuf_, win_, P, pnorm);
     ++launches_;
-    static const bool jump_v1 = [] {
-      const char* e = std::getenv("DSX_JUMP");
-      return e && e[0] == '1';
-    }();
-    if (jump_v1) {
-      dim3 grid((P - 1 + kJumpsPerCta - 1) / kJumpsPerCta, kl_);
-      mt_jump_kernel<<<grid, kJumpWarps * 32, 8 * kPrefixWords, stream>>>(ybuf_, c.jbits, win_, P);
-    } else {
-      // DSX_JUMP_PARTS: 4 (default) or 8 warps per jump
-      static const int parts = [] {
-        const char* e = std::getenv("DSX_JUMP_PARTS");
-        return e && std::atoi(e) == 8 ? 8 : 4;
-      }();
-      dim3 grid((P - 1 + kJ2PerCta - 1) / kJ2PerCta, kl_);
-      if (parts == 8)
-        mt_jump2_kernel<8><<<grid, kJ2PerCta * 8 * 32, 8 * (kPrefixWords + kJ2PerCta * 8 * kMtN), stream>>>(
-            ybuf_, c.jbits, win_, P);
-      else
-        mt_jump2_kernel<4><<<grid, kJ2PerCta * 4 * 32, 8 * (kPrefixWords + kJ2PerCta * 4 * kMtN), stream>>>(
-            ybuf_, c.jbits, win_, P);
-    }
+    // 4 warps per jump (8 was measured slower)
+    dim3 grid((P - 1 + kJ2PerCta - 1) / kJ2PerCta, kl_);
+    mt_jump2_kernel<4><<<grid, kJ2PerCta * 4 * 32, 8 * (kPrefixWords + kJ2PerCta * 4 * kMtN), stream>>>(
+        ybuf_, c.jbits, win_, P);
     ++launches_;
   }
-  // DSX_SEG_WS: 2 (default) v5 kernel, 1 single-twister warp-specialized, 0 v3;
-  // DSX_NOISE_RAW=1: v5 stores the raw accepted attempts and the update
-  // kernel applies the polar transform (+3-7 % it/s, but the update kernel
-  // then runs at ~0.64 of HBM instead of ~0.83; off by default)
-  static const int ws = [] {
-    const char* e = std::getenv("DSX_SEG_WS");
-    return e ? std::atoi(e) : 2;
-  }();
+  // DSX_NOISE_RAW=1: the segment kernel stores the raw accepted attempts
+  // and the update kernel applies the polar transform (+3-7 % it/s, but the
+  // update kernel then runs at ~0.64 of HBM instead of ~0.83; off by default)
   static const bool raw_ok = [] {
     const char* e = std::getenv("DSX_NOISE_RAW");
     return e && e[0] == '1';
   }();
-  const int raw = ws == 2 && raw_ok ? 1 : 0;
+  const int raw = raw_ok ? 1 : 0;
   raw_[set] = raw;
   stddev_[set] = stddev;
-  // DSX_SEG_PAD: extra (unused) shared memory per segment CTA, bytes — caps
-  // the engine at fewer CTAs per SM so update CTAs can share its SMs
-  static const int pad = [] {
-    const char* e = std::getenv("DSX_SEG_PAD");
-    const int v = e ? std::atoi(e) : 0;
-    const int p4 = (int)Ws2Smem<4>::kBytes + std::max(0, v), p6 = (int)Ws2Smem<6>::kBytes + std::max(0, v);
-    cudaFuncSetAttribute(mt_segment_ws2_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p4);
-    cudaFuncSetAttribute(mt_segment_ws2_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p4);
-    cudaFuncSetAttribute(mt_segment_ws2_kernel<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, p6);
-    cudaFuncSetAttribute(mt_segment_ws2_kernel<false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, p6);
-    return v > 0 ? v : 0;
-  }();
-  if (ws == 2) {
-    // generations per round (DSX_SEG_R: 4 or 6; checkpoints every 16 / 12)
-    auto go = [&](auto kern, size_t smem) {
-      kern<<<dim3(P, kl_), kWs2Threads, smem + pad, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_,
-                                                               c.nck, stddev, slots, c.cap, cnt, ck_, tail_);
-    };
-    if (seg_r_ == 6) {
-      if (raw) go(mt_segment_ws2_kernel<true, 6>, Ws2Smem<6>::kBytes);
-      else go(mt_segment_ws2_kernel<false, 6>, Ws2Smem<6>::kBytes);
-    } else {
-      if (raw) go(mt_segment_ws2_kernel<true, 4>, Ws2Smem<4>::kBytes);
-      else go(mt_segment_ws2_kernel<false, 4>, Ws2Smem<4>::kBytes);
-    }
-  } else if (ws == 1) {
-    mt_segment_ws_kernel<<<dim3(P, kl_), kWsThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
-                                                                   ck_every_, c.nck, stddev, slots, c.cap,
-                                                                   cnt, ck_, tail_);
+  // dynamic shared memory opt-in, per device (one process may drive several)
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ws2Smem<4>::kBytes);
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ws2Smem<4>::kBytes);
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ws2Smem<6>::kBytes);
+    cudaFuncSetAttribute(mt_segment_ws2_kernel<false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ws2Smem<6>::kBytes);
+  });
+  // generations per round (DSX_SEG_R: 4 or 6; checkpoints every 16 / 12)
+  auto go = [&](auto kern, size_t smem) {
+    kern<<<dim3(P, kl_), kWs2Threads, smem, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens, ck_every_, c.nck,
+                                                       stddev, slots, c.cap, cnt, ck_, tail_);
+  };
+  if (seg_r_ == 6) {
+    if (raw) go(mt_segment_ws2_kernel<true, 6>, Ws2Smem<6>::kBytes);
+    else go(mt_segment_ws2_kernel<false, 6>, Ws2Smem<6>::kBytes);
   } else {
-    mt_segment_kernel<<<dim3(P, kl_), kThreads, 0, stream>>>(mt_src, win_, pnorm, pnorm2, P, c.gens,
-                                                              ck_every_, c.nck, stddev, slots, c.cap,
-                                                              cnt, ck_, tail_);
+    if (raw) go(mt_segment_ws2_kernel<true, 4>, Ws2Smem<4>::kBytes);
+    else go(mt_segment_ws2_kernel<false, 4>, Ws2Smem<4>::kBytes);
   }
   mt_finish_kernel<<<dim3(kl_, steps), kThreads, 0, stream>>>(mt_dst, pnorm2, P, c.gens, ck_every_, c.nck,
                                                               (dim_ + 1) / 2, stddev, slots, c.cap, cnt, pfx,

@@ -31,19 +31,6 @@ def test_multirank_sync_bit_exact(world):
     assert '"pass": true' in out.stdout
 
 
-@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-def test_multirank_fused_update_average_bit_exact():
-    """The opt-in fused update + cross-rank average (DSX_FUSED=1: one kernel,
-    per-tile peer-memory handshake) is bit-identical too."""
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29517",
-           os.path.join(REPO, "tests", "multigpu_parity.py")]
-    env = dict(os.environ, DSX_FUSED="1")
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
-    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
-    assert '"pass": true' in out.stdout
-
-
 # ---- the drop-in C++ API on several GPUs in one process (DREAMSCHED_GPUS) ----
 # plsgd_step / run_training split the K workers over N labs (one per GPU,
 # one host thread each, dsx_lab_comm_init_local): the reference's goldens
