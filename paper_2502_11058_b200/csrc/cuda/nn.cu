@@ -147,34 +147,67 @@ struct OptArgs {
   float lr, mu, b1, b2, eps, wd, bc1, bc2;  // bc = 1 - beta^t
 };
 
-// Fused optimizer over one layer range [lo, lo+n) of every local worker:
-// reads w, g (+ states), writes w, states and the bf16 GEMM copy.
-__global__ void optimizer_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
-                                 float* __restrict__ v, __nv_bfloat16* __restrict__ wb, long long ld, long long lo,
-                                 long long n, OptArgs o) {
-  const int b = blockIdx.y;
-  const long long base = (long long)b * ld + lo;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long j = base + i;
-    float wj = w[j];
-    float gj = g[j];
-    if (o.kind == DSX_OPT_SGD) {
-      if (o.wd != 0.f) gj += o.wd * wj;
-      wj -= o.lr * gj;
-    } else if (o.kind == DSX_OPT_MOMENTUM) {
-      if (o.wd != 0.f) gj += o.wd * wj;
-      const float mj = o.mu * m[j] + gj;
-      m[j] = mj;
-      wj -= o.lr * mj;
-    } else {  // Adam(W)
-      const float mj = o.b1 * m[j] + (1.f - o.b1) * gj;
-      const float vj = o.b2 * v[j] + (1.f - o.b2) * gj * gj;
-      m[j] = mj;
-      v[j] = vj;
-      const float mh = mj / o.bc1, vh = vj / o.bc2;
-      wj -= o.lr * (mh / (sqrtf(vh) + o.eps) + o.wd * wj);
+__device__ __forceinline__ float opt_one(const OptArgs& o, float w, float g, float* m, float* v) {
+  if (o.kind == DSX_OPT_SGD) {
+    if (o.wd != 0.f) g += o.wd * w;
+    return w - o.lr * g;
+  }
+  if (o.kind == DSX_OPT_MOMENTUM) {
+    if (o.wd != 0.f) g += o.wd * w;
+    *m = o.mu * *m + g;
+    return w - o.lr * *m;
+  }
+  // Adam(W)
+  *m = o.b1 * *m + (1.f - o.b1) * g;
+  *v = o.b2 * *v + (1.f - o.b2) * g * g;
+  const float mh = *m / o.bc1, vh = *v / o.bc2;
+  return w - o.lr * (mh / (sqrtf(vh) + o.eps) + o.wd * w);
+}
+
+// Fused optimizer over one layer range [lo, lo+n) of every local worker
+// (blockIdx.y): reads w, g (+ states), writes w, states and the bf16 GEMM
+// copy.  HBM-bound: 16-B vector loads/stores (lo is 64-element aligned),
+// two vectors per thread in flight, scalar tail.
+__global__ void __launch_bounds__(256) optimizer_kernel(float* __restrict__ w, const float* __restrict__ g,
+                                                        float* __restrict__ m, float* __restrict__ v,
+                                                        __nv_bfloat16* __restrict__ wb, long long ld, long long lo,
+                                                        long long n, OptArgs o) {
+  const long long base = (long long)blockIdx.y * ld + lo;
+  const long long nv4 = n / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const bool mom = o.kind != DSX_OPT_SGD, adam = o.kind == DSX_OPT_ADAM;
+  auto vec = [&](long long q) {
+    const long long j = base + 4 * q;
+    float4 wv = *reinterpret_cast<const float4*>(w + j);
+    const float4 gv = *reinterpret_cast<const float4*>(g + j);
+    float4 mv = mom ? *reinterpret_cast<const float4*>(m + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 vv = adam ? *reinterpret_cast<const float4*>(v + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    wv.x = opt_one(o, wv.x, gv.x, &mv.x, &vv.x);
+    wv.y = opt_one(o, wv.y, gv.y, &mv.y, &vv.y);
+    wv.z = opt_one(o, wv.z, gv.z, &mv.z, &vv.z);
+    wv.w = opt_one(o, wv.w, gv.w, &mv.w, &vv.w);
+    *reinterpret_cast<float4*>(w + j) = wv;
+    if (mom) *reinterpret_cast<float4*>(m + j) = mv;
+    if (adam) *reinterpret_cast<float4*>(v + j) = vv;
+    if (wb) {
+      __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(wb + j);
+      d[0] = __floats2bfloat162_rn(wv.x, wv.y);
+      d[1] = __floats2bfloat162_rn(wv.z, wv.w);
     }
+  };
+  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; q + stride < nv4; q += 2 * stride) {
+    vec(q);
+    vec(q + stride);
+  }
+  if (q < nv4) vec(q);
+  for (long long i = 4 * nv4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long j = base + i;
+    float mj = mom ? m[j] : 0.f, vj = adam ? v[j] : 0.f;
+    const float wj = opt_one(o, w[j], g[j], &mj, &vj);
     w[j] = wj;
+    if (mom) m[j] = mj;
+    if (adam) v[j] = vj;
     if (wb) wb[j] = __float2bfloat16_rn(wj);
   }
 }
@@ -449,7 +482,9 @@ dsx_status backward_layer(dsx_mlp* m, int l, void* dz_cur, void* dz_prev, const 
   }
   // the layer's optimizer step (W and b are one contiguous range)
   const long long lo = m->off[l], n = m->boff[l] + out - m->off[l];
-  dim3 grid(blocks_for(n, m->nsm) / std::max(1, m->kl) + 1, m->kl);
+  // ~4 resident blocks per SM over all workers, each thread 2 x 16 B per pass
+  const long long want = (n / 8 + 255) / 256;
+  dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(want, (long long)m->nsm * 8 / m->kl)), m->kl);
   optimizer_kernel<<<grid, 256, 0, m->stream>>>(m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P,
                                                 lo, n, o);
   ++m->launches;
