@@ -234,6 +234,13 @@ dsx_status dsx_mt_jump_selftest(unsigned long long jump, int* ok);
  * (the ssgd mode). */
 dsx_status dsx_lab_last_timeline(dsx_lab* lab, float* bp, float* comm);
 
+/* Self-test of the cross-rank averaging kernel for `nranks` ranks spread
+ * round-robin over the visible GPUs in this process (peer access): every
+ * rank's slice averaged from every rank's buffer over NVLink, compared
+ * with the reference's pairwise tree / K on the host.  *max_abs_err is 0
+ * when bit-exact.  Exercises the 8-rank kernel on a 2- or 4-GPU box. */
+dsx_status dsx_p2p_average_selftest(int nranks, long long n, double* max_abs_err);
+
 /* Number of kernel launches issued by this lab since creation. */
 dsx_status dsx_lab_launch_count(dsx_lab* lab, uint64_t* out);
 

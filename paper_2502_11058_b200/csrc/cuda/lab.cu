@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <random>
 #include <sstream>
 #include <string>
@@ -483,7 +484,11 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
 // stores — the memory pipeline costs no registers, so fewer SMs can carry
 // the full HBM stream and the rest stay free for the noise engine.
 // ---------------------------------------------------------------------------
-constexpr int kBChunk = 512;                 // coordinates per chunk
+constexpr int kBChunk = 512;                 // coordinates per chunk with 8 local rows
+// chunk length by local row count: every stage moves the same 64 KB (rows +
+// noise), so 1-4 rows carry as many bytes per mbarrier round trip as 8
+template <int KL>
+__host__ __device__ constexpr int bulk_chunk() { return kBChunk * 8 / KL; }
 constexpr int kBStages = 3;
 constexpr int kBConsumers = 256;             // one pair per consumer thread
 constexpr int kBThreads = kBConsumers + 32;  // + producer warp
@@ -527,13 +532,14 @@ template <int KL, int NM>
 __global__ void __launch_bounds__(kBThreads, 1)
 lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
   constexpr bool NOISE = NM != 0;
-  extern __shared__ __align__(128) double bsm[];  // [stage][2: w, x][KL][kBChunk]
+  constexpr int CH = bulk_chunk<KL>();
+  extern __shared__ __align__(128) double bsm[];  // [stage][2: w, x][KL][CH]
   __shared__ __align__(8) uint64_t full[kBStages], empty[kBStages];
   __shared__ BulkChunk info[kBStages];
   __shared__ double red[kBConsumers / 32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  auto wbuf = [&](int st, int k) { return bsm + ((long long)(st * 2 + 0) * KL + k) * kBChunk; };
-  auto xbuf = [&](int st, int k) { return bsm + ((long long)(st * 2 + 1) * KL + k) * kBChunk; };
+  auto wbuf = [&](int st, int k) { return bsm + ((long long)(st * 2 + 0) * KL + k) * CH; };
+  auto xbuf = [&](int st, int k) { return bsm + ((long long)(st * 2 + 1) * KL + k) * CH; };
   if (tid == 0) {
     for (int st = 0; st < kBStages; ++st) {
       mbar_init(&full[st], 1);
@@ -571,8 +577,8 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
       // lazy multi-rank rows: a layer averaged last step is read once (its mean)
       const bool stale = a.mean_in != nullptr && mask_has(a.stale, t.block);
       const long long lo = t.start & ~1LL, hi = (t.start + t.len + 1) & ~1LL;
-      for (long long a0 = lo; a0 < hi; a0 += kBChunk, ++j) {
-        const long long a1 = a0 + kBChunk < hi ? a0 + kBChunk : hi;
+      for (long long a0 = lo; a0 < hi; a0 += CH, ++j) {
+        const long long a1 = a0 + CH < hi ? a0 + CH : hi;
         const int st = j % kBStages, u = j / kBStages;
         if (u > 0) mbar_wait(&empty[st], (u - 1) & 1);
         if (lane == 0) {
@@ -609,12 +615,13 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
     const bool part = a.partial_out != nullptr && mask_has(a.mask, t.block);
     const bool stale = a.mean_in != nullptr && mask_has(a.stale, t.block);
     const long long lo = t.start & ~1LL, hi = (t.start + t.len + 1) & ~1LL;
-    for (long long a0 = lo; a0 < hi; a0 += kBChunk, ++j) {
+    for (long long a0 = lo; a0 < hi; a0 += CH, ++j) {
       const int st = j % kBStages, u = j / kBStages;
       mbar_wait(&full[st], u & 1);
       const BulkChunk ci = info[st];
       const long long a1 = ci.a1;
-      const int p = tid;  // pair of the chunk
+#pragma unroll
+      for (int p = tid; p < CH / 2; p += kBConsumers) {  // pairs of the chunk
       const long long i = a0 + 2 * (long long)p;
       const bool in0 = i < a1 && i >= t.start && i < t.start + t.len;
       const bool in1 = i + 1 < a1 && i + 1 >= t.start && i + 1 < t.start + t.len;
@@ -672,6 +679,7 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
           }
         }
       }
+      }  // pairs of the chunk
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"n"(kBConsumers) : "memory");
       if (tid == 0) {
@@ -1368,7 +1376,7 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
   a.mean_in = lab->stale_any ? static_cast<const T*>(lab->staging) : nullptr;
   a.stale = lab->stale_bits;
   if (lab->engine) a.nv = lab->engine->view(lab->cur_set, lab->cur_t);
-  if constexpr (std::is_same_v<T, double> && (KL == 2 || KL == 4 || KL == 8)) {
+  if constexpr (std::is_same_v<T, double> && (KL == 1 || KL == 2 || KL == 4 || KL == 8)) {
     // bulk-copy kernel: the default with engine noise (0.91 vs 0.84 of HBM at
     // sigma=1); the register-staged kernel stays faster without noise (0.83
     // vs 0.80).  DSX_UPD_BULK=0 off, =1 on (one CTA per SM), =n n CTAs.
@@ -1380,7 +1388,7 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
     // mbarrier round trip: 4 GPUs 0.29 vs 0.17 ms, so 8 rows only by default)
     const int bulk_ctas = bulk_env >= 0 ? bulk_env : (nm == 2 && KL == 8 ? 1 : 0);
     if (bulk_ctas > 0 && (nm == 0 || nm == 2)) {
-      constexpr size_t smem = sizeof(double) * kBStages * 2 * KL * kBChunk;
+      constexpr size_t smem = sizeof(double) * kBStages * 2 * KL * bulk_chunk<KL>();
       static std::atomic<unsigned long long> attr{0};
       dsx::once_per_device(attr, [] {
         cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2888,6 +2896,81 @@ dsx_status dsx_lab_comm_init_local(dsx_lab* const* labs, int n, int sync_algo) {
     DSX_CUDA(cudaSetDevice(devs[r]));
     DSX_TRY(comm_finish(labs[r], ok, n));
   }
+  return DSX_OK;
+}
+
+dsx_status dsx_p2p_average_selftest(int nranks, long long n, double* max_abs_err) {
+  if (!max_abs_err || nranks < 1 || nranks > kMaxProg || n < 1) return fail(DSX_ERR_ARGUMENT, "bad selftest args");
+  *max_abs_err = -1.0;
+  int ndev = 0;
+  DSX_CUDA(cudaGetDeviceCount(&ndev));
+  if (ndev < 1) return fail(DSX_ERR_CUDA, "no CUDA device");
+  std::vector<int> dev(nranks);
+  for (int r = 0; r < nranks; ++r) dev[r] = r % ndev;
+  for (int a = 0; a < std::min(ndev, nranks); ++a) {
+    DSX_CUDA(cudaSetDevice(a));
+    for (int b = 0; b < std::min(ndev, nranks); ++b) {
+      if (a == b) continue;
+      int can = 0;
+      DSX_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) return fail(DSX_ERR_CUDA, "no peer access between the devices");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(DSX_ERR_CUDA, "peer access");
+      cudaGetLastError();
+    }
+  }
+  // rank r's row: distinct, non-representable-sum values (rounding matters)
+  std::vector<std::vector<double>> host(nranks, std::vector<double>(n));
+  for (int r = 0; r < nranks; ++r)
+    for (long long i = 0; i < n; ++i) host[r][i] = std::sin(0.37 * (double)i + 1.7 * r) * (1.0 + 0.1 * r) + 1e-3 * r;
+  PeerPtrs peers{};
+  for (int r = 0; r < nranks; ++r) {
+    DSX_CUDA(cudaSetDevice(dev[r]));
+    DSX_CUDA(cudaMalloc(&peers.p[r], 8 * n));
+    DSX_CUDA(cudaMemcpy(peers.p[r], host[r].data(), 8 * n, cudaMemcpyHostToDevice));
+  }
+  PairProg prog{};
+  build_prog(nranks, &prog);
+  // every rank averages its slice, like the step's averaging kernel
+  for (int r = 0; r < nranks; ++r) {
+    DSX_CUDA(cudaSetDevice(dev[r]));
+    const long long base = n / nranks, extra = n % nranks;
+    const long long a = r * base + std::min<long long>(r, extra);
+    const long long e = a + base + (r < extra ? 1 : 0);
+    const int blocks = (int)std::min<long long>(592, ((e - a) / 2 + 255) / 256 + 1);
+    switch (nranks) {
+      case 2: p2p_average_kernel<double, 2><<<blocks, 256>>>(peers, a, e, nranks, prog, Signal{}); break;
+      case 4: p2p_average_kernel<double, 4><<<blocks, 256>>>(peers, a, e, nranks, prog, Signal{}); break;
+      case 8: p2p_average_kernel<double, 8><<<blocks, 256>>>(peers, a, e, nranks, prog, Signal{}); break;
+      default: p2p_average_kernel<double, 0><<<blocks, 256>>>(peers, a, e, nranks, prog, Signal{});
+    }
+    DSX_CUDA(cudaGetLastError());
+  }
+  for (int d = 0; d < std::min(ndev, nranks); ++d) {
+    DSX_CUDA(cudaSetDevice(d));
+    DSX_CUDA(cudaDeviceSynchronize());
+  }
+  // expected: pairwise_coord_sum over the ranks / K (trainer.cpp:31-38)
+  std::vector<double> col(nranks);
+  std::function<double(int, int)> pw = [&](int lo, int cnt) -> double {
+    if (cnt == 1) return col[lo];
+    if (cnt == 2) return col[lo] + col[lo + 1];
+    return pw(lo, cnt / 2) + pw(lo + cnt / 2, cnt - cnt / 2);
+  };
+  double worst = 0.0;
+  std::vector<double> got(n);
+  std::vector<double> want(n);
+  for (long long i = 0; i < n; ++i) {
+    for (int r = 0; r < nranks; ++r) col[r] = host[r][i];
+    want[i] = pw(0, nranks) / (double)nranks;
+  }
+  for (int r = 0; r < nranks; ++r) {
+    DSX_CUDA(cudaSetDevice(dev[r]));
+    DSX_CUDA(cudaMemcpy(got.data(), peers.p[r], 8 * n, cudaMemcpyDeviceToHost));
+    for (long long i = 0; i < n; ++i) worst = std::max(worst, std::fabs(got[i] - want[i]));
+    cudaFree(peers.p[r]);
+  }
+  *max_abs_err = worst;
   return DSX_OK;
 }
 

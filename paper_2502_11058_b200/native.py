@@ -111,6 +111,7 @@ _SIGS = {
     "dsx_lab_launch_count": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
     "dsx_mt_jump_selftest": ([C.c_ulonglong, C.POINTER(C.c_int)], C.c_int),
     "dsx_sync_plan": ([C.c_int, C.c_int, C.POINTER(C.c_int)], C.c_int),
+    "dsx_p2p_average_selftest": ([C.c_int, C.c_longlong, C.POINTER(C.c_double)], C.c_int),
 }
 
 

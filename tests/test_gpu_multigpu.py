@@ -62,3 +62,17 @@ def test_reference_unit_suite_trainer_cases_on_two_gpus(monkeypatch):
     from tests import test_unit_suite as U
     monkeypatch.setenv("DREAMSCHED_GPUS", "2")
     U.test_reference_unit_suite_trainer_cases_on_gpu()
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4, 6, 8])
+def test_p2p_average_kernel_ranks_bit_exact(nranks):
+    """The cross-rank averaging kernel for up to 8 ranks (the 8-GPU
+    instantiation included), ranks spread round-robin over this box's GPUs
+    in one process: bit-identical to the reference's pairwise tree / K."""
+    if _gpus() < 2:
+        pytest.skip("needs >= 2 GPUs (peer access)")
+    import ctypes as C
+    from paper_2502_11058_b200 import native as N
+    err = C.c_double()
+    N.call("dsx_p2p_average_selftest", nranks, 100003, C.byref(err))
+    assert err.value == 0.0, err.value
