@@ -358,72 +358,89 @@ lab_update_kernel(UpdateArgs<T> a, PairProg prog) {
     auto pairs = [&](auto stale_c, auto simple_c) {
       constexpr bool STALE = decltype(stale_c)::value;
       constexpr bool SIMPLE = decltype(simple_c)::value;
-      for (int pr = threadIdx.x; pr < npairs; pr += kThreads) {
-        const long long i = first + 2 * (long long)pr;
-        double lam0, opt0, lam1, opt1;
-        quad_coeffs(a.q, i, &lam0, &opt0);
-        quad_coeffs(a.q, i + 1, &lam1, &opt1);
-        V2 wv[KL];
-        double2 xv[KL];
-        if constexpr (STALE) {
-          const V2 m = *reinterpret_cast<const V2*>(a.mean_in + i);
+      // U pairs per thread per iteration, all their loads issued before any
+      // compute: with 1-2 local rows a single pair keeps too few bytes in
+      // flight to cover HBM latency (ncu, 2 rows: long_scoreboard 59 %,
+      // 0.53 of DRAM peak)
+      constexpr int U = KL >= 4 ? 1 : (KL == 2 ? 2 : 4);
+      for (int pr0 = threadIdx.x; pr0 < npairs; pr0 += kThreads * U) {
+        V2 wv[U][KL];
+        double2 xv[U][KL];
 #pragma unroll
-          for (int k = 0; k < KL; ++k) wv[k] = m;
-        } else {
+        for (int u = 0; u < U; ++u) {
+          const int pr = pr0 + u * kThreads;
+          if (pr >= npairs) break;
+          const long long i = first + 2 * (long long)pr;
+          if constexpr (STALE) {
+            const V2 m = *reinterpret_cast<const V2*>(a.mean_in + i);
 #pragma unroll
-          for (int k = 0; k < KL; ++k) wv[k] = *reinterpret_cast<const V2*>(a.w + k * a.ld + i);
-        }
-        if constexpr (NM == 1) {
-#pragma unroll
-          for (int k = 0; k < KL; ++k) xv[k] = __ldcs(reinterpret_cast<const double2*>(a.noise + k * a.ld + i));
-        }
-        if constexpr (SEG) {
-          if constexpr (SIMPLE) {
-            const unsigned long long m = (unsigned long long)i >> 1;
-            const double* np[KL];
-#pragma unroll
-            for (int k = 0; k < KL; ++k) np[k] = s_base[k][m >= s_bound[k] ? 1 : 0];
-#pragma unroll
-            for (int k = 0; k < KL; ++k) xv[k] = __ldcs(reinterpret_cast<const double2*>(np[k] + i));
-            if constexpr (NM == 3) {
-              // the polar transform of the engine's raw attempts, here where
-              // the issue slots idle on HBM latency anyway
-#pragma unroll
-              for (int k = 0; k < KL; ++k) xv[k] = mt_polar_normals(xv[k].x, xv[k].y, a.nv.stddev);
-            }
+            for (int k = 0; k < KL; ++k) wv[u][k] = m;
           } else {
 #pragma unroll
-            for (int k = 0; k < KL; ++k) xv[k] = make_double2(noise_at(k, i), noise_at(k, i + 1));
+            for (int k = 0; k < KL; ++k) wv[u][k] = *reinterpret_cast<const V2*>(a.w + k * a.ld + i);
+          }
+          if constexpr (NM == 1) {
+#pragma unroll
+            for (int k = 0; k < KL; ++k)
+              xv[u][k] = __ldcs(reinterpret_cast<const double2*>(a.noise + k * a.ld + i));
+          }
+          if constexpr (SEG) {
+            if constexpr (SIMPLE) {
+              const unsigned long long m = (unsigned long long)i >> 1;
+              const double* np[KL];
+#pragma unroll
+              for (int k = 0; k < KL; ++k) np[k] = s_base[k][m >= s_bound[k] ? 1 : 0];
+#pragma unroll
+              for (int k = 0; k < KL; ++k) xv[u][k] = __ldcs(reinterpret_cast<const double2*>(np[k] + i));
+            } else {
+#pragma unroll
+              for (int k = 0; k < KL; ++k) xv[u][k] = make_double2(noise_at(k, i), noise_at(k, i + 1));
+            }
           }
         }
-        T w0[KL], w1[KL];
 #pragma unroll
-        for (int k = 0; k < KL; ++k) {
-          const double x0 = NOISE ? xv[k].x : 0.0, x1 = NOISE ? xv[k].y : 0.0;
-          const auto g0 = grad_step(wv[k].x, lam0, opt0, x0, a.eta, NOISE, &w0[k]);
-          const auto g1 = grad_step(wv[k].y, lam1, opt1, x1, a.eta, NOISE, &w1[k]);
-          nsq[k] += to_d(g0) * to_d(g0) + to_d(g1) * to_d(g1);
-        }
-        if (avg) {
-          V2 m;
-          m.x = psum<0, KL, T>(w0) / (T)a.k_total;
-          m.y = psum<0, KL, T>(w1) / (T)a.k_total;
+        for (int u = 0; u < U; ++u) {
+          const int pr = pr0 + u * kThreads;
+          if (pr >= npairs) break;
+          const long long i = first + 2 * (long long)pr;
+          double lam0, opt0, lam1, opt1;
+          quad_coeffs(a.q, i, &lam0, &opt0);
+          quad_coeffs(a.q, i + 1, &lam1, &opt1);
+          if constexpr (NM == 3 && SIMPLE) {
+            // the polar transform of the engine's raw attempts, here where
+            // the issue slots idle on HBM latency anyway
 #pragma unroll
-          for (int k = 0; k < KL; ++k) *reinterpret_cast<V2*>(a.w + k * a.ld + i) = m;
-        } else if (part) {
-          // multi-rank synced tile: only this rank's subtree sum leaves the
-          // kernel; the rows are rewritten by the cross-rank average
-          V2 m;
-          m.x = psum<0, KL, T>(w0);
-          m.y = psum<0, KL, T>(w1);
-          *reinterpret_cast<V2*>(part_dst + i) = m;
-        } else {
+            for (int k = 0; k < KL; ++k) xv[u][k] = mt_polar_normals(xv[u][k].x, xv[u][k].y, a.nv.stddev);
+          }
+          T w0[KL], w1[KL];
 #pragma unroll
           for (int k = 0; k < KL; ++k) {
-            V2 o;
-            o.x = w0[k];
-            o.y = w1[k];
-            *reinterpret_cast<V2*>(a.w + k * a.ld + i) = o;
+            const double x0 = NOISE ? xv[u][k].x : 0.0, x1 = NOISE ? xv[u][k].y : 0.0;
+            const auto g0 = grad_step(wv[u][k].x, lam0, opt0, x0, a.eta, NOISE, &w0[k]);
+            const auto g1 = grad_step(wv[u][k].y, lam1, opt1, x1, a.eta, NOISE, &w1[k]);
+            nsq[k] += to_d(g0) * to_d(g0) + to_d(g1) * to_d(g1);
+          }
+          if (avg) {
+            V2 m;
+            m.x = psum<0, KL, T>(w0) / (T)a.k_total;
+            m.y = psum<0, KL, T>(w1) / (T)a.k_total;
+#pragma unroll
+            for (int k = 0; k < KL; ++k) *reinterpret_cast<V2*>(a.w + k * a.ld + i) = m;
+          } else if (part) {
+            // multi-rank synced tile: only this rank's subtree sum leaves the
+            // kernel; the rows are rewritten by the cross-rank average
+            V2 m;
+            m.x = psum<0, KL, T>(w0);
+            m.y = psum<0, KL, T>(w1);
+            *reinterpret_cast<V2*>(part_dst + i) = m;
+          } else {
+#pragma unroll
+            for (int k = 0; k < KL; ++k) {
+              V2 o;
+              o.x = w0[k];
+              o.y = w1[k];
+              *reinterpret_cast<V2*>(a.w + k * a.ld + i) = o;
+            }
           }
         }
       }
@@ -2709,12 +2726,11 @@ dsx_status comm_prepare(dsx_lab* lab, int nranks, int rank, int sync_algo) {
   DSX_CUDA(cudaMalloc(&lab->bar, 4));
   DSX_CUDA(cudaMemset(lab->bar, 0, 4));
   for (auto& ev : lab->ev_chunk) DSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  // Overlap groups: with 4+ local workers the update and the pipelined noise
-  // engine already keep the GPU busy while the average runs on the sync
-  // stream, and splitting the update only adds launch tails (measured at
-  // 2 GPUs: 1610 vs 1500 it/s); with fewer local workers the backward-order
-  // groups pay off (4 GPUs: 2615 vs 2370 it/s, one group vs four).
-  lab->chunks = lab->kl >= 4 ? 1 : 6;  // 4 GPUs: 6 groups 2510, 4 groups 2370, 2 groups 2470 it/s
+  // Overlap groups: the local step runs in backward-order tile groups and
+  // each group's average starts while the next group updates.  Round 2, exact-window timing, 2 GPUs x 4 rows: 1 group 1607 it/s with
+  // 99 % of the sync exposed; 2 / 3 / 6 groups 1628 / 1620 / 1614 it/s with
+  // 54 / 43 / 33 % exposed -> 6 groups everywhere
+  lab->chunks = 6;
   if (const char* c = std::getenv("DSX_SYNC_CHUNKS")) lab->chunks = std::max(1, std::min(kMaxChunks, std::atoi(c)));
   {
     const int nm = lab->sigma > 0.0 ? 2 : 0;
