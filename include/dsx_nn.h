@@ -122,6 +122,14 @@ dsx_status dsx_mlp_profile(dsx_mlp* m, int reps, double* t_fp, double* t_bp, dou
 dsx_status dsx_mlp_event_record(dsx_mlp* m, int slot);
 dsx_status dsx_mlp_event_elapsed(dsx_mlp* m, int from_slot, int to_slot, float* ms);
 dsx_status dsx_mlp_launch_count(dsx_mlp* m, uint64_t* out);
+/* Throttled link (the paper's low-bandwidth regime): every synced layer
+ * additionally occupies the FIFO sync stream for latency + layer_bytes /
+ * bandwidth seconds (comm_time, profile.cpp:103-110).  bandwidth <= 0: off. */
+dsx_status dsx_mlp_set_link(dsx_mlp* m, double bandwidth, double latency);
+/* enabled (default): a layer's average starts as soon as its BP + update is
+ * done (wfbp / plsgd); 0: all averages after the whole local step (the ssgd
+ * and flsgd modes). */
+dsx_status dsx_mlp_set_overlap(dsx_mlp* m, int enabled);
 /* Capture the step into a CUDA graph (replayed by dsx_mlp_step for the same
  * mask; device-resident batches only).  0 disables. */
 dsx_status dsx_mlp_set_graphs(dsx_mlp* m, int enabled);

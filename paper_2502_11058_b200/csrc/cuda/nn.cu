@@ -264,6 +264,18 @@ __global__ void cast_bf16_kernel(const float* __restrict__ w, __nv_bfloat16* __r
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     for (int k = 0; k < kl; ++k) wb[(long long)k * ld + lo + i] = __float2bfloat16_rn(w[(long long)k * ld + lo + i]);
 }
+// Throttled link (the paper's low-bandwidth regime): the sync stream is a
+// FIFO link; after a layer's average it stays busy latency + bytes/bandwidth
+// (comm_time, profile.cpp:103-110).
+__global__ void nn_link_spin_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 __global__ void x_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16_rn(x[i]);
@@ -316,6 +328,8 @@ struct dsx_mlp {
 
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  double link_bw = 0.0, link_lat = 0.0;  // throttled link (bw <= 0: off)
+  bool overlap = true;                   // false: averages after the whole BP (ssgd/flsgd modes)
 };
 
 namespace dsx_nn {
@@ -541,19 +555,36 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
   // starts on the side stream as soon as its update is done
   int cur = 0;
   bool any = false;
+  // one layer's sync on the side stream (+ the throttled link's busy time)
+  auto sync_layer = [&](int l) -> dsx_status {
+    if (m->instrument && !any) NN_CUDA(cudaEventRecord(m->ev[7], m->side));
+    NN_TRY(average_layer(m, l, m->side));
+    if (m->link_bw > 0.0) {
+      const double bytes = 4.0 * (double)(m->boff[l] + m->widths[l + 1] - m->off[l]);
+      nn_link_spin_kernel<<<1, 1, 0, m->side>>>((unsigned long long)((m->link_lat + bytes / m->link_bw) * 1e9));
+      ++m->launches;
+    }
+    NN_CUDA(cudaEventRecord(m->ev_sync[l], m->side));
+    any = true;
+    return DSX_OK;
+  };
   for (int l = m->L - 1; l >= 0; --l) {
     NN_TRY(backward_layer(m, l, m->dz[cur], m->dz[cur ^ 1], o));
     cur ^= 1;
     const bool sync_l = mask[l + 1] != 0 && m->K > 1;
     m->synced_prev[l] = sync_l ? 1 : 0;
-    if (sync_l) {
+    if (sync_l && m->overlap) {
       NN_CUDA(cudaEventRecord(m->ev_upd[l], m->stream));
       NN_CUDA(cudaStreamWaitEvent(m->side, m->ev_upd[l], 0));
-      if (m->instrument && !any) NN_CUDA(cudaEventRecord(m->ev[7], m->side));
-      NN_TRY(average_layer(m, l, m->side));
-      NN_CUDA(cudaEventRecord(m->ev_sync[l], m->side));
-      any = true;
+      NN_TRY(sync_layer(l));
     }
+  }
+  if (!m->overlap) {
+    // ssgd / flsgd: the transfers start after the whole local step
+    NN_CUDA(cudaEventRecord(m->ev_upd[0], m->stream));
+    NN_CUDA(cudaStreamWaitEvent(m->side, m->ev_upd[0], 0));
+    for (int l = m->L - 1; l >= 0; --l)
+      if (m->synced_prev[l]) NN_TRY(sync_layer(l));
   }
   m->any_synced = any;
   if (m->instrument) {
@@ -957,6 +988,20 @@ dsx_status dsx_mlp_event_elapsed(dsx_mlp* m, int a, int b, float* ms) {
 dsx_status dsx_mlp_launch_count(dsx_mlp* m, uint64_t* out) {
   if (!m || !out) return nfail(DSX_ERR_ARGUMENT, "null argument");
   *out = m->launches;
+  return DSX_OK;
+}
+
+dsx_status dsx_mlp_set_link(dsx_mlp* m, double bandwidth, double latency) {
+  NN_TRY(check(m));
+  if (!(latency >= 0.0)) return nfail(DSX_ERR_ARGUMENT, "latency must be >= 0");
+  m->link_bw = bandwidth > 0.0 ? bandwidth : 0.0;
+  m->link_lat = latency;
+  return DSX_OK;
+}
+
+dsx_status dsx_mlp_set_overlap(dsx_mlp* m, int enabled) {
+  NN_TRY(check(m));
+  m->overlap = enabled != 0;
   return DSX_OK;
 }
 

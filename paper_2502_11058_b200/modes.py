@@ -146,3 +146,77 @@ def run(block_sizes, workers=4, period=4, bandwidth=None, latency=5e-6, comm_rat
         res["S1_" + kind.split("_")[0]] = m["wfbp"][kind] / m["plsgd"][kind]
         res["S2_" + kind.split("_")[0]] = m["flsgd"][kind] / m["plsgd"][kind]
     return res
+
+
+def run_mlp(widths, batch_size=256, workers=4, period=4, optimizer="adam", lr=1e-3, dtype="bf16",
+            comm_ratio=2.0, latency=5e-6, iters=None, device=0, reps=5, seed=1):
+    """The four modes on the NN local step (the paper's Table 1 experiment on
+    a real network): a K-worker MLP on one B200 whose sync stream is a
+    throttled FIFO link (dsx_mlp_set_link); the CUDA-event profile of every
+    layer's FP and BP + update feeds write_profile -> schedule_dfs +
+    bubble_fill (plsgd) and simulate_run (the prediction).  bandwidth is
+    chosen so the whole model's transfer takes comm_ratio x the measured
+    FP + BP (a communication-bound setting, like the paper's 1-20 GB/s
+    Ethernet).  Returns {mode: measured_s, predicted_s} and S1 / S2."""
+    import torch
+
+    from .nn import Mlp, batch, init_params, layer_sizes, teacher
+    L = len(widths) - 1
+    iters = iters or 4 * period
+    m = Mlp(widths, batch_size, workers, dtype=dtype, optimizer=optimizer,
+            eps=1e-6 if optimizer == "adam" else 1e-8, device=device)
+    init = init_params(seed, widths)
+    for k in range(workers):
+        m.set_params(k, init)
+    t = teacher(seed, widths[0], widths[-1])
+    xs, ys = zip(*[zip(*[batch(seed, k, p, batch_size, widths[0], t) for k in range(workers)]) for p in range(4)])
+    dx = torch.from_numpy(np.stack([np.stack(x) for x in xs])).to(f"cuda:{device}")
+    dy = torch.from_numpy(np.stack([np.stack(y) for y in ys])).to(f"cuda:{device}")
+    m.set_batch_ptr(dx[0].data_ptr(), dy[0].data_ptr(), True)
+    t_fp, t_bp, _ = m.profile(reps=reps)
+    sizes = layer_sizes(widths)
+    pbytes = [4 * s for s in sizes]
+    bandwidth = float(sum(pbytes)) / max(comm_ratio * float(np.sum(t_fp) + np.sum(t_bp)) - L * latency, 1e-6)
+    tmp = tempfile.mkdtemp(prefix="dreamddp_nn_modes_")
+    prof = os.path.join(tmp, "measured.profile")
+    write_profile(prof, pbytes, t_fp, t_bp, None, bandwidth, latency)
+    sets, fills, objective, sched_text = schedule_from_profile(prof, period)
+    res = {"profile": prof, "schedule": sched_text, "widths": list(widths), "batch": batch_size,
+           "workers": workers, "period": period, "optimizer": optimizer, "dtype": dtype,
+           "bandwidth_Bps": bandwidth, "latency_s": latency, "iters": iters,
+           "t_fp_total_s": float(np.sum(t_fp)), "t_bp_total_s": float(np.sum(t_bp)), "modes": {}}
+    everything = np.ones(L + 1, dtype=np.uint8)
+    nothing = np.zeros(L + 1, dtype=np.uint8)
+    m.set_link(bandwidth, latency)
+    r_global = 0
+    for mode in MODES:
+        predicted, _ = simulate(prof, mode, period, iters)
+        m.set_overlap(mode in ("wfbp", "plsgd"))
+
+        def mask_of(r):
+            if mode in ("ssgd", "wfbp"):
+                return everything
+            if mode == "flsgd":
+                return everything if (r + 1) % period == 0 else nothing
+            return sync_mask("partial", period, r, L, sets, fills)
+        for r in range(period):  # warm-up, same mode
+            m.set_batch_ptr(dx[r % 4].data_ptr(), dy[r % 4].data_ptr(), True)
+            m.step(lr, r_global, mask_of(r))
+            r_global += 1
+        m.sync()
+        m.record(0)
+        for r in range(iters):
+            m.set_batch_ptr(dx[r % 4].data_ptr(), dy[r % 4].data_ptr(), True)
+            m.step(lr, r_global, mask_of(r))
+            r_global += 1
+        m.record(1)
+        measured = m.elapsed_ms(0, 1) * 1e-3
+        m.sync()
+        res["modes"][mode] = {"measured_s": measured, "predicted_s": predicted}
+    m.set_link(0.0, 0.0)
+    m.close()
+    mm = res["modes"]
+    for kind in ("measured_s", "predicted_s"):
+        res["S1_" + kind.split("_")[0]] = mm["wfbp"][kind] / mm["plsgd"][kind]
+        res["S2_" + kind.split("_")[0]] = mm["flsgd"][kind] / mm["plsgd"][kind]
+    return res

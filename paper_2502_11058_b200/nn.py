@@ -150,6 +150,13 @@ class Mlp:
     def set_instrument(self, on: bool) -> None:
         N.call("dsx_mlp_set_instrument", self.h, int(on))
 
+    def set_link(self, bandwidth: float, latency: float = 0.0) -> None:
+        """Throttled sync link (bytes/s, s); bandwidth <= 0 disables."""
+        N.call("dsx_mlp_set_link", self.h, bandwidth, latency)
+
+    def set_overlap(self, on: bool) -> None:
+        N.call("dsx_mlp_set_overlap", self.h, int(on))
+
     def last_step_times(self):
         out = (C.c_float * 4)()
         N.call("dsx_mlp_last_step_times", self.h, out)
