@@ -42,3 +42,19 @@ def test_four_modes_measured_vs_simulated(tmp_path):
         comms.sort(key=lambda e: e["ts"])
         for a, b in zip(comms, comms[1:]):
             assert b["ts"] >= a["ts"] + a["dur"] - 2
+
+
+def test_four_modes_on_the_nn_local_step():
+    """The paper's Table 1 experiment on a real network: a 4-worker MLP with
+    local Adam (BASELINE configs[0] shape, configs[3]'s 'partial local Adam,
+    bandwidth-throttled sync') on a throttled FIFO link; the measured mode
+    times follow simulate_run's prediction from the CUDA-event profile, and
+    plsgd (DFS + bubble fill on that profile) beats wfbp and flsgd."""
+    from paper_2502_11058_b200 import modes
+    res = modes.run_mlp([1024] * 8 + [10], batch_size=256, workers=4, period=4, optimizer="adam",
+                        lr=1e-3, comm_ratio=2.0)
+    m = res["modes"]
+    for mode in modes.MODES:
+        assert m[mode]["measured_s"] == pytest.approx(m[mode]["predicted_s"], rel=0.25), (mode, res)
+    assert res["S1_measured"] > 1.3 and res["S2_measured"] > 1.1, res
+    assert res["S2_measured"] == pytest.approx(res["S2_predicted"], rel=0.2)
