@@ -85,6 +85,7 @@ def parse_args(argv=None):
                     help="steps of the full-size parity pass vs the reference (default per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true", help="also skips the parity pass")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="mlp: eager launches instead of CUDA graphs")
     ap.add_argument("--schedule", default="auto", choices=["auto", "measured", "profile"],
                     help="multi-GPU: schedule from the CUDA-event profile measured on these GPUs "
                          "(auto for N>1) or from --profile's times")
@@ -750,7 +751,7 @@ def mlp_reference_arm(args, world, rank):
 def mlp_config(args, world, schedule_src):
     return {"workload": args.workload, "config": args.config, "widths": args.widths, "batch_per_worker": args.batch,
             "workers": args.workers, "period": args.period, "optimizer": args.optimizer, "lr": args.lr,
-            "schedule": schedule_src, "seed": args.seed,
+            "schedule": schedule_src, "seed": args.seed, "cuda_graphs": not args.no_graphs,
             "parallelism": f"dp{world} ({args.workers // world} workers/GPU)",
             "sync": ("NCCL ncclAvg in place per layer on the side stream" if world > 1 else
                      "pairwise local average kernel per layer on the side stream"),
@@ -782,6 +783,8 @@ def mlp_arm(args, world, rank, local_rank, dist):
     init = init_params(args.seed, args.widths)
     for k in range(kl):
         m.set_params(k, init)
+    # the step replays one captured CUDA graph per sync mask
+    m.set_graphs(not args.no_graphs)
     npool = 8
     xs, ys = mlp_data_pool(args, kl, rank, npool)
     dx = torch.from_numpy(xs).to(f"cuda:{local_rank}")

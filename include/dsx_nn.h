@@ -130,8 +130,11 @@ dsx_status dsx_mlp_set_link(dsx_mlp* m, double bandwidth, double latency);
  * done (wfbp / plsgd); 0: all averages after the whole local step (the ssgd
  * and flsgd modes). */
 dsx_status dsx_mlp_set_overlap(dsx_mlp* m, int enabled);
-/* Capture the step into a CUDA graph (replayed by dsx_mlp_step for the same
- * mask; device-resident batches only).  0 disables. */
+/* Replay the step from CUDA graphs: one captured per distinct sync mask on
+ * first use (the step's lr / bias corrections / batch pointers are read from
+ * device memory, so every step replays the same graph), the sync stream's
+ * averages joined at the end of each.  Single rank; with several ranks the
+ * step stays eager (NCCL).  0 disables (default). */
 dsx_status dsx_mlp_set_graphs(dsx_mlp* m, int enabled);
 
 #ifdef __cplusplus

@@ -63,6 +63,14 @@ dsx_status nfail(dsx_status code, const std::string& msg) {
 
 namespace {
 
+// Per-step scalars and data pointers, read by the kernels from device memory
+// so that one captured CUDA graph per sync mask replays every step.
+struct StepDev {
+  float lr, bc1, bc2, pad;
+  const float* x;
+  const int* labels;
+};
+
 // ---------------------------------------------------------------------------
 // MLP kernels
 // ---------------------------------------------------------------------------
@@ -71,8 +79,10 @@ namespace {
 // loss partials, and dlogits = (softmax - onehot) / batch written in T.
 template <typename T>
 __global__ void softmax_xent_kernel(const float* __restrict__ logits, long long ld_logit, long long s_logit,
-                                    const int* __restrict__ labels, int batch, int C, T* __restrict__ dz,
-                                    long long ld_dz, long long s_dz, float* __restrict__ loss_part) {
+                                    const int* __restrict__ labels_arg, int batch, int C, T* __restrict__ dz,
+                                    long long ld_dz, long long s_dz, float* __restrict__ loss_part,
+                                    const StepDev* __restrict__ sp) {
+  const int* __restrict__ labels = sp ? sp->labels : labels_arg;
   const int b = blockIdx.y;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= batch) return;
@@ -171,7 +181,12 @@ __device__ __forceinline__ float opt_one(const OptArgs& o, float w, float g, flo
 __global__ void __launch_bounds__(256) optimizer_kernel(float* __restrict__ w, const float* __restrict__ g,
                                                         float* __restrict__ m, float* __restrict__ v,
                                                         __nv_bfloat16* __restrict__ wb, long long ld, long long lo,
-                                                        long long n, OptArgs o) {
+                                                        long long n, OptArgs o, const StepDev* __restrict__ sp) {
+  if (sp) {
+    o.lr = sp->lr;
+    o.bc1 = sp->bc1;
+    o.bc2 = sp->bc2;
+  }
   const long long base = (long long)blockIdx.y * ld + lo;
   const long long nv4 = n / 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -276,9 +291,12 @@ __global__ void nn_link_spin_kernel(unsigned long long ns) {
   } while (t - t0 < ns);
 }
 
-__global__ void x_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, long long n) {
+// the step's input batch -> act[0] (bf16 for the tensor-core path)
+template <typename T>
+__global__ void load_x_kernel(const StepDev* __restrict__ sp, T* __restrict__ y, long long n) {
+  const float* __restrict__ x = sp->x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    y[i] = __float2bfloat16_rn(x[i]);
+    y[i] = from_f<T>(x[i]);
 }
 
 }  // namespace
@@ -330,6 +348,23 @@ struct dsx_mlp {
   int nranks = 1, rank = 0;
   double link_bw = 0.0, link_lat = 0.0;  // throttled link (bw <= 0: off)
   bool overlap = true;                   // false: averages after the whole BP (ssgd/flsgd modes)
+  // per-step scalars: device copy + pinned ring of host slots (one per step
+  // in flight); CUDA graphs, one per distinct sync mask
+  dsx_nn::StepDev* sp = nullptr;
+  dsx_nn::StepDev* ring = nullptr;
+  std::vector<cudaEvent_t> ring_ev;
+  unsigned long long ring_i = 0;
+  bool graphs = false;
+  bool side_used = false;                // the last step_impl put work on the sync stream
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;
+  };
+  std::vector<std::pair<std::string, Graph>> graph_cache;
+  // events used only inside captures (an event recorded in a capture cannot
+  // be waited on eagerly afterwards), and the pre-capture drain
+  std::vector<cudaEvent_t> gev_upd, gev_sync;
+  cudaEvent_t ev_join = nullptr, ev_drain = nullptr;
 };
 
 namespace dsx_nn {
@@ -433,7 +468,7 @@ dsx_status forward_layer(dsx_mlp* m, int l) {
 
 // BP of layer l (0-based): dz_cur = dL/d(pre-activation of layer l) ->
 // dW, db, (dz_prev), then the optimizer update
-dsx_status backward_layer(dsx_mlp* m, int l, void* dz_cur, void* dz_prev, const OptArgs& o) {
+dsx_status backward_layer(dsx_mlp* m, int l, void* dz_cur, void* dz_prev, const OptArgs& o, const StepDev* sp) {
   const int in = m->widths[l], out = m->widths[l + 1];
   const long long ld_cur = ldz(m, l + 1), ld_prev = ldz(m, l);
   // wgrad: dW[out][in] = dz^T x : A = dz (M-major), B = x (N-major)
@@ -500,25 +535,43 @@ dsx_status backward_layer(dsx_mlp* m, int l, void* dz_cur, void* dz_prev, const 
   const long long want = (n / 8 + 255) / 256;
   dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(want, (long long)m->nsm * 8 / m->kl)), m->kl);
   optimizer_kernel<<<grid, 256, 0, m->stream>>>(m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P,
-                                                lo, n, o);
+                                                lo, n, o, sp);
   ++m->launches;
   NN_CUDA(cudaGetLastError());
   return DSX_OK;
 }
 
-dsx_status prepare_input(dsx_mlp* m) {
+// The step's scalars (lr, Adam bias corrections) and batch pointers into the
+// device StepDev, through a pinned ring slot (copied on the compute stream, so
+// a captured graph replayed after it reads this step's values).
+dsx_status write_step(dsx_mlp* m, double lr, long long t) {
   if (!m->x_dev || !m->labels_dev) return nfail(DSX_ERR_STATE, "dsx_mlp_step: no batch set (dsx_mlp_set_batch)");
-  const long long n = (long long)m->kl * m->batch * m->widths[0];
-  if (m->bf16) {
-    x_to_bf16_kernel<<<blocks_for(n, m->nsm), 256, 0, m->stream>>>(m->x_dev, static_cast<__nv_bfloat16*>(m->act[0]), n);
-    ++m->launches;
-  } else if (m->x_dev != m->act[0]) {
-    NN_CUDA(cudaMemcpyAsync(m->act[0], m->x_dev, n * 4, cudaMemcpyDeviceToDevice, m->stream));
-  }
+  const int slot = (int)(m->ring_i++ % m->ring_ev.size());
+  NN_CUDA(cudaEventSynchronize(m->ring_ev[slot]));  // the slot's previous copy has run
+  StepDev& h = m->ring[slot];
+  h.lr = (float)lr;
+  h.bc1 = (float)(1.0 - std::pow((double)m->b1, (double)(t + 1)));
+  h.bc2 = (float)(1.0 - std::pow((double)m->b2, (double)(t + 1)));
+  h.pad = 0.f;
+  h.x = m->x_dev;
+  h.labels = m->labels_dev;
+  NN_CUDA(cudaMemcpyAsync(m->sp, &h, sizeof(StepDev), cudaMemcpyHostToDevice, m->stream));
+  NN_CUDA(cudaEventRecord(m->ring_ev[slot], m->stream));
   return DSX_OK;
 }
 
-dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* mask) {
+dsx_status prepare_input(dsx_mlp* m) {
+  const long long n = (long long)m->kl * m->batch * m->widths[0];
+  if (m->bf16)
+    load_x_kernel<__nv_bfloat16><<<blocks_for(n, m->nsm), 256, 0, m->stream>>>(
+        m->sp, static_cast<__nv_bfloat16*>(m->act[0]), n);
+  else
+    load_x_kernel<float><<<blocks_for(n, m->nsm), 256, 0, m->stream>>>(m->sp, static_cast<float*>(m->act[0]), n);
+  ++m->launches;
+  return DSX_OK;
+}
+
+dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* mask, bool capturing) {
   OptArgs o{};
   o.kind = m->opt;
   o.lr = (float)lr;
@@ -531,9 +584,10 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
   o.bc2 = (float)(1.0 - std::pow((double)m->b2, (double)(t + 1)));
   if (m->instrument) NN_CUDA(cudaEventRecord(m->iev[0], m->stream));
   NN_TRY(prepare_input(m));
-  // FP: layer l waits for last step's average of layer l (in place)
+  // FP: layer l waits for last step's average of layer l (in place); a
+  // replayed graph already joined its averages before it ended
   for (int l = 0; l < m->L; ++l) {
-    if (m->synced_prev[l]) NN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_sync[l], 0));
+    if (m->synced_prev[l] && !capturing) NN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_sync[l], 0));
     NN_TRY(forward_layer(m, l));
   }
   // loss + dlogits
@@ -542,12 +596,12 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
     dim3 grid((m->batch * 32 + 255) / 256, m->kl);
     if (m->bf16)
       softmax_xent_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(
-          m->logits, C, (long long)m->batch * C, m->labels_dev, m->batch, C, static_cast<__nv_bfloat16*>(m->dz[0]), ldz(m, m->L),
-          (long long)m->batch * m->maxw, m->loss_part);
+          m->logits, C, (long long)m->batch * C, nullptr, m->batch, C, static_cast<__nv_bfloat16*>(m->dz[0]), ldz(m, m->L),
+          (long long)m->batch * m->maxw, m->loss_part, m->sp);
     else
-      softmax_xent_kernel<float><<<grid, 256, 0, m->stream>>>(m->logits, C, (long long)m->batch * C, m->labels_dev,
+      softmax_xent_kernel<float><<<grid, 256, 0, m->stream>>>(m->logits, C, (long long)m->batch * C, nullptr,
                                                               m->batch, C, static_cast<float*>(m->dz[0]), ldz(m, m->L),
-                                                              (long long)m->batch * m->maxw, m->loss_part);
+                                                              (long long)m->batch * m->maxw, m->loss_part, m->sp);
     loss_mean_kernel<<<m->kl, 256, 0, m->stream>>>(m->loss_part, m->batch, m->loss);
     m->launches += 2;
   }
@@ -555,6 +609,8 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
   // starts on the side stream as soon as its update is done
   int cur = 0;
   bool any = false;
+  std::vector<cudaEvent_t>& ev_upd = capturing ? m->gev_upd : m->ev_upd;
+  std::vector<cudaEvent_t>& ev_sync = capturing ? m->gev_sync : m->ev_sync;
   // one layer's sync on the side stream (+ the throttled link's busy time)
   auto sync_layer = [&](int l) -> dsx_status {
     if (m->instrument && !any) NN_CUDA(cudaEventRecord(m->ev[7], m->side));
@@ -564,29 +620,30 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
       nn_link_spin_kernel<<<1, 1, 0, m->side>>>((unsigned long long)((m->link_lat + bytes / m->link_bw) * 1e9));
       ++m->launches;
     }
-    NN_CUDA(cudaEventRecord(m->ev_sync[l], m->side));
+    NN_CUDA(cudaEventRecord(ev_sync[l], m->side));
     any = true;
     return DSX_OK;
   };
   for (int l = m->L - 1; l >= 0; --l) {
-    NN_TRY(backward_layer(m, l, m->dz[cur], m->dz[cur ^ 1], o));
+    NN_TRY(backward_layer(m, l, m->dz[cur], m->dz[cur ^ 1], o, m->sp));
     cur ^= 1;
     const bool sync_l = mask[l + 1] != 0 && m->K > 1;
     m->synced_prev[l] = sync_l ? 1 : 0;
     if (sync_l && m->overlap) {
-      NN_CUDA(cudaEventRecord(m->ev_upd[l], m->stream));
-      NN_CUDA(cudaStreamWaitEvent(m->side, m->ev_upd[l], 0));
+      NN_CUDA(cudaEventRecord(ev_upd[l], m->stream));
+      NN_CUDA(cudaStreamWaitEvent(m->side, ev_upd[l], 0));
       NN_TRY(sync_layer(l));
     }
   }
   if (!m->overlap) {
     // ssgd / flsgd: the transfers start after the whole local step
-    NN_CUDA(cudaEventRecord(m->ev_upd[0], m->stream));
-    NN_CUDA(cudaStreamWaitEvent(m->side, m->ev_upd[0], 0));
+    NN_CUDA(cudaEventRecord(ev_upd[0], m->stream));
+    NN_CUDA(cudaStreamWaitEvent(m->side, ev_upd[0], 0));
     for (int l = m->L - 1; l >= 0; --l)
       if (m->synced_prev[l]) NN_TRY(sync_layer(l));
   }
-  m->any_synced = any;
+  m->any_synced = any && !capturing;
+  m->side_used = any;
   if (m->instrument) {
     NN_CUDA(cudaEventRecord(m->iev[1], m->stream));
     NN_CUDA(cudaEventRecord(m->iev[2], m->side));
@@ -694,6 +751,19 @@ dsx_status dsx_mlp_create(const dsx_mlp_desc* d, dsx_mlp** out) {
   for (auto& e : m->ev) cudaEventCreate(&e);
   for (auto& e : m->iev) cudaEventCreate(&e);
   m->synced_prev.assign(m->L, 0);
+  cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&m->ev_drain, cudaEventDisableTiming);
+  m->gev_upd.assign(m->L, nullptr);
+  m->gev_sync.assign(m->L, nullptr);
+  for (int l = 0; l < m->L; ++l) {
+    cudaEventCreateWithFlags(&m->gev_upd[l], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&m->gev_sync[l], cudaEventDisableTiming);
+  }
+  m->ring_ev.assign(64, nullptr);
+  for (auto& e : m->ring_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cudaMalloc(&m->sp, sizeof(StepDev)) != cudaSuccess ||
+      cudaHostAlloc(&m->ring, sizeof(StepDev) * m->ring_ev.size(), cudaHostAllocDefault) != cudaSuccess)
+    return cleanup(nfail(DSX_ERR_CUDA, "step-parameter buffers"));
   const cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cleanup(nfail(DSX_ERR_CUDA, std::string("mlp init: ") + cudaGetErrorString(e)));
   *out = m;
@@ -719,6 +789,17 @@ dsx_status dsx_mlp_destroy(dsx_mlp* m) {
     if (e) cudaEventDestroy(e);
   for (auto e : m->iev)
     if (e) cudaEventDestroy(e);
+  for (auto& kv : m->graph_cache) cudaGraphExecDestroy(kv.second.exec);
+  for (auto e : m->ring_ev)
+    if (e) cudaEventDestroy(e);
+  if (m->ev_join) cudaEventDestroy(m->ev_join);
+  if (m->ev_drain) cudaEventDestroy(m->ev_drain);
+  for (auto e : m->gev_upd)
+    if (e) cudaEventDestroy(e);
+  for (auto e : m->gev_sync)
+    if (e) cudaEventDestroy(e);
+  if (m->sp) cudaFree(m->sp);
+  if (m->ring) cudaFreeHost(m->ring);
   if (m->stream) cudaStreamDestroy(m->stream);
   if (m->side) cudaStreamDestroy(m->side);
   delete m;
@@ -797,7 +878,47 @@ dsx_status dsx_mlp_set_batch(dsx_mlp* m, const float* x, const int32_t* labels, 
 dsx_status dsx_mlp_step(dsx_mlp* m, double lr, long long step_index, const unsigned char* mask) {
   NN_TRY(check(m));
   if (!mask) return nfail(DSX_ERR_ARGUMENT, "null mask");
-  return step_impl(m, lr, step_index, mask);
+  NN_TRY(write_step(m, lr, step_index));
+  // graphs: single rank (NCCL collectives stay eager)
+  if (!m->graphs || m->instrument || m->nranks > 1) return step_impl(m, lr, step_index, mask, false);
+  // one graph per distinct mask (H of them for a partial schedule), captured
+  // on first use; the averages are joined into the compute stream at the end
+  const std::string key(reinterpret_cast<const char*>(mask), (size_t)m->L + 1);
+  dsx_mlp::Graph* g = nullptr;
+  for (auto& kv : m->graph_cache)
+    if (kv.first == key) g = &kv.second;
+  if (!g) {
+    // a capture starts with the eager side-stream work joined in
+    NN_CUDA(cudaEventRecord(m->ev_drain, m->side));
+    NN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_drain, 0));
+    const uint64_t before = m->launches;
+    NN_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+    dsx_status st = step_impl(m, lr, step_index, mask, true);
+    if (st == DSX_OK && m->side_used) {  // (a mask with nothing to average never forks)
+      if (cudaEventRecord(m->ev_join, m->side) != cudaSuccess ||
+          cudaStreamWaitEvent(m->stream, m->ev_join, 0) != cudaSuccess)
+        st = nfail(DSX_ERR_CUDA, "graph capture: joining the sync stream failed");
+    }
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(m->stream, &graph);
+    if (st != DSX_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (ce != cudaSuccess) return nfail(DSX_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    dsx_mlp::Graph ng;
+    const cudaError_t ie = cudaGraphInstantiate(&ng.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return nfail(DSX_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    ng.launches = m->launches - before;
+    m->launches = before;
+    m->graph_cache.emplace_back(key, ng);
+    g = &m->graph_cache.back().second;
+  }
+  NN_CUDA(cudaGraphLaunch(g->exec, m->stream));
+  m->launches += g->launches;
+  for (int l = 0; l < m->L; ++l) m->synced_prev[l] = (mask[l + 1] != 0 && m->K > 1) ? 1 : 0;
+  return DSX_OK;
 }
 
 dsx_status dsx_mlp_last_loss(dsx_mlp* m, float* loss) {
@@ -864,6 +985,7 @@ dsx_status dsx_mlp_profile(dsx_mlp* m, int reps, double* t_fp, double* t_bp, dou
   if (!t_fp || !t_bp || !t_comm) return nfail(DSX_ERR_ARGUMENT, "null out");
   if (!m->x_dev) return nfail(DSX_ERR_STATE, "profile needs a batch (dsx_mlp_set_batch)");
   reps = std::max(1, reps);
+  NN_TRY(write_step(m, 0.0, 0));
   NN_CUDA(cudaStreamSynchronize(m->side));
   NN_CUDA(cudaStreamSynchronize(m->stream));
   // the profile must not change the state: snapshot params / states
@@ -905,16 +1027,16 @@ dsx_status dsx_mlp_profile(dsx_mlp* m, int reps, double* t_fp, double* t_bp, dou
     dim3 grid((m->batch * 32 + 255) / 256, m->kl);
     if (m->bf16)
       softmax_xent_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(
-          m->logits, C, (long long)m->batch * C, m->labels_dev, m->batch, C, static_cast<__nv_bfloat16*>(m->dz[0]), ldz(m, m->L),
-          (long long)m->batch * m->maxw, m->loss_part);
+          m->logits, C, (long long)m->batch * C, nullptr, m->batch, C, static_cast<__nv_bfloat16*>(m->dz[0]), ldz(m, m->L),
+          (long long)m->batch * m->maxw, m->loss_part, m->sp);
     else
-      softmax_xent_kernel<float><<<grid, 256, 0, m->stream>>>(m->logits, C, (long long)m->batch * C, m->labels_dev,
+      softmax_xent_kernel<float><<<grid, 256, 0, m->stream>>>(m->logits, C, (long long)m->batch * C, nullptr,
                                                               m->batch, C, static_cast<float*>(m->dz[0]), ldz(m, m->L),
-                                                              (long long)m->batch * m->maxw, m->loss_part);
+                                                              (long long)m->batch * m->maxw, m->loss_part, m->sp);
     NN_CUDA(cudaEventRecord(e[m->L + 1], m->stream));
     int cur = 0;
     for (int l = m->L - 1; l >= 0; --l) {
-      NN_TRY(backward_layer(m, l, m->dz[cur], m->dz[cur ^ 1], o));
+      NN_TRY(backward_layer(m, l, m->dz[cur], m->dz[cur ^ 1], o, nullptr));
       cur ^= 1;
       NN_CUDA(cudaEventRecord(e[m->L + 1 + (m->L - l)], m->stream));
     }
@@ -996,18 +1118,22 @@ dsx_status dsx_mlp_set_link(dsx_mlp* m, double bandwidth, double latency) {
   if (!(latency >= 0.0)) return nfail(DSX_ERR_ARGUMENT, "latency must be >= 0");
   m->link_bw = bandwidth > 0.0 ? bandwidth : 0.0;
   m->link_lat = latency;
-  return DSX_OK;
+  return dsx_mlp_set_graphs(m, m->graphs ? 1 : 0);
 }
 
 dsx_status dsx_mlp_set_overlap(dsx_mlp* m, int enabled) {
   NN_TRY(check(m));
   m->overlap = enabled != 0;
-  return DSX_OK;
+  return dsx_mlp_set_graphs(m, m->graphs ? 1 : 0);
 }
 
 dsx_status dsx_mlp_set_graphs(dsx_mlp* m, int enabled) {
   NN_TRY(check(m));
-  if (enabled) return nfail(DSX_ERR_STATE, "CUDA-graph replay of the MLP step is not available yet");
+  NN_CUDA(cudaStreamSynchronize(m->stream));
+  NN_CUDA(cudaStreamSynchronize(m->side));
+  for (auto& kv : m->graph_cache) cudaGraphExecDestroy(kv.second.exec);
+  m->graph_cache.clear();  // link / overlap settings are baked into a graph
+  m->graphs = enabled != 0;
   return DSX_OK;
 }
 

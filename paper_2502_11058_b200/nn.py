@@ -150,6 +150,10 @@ class Mlp:
     def set_instrument(self, on: bool) -> None:
         N.call("dsx_mlp_set_instrument", self.h, int(on))
 
+    def set_graphs(self, on: bool) -> None:
+        """Replay the step from one CUDA graph per sync mask (captured on first use)."""
+        N.call("dsx_mlp_set_graphs", self.h, int(on))
+
     def set_link(self, bandwidth: float, latency: float = 0.0) -> None:
         """Throttled sync link (bytes/s, s); bandwidth <= 0 disables."""
         N.call("dsx_mlp_set_link", self.h, bandwidth, latency)

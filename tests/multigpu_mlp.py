@@ -35,6 +35,8 @@ def main():
     uid = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     m.comm_init(uid[0], world, rank)
+    graphs = os.environ.get("DSX_TEST_GRAPHS") == "1"
+    m.set_graphs(graphs)  # NCCL averages captured in the step graphs
     for k in range(kl):
         m.set_params(k, init)
     for r in range(steps):
@@ -46,7 +48,7 @@ def main():
     allp = [None] * world
     dist.all_gather_object(allp, mine)
     ok = True
-    res = {"world": world, "workers_per_rank": kl}
+    res = {"world": world, "workers_per_rank": kl, "graphs": graphs}
     if rank == 0:
         got = [w for part in allp for w in part]
         one = Mlp(widths, bsz, K, device=dev)

@@ -19,13 +19,15 @@ def _gpus():
         return 0
 
 
+@pytest.mark.parametrize("graphs", [False, True])  # graphs: single-rank only, falls back to eager
 @pytest.mark.parametrize("world", [2, 4])
-def test_mlp_multirank_matches_single_gpu(world):
+def test_mlp_multirank_matches_single_gpu(world, graphs):
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world + 10 * graphs),
            os.path.join(REPO, "tests", "multigpu_mlp.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, DSX_TEST_GRAPHS="1" if graphs else "0")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert '"pass": true' in out.stdout

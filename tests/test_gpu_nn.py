@@ -235,3 +235,56 @@ def test_mlp_bf16_tensor_cores_train_and_track_fp32():
     for k in range(K):
         err = np.linalg.norm(got16[k] - orc.w[k]) / np.linalg.norm(orc.w[k])
         assert err < 2e-2, (k, err)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_mlp_cuda_graph_replay_bit_identical(dtype):
+    """The step replayed from one captured CUDA graph per sync mask gives
+    bit-identical parameters, optimizer states and losses to eager launches."""
+    widths, K, H, bsz, seed = [256] * 8 + [10], 4, 4, 64, 2
+    L = len(widths) - 1
+    t = teacher(seed, widths[0], widths[-1])
+    init = init_params(seed, widths)
+    sets = enp(L, H)
+    out = []
+    for graphs in (False, True):
+        m = Mlp(widths, bsz, K, dtype=dtype, optimizer="adam", eps=1e-6)
+        m.set_graphs(graphs)
+        for k in range(K):
+            m.set_params(k, init)
+        losses = []
+        for r in range(3 * H):
+            bs = [batch(seed, k, r, bsz, widths[0], t) for k in range(K)]
+            m.set_batch(np.stack([b[0] for b in bs]), np.stack([b[1] for b in bs]))
+            m.step(1e-3, r, sync_mask("partial", H, r, L, sets))
+            losses.append(m.last_loss().copy())
+        out.append(([m.get_params(k) for k in range(K)], [m.get_state(k) for k in range(K)], losses))
+        m.close()
+    (pa, sa, la), (pb, sb, lb) = out
+    for k in range(K):
+        assert np.array_equal(pa[k], pb[k])
+        assert np.array_equal(sa[k][0], sb[k][0]) and np.array_equal(sa[k][1], sb[k][1])
+    for x, y in zip(la, lb):
+        assert np.array_equal(x, y)
+
+
+def test_mlp_cuda_graph_with_empty_masks():
+    """Steps that average nothing (flsgd between periods, the bench's no-sync
+    window) capture a graph without the sync stream."""
+    widths, K, bsz, seed = [128] * 4 + [10], 2, 32, 3
+    t = teacher(seed, widths[0], widths[-1])
+    m = Mlp(widths, bsz, K, dtype="bf16")
+    m.set_graphs(True)
+    init = init_params(seed, widths)
+    for k in range(K):
+        m.set_params(k, init)
+    none = np.zeros(len(widths), dtype=np.uint8)
+    every = np.ones(len(widths), dtype=np.uint8)
+    for r in range(6):
+        bs = [batch(seed, k, r, bsz, widths[0], t) for k in range(K)]
+        m.set_batch(np.stack([b[0] for b in bs]), np.stack([b[1] for b in bs]))
+        m.step(1e-3, r, every if r % 3 == 2 else none)
+    m.sync()
+    w = [m.get_params(k) for k in range(K)]
+    assert np.array_equal(w[0], w[1])  # the last step averaged everything
+    m.close()
