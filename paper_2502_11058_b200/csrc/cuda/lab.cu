@@ -2005,49 +2005,67 @@ dsx_status after_update(dsx_lab* lab, int mode) {
   return DSX_OK;
 }
 
-// fp32 labs keep the fp64 host interface: whole-state transfers go through a
-// dense fp64 staging buffer in HBM and one narrowing / widening pass on the
-// lab stream (round-to-nearest, the same rounding as a host double->float
-// conversion), instead of a host conversion and one pageable copy per row.
+// fp32 labs: narrowing / widening between fp64 staging and fp32 rows
+// (round-to-nearest, the same rounding as a host double->float conversion).
+// staged element e of a chunk starting at flat index off <-> row (off+e)/dim
 __global__ void narrow_rows_kernel(const double* __restrict__ src, float* __restrict__ dst, long long ld,
-                                   long long dim, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    dst[(i / dim) * ld + i % dim] = __double2float_rn(src[i]);
+                                   long long dim, long long off, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long f = off + i;
+    dst[(f / dim) * ld + f % dim] = __double2float_rn(src[i]);
+  }
 }
 
 __global__ void widen_rows_kernel(const float* __restrict__ src, double* __restrict__ dst, long long ld,
-                                  long long dim, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    dst[i] = (double)src[(i / dim) * ld + i % dim];
+                                  long long dim, long long off, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long f = off + i;
+    dst[i] = (double)src[(f / dim) * ld + f % dim];
+  }
 }
+
+// fp32 labs keep the fp64 host interface: whole-state transfers go through a
+// bounded fp64 staging chunk (at most 256 MB, allocated on first use), one
+// chunk at a time on the lab stream.  Both directions return with the copies
+// complete (the caller may reuse / read its buffer immediately).
+constexpr long long kStageElems = 32ll << 20;
 
 dsx_status ensure_stage64(dsx_lab* lab) {
   if (lab->stage64) return DSX_OK;
-  DSX_CUDA(cudaMalloc(&lab->stage64, 8 * (size_t)lab->dim * lab->kl));
+  const long long n = std::min<long long>(kStageElems, (long long)lab->dim * lab->kl);
+  DSX_CUDA(cudaMalloc(&lab->stage64, 8 * (size_t)n));
   return DSX_OK;
 }
 
-// host fp64 [kl][dim] -> fp32 rows (async on the lab stream)
+// host fp64 [kl][dim] -> fp32 rows
 dsx_status set_all_f32(dsx_lab* lab, const double* w) {
   DSX_TRY(ensure_stage64(lab));
   const long long n = (long long)lab->dim * lab->kl;
-  DSX_CUDA(cudaMemcpyAsync(lab->stage64, w, 8 * (size_t)n, cudaMemcpyHostToDevice, lab->stream));
-  narrow_rows_kernel<<<4 * lab->nsm, 256, 0, lab->stream>>>(lab->stage64, static_cast<float*>(lab->w), lab->ld,
-                                                           lab->dim, n);
-  DSX_CUDA(cudaGetLastError());
-  ++lab->launches;
+  for (long long off = 0; off < n; off += kStageElems) {
+    const long long len = std::min(kStageElems, n - off);
+    DSX_CUDA(cudaMemcpyAsync(lab->stage64, w + off, 8 * (size_t)len, cudaMemcpyHostToDevice, lab->stream));
+    narrow_rows_kernel<<<4 * lab->nsm, 256, 0, lab->stream>>>(lab->stage64, static_cast<float*>(lab->w), lab->ld,
+                                                             lab->dim, off, len);
+    DSX_CUDA(cudaGetLastError());
+    ++lab->launches;
+  }
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
   return DSX_OK;
 }
 
-// fp32 rows -> host fp64 [kl][dim] (async on the lab stream)
+// fp32 rows -> host fp64 [kl][dim]
 dsx_status get_all_f32(dsx_lab* lab, double* w) {
   DSX_TRY(ensure_stage64(lab));
   const long long n = (long long)lab->dim * lab->kl;
-  widen_rows_kernel<<<4 * lab->nsm, 256, 0, lab->stream>>>(static_cast<const float*>(lab->w), lab->stage64, lab->ld,
-                                                          lab->dim, n);
-  DSX_CUDA(cudaGetLastError());
-  ++lab->launches;
-  DSX_CUDA(cudaMemcpyAsync(w, lab->stage64, 8 * (size_t)n, cudaMemcpyDeviceToHost, lab->stream));
+  for (long long off = 0; off < n; off += kStageElems) {
+    const long long len = std::min(kStageElems, n - off);
+    widen_rows_kernel<<<4 * lab->nsm, 256, 0, lab->stream>>>(static_cast<const float*>(lab->w), lab->stage64, lab->ld,
+                                                            lab->dim, off, len);
+    DSX_CUDA(cudaGetLastError());
+    ++lab->launches;
+    DSX_CUDA(cudaMemcpyAsync(w + off, lab->stage64, 8 * (size_t)len, cudaMemcpyDeviceToHost, lab->stream));
+  }
+  DSX_CUDA(cudaStreamSynchronize(lab->stream));
   return DSX_OK;
 }
 
