@@ -6,6 +6,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <string>
 
 #include "device_once.cuh"
@@ -89,6 +91,35 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   return DSX_OK;
 }
 
+// CTA-pair kernel: grid = 2 x clusters (compile-time cluster dims 2x1x1)
+template <int BN, bool AM, bool BM_, typename TOut>
+dsx_status launch_tc2_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+  static std::atomic<unsigned long long> attr{0};
+  auto kern = gemm_tc2_kernel<BN, AM, BM_, TOut>;
+  dsx::once_per_device(attr, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg<BN>::kSmem);
+  });
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long long tiles = (long long)((g.N + BN - 1) / BN) * ((g.M + 2 * kBM - 1) / (2 * kBM)) * g.batch;
+  const int clusters = (int)std::min<long long>(tiles, nsm / 2);
+  kern<<<2 * clusters, 192, Tc2Cfg<BN>::kSmem, s>>>(ta, tb, g);
+  NN_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
+template <int BN>
+dsx_status launch_tc2_bn(bool am, bool bm, bool ob, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
+                         cudaStream_t s) {
+  if (!am && !bm) return ob ? launch_tc2_t<BN, false, false, __nv_bfloat16>(ta, tb, g, s)
+                            : launch_tc2_t<BN, false, false, float>(ta, tb, g, s);
+  if (!am && bm) return ob ? launch_tc2_t<BN, false, true, __nv_bfloat16>(ta, tb, g, s)
+                           : launch_tc2_t<BN, false, true, float>(ta, tb, g, s);
+  if (am && bm && !ob) return launch_tc2_t<BN, true, true, float>(ta, tb, g, s);
+  return nfail(DSX_ERR_ARGUMENT, "gemm: unsupported operand-major / output combination for the tensor-core path");
+}
+
 // the operand-major / output-type combinations the Linear layers use:
 // forward (K,K) -> bf16 activations or fp32 logits, dgrad (K,N) -> bf16,
 // wgrad (M,N) -> fp32 dW
@@ -133,7 +164,28 @@ dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm) {
   }
   const int bn = c.bn ? c.bn : pick_bn(g, nsm);
   if (bn != 64 && bn != 128 && bn != 256) return nfail(DSX_ERR_ARGUMENT, "gemm: bn must be 64, 128 or 256");
+  const bool ob2 = c.out_bf16 && g.epi != kEpiF32;
+  // CTA pairs (M=256 MMAs, half the B traffic per SM) once there are enough
+  // 256-row tiles to give every SM pair one; DSX_GEMM_2SM=0 turns them off,
+  // =1 forces them (tests)
+  static const int two_sm_env = [] {
+    const char* e = std::getenv("DSX_GEMM_2SM");
+    return e ? std::atoi(e) : -1;
+  }();
+  const long long tiles2 = (long long)((g.N + bn - 1) / bn) * ((g.M + 2 * kBM - 1) / (2 * kBM)) * g.batch;
+  // (measured: 256-wide pairs 1290 -> 1431 TFLOP/s at 8192^3; 128-wide pairs
+  // lose to single-CTA 128 tiles, so auto mode pairs only 256-wide tiles)
+  const bool two_sm = bn >= 128 && two_sm_env != 0 &&
+                      (two_sm_env == 1 || (bn == 256 && tiles2 >= nsm / 2));
   CUtensorMap ta, tb;
+  if (two_sm) {
+    if (!c.a_mn) NN_TRY(make_map(&ta, c.A, g.K, g.M, g.batch, c.lda, c.sA, kBM));
+    else NN_TRY(make_map(&ta, c.A, g.M, g.K, g.batch, c.lda, c.sA, kBK));
+    if (!c.b_mn) NN_TRY(make_map(&tb, c.B, g.K, g.N, g.batch, c.ldb, c.sB, bn / 2));
+    else NN_TRY(make_map(&tb, c.B, g.N, g.K, g.batch, c.ldb, c.sB, kBK));
+    return bn == 128 ? launch_tc2_bn<128>(c.a_mn, c.b_mn, ob2, ta, tb, g, s)
+                     : launch_tc2_bn<256>(c.a_mn, c.b_mn, ob2, ta, tb, g, s);
+  }
   if (!c.a_mn) NN_TRY(make_map(&ta, c.A, g.K, g.M, g.batch, c.lda, c.sA, kBM));
   else NN_TRY(make_map(&ta, c.A, g.M, g.K, g.batch, c.lda, c.sA, kBK));
   if (!c.b_mn) NN_TRY(make_map(&tb, c.B, g.K, g.N, g.batch, c.ldb, c.sB, bn));

@@ -182,6 +182,65 @@ __device__ __forceinline__ float epi_value(const GemmArgs& g, int b, int m, int 
   return acc;
 }
 
+// Epilogue of one 32-row x 32-column accumulator chunk: tcgen05.ld (this
+// warp's TMEM lanes), transpose through padded smem, coalesced row stores
+// with the epilogue op applied on the coalesced side.  m0 / n0: the chunk's
+// first row / column in C.
+template <typename TOut>
+__device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, float* st, int lane, int b, int m0,
+                                          int n0, bool ob) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  // row-per-lane -> padded smem (conflict-free: bank = (lane + j) % 32)
+#pragma unroll
+  for (int j = 0; j < 32; ++j) st[lane * 33 + j] = __uint_as_float(r[j]);
+  __syncwarp();
+  if (ob) {
+    // bf16: two rows per instruction, 16 lanes x 2 columns each
+#pragma unroll 4
+    for (int i2 = 0; i2 < 16; ++i2) {
+      const int row = 2 * i2 + (lane >> 4), cc = 2 * (lane & 15);
+      const int m = m0 + row, n = n0 + cc;
+      if (m < g.M && n < g.N) {
+        TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+        const float v0 = epi_value<TOut>(g, b, m, n, st[row * 33 + cc]);
+        if (n + 1 < g.N) {
+          const float v1 = epi_value<TOut>(g, b, m, n + 1, st[row * 33 + cc + 1]);
+          *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
+        } else {
+          *dst = from_f<TOut>(v0);
+        }
+      }
+    }
+  } else {
+    // fp32 (or scalar bf16): one row per instruction, one column per lane
+#pragma unroll 4
+    for (int row = 0; row < 32; ++row) {
+      const int m = m0 + row, n = n0 + lane;
+      if (m < g.M && n < g.N) {
+        const float v = st[row * 33 + lane];
+        if (g.epi == kEpiF32) {
+          float* dst = static_cast<float*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+          *dst = g.accumulate ? *dst + v : v;
+        } else {
+          TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+          *dst = from_f<TOut>(epi_value<TOut>(g, b, m, n, v));
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
 template <int BN, bool A_MN, bool B_MN, typename TOut>
 __global__ void __launch_bounds__(192, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g) {
@@ -302,56 +361,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         if (n0 + c >= g.N) break;
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-              "=r"(r[30]), "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        // row-per-lane -> padded smem (conflict-free: bank = (lane + j) % 32)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) st[lane * 33 + j] = __uint_as_float(r[j]);
-        __syncwarp();
-        if (ob) {
-          // bf16: two rows per instruction, 16 lanes x 2 columns each
-#pragma unroll 4
-          for (int i2 = 0; i2 < 16; ++i2) {
-            const int row = 2 * i2 + (lane >> 4), cc = 2 * (lane & 15);
-            const int m = m0 + row, n = n0 + c + cc;
-            if (m < g.M && n < g.N) {
-              TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
-              const float v0 = epi_value<TOut>(g, b, m, n, st[row * 33 + cc]);
-              if (n + 1 < g.N) {
-                const float v1 = epi_value<TOut>(g, b, m, n + 1, st[row * 33 + cc + 1]);
-                *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
-              } else {
-                *dst = from_f<TOut>(v0);
-              }
-            }
-          }
-        } else {
-          // fp32 (or scalar bf16): one row per instruction, one column per lane
-#pragma unroll 4
-          for (int row = 0; row < 32; ++row) {
-            const int m = m0 + row, n = n0 + c + lane;
-            if (m < g.M && n < g.N) {
-              const float v = st[row * 33 + lane];
-              if (g.epi == kEpiF32) {
-                float* dst = static_cast<float*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
-                *dst = g.accumulate ? *dst + v : v;
-              } else {
-                TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
-                *dst = from_f<TOut>(epi_value<TOut>(g, b, m, n, v));
-              }
-            }
-          }
-        }
+        epi_chunk<TOut>(g, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob);
         __syncwarp();
       }
       // this warp's TMEM reads of buffer `acc` are complete (wait::ld above)
@@ -364,6 +374,215 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 GEMM on CTA pairs (cta_group::2): a cluster of 2 CTAs on paired
+// SMs computes a 256 x BN tile with M=256 MMAs issued by the leader CTA.
+// Each CTA stages its own 128 rows of A and BN/2 rows of B (TMA
+// .cta_group::2: both CTAs' bytes complete on the leader's full barrier), so
+// per SM the B traffic and smem footprint halve; each CTA's TMEM holds its
+// 128 rows x BN accumulator (double-buffered) and its 4 epilogue warps drain
+// it.  MMA completion is multicast to both CTAs' barriers; the peer's
+// epilogue releases the leader's tempty barrier remotely (mapa).
+// ---------------------------------------------------------------------------
+template <int BN>
+struct Tc2Cfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = (BN / 2) * kBK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStages = BN >= 256 ? 6 : 8;
+  static constexpr int kEpiBytes = 4 * 32 * 33 * 4;
+  static constexpr int kSmem = kStages * kStage + kEpiBytes + 1024 + 256;
+  static constexpr int kTmemCols = 2 * BN;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// both CTAs' transaction bytes land on the leader's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(map), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc2_mma(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          su32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+// bounded wait (a protocol error traps instead of hanging the GPU)
+__device__ __forceinline__ void nn_mbar_wait_bounded(uint64_t* b, unsigned parity) {
+  unsigned ok = 0;
+  unsigned long long t0 = 0;
+  for (int it = 0;; ++it) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (it == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if ((it & 1023) == 1023) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) __trap();  // 10 s
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, typename TOut>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g) {
+  using Cfg = Tc2Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* epi_smem = reinterpret_cast<float*>(smem + Cfg::kStages * Cfg::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage + Cfg::kEpiBytes);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;  // [2]
+  uint64_t* tempty = tfull + 2;            // [2] (the leader's counts both CTAs' epilogues)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nk = (g.K + kBK - 1) / kBK;
+  const int mt = (g.M + 2 * kBM - 1) / (2 * kBM), ntl = (g.N + BN - 1) / BN;
+  const int tiles = mt * ntl * g.batch;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&ta) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tb) : "memory");
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      nn_mbar_init(&full[s], 1);
+      nn_mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      nn_mbar_init(&tfull[a], 1);
+      nn_mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(Cfg::kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs: each stages its half)
+      int it = 0;
+      for (int tile = cid; tile < tiles; tile += ncl) {
+        const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+        const int m0 = mb * 2 * kBM + (int)rank * kBM, n0 = nb * BN + (int)rank * (BN / 2);
+        for (int k = 0; k < nk; ++k, ++it) {
+          const int s = it % Cfg::kStages;
+          const unsigned ph = (unsigned)(it / Cfg::kStages) & 1u;
+          nn_mbar_wait_bounded(&empty[s], ph ^ 1u);
+          uint8_t* sa = smem + s * Cfg::kStage;
+          uint8_t* sb = sa + Cfg::kABytes;
+          if (leader) nn_mbar_expect_tx(&full[s], 2 * Cfg::kStage);
+          if constexpr (!A_MN) {
+            tma_load_3d_2sm(sa, &ta, &full[s], k * kBK, m0, b);
+          } else {
+#pragma unroll
+            for (int i = 0; i < kBM / 64; ++i)
+              tma_load_3d_2sm(sa + i * 64 * kBK * 2, &ta, &full[s], m0 + 64 * i, k * kBK, b);
+          }
+          if constexpr (!B_MN) {
+            tma_load_3d_2sm(sb, &tb, &full[s], k * kBK, n0, b);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 2 / 64; ++i)
+              tma_load_3d_2sm(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, k * kBK, b);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // MMA issuer: the leader CTA only
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                             ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)((2 * kBM) >> 4) << 24);
+      int it = 0, tc = 0;
+      for (int tile = cid; tile < tiles; tile += ncl, ++tc) {
+        const int acc = tc & 1;
+        nn_mbar_wait_bounded(&tempty[acc], ((unsigned)(tc >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int k = 0; k < nk; ++k, ++it) {
+          const int s = it % Cfg::kStages;
+          nn_mbar_wait_bounded(&full[s], (unsigned)(it / Cfg::kStages) & 1u);
+          tc_fence_after();
+          const unsigned sa = su32(smem + s * Cfg::kStage);
+          const unsigned sb = sa + Cfg::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
+            const uint64_t ad = A_MN ? smem_desc(sa + kk * kUmmaK * 128, kBK * 128, 1024)
+                                     : smem_desc(sa + kk * kUmmaK * 2, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(sb + kk * kUmmaK * 128, kBK * 128, 1024)
+                                     : smem_desc(sb + kk * kUmmaK * 2, 16, 1024);
+            tc2_mma(d, ad, bd, idesc, (k | kk) != 0 ? 1u : 0u);
+          }
+          tc2_commit_both(&empty[s]);  // frees the stage in both CTAs
+        }
+        tc2_commit_both(&tfull[acc]);  // both CTAs' accumulator halves ready
+      }
+    }
+  } else {  // epilogue warps 2..5 of both CTAs
+    const int q = warp & 3;
+    float* st = epi_smem + (warp - 2) * 32 * 33;
+    const bool ob = sizeof(TOut) == 2 && g.epi != kEpiF32 && (g.ldc & 1) == 0;
+    uint32_t tempty_leader[2];
+    for (int a = 0; a < 2; ++a)
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(tempty_leader[a]) : "r"(su32(&tempty[a])));
+    int tc = 0;
+    for (int tile = cid; tile < tiles; tile += ncl, ++tc) {
+      const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+      const int m0 = mb * 2 * kBM + (int)rank * kBM + 32 * q, n0 = nb * BN;
+      const int acc = tc & 1;
+      nn_mbar_wait_bounded(&tfull[acc], (unsigned)(tc >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        if (n0 + c >= g.N) break;
+        epi_chunk<TOut>(g, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob);
+      }
+      tc_fence_before();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader[acc])
+                     : "memory");
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols) : "memory");
   }
 }
 
