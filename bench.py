@@ -54,6 +54,14 @@ CONFIGS = {
             "widths": [1024] * 8 + [10], "batch": 256,
             "workload": "configs[0] MLP: 8 Linear layers (1024 wide -> 10 classes, 7,357,450 "
                         "params/worker), batch 256/worker, 4 workers, H=4, SGD momentum"},
+    # BASELINE configs[3] at its parameter scale as an NN: a Llama-1B-shaped
+    # stack (d_model 2048, ffn 5632: 48 up/down blocks + a 32000-class head,
+    # 1.17 B parameters per worker, 97 registered layers), batch 4096
+    # tokens/worker, partial local Adam
+    "llama_mlp": {"profile": MLP_PROFILE, "workers": 4, "period": 4, "parity_steps": 0, "nn": True,
+                  "widths": [2048] + [5632, 2048] * 48 + [32000], "batch": 4096, "optimizer": "adam",
+                  "workload": "configs[3]-scale MLP stack: 97 Linear layers (2048 <-> 5632, 32000-class head, "
+                              "1.17e9 params/worker), batch 4096/worker, 4 workers, H=4, local Adam"},
     # the same step at a compute-bound size (tensor-pipe roofline)
     "mlp_wide": {"profile": MLP_PROFILE, "workers": 4, "period": 4, "parity_steps": 0, "nn": True,
                  "widths": [4096] * 8 + [16], "batch": 2048,
@@ -75,7 +83,7 @@ def parse_args(argv=None):
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--dtype", default=None, choices=["f64", "f32", "bf16"],
                     help="lab: f64 (default) / f32; mlp: bf16 (default, tcgen05) / f32 (SIMT)")
-    ap.add_argument("--optimizer", default="momentum", choices=["sgd", "momentum", "adam"])
+    ap.add_argument("--optimizer", default=None, choices=["sgd", "momentum", "adam"])
     ap.add_argument("--lr", type=float, default=None)
     ap.add_argument("--profile", default=None)
     ap.add_argument("--sync-algo", default="pairwise", choices=["pairwise", "nccl_avg"])
@@ -104,6 +112,7 @@ def parse_args(argv=None):
         ap.error("the MLP computes in bf16 (tensor cores) or f32")
     if not a.nn and a.dtype == "bf16":
         ap.error("the quadratic lab computes in f64 or f32")
+    a.optimizer = a.optimizer or c.get("optimizer", "momentum")
     if a.lr is None:
         a.lr = {"sgd": 0.05, "momentum": 0.01, "adam": 1e-3}[a.optimizer]
     return a
@@ -684,17 +693,9 @@ def mlp_flops_per_worker(widths, batch):
 
 
 def mlp_data_pool(args, kl, rank, npool):
-    import numpy as np
-
-    from paper_2502_11058_b200.nn import batch as make_batch
-    from paper_2502_11058_b200.nn import teacher
-    t = teacher(args.seed, args.widths[0], args.widths[-1])
-    xs = np.empty((npool, kl, args.batch, args.widths[0]), dtype=np.float32)
-    ys = np.empty((npool, kl, args.batch), dtype=np.int32)
-    for p in range(npool):
-        for k in range(kl):
-            xs[p, k], ys[p, k] = make_batch(args.seed, rank * kl + k, p, args.batch, args.widths[0], t)
-    return xs, ys
+    from paper_2502_11058_b200.nn import batch_pool
+    return batch_pool(args.seed, [rank * kl + k for k in range(kl)], npool, args.batch, args.widths[0],
+                      args.widths[-1], int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def mlp_cpu_oracle(args, K, steps, masks):

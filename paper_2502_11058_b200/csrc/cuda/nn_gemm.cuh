@@ -182,13 +182,41 @@ __device__ __forceinline__ float epi_value(const GemmArgs& g, int b, int m, int 
   return acc;
 }
 
+// Tile order: within a batch entry, groups of 8 M-tiles walk the N-tiles
+// column by column, so the CTAs running at once share B panels through L2
+// (the 32000-class head read its 131 MB weight 16x from DRAM in row order).
+__device__ __forceinline__ void tile_coords(int tile, int mt, int ntl, int* b, int* mb, int* nb) {
+  constexpr int G = 8;
+  const int per = mt * ntl;
+  *b = tile / per;
+  const int t = tile % per;
+  const int group = t / (G * ntl), first = group * G;
+  const int gsz = min(G, mt - first);
+  const int r = t % (G * ntl);
+  *mb = first + r % gsz;
+  *nb = r / gsz;
+}
+
+// ReLU' mask words of one 32x32 bf16 chunk, the layout epi_chunk's bf16 path
+// uses (lane: rows 2*i2 + lane/16, columns n, n+1), one 4-B load per row.
+template <typename TOut>
+__device__ __forceinline__ void load_mask_words(const GemmArgs& g, int b, int m0, int n, int lane, uint32_t w[16]) {
+  const bool ok = n + 1 < g.N;
+  const TOut* mp = static_cast<const TOut*>(g.mask) + (long long)b * g.strideMask + n;
+#pragma unroll
+  for (int i2 = 0; i2 < 16; ++i2) {
+    const int m = m0 + 2 * i2 + (lane >> 4);
+    w[i2] = (ok && m < g.M) ? *reinterpret_cast<const uint32_t*>(mp + (long long)m * g.ldmask) : 0u;
+  }
+}
+
 // Epilogue of one 32-row x 32-column accumulator chunk: tcgen05.ld (this
 // warp's TMEM lanes), transpose through padded smem, coalesced row stores
 // with the epilogue op applied on the coalesced side.  m0 / n0: the chunk's
 // first row / column in C.
 template <typename TOut>
 __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, float* st, int lane, int b, int m0,
-                                          int n0, bool ob) {
+                                          int n0, bool ob, const uint32_t* mwords) {
   uint32_t r[32];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
@@ -204,36 +232,97 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
 #pragma unroll
   for (int j = 0; j < 32; ++j) st[lane * 33 + j] = __uint_as_float(r[j]);
   __syncwarp();
+  // Epilogue operands are fetched before any store, all loads of the chunk in
+  // flight at once (stores to C could alias them, so the compiler would
+  // otherwise serialise one global-latency round trip per row): bias once
+  // per column, the ReLU' mask of every row of the chunk.
   if (ob) {
     // bf16: two rows per instruction, 16 lanes x 2 columns each
-#pragma unroll 4
-    for (int i2 = 0; i2 < 16; ++i2) {
-      const int row = 2 * i2 + (lane >> 4), cc = 2 * (lane & 15);
-      const int m = m0 + row, n = n0 + cc;
-      if (m < g.M && n < g.N) {
-        TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
-        const float v0 = epi_value<TOut>(g, b, m, n, st[row * 33 + cc]);
-        if (n + 1 < g.N) {
-          const float v1 = epi_value<TOut>(g, b, m, n + 1, st[row * 33 + cc + 1]);
-          *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
-        } else {
-          *dst = from_f<TOut>(v0);
+    const int cc = 2 * (lane & 15), n = n0 + cc;
+    const bool n_ok = n < g.N, n1_ok = n + 1 < g.N;
+    float b0 = 0.f, b1 = 0.f;
+    if (g.epi == kEpiBiasAct && g.bias) {
+      const float* bp = g.bias + (long long)b * g.strideBias + n;
+      if (n_ok) b0 = bp[0];
+      if (n1_ok) b1 = bp[1];
+    }
+    float mk0[16], mk1[16];
+    if (g.epi == kEpiDRelu) {
+      if (mwords && n1_ok) {  // prefetched by the caller one chunk ahead
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          mk0[i2] = __uint_as_float(mwords[i2] << 16);
+          mk1[i2] = __uint_as_float(mwords[i2] & 0xFFFF0000u);
         }
+      } else {
+        const TOut* mp = static_cast<const TOut*>(g.mask) + (long long)b * g.strideMask + n;
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          const int m = m0 + 2 * i2 + (lane >> 4);
+          mk0[i2] = (m < g.M && n_ok) ? to_f<TOut>(mp[(long long)m * g.ldmask]) : 0.f;
+          mk1[i2] = (m < g.M && n1_ok) ? to_f<TOut>(mp[(long long)m * g.ldmask + 1]) : 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int i2 = 0; i2 < 16; ++i2) {
+      const int row = 2 * i2 + (lane >> 4);
+      const int m = m0 + row;
+      if (m < g.M && n_ok) {
+        TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+        float v0 = st[row * 33 + cc], v1 = st[row * 33 + cc + 1];
+        if (g.epi == kEpiBiasAct) {
+          v0 += b0;
+          v1 += b1;
+          if (g.relu) {
+            v0 = fmaxf(v0, 0.f);
+            v1 = fmaxf(v1, 0.f);
+          }
+        } else if (g.epi == kEpiDRelu) {
+          v0 = mk0[i2] > 0.f ? v0 : 0.f;
+          v1 = mk1[i2] > 0.f ? v1 : 0.f;
+        }
+        if (n1_ok) *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
+        else *dst = from_f<TOut>(v0);
       }
     }
   } else {
     // fp32 (or scalar bf16): one row per instruction, one column per lane
-#pragma unroll 4
-    for (int row = 0; row < 32; ++row) {
-      const int m = m0 + row, n = n0 + lane;
-      if (m < g.M && n < g.N) {
-        const float v = st[row * 33 + lane];
-        if (g.epi == kEpiF32) {
-          float* dst = static_cast<float*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
-          *dst = g.accumulate ? *dst + v : v;
-        } else {
-          TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
-          *dst = from_f<TOut>(epi_value<TOut>(g, b, m, n, v));
+    const int n = n0 + lane;
+    const bool n_ok = n < g.N;
+    const float bv = (g.epi == kEpiBiasAct && g.bias && n_ok) ? g.bias[(long long)b * g.strideBias + n] : 0.f;
+#pragma unroll
+    for (int r0 = 0; r0 < 32; r0 += 8) {
+      float mk[8];
+      if (g.epi == kEpiDRelu) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int m = m0 + r0 + u;
+          mk[u] = (m < g.M && n_ok)
+                      ? to_f<TOut>(static_cast<const TOut*>(g.mask)[(long long)b * g.strideMask +
+                                                                   (long long)m * g.ldmask + n])
+                      : 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int row = r0 + u, m = m0 + row;
+        if (m < g.M && n_ok) {
+          const float v = st[row * 33 + lane];
+          if (g.epi == kEpiF32) {
+            float* dst = static_cast<float*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+            *dst = g.accumulate ? *dst + v : v;
+          } else {
+            float o = v;
+            if (g.epi == kEpiBiasAct) {
+              o += bv;
+              if (g.relu) o = fmaxf(o, 0.f);
+            } else if (g.epi == kEpiDRelu) {
+              o = mk[u] > 0.f ? o : 0.f;
+            }
+            TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
+            *dst = from_f<TOut>(o);
+          }
         }
       }
     }
@@ -286,7 +375,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
     if (lane == 0) {  // TMA producer
       int it = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+        int b, mb, nb;
+        tile_coords(tile, mt, ntl, &b, &mb, &nb);
         const int m0 = mb * kBM, n0 = nb * BN;
         for (int k = 0; k < nk; ++k, ++it) {
           const int s = it % Cfg::kStages;
@@ -353,15 +443,26 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
     const bool ob = sizeof(TOut) == 2 && g.epi != kEpiF32 && (g.ldc & 1) == 0;
     int tc = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tc) {
-      const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+      int b, mb, nb;
+      tile_coords(tile, mt, ntl, &b, &mb, &nb);
       const int m0 = mb * kBM + 32 * q, n0 = nb * BN;
       const int acc = tc & 1;
       nn_mbar_wait(&tfull[acc], (unsigned)(tc >> 1) & 1u);
       tc_fence_after();
+      // bf16 dgrad: the ReLU' mask words of chunk c+1 load while chunk c drains
+      const bool pre = ob && g.epi == kEpiDRelu && (g.ldmask & 1) == 0;
+      uint32_t mw_cur[16], mw_nxt[16];
+      if (pre) load_mask_words<TOut>(g, b, m0, n0 + 2 * (lane & 15), lane, mw_cur);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         if (n0 + c >= g.N) break;
-        epi_chunk<TOut>(g, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob);
+        const bool more = pre && c + 32 < BN && n0 + c + 32 < g.N;
+        if (more) load_mask_words<TOut>(g, b, m0, n0 + c + 32 + 2 * (lane & 15), lane, mw_nxt);
+        epi_chunk<TOut>(g, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob,
+                        pre ? mw_cur : nullptr);
+        if (more)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) mw_cur[i] = mw_nxt[i];
         __syncwarp();
       }
       // this warp's TMEM reads of buffer `acc` are complete (wait::ld above)
@@ -497,7 +598,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ 
     if (lane == 0) {  // TMA producer (both CTAs: each stages its half)
       int it = 0;
       for (int tile = cid; tile < tiles; tile += ncl) {
-        const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+        int b, mb, nb;
+        tile_coords(tile, mt, ntl, &b, &mb, &nb);
         const int m0 = mb * 2 * kBM + (int)rank * kBM, n0 = nb * BN + (int)rank * (BN / 2);
         for (int k = 0; k < nk; ++k, ++it) {
           const int s = it % Cfg::kStages;
@@ -562,15 +664,26 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ 
       asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(tempty_leader[a]) : "r"(su32(&tempty[a])));
     int tc = 0;
     for (int tile = cid; tile < tiles; tile += ncl, ++tc) {
-      const int nb = tile % ntl, mb = (tile / ntl) % mt, b = tile / (ntl * mt);
+      int b, mb, nb;
+      tile_coords(tile, mt, ntl, &b, &mb, &nb);
       const int m0 = mb * 2 * kBM + (int)rank * kBM + 32 * q, n0 = nb * BN;
       const int acc = tc & 1;
       nn_mbar_wait_bounded(&tfull[acc], (unsigned)(tc >> 1) & 1u);
       tc_fence_after();
+      // bf16 dgrad: the ReLU' mask words of chunk c+1 load while chunk c drains
+      const bool pre = ob && g.epi == kEpiDRelu && (g.ldmask & 1) == 0;
+      uint32_t mw_cur[16], mw_nxt[16];
+      if (pre) load_mask_words<TOut>(g, b, m0, n0 + 2 * (lane & 15), lane, mw_cur);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         if (n0 + c >= g.N) break;
-        epi_chunk<TOut>(g, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob);
+        const bool more = pre && c + 32 < BN && n0 + c + 32 < g.N;
+        if (more) load_mask_words<TOut>(g, b, m0, n0 + c + 32 + 2 * (lane & 15), lane, mw_nxt);
+        epi_chunk<TOut>(g, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob,
+                        pre ? mw_cur : nullptr);
+        if (more)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) mw_cur[i] = mw_nxt[i];
       }
       tc_fence_before();
       if (lane == 0)

@@ -160,7 +160,7 @@ def run_mlp(widths, batch_size=256, workers=4, period=4, optimizer="adam", lr=1e
     Ethernet).  Returns {mode: measured_s, predicted_s} and S1 / S2."""
     import torch
 
-    from .nn import Mlp, batch, init_params, layer_sizes, teacher
+    from .nn import Mlp, batch_pool, init_params, layer_sizes
     L = len(widths) - 1
     iters = iters or 4 * period
     m = Mlp(widths, batch_size, workers, dtype=dtype, optimizer=optimizer,
@@ -168,10 +168,9 @@ def run_mlp(widths, batch_size=256, workers=4, period=4, optimizer="adam", lr=1e
     init = init_params(seed, widths)
     for k in range(workers):
         m.set_params(k, init)
-    t = teacher(seed, widths[0], widths[-1])
-    xs, ys = zip(*[zip(*[batch(seed, k, p, batch_size, widths[0], t) for k in range(workers)]) for p in range(4)])
-    dx = torch.from_numpy(np.stack([np.stack(x) for x in xs])).to(f"cuda:{device}")
-    dy = torch.from_numpy(np.stack([np.stack(y) for y in ys])).to(f"cuda:{device}")
+    xs, ys = batch_pool(seed, list(range(workers)), 4, batch_size, widths[0], widths[-1], device)
+    dx = torch.from_numpy(xs).to(f"cuda:{device}")
+    dy = torch.from_numpy(ys).to(f"cuda:{device}")
     m.set_batch_ptr(dx[0].data_ptr(), dy[0].data_ptr(), True)
     t_fp, t_bp, _ = m.profile(reps=reps)
     sizes = layer_sizes(widths)

@@ -34,6 +34,29 @@ def batch(seed: int, worker: int, step: int, size: int, in_dim: int, t: np.ndarr
     return x, y
 
 
+def batch_pool(seed: int, workers, npool: int, size: int, in_dim: int, classes: int, device: int = 0):
+    """Device-resident batches [npool][len(workers)][size][in] (fp32) and
+    labels [npool][len(workers)][size] (int32) for the given global worker
+    ids, batch p of worker k = batch(seed, k, p).  Heads wider than 1024
+    classes take the teacher's argmax on the GPU in fp32 (the float64 host
+    argmax would take minutes; those configs have no CPU parity run)."""
+    import torch
+    dev = torch.device(f"cuda:{device}")
+    t = teacher(seed, in_dim, classes)
+    xs = np.empty((npool, len(workers), size, in_dim), dtype=np.float32)
+    ys = np.empty((npool, len(workers), size), dtype=np.int32)
+    tt = torch.from_numpy(t).to(dev) if classes > 1024 else None
+    for p in range(npool):
+        for j, k in enumerate(workers):
+            if tt is None:
+                xs[p, j], ys[p, j] = batch(seed, k, p, size, in_dim, t)
+            else:
+                rng = np.random.default_rng([seed, k, p])
+                xs[p, j] = rng.standard_normal((size, in_dim), dtype=np.float32)
+                ys[p, j] = torch.argmax(torch.from_numpy(xs[p, j]).to(dev) @ tt.T, dim=1).int().cpu().numpy()
+    return xs, ys
+
+
 def init_params(seed: int, widths) -> np.ndarray:
     """Packed per-worker parameters (layer l: W[out][in] then b[out]): He
     initialisation W ~ N(0, 2/in) (keeps the 8-layer ReLU stack's signal

@@ -10,7 +10,8 @@ from paper_2502_11058_b200 import modes  # noqa: E402
 out = {}
 for name, widths, bsz, ratio in [("mlp_configs0_adam", [1024] * 8 + [10], 256, 2.0),
                                  ("mlp_configs0_adam_ratio1", [1024] * 8 + [10], 256, 1.0),
-                                 ("mlp_wide_adam", [4096] * 8 + [16], 2048, 2.0)]:
+                                 ("mlp_wide_adam", [4096] * 8 + [16], 2048, 2.0)] + (
+        [("llama_scale_mlp_adam", [2048] + [5632, 2048] * 48 + [32000], 4096, 2.0)] if "--llama" in sys.argv else []):
     out[name] = modes.run_mlp(widths, batch_size=bsz, workers=4, period=4, optimizer="adam", lr=1e-3,
                               comm_ratio=ratio)
     r = out[name]
