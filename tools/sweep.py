@@ -51,6 +51,7 @@ def run_mode(lab, masks_of, H, steps, dist_):
         lab.step(bench.learning_rate(r, H), masks_of(r))
         r += 1
     lab.sync()
+    lab.set_noise_horizon(steps)  # exact window: the engine generates only these steps' noise
     dist_.barrier()
     lab.record(0)
     for _ in range(steps):
@@ -59,6 +60,7 @@ def run_mode(lab, masks_of, H, steps, dist_):
     lab.record(1)
     ms = lab.elapsed_ms(0, 1)
     lab.sync()
+    lab.set_noise_horizon(-1)
     lab.set_pipeline(False)
     lab.set_instrument(True)
     per = []
