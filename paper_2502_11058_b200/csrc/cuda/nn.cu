@@ -880,14 +880,9 @@ dsx_status dsx_mlp_step(dsx_mlp* m, double lr, long long step_index, const unsig
   NN_TRY(check(m));
   if (!mask) return nfail(DSX_ERR_ARGUMENT, "null mask");
   NN_TRY(write_step(m, lr, step_index));
-  // graphs: single rank by default; DSX_MLP_GRAPHS_NCCL=1 also captures the
-  // NCCL averages of a multi-rank step
-  static const bool nccl_graphs = [] {
-    const char* e = std::getenv("DSX_MLP_GRAPHS_NCCL");
-    return e && e[0] == '1';
-  }();
-  if (!m->graphs || m->instrument || (m->nranks > 1 && !nccl_graphs))
-    return step_impl(m, lr, step_index, mask, false);
+  // graphs: single rank (capturing the NCCL averages of a multi-rank step
+  // hung at 2 GPUs, so those steps stay eager)
+  if (!m->graphs || m->instrument || m->nranks > 1) return step_impl(m, lr, step_index, mask, false);
   // one graph per distinct mask (H of them for a partial schedule), captured
   // on first use; the averages are joined into the compute stream at the end
   const std::string key(reinterpret_cast<const char*>(mask), (size_t)m->L + 1);
