@@ -137,6 +137,49 @@ dsx_status dsx_mlp_set_overlap(dsx_mlp* m, int enabled);
  * step stays eager (NCCL).  0 disables (default). */
 dsx_status dsx_mlp_set_graphs(dsx_mlp* m, int enabled);
 
+/* ---- conv stack: BASELINE configs[1] (ResNet-18 shape) as a network ----
+ * CIFAR ResNet-18 geometry without normalisation layers: 3x3 stem (in_channels
+ * zero-padded to 8) -> 4 stages x 2 basic blocks of widths width<<s (stride 2
+ * and a 1x1 projection shortcut entering stages 1-3) -> global average pool ->
+ * linear head.  Registered layers (1-based, forward order): the stem, per
+ * block conv a, conv b, [shortcut], then the head (21 for ResNet-18); layer
+ * l's packed parameters are W_l [Cout][kh][kw][Cin] then b_l [Cout].  BP
+ * runs a block's shortcut, b, a; each layer's optimizer runs right after its
+ * gradients and a scheduled layer's average starts on the side stream — the
+ * same step semantics as dsx_mlp_step. */
+typedef struct dsx_cnn dsx_cnn;
+typedef struct dsx_cnn_desc {
+  int device;
+  int dtype;                 /* DSX_F32 (SIMT, parity) | DSX_BF16 (tcgen05) */
+  int workers_total, worker_begin, workers_local;  /* workers_local in {1,2,4,8} */
+  int width;                 /* stem width (ResNet-18: 64), multiple of 8 */
+  int image;                 /* square input side (32), multiple of 8 */
+  int in_channels;           /* 1..8 (3) */
+  int classes;               /* head outputs (10) */
+  int batch;                 /* per-worker batch */
+  int optimizer;             /* DSX_OPT_* */
+  double momentum, beta1, beta2, eps, weight_decay;
+} dsx_cnn_desc;
+
+dsx_status dsx_cnn_create(const dsx_cnn_desc* desc, dsx_cnn** out);
+dsx_status dsx_cnn_destroy(dsx_cnn* m);
+/* layers, packed total and offsets [layers+1], fan-in per layer (k*k*Cin) */
+dsx_status dsx_cnn_param_layout(dsx_cnn* m, int* layers, uint64_t* total, uint64_t* offsets, int* fan_in);
+dsx_status dsx_cnn_set_params(dsx_cnn* m, int local, const float* packed);
+dsx_status dsx_cnn_get_params(dsx_cnn* m, int local, float* packed);
+/* x: fp32 NHWC [workers_local][batch][image][image][in_channels], labels
+ * int32 [workers_local][batch]; on_device as in dsx_mlp_set_batch */
+dsx_status dsx_cnn_set_batch(dsx_cnn* m, const float* x, const int32_t* labels, int on_device);
+dsx_status dsx_cnn_step(dsx_cnn* m, double lr, long long step_index, const unsigned char* mask);
+dsx_status dsx_cnn_last_loss(dsx_cnn* m, float* loss /* [workers_local] */);
+dsx_status dsx_cnn_sync(dsx_cnn* m);
+dsx_status dsx_cnn_comm_init(dsx_cnn* m, const unsigned char id[128], int nranks, int rank);
+dsx_status dsx_cnn_set_instrument(dsx_cnn* m, int enabled);
+dsx_status dsx_cnn_last_step_times(dsx_cnn* m, float* out4);
+dsx_status dsx_cnn_event_record(dsx_cnn* m, int slot);
+dsx_status dsx_cnn_event_elapsed(dsx_cnn* m, int from_slot, int to_slot, float* ms);
+dsx_status dsx_cnn_launch_count(dsx_cnn* m, uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,15 @@ class MlpDescC(C.Structure):
     ]
 
 
+class CnnDescC(C.Structure):
+    _fields_ = [
+        ("device", C.c_int), ("dtype", C.c_int), ("workers_total", C.c_int), ("worker_begin", C.c_int),
+        ("workers_local", C.c_int), ("width", C.c_int), ("image", C.c_int), ("in_channels", C.c_int),
+        ("classes", C.c_int), ("batch", C.c_int), ("optimizer", C.c_int), ("momentum", C.c_double),
+        ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double),
+    ]
+
+
 _dsx = None
 
 _SIGS = {
@@ -138,6 +147,22 @@ _NN_SIGS = {
     "dsx_mlp_set_graphs": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_mlp_set_link": ([C.c_void_p, C.c_double, C.c_double], C.c_int),
     "dsx_mlp_set_overlap": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_cnn_create": ([C.POINTER(CnnDescC), C.POINTER(C.c_void_p)], C.c_int),
+    "dsx_cnn_destroy": ([C.c_void_p], C.c_int),
+    "dsx_cnn_param_layout": ([C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p],
+                             C.c_int),
+    "dsx_cnn_set_params": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "dsx_cnn_get_params": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "dsx_cnn_set_batch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int], C.c_int),
+    "dsx_cnn_step": ([C.c_void_p, C.c_double, C.c_longlong, C.c_void_p], C.c_int),
+    "dsx_cnn_last_loss": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_cnn_sync": ([C.c_void_p], C.c_int),
+    "dsx_cnn_comm_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
+    "dsx_cnn_set_instrument": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_cnn_last_step_times": ([C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_cnn_event_record": ([C.c_void_p, C.c_int], C.c_int),
+    "dsx_cnn_event_elapsed": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
+    "dsx_cnn_launch_count": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
 }
 _SIGS.update(_NN_SIGS)
 
