@@ -180,18 +180,35 @@ __global__ void col2im_kernel(const T* __restrict__ dcol, T* __restrict__ dx, in
   }
 }
 
-// y = relu(a + s) (the block output), all local workers (flat)
+// y = relu(a + s) (the block output); n elements per worker (multiple of
+// 8), worker blockIdx.y at stride sx
 template <typename T>
-__global__ void add_relu_kernel(const T* __restrict__ a, const T* __restrict__ s, T* __restrict__ y, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    y[i] = from_f<T>(fmaxf(to_f<T>(a[i]) + to_f<T>(s[i]), 0.f));
+__global__ void add_relu_kernel(const T* __restrict__ a, const T* __restrict__ s, T* __restrict__ y, long long n,
+                                long long sx) {
+  const long long o = blockIdx.y * sx;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8; i < n;
+       i += (long long)gridDim.x * blockDim.x * 8) {
+    const Vec8<T> va = ld8(a + o + i), vs = ld8(s + o + i);
+    Vec8<T> out;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) set_el(out, j, fmaxf(el(va, j) + el(vs, j), 0.f));
+    st8(y + o + i, out);
+  }
 }
 
-// out = g * (y > 0)
+// out = g * (y > 0), same geometry
 template <typename T>
-__global__ void relu_grad_kernel(const T* __restrict__ g, const T* __restrict__ y, T* __restrict__ out, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    out[i] = to_f<T>(y[i]) > 0.f ? g[i] : from_f<T>(0.f);
+__global__ void relu_grad_kernel(const T* __restrict__ g, const T* __restrict__ y, T* __restrict__ out, long long n,
+                                 long long sx) {
+  const long long o = blockIdx.y * sx;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8; i < n;
+       i += (long long)gridDim.x * blockDim.x * 8) {
+    const Vec8<T> vg = ld8(g + o + i), vy = ld8(y + o + i);
+    Vec8<T> r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) set_el(r, j, el(vy, j) > 0.f ? el(vg, j) : 0.f);
+    st8(out + o + i, r);
+  }
 }
 
 // global average pool: p[w][b][c] = mean over HW of y[w][b][hw][c]
@@ -218,16 +235,18 @@ __global__ void pool_bwd_kernel(const T* __restrict__ dp, T* __restrict__ gy, in
   }
 }
 
-// NHWC fp32 input with Cin channels -> T with Cp (>= Cin, zero-padded) channels
+// NHWC fp32 input with Cin channels -> T with Cp (>= Cin, zero-padded)
+// channels; worker blockIdx.y (pixels per worker, activation stride sx)
 template <typename T>
 __global__ void load_image_kernel(const StepDev* __restrict__ sp, T* __restrict__ x0, long long pixels, int cin,
-                                  int cp) {
-  const float* __restrict__ x = sp->x;
+                                  int cp, long long sx) {
+  const float* __restrict__ x = sp->x + blockIdx.y * pixels * cin;
+  T* __restrict__ xw = x0 + blockIdx.y * sx;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < pixels * cp;
        i += (long long)gridDim.x * blockDim.x) {
     const long long px = i / cp;
     const int c = (int)(i % cp);
-    x0[i] = from_f<T>(c < cin ? x[px * cin + c] : 0.f);
+    xw[i] = from_f<T>(c < cin ? x[px * cin + c] : 0.f);
   }
 }
 
@@ -432,16 +451,17 @@ dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const v
   return DSX_OK;
 }
 
+dim3 ew_grid(const dsx_cnn* m, long long n) { return dim3(blocks_for(n / 8, m->nsm) / m->kl + 1, m->kl); }
 template <typename T>
 void launch_add_relu(dsx_cnn* m, const void* a, const void* s, void* y, long long n) {
-  add_relu_kernel<T><<<blocks_for(n, m->nsm), 256, 0, m->stream>>>(static_cast<const T*>(a), static_cast<const T*>(s),
-                                                                  static_cast<T*>(y), n);
+  add_relu_kernel<T><<<ew_grid(m, n), 256, 0, m->stream>>>(static_cast<const T*>(a), static_cast<const T*>(s),
+                                                           static_cast<T*>(y), n, m->act_max);
   ++m->launches;
 }
 template <typename T>
 void launch_relu_grad(dsx_cnn* m, const void* g, const void* y, void* out, long long n) {
-  relu_grad_kernel<T><<<blocks_for(n, m->nsm), 256, 0, m->stream>>>(static_cast<const T*>(g), static_cast<const T*>(y),
-                                                                   static_cast<T*>(out), n);
+  relu_grad_kernel<T><<<ew_grid(m, n), 256, 0, m->stream>>>(static_cast<const T*>(g), static_cast<const T*>(y),
+                                                            static_cast<T*>(out), n, m->act_max);
   ++m->launches;
 }
 
@@ -472,13 +492,14 @@ dsx_status write_step(dsx_cnn* m, double lr, long long t) {
 
 // forward pass up to the logits (the layer waits handle last step's averages)
 dsx_status forward(dsx_cnn* m, bool wait_syncs) {
-  const long long pixels = (long long)m->kl * m->batch * m->image * m->image;
+  const long long pixels = (long long)m->batch * m->image * m->image;
+  const dim3 lgrid(blocks_for(pixels * m->cp, m->nsm) / m->kl + 1, m->kl);
   if (m->bf16)
-    load_image_kernel<__nv_bfloat16><<<blocks_for(pixels * m->cp, m->nsm), 256, 0, m->stream>>>(
-        m->sp, static_cast<__nv_bfloat16*>(m->x0), pixels, m->cin, m->cp);
+    load_image_kernel<__nv_bfloat16><<<lgrid, 256, 0, m->stream>>>(m->sp, static_cast<__nv_bfloat16*>(m->x0),
+                                                                   pixels, m->cin, m->cp, m->act_max);
   else
-    load_image_kernel<float><<<blocks_for(pixels * m->cp, m->nsm), 256, 0, m->stream>>>(
-        m->sp, static_cast<float*>(m->x0), pixels, m->cin, m->cp);
+    load_image_kernel<float><<<lgrid, 256, 0, m->stream>>>(m->sp, static_cast<float*>(m->x0), pixels, m->cin,
+                                                           m->cp, m->act_max);
   ++m->launches;
   auto wait_layer = [&](int l) -> dsx_status {
     if (wait_syncs && m->synced_prev[l]) CN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_sync[l], 0));
@@ -499,7 +520,7 @@ dsx_status forward(dsx_cnn* m, bool wait_syncs) {
       CN_TRY(conv_forward(m, m->convs[bk.sc]));
       shortcut = m->convs[bk.sc].out;
     }
-    const long long n = m->act_max * m->kl;  // flat over workers (strided by act_max)
+    const long long n = (long long)m->batch * b.rows() * b.cout;
     if (m->bf16) launch_add_relu<__nv_bfloat16>(m, b.out, shortcut, bk.y, n);
     else launch_add_relu<float>(m, b.out, shortcut, bk.y, n);
   }
@@ -653,14 +674,14 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
   // blocks, last to first: gy (grad of the block output) lives in g0/g1
   void* gy = m->g0;
   void* gnext = m->g1;
-  const long long nflat = m->act_max * m->kl;
   for (int bi = (int)m->blocks.size() - 1; bi >= 0; --bi) {
     const Block& bk = m->blocks[bi];
     const Conv& a = m->convs[bk.a];
     const Conv& b = m->convs[bk.b];
     // ga = gy * (y > 0): the gradient of both the second conv and the shortcut
-    if (m->bf16) launch_relu_grad<__nv_bfloat16>(m, gy, bk.y, m->ga, nflat);
-    else launch_relu_grad<float>(m, gy, bk.y, m->ga, nflat);
+    const long long nb = (long long)m->batch * b.rows() * b.cout;
+    if (m->bf16) launch_relu_grad<__nv_bfloat16>(m, gy, bk.y, m->ga, nb);
+    else launch_relu_grad<float>(m, gy, bk.y, m->ga, nb);
     const void* sc_grad = m->ga;  // identity shortcut: dx gets ga
     if (bk.sc >= 0) {
       const Conv& s = m->convs[bk.sc];
@@ -683,8 +704,9 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
   // stem: its output relu(conv(x0)) gets gy * (out > 0); wgrad only
   {
     const Conv& st = m->convs[0];
-    if (m->bf16) launch_relu_grad<__nv_bfloat16>(m, gy, st.out, m->ga, nflat);
-    else launch_relu_grad<float>(m, gy, st.out, m->ga, nflat);
+    const long long ns = (long long)m->batch * st.rows() * st.cout;
+    if (m->bf16) launch_relu_grad<__nv_bfloat16>(m, gy, st.out, m->ga, ns);
+    else launch_relu_grad<float>(m, gy, st.out, m->ga, ns);
     CN_TRY(conv_backward(m, st, m->ga, false, o, m->sp));
     CN_TRY(done_layer(st.layer));
   }
