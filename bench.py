@@ -62,6 +62,14 @@ CONFIGS = {
                   "widths": [2048] + [5632, 2048] * 48 + [32000], "batch": 4096, "optimizer": "adam",
                   "workload": "configs[3]-scale MLP stack: 97 Linear layers (2048 <-> 5632, 32000-class head, "
                               "1.17e9 params/worker), batch 4096/worker, 4 workers, H=4, local Adam"},
+    # BASELINE configs[1] as the real network: a ResNet-18-shaped conv stack
+    # (CIFAR geometry, 21 registered layers, 11.17M params/worker) on 32x32x3
+    # synthetic batches, 8 workers, H=5; bf16 tcgen05 implicit-GEMM convs
+    "resnet18_cnn": {"profile": PROFILE, "workers": 8, "period": 5, "parity_steps": 2, "nn": True, "cnn": True,
+                     "batch": 128,
+                     "workload": "configs[1] ResNet-18-shaped conv stack (CIFAR geometry, 21 registered layers, "
+                                 "11,172,042 params/worker), batch 128 32x32x3/worker, 8 workers, H=5, "
+                                 "SGD momentum"},
     # the same step at a compute-bound size (tensor-pipe roofline)
     "mlp_wide": {"profile": MLP_PROFILE, "workers": 4, "period": 4, "parity_steps": 0, "nn": True,
                  "widths": [4096] * 8 + [16], "batch": 2048,
@@ -105,6 +113,7 @@ def parse_args(argv=None):
     a.parity_steps = c["parity_steps"] if a.parity_steps is None else a.parity_steps
     a.workload = c["workload"]
     a.nn = bool(c.get("nn"))
+    a.cnn = bool(c.get("cnn"))
     a.widths = c.get("widths")
     a.batch = c.get("batch")
     a.dtype = a.dtype or ("bf16" if a.nn else "f64")
@@ -1003,6 +1012,265 @@ def mlp_arm(args, world, rank, local_rank, dist):
     return line
 
 
+# ------------------------------------------------------- the conv-stack arm ---
+
+CNN_PARITY_BATCH = 4  # per worker: the float64 restatement's bounded sample
+
+
+def cnn_oracle_run(args, K, steps, masks, init, bsz):
+    """The float64 restatement (oracle/cnn_oracle.py; checker and CPU baseline
+    only): (oracle after `steps` steps at batch bsz/worker, their seconds)."""
+    from oracle.cnn_oracle import CnnOracle
+    from paper_2502_11058_b200.cnn import batch as make_batch
+    from paper_2502_11058_b200.cnn import teacher
+    t = teacher(args.seed, 32, 3, 10)
+    orc = CnnOracle(64, 32, 3, 10, init, K, optimizer=args.optimizer)
+    t0 = time.perf_counter()
+    for r in range(steps):
+        orc.step([make_batch(args.seed, k, r, bsz, 32, 3, t) for k in range(K)], args.lr, r, masks[r % len(masks)])
+    return orc, time.perf_counter() - t0
+
+
+def cnn_reference_arm(args, world, rank):
+    """The reference has no network: its CPU implementation of
+    this path is the restatement of plsgd_step with the conv stack's gradient
+    (oracle/cnn_oracle.py, float64 numpy, all BLAS threads), timed on a
+    bounded sample (batch 4/worker) and scaled to the workload's batch."""
+    if rank != 0:
+        return None
+    from paper_2502_11058_b200.lab import enp, sync_mask
+    L, H = 21, args.period
+    masks = [sync_mask("partial", H, r, L, enp(L, H)) for r in range(H)]
+    steps = max(2, min(args.steps, 3))
+    _, sec = cnn_oracle_run(args, args.workers, steps, masks, cnn_init_host(args.seed), CNN_PARITY_BATCH)
+    it_s = steps / sec * CNN_PARITY_BATCH / args.batch
+    cores = blas_threads()
+    return {"impl": "reference", "metric": METRIC, "value": it_s, "unit": "iterations/s", "n_gpus": world,
+            "steps": steps, "warmup": 0, "ms_per_step": 1e3 / it_s, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": cnn_config(args, world, "enp"),
+            "cpu_baseline": {"value": it_s, "unit": "iterations/s", "cores": cores, "kind": "port",
+                             "sample": f"{steps} steps of all {args.workers} workers at "
+                                       f"batch {CNN_PARITY_BATCH}/worker, scaled x{CNN_PARITY_BATCH}/{args.batch} "
+                                       "to the workload's batch; oracle/cnn_oracle.py float64 numpy"},
+            "e2e": {"value": it_s, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def cnn_init_host(seed):
+    """cnn_init without a device handle (the packed layout is fixed by the topology)."""
+    from oracle.cnn_oracle import layer_sizes, topology
+    from paper_2502_11058_b200.cnn import init_params
+    convs, _, head = topology(64, 32, 8, 10)
+    fan = [c["k"] * c["k"] * c["cin"] for c in convs] + [head["cin"]]
+    roles = [c["role"] for c in convs] + ["head"]
+    return init_params(seed, layer_sizes(64, 32, 8, 10), fan, roles)
+
+
+def cnn_config(args, world, schedule_src):
+    return {"workload": args.workload, "config": args.config, "batch_per_worker": args.batch,
+            "workers": args.workers, "period": args.period, "optimizer": args.optimizer, "lr": args.lr,
+            "schedule": schedule_src, "seed": args.seed,
+            "parallelism": f"dp{world} ({args.workers // world} workers/GPU)",
+            "sync": ("NCCL ncclAvg in place per layer on the side stream" if world > 1 else
+                     "pairwise local average kernel per layer on the side stream"),
+            "l2": "activations + im2col buffers per step (GBs) far exceed L2"}
+
+
+def cnn_arm(args, world, rank, local_rank, dist):
+    import tempfile
+
+    import numpy as np
+    import torch
+
+    from paper_2502_11058_b200.cnn import Cnn, batch as make_batch, teacher
+    from paper_2502_11058_b200.lab import enp, nccl_unique_id, schedule_from_profile, sync_mask, write_profile
+
+    K, H = args.workers, args.period
+    if K % world:
+        raise SystemExit(f"--workers {K} must be divisible by the GPU count {world}")
+    kl = K // world
+    torch.cuda.set_device(local_rank)
+    dev = torch.device(f"cuda:{local_rank}")
+
+    def make(bsz):
+        mm = Cnn(bsz, K, workers_local=kl, worker_begin=rank * kl, dtype=args.dtype, optimizer=args.optimizer,
+                 device=local_rank)
+        if world > 1:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            mm.comm_init(obj[0], world, rank)
+        return mm
+
+    m = make(args.batch)
+    L = m.L
+    init = cnn_init_host(args.seed)
+    for k in range(kl):
+        m.set_params(k, init)
+    npool = 4
+    t = teacher(args.seed, 32, 3, 10)
+    xs = np.empty((npool, kl, args.batch, 32, 32, 3), dtype=np.float32)
+    ys = np.empty((npool, kl, args.batch), dtype=np.int32)
+    for p in range(npool):
+        for j in range(kl):
+            xs[p, j], ys[p, j] = make_batch(args.seed, rank * kl + j, p, args.batch, 32, 3, t)
+    dx = torch.from_numpy(xs).to(dev)
+    dy = torch.from_numpy(ys).to(dev)
+
+    def use_batch(r):
+        p = r % npool
+        m.set_batch_ptr(dx[p].data_ptr(), dy[p].data_ptr(), True)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_ranks(vals):
+        if dist is None:
+            return vals
+        tt = torch.tensor(vals, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return [float(x) for x in tt]
+
+    # DreamDDP's loop on the network: CUDA-event profile -> profile v1 -> DFS
+    use_batch(0)
+    t_fp, t_bp, t_comm = m.profile(reps=5)
+    t_fp, t_bp, t_comm = (np.asarray(max_ranks(list(v))) for v in (t_fp, t_bp, t_comm))
+    path = os.path.join(tempfile.mkdtemp(prefix=f"dreamddp_cnn_r{rank}_"), "measured.profile")
+    sizes = m.layer_sizes()
+    write_profile(path, [4 * s_ for s_ in sizes], t_fp, t_bp, t_comm, bandwidth=1.0, latency=0.0)
+    sets, fills, _, sched_text = schedule_from_profile(path, H, fill=True)
+    masks = [sync_mask("partial", H, r, L, sets, fills) for r in range(H)]
+    sz = np.asarray(sizes, dtype=np.float64)
+    synced_frac = float(np.mean([np.dot(mk[1:], sz) / sz.sum() for mk in masks]))
+
+    r = 0
+
+    def run(nsteps, mask_list):
+        nonlocal r
+        for _ in range(nsteps):
+            use_batch(r)
+            m.step(args.lr, r, mask_list[r % H])
+            r += 1
+
+    def timed(nsteps, mask_list):
+        m.sync()
+        barrier()
+        m.record(0)
+        run(nsteps, mask_list)
+        m.record(1)
+        ms = m.elapsed_ms(0, 1)
+        m.sync()
+        return max_ranks([ms])[0]
+
+    run(max(3, args.warmup), masks)
+    m.sync()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    l0 = m.launches()
+    ms_max = timed(args.steps, masks)
+    clocks.stop()
+    launches = m.launches() - l0
+    value = args.steps / (ms_max / 1e3)
+    ms_step = ms_max / args.steps
+    none = np.zeros(L + 1, dtype=np.uint8)
+    ms_nosync = timed(args.steps, [none] * H) / args.steps
+    m.set_instrument(True)
+    per = []
+    for _ in range(2 * H):
+        run(1, masks)
+        per.append(m.last_step_times())
+    m.set_instrument(False)
+    comp, span, exp_ = (max_ranks([statistics.mean(p_[i] for p_ in per)])[0] for i in (1, 2, 3))
+
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        peak_tf, peak_kind = float(pk["bf16_tflops"]), "measured (cuBLAS bf16 burst, MEASURED_PEAKS.json)"
+    except Exception:  # noqa: BLE001
+        peak_tf, peak_kind = 2250.0, "fallback nominal dense bf16"
+    step_flops = m.flops_per_worker() * kl
+    step_tf = step_flops / (ms_step * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "unit": "TFLOP/s", "peak": peak_tf, "peak_kind": peak_kind,
+                "achieved": round(step_tf, 2), "frac": round(step_tf / peak_tf, 4), "traffic": None,
+                "scope": "whole step: implicit-GEMM conv flops (forward, wgrad, dgrad) / step time",
+                "step": {"gemm_flops_per_step": step_flops, "ms_per_step": round(ms_step, 5),
+                         "t_roof_ms": round(step_flops / (peak_tf * 1e12) * 1e3, 5)}}
+
+    # parity + CPU baseline: the float64 restatement, all K workers at batch
+    # CNN_PARITY_BATCH, same schedule, same init, parity_steps steps
+    parity, cpu = None, None
+    if args.parity_steps > 0 and not args.no_cpu_baseline:
+        pm = make(CNN_PARITY_BATCH)
+        for k in range(kl):
+            pm.set_params(k, init)
+        for rr in range(args.parity_steps):
+            bs = [make_batch(args.seed, rank * kl + j, rr, CNN_PARITY_BATCH, 32, 3, t) for j in range(kl)]
+            pm.set_batch(np.stack([b[0] for b in bs]), np.stack([b[1] for b in bs]))
+            pm.step(args.lr, rr, masks[rr % H])
+        pm.sync()
+        mine = [pm.get_params(k) for k in range(kl)]
+        pm.close()
+        if dist is not None:
+            allv = [None] * world
+            dist.all_gather_object(allv, mine)
+            mine = [w for part in allv for w in part]
+        if rank == 0:
+            orc, sec = cnn_oracle_run(args, K, args.parity_steps, masks, init, CNN_PARITY_BATCH)
+            errs = [float(np.linalg.norm(w - o) / np.linalg.norm(o)) for w, o in zip(mine, orc.w)]
+            tol = 3e-2 if args.dtype == "bf16" else 1e-4
+            parity = {"ok": max(errs) <= tol, "max_rel_l2": max(errs), "tolerance_rel_l2": tol,
+                      "steps": args.parity_steps, "workers": K, "batch_per_worker": CNN_PARITY_BATCH,
+                      "reference": "oracle/cnn_oracle.py float64 restatement (parity unpinned by the reference: "
+                                   "it has no NN)"}
+            it_s = args.parity_steps / sec * CNN_PARITY_BATCH / args.batch
+            cpu = {"value": it_s, "unit": "iterations/s", "cores": blas_threads(), "kind": "port",
+                   "sample": f"{args.parity_steps} steps of all {K} workers at batch {CNN_PARITY_BATCH}/worker "
+                             f"(oracle/cnn_oracle.py float64 numpy), scaled x{CNN_PARITY_BATCH}/{args.batch}"}
+
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        hx = torch.from_numpy(xs).pin_memory()
+        hy = torch.from_numpy(ys).pin_memory()
+        m.sync()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            p = r % npool
+            m.set_batch_ptr(hx[p].data_ptr(), hy[p].data_ptr(), False)
+            m.step(args.lr, r, masks[r % H])
+            m.last_loss()
+            r += 1
+        m.sync()
+        el = max_ranks([time.perf_counter() - t0])[0]
+        e2e = {"value": args.e2e_steps / el, "unit": "iterations/s",
+               "h2d_bytes_per_step": int(xs[0].nbytes + ys[0].nbytes), "d2h_bytes_per_step": 4 * kl,
+               "path": "dsx_cnn_set_batch (pinned host x + labels) + dsx_cnn_step + dsx_cnn_last_loss every step"}
+    if rank != 0:
+        m.close()
+        return None
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (N(0,1) 32x32x3 images, linear-teacher labels; device-resident pool of 4 batches/worker)",
+        "config": cnn_config(args, world, "measured"),
+        "exposed_sync_ms_per_iter": round(exp_, 5), "sync_ms_per_iter": round(span, 5),
+        "exposed_sync_frac": round(exp_ / span, 4) if span > 0 else None,
+        "compute_ms_per_iter": round(comp, 5),
+        "ms_per_step_without_sync": round(ms_nosync, 5),
+        "sync_added_ms_per_iter": round(ms_step - ms_nosync, 5),
+        "schedule": {"source": "dsx_cnn_profile -> write_profile -> schedule_dfs + bubble_fill",
+                     "text": sched_text, "synced_param_frac_per_step": round(synced_frac, 4),
+                     "profile_ms": {"fp": [round(x * 1e3, 4) for x in t_fp], "bp": [round(x * 1e3, 4) for x in t_bp],
+                                    "comm": [round(x * 1e3, 4) for x in t_comm]}},
+        "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+    m.close()
+    return line
+
+
 def spawn_ranks(args_argv, n):
     """`python bench.py --gpus N` without torchrun: launch N ranks on this
     node (torch.distributed.run, 127.0.0.1) and relay rank 0's line."""
@@ -1033,7 +1301,10 @@ def main():
         import torch.distributed as dist_mod
         dist_mod.init_process_group("gloo")
         dist = dist_mod
-    if args.nn:
+    if args.cnn:
+        line = (cnn_reference_arm(args, world, rank) if args.impl == "reference"
+                else cnn_arm(args, world, rank, local_rank, dist))
+    elif args.nn:
         line = (mlp_reference_arm(args, world, rank) if args.impl == "reference"
                 else mlp_arm(args, world, rank, local_rank, dist))
     elif args.impl == "reference":

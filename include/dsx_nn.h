@@ -65,6 +65,8 @@ typedef struct dsx_gemm_desc {
   long long ldmask, strideMask;
   int bn;                    /* tensor-core tile width 64/128/256 (0: auto) */
   void* stream;              /* cudaStream_t (NULL: default stream) */
+  int ksplit;                /* split-K (bf16, DSX_EPI_F32, no accumulate): split s of K writes */
+  long long strideSplit;     /* its partial at C + s * strideSplit; 0/1: off */
 } dsx_gemm_desc;
 dsx_status dsx_gemm(const dsx_gemm_desc* d);
 
@@ -178,6 +180,10 @@ dsx_status dsx_cnn_set_instrument(dsx_cnn* m, int enabled);
 dsx_status dsx_cnn_last_step_times(dsx_cnn* m, float* out4);
 dsx_status dsx_cnn_event_record(dsx_cnn* m, int slot);
 dsx_status dsx_cnn_event_elapsed(dsx_cnn* m, int from_slot, int to_slot, float* ms);
+/* CUDA-event per-layer FP / BP (+ update) / average times in seconds (median
+ * of reps lr-0 steps; parameters and optimizer states restored) — the input
+ * of dsc_write_profile -> the DFS scheduler, as dsx_mlp_profile. */
+dsx_status dsx_cnn_profile(dsx_cnn* m, int reps, double* t_fp, double* t_bp, double* t_comm);
 dsx_status dsx_cnn_launch_count(dsx_cnn* m, uint64_t* out);
 
 #ifdef __cplusplus

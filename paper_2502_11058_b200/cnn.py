@@ -49,6 +49,29 @@ def init_params(seed: int, sizes, fan_in, roles) -> np.ndarray:
     return np.concatenate(parts)
 
 
+def conv_geometry(width: int, image: int):
+    """(Cin, Cout, k, Ho) of every conv in registration order (dsx_cnn_create)."""
+    out = [(8, width, 3, image)]
+    cin, H = width, image
+    for s in range(4):
+        w = width << s
+        for blk in range(2):
+            stride = 2 if (s > 0 and blk == 0) else 1
+            Ho = (H - 1) // stride + 1
+            out += [(cin, w, 3, Ho), (w, w, 3, Ho)]
+            if stride != 1 or cin != w:
+                out.append((cin, w, 1, Ho))
+            cin, H = w, Ho
+    return out
+
+
+def conv_stack_flops(width: int, image: int, classes: int, batch: int) -> float:
+    f = 0.0
+    for i, (cin, cout, k, Ho) in enumerate(conv_geometry(width, image)):
+        f += 2.0 * batch * Ho * Ho * cout * k * k * cin * (2 if i == 0 else 3)
+    return f + 3 * 2.0 * batch * (width << 3) * classes
+
+
 class Cnn:
     """K (or K/N per rank) device-resident conv-stack workers."""
 
@@ -144,6 +167,16 @@ class Cnn:
         out = (C.c_float * 4)()
         N.call("dsx_cnn_last_step_times", self.h, out)
         return tuple(out)
+
+    def profile(self, reps: int = 5):
+        """Per-layer FP / BP / average seconds (dsx_cnn_profile)."""
+        fp, bp, cm = (np.empty(self.L) for _ in range(3))
+        N.call("dsx_cnn_profile", self.h, reps, fp.ctypes.data, bp.ctypes.data, cm.ctypes.data)
+        return fp, bp, cm
+
+    def flops_per_worker(self) -> float:
+        """GEMM flops of one local step: forward, wgrad and dgrad (none into the stem's input)."""
+        return conv_stack_flops(self.width, self.image, self.classes, self.batch)
 
     def record(self, slot: int) -> None:
         N.call("dsx_cnn_event_record", self.h, slot)

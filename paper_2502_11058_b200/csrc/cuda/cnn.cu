@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -253,9 +254,11 @@ __global__ void load_image_kernel(const StepDev* __restrict__ sp, T* __restrict_
 struct Conv {
   int cin, cout, k, stride, pad, H, W, Ho, Wo;
   bool relu;          // epilogue ReLU (stem, first conv of a block)
+  bool implicit = false;  // tensor-core implicit GEMM (3x3 stride 1, 64-channel multiples): no col buffers
   int layer;          // registered layer (0-based)
   void* in = nullptr;   // input activation (not owned)
-  void* col = nullptr;  // im2col buffer (owned)
+  void* col = nullptr;  // im2col buffer (owned), worker stride col_stride
+  long long col_stride = 0;
   void* out = nullptr;  // output activation (owned)
   long long rows() const { return (long long)Ho * Wo; }
   long long kc() const { return (long long)k * k * cin; }
@@ -294,6 +297,7 @@ struct dsx_cnn {
   void* dlog = nullptr;          // [kl][B][ldc] T
   void* dpool = nullptr;         // [kl][B][C]
   void *g0 = nullptr, *g1 = nullptr, *ga = nullptr, *gh = nullptr, *gcol = nullptr, *gsc = nullptr;
+  float* wpart = nullptr;  // split-K wgrad partials
   long long act_max = 0, col_max = 0;  // elements per worker
   float *loss_part = nullptr, *loss = nullptr;
   float* xin = nullptr;
@@ -309,6 +313,8 @@ struct dsx_cnn {
   std::vector<unsigned char> synced_prev;
   cudaEvent_t ev[8] = {};
   cudaEvent_t iev[4] = {};
+  std::vector<cudaEvent_t> pf, pb;  // dsx_cnn_profile: after each layer's FP / BP
+  bool prof = false;
   bool instrument = false, any_synced = false;
   uint64_t launches = 0;
   ncclComm_t comm = nullptr;
@@ -333,22 +339,43 @@ const void* wptr(const dsx_cnn* m, int l) {
   return m->bf16 ? static_cast<const void*>(m->pbf + m->off[l]) : static_cast<const void*>(m->params + m->off[l]);
 }
 
+ConvGeom geom(const dsx_cnn* m, const Conv& cv, int mode) {
+  return ConvGeom{mode, cv.H, cv.W, m->batch, cv.cin, cv.cout};
+}
+
 dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
   const long long M = (long long)m->batch * cv.rows(), Kc = cv.kc();
+  if (cv.implicit) {
+    GemmCall c = cbase(m);
+    c.A = cv.in;
+    c.sA = m->act_max;
+    c.B = wptr(m, cv.layer);
+    c.ldb = Kc;
+    c.sB = m->P;
+    c.g.epi = kEpiBiasAct;
+    c.g.relu = cv.relu ? 1 : 0;
+    c.g.bias = m->params + m->boff[cv.layer];
+    c.g.strideBias = m->P;
+    c.g.C = cv.out;
+    c.g.ldc = cv.cout;
+    c.g.strideC = m->act_max;
+    ++m->launches;
+    return conv_gemm(c, geom(m, cv, kConvFwd), m->stream, m->nsm);
+  }
   const int grid = blocks_for(M * cv.k * cv.k * (cv.cin / 8), m->nsm) / std::max(1, m->kl) + 1;
   if (m->bf16)
     im2col_kernel<__nv_bfloat16><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
         static_cast<const __nv_bfloat16*>(cv.in), static_cast<__nv_bfloat16*>(cv.col), m->batch, cv.H, cv.W, cv.cin,
-        cv.Ho, cv.Wo, cv.k, cv.stride, cv.pad, m->act_max, m->col_max);
+        cv.Ho, cv.Wo, cv.k, cv.stride, cv.pad, m->act_max, cv.col_stride);
   else
     im2col_kernel<float><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
         static_cast<const float*>(cv.in), static_cast<float*>(cv.col), m->batch, cv.H, cv.W, cv.cin, cv.Ho, cv.Wo,
-        cv.k, cv.stride, cv.pad, m->act_max, m->col_max);
+        cv.k, cv.stride, cv.pad, m->act_max, cv.col_stride);
   ++m->launches;
   GemmCall c = cbase(m);
   c.A = cv.col;
   c.lda = Kc;
-  c.sA = m->col_max;
+  c.sA = cv.col_stride;
   c.B = wptr(m, cv.layer);
   c.ldb = Kc;
   c.sB = m->P;
@@ -366,11 +393,59 @@ dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
   return gemm(c, m->stream, m->nsm);
 }
 
-// wgrad + bias grad (+ dgrad into gcol when dgrad) of one conv, then its
-// optimizer step; g = dL/d(conv output) [B*Ho*Wo][Cout]
-dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, bool dgrad, const OptArgs& o, const StepDev* sp) {
+// wgrad tiling: the widest tile, and split-K over the B*Ho*Wo reduction when
+// the (Cout x k*k*Cin) output has fewer than two waves of tiles (the 64-wide
+// stage-0 convs: 8 workers x 3 tiles for a 131072-long K)
+void wgrad_plan(const dsx_cnn* m, const Conv& cv, int* bn, int* ks) {
+  const long long Kc = cv.kc(), Kg = (long long)m->batch * cv.rows();
+  *bn = Kc >= 256 ? 256 : Kc >= 128 ? 128 : 64;
+  const long long units = ((cv.cout + kBM - 1) / kBM) * ((Kc + *bn - 1) / *bn) * m->kl;
+  const long long nk = (Kg + kBK - 1) / kBK;
+  *ks = 1;
+  if (m->bf16 && units < 2LL * m->nsm)
+    *ks = (int)std::max<long long>(1, std::min<long long>((2LL * m->nsm + units - 1) / units, nk / 8));
+}
+
+dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const void* mask);
+
+// wgrad + bias grad + (dx != null) the input gradient dx = dgrad (+ add)
+// (* (mask > 0)), then the layer's optimizer step; g = dL/d(conv output)
+// [B*Ho*Wo][Cout].  Implicit convs produce dx in the dgrad GEMM's epilogue;
+// the others through gcol + col2im.
+dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, const void* add, const void* mask,
+                         const OptArgs& o, const StepDev* sp) {
   const long long M = (long long)m->batch * cv.rows(), Kc = cv.kc();
-  {
+  const bool dgrad = dx != nullptr;
+  if (cv.implicit) {
+    GemmCall c = cbase(m);
+    c.A = g;
+    c.lda = cv.cout;
+    c.sA = m->act_max;
+    c.B = cv.in;
+    c.sB = m->act_max;
+    c.g.epi = kEpiF32;
+    int ks = 1;
+    wgrad_plan(m, cv, &c.bn, &ks);
+    c.g.ldc = Kc;
+    if (ks > 1) {
+      c.g.C = m->wpart;
+      c.g.strideC = (long long)cv.cout * Kc;
+      c.g.ksplit = ks;
+      c.g.strideSplit = (long long)m->kl * cv.cout * Kc;
+    } else {
+      c.g.C = m->grads + m->off[cv.layer];
+      c.g.strideC = m->P;
+    }
+    ++m->launches;
+    CN_TRY(conv_gemm(c, geom(m, cv, kConvWgrad), m->stream, m->nsm));
+    if (ks > 1) {
+      const long long nk = (M + kBK - 1) / kBK, kper = (nk + ks - 1) / ks;
+      const long long n = (long long)cv.cout * Kc;
+      splitk_reduce_kernel<<<dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream>>>(
+          m->wpart, (int)((nk + kper - 1) / kper), c.g.strideSplit, n, m->grads + m->off[cv.layer], m->P);
+      ++m->launches;
+    }
+  } else {
     GemmCall c = cbase(m);
     c.a_mn = true;
     c.b_mn = true;
@@ -379,16 +454,35 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, bool dgrad, 
     c.sA = m->act_max;
     c.B = cv.col;
     c.ldb = Kc;
-    c.sB = m->col_max;
+    c.sB = cv.col_stride;
     c.g.M = cv.cout;
     c.g.N = (int)Kc;
     c.g.K = (int)M;
     c.g.epi = kEpiF32;
-    c.g.C = m->grads + m->off[cv.layer];
+    int ks = 1;
+    wgrad_plan(m, cv, &c.bn, &ks);
     c.g.ldc = Kc;
-    c.g.strideC = m->P;
+    if (ks > 1) {
+      c.g.C = m->wpart;
+      c.g.strideC = (long long)cv.cout * Kc;
+      c.g.ksplit = ks;
+      c.g.strideSplit = (long long)m->kl * cv.cout * Kc;
+    } else {
+      c.g.C = m->grads + m->off[cv.layer];
+      c.g.strideC = m->P;
+    }
     ++m->launches;
     CN_TRY(gemm(c, m->stream, m->nsm));
+    if (ks > 1) {
+      // gemm() may have lowered ks to keep every split non-empty: the unused
+      // partial slots are never read (same rounding as in gemm())
+      const long long nk = ((long long)M + kBK - 1) / kBK, kper = (nk + ks - 1) / ks;
+      const int ks_eff = (int)((nk + kper - 1) / kper);
+      const long long n = (long long)cv.cout * Kc;
+      splitk_reduce_kernel<<<dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream>>>(
+          m->wpart, ks_eff, c.g.strideSplit, n, m->grads + m->off[cv.layer], m->P);
+      ++m->launches;
+    }
   }
   {
     dim3 grid((cv.cout + 31) / 32, m->kl);
@@ -401,7 +495,24 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, bool dgrad, 
                                                         cv.cout, m->grads + m->boff[cv.layer], m->P);
     ++m->launches;
   }
-  if (dgrad) {
+  if (dgrad && cv.implicit) {
+    GemmCall c = cbase(m);
+    c.A = g;
+    c.sA = m->act_max;
+    c.B = wptr(m, cv.layer);
+    c.sB = m->P;
+    c.g.epi = add ? kEpiAdd : (mask ? kEpiDRelu : kEpiBiasAct);
+    c.g.relu = 0;
+    c.g.bias = nullptr;
+    c.g.mask = add ? add : mask;
+    c.g.ldmask = cv.cin;
+    c.g.strideMask = m->act_max;
+    c.g.C = dx;
+    c.g.ldc = cv.cin;
+    c.g.strideC = m->act_max;
+    ++m->launches;
+    CN_TRY(conv_gemm(c, geom(m, cv, kConvDgrad), m->stream, m->nsm));
+  } else if (dgrad) {
     GemmCall c = cbase(m);
     c.a_mn = false;
     c.b_mn = true;
@@ -430,6 +541,7 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, bool dgrad, 
                                                 lo, n, o, sp);
   ++m->launches;
   CN_CUDA(cudaGetLastError());
+  if (dgrad && !cv.implicit) return col2im(m, cv, dx, add, mask);
   return DSX_OK;
 }
 
@@ -505,19 +617,28 @@ dsx_status forward(dsx_cnn* m, bool wait_syncs) {
     if (wait_syncs && m->synced_prev[l]) CN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_sync[l], 0));
     return DSX_OK;
   };
+  auto mark = [&](int l) -> dsx_status {
+    if (m->prof) CN_CUDA(cudaEventRecord(m->pf[l], m->stream));
+    return DSX_OK;
+  };
+  CN_TRY(mark(0));
   CN_TRY(wait_layer(m->convs[0].layer));
   CN_TRY(conv_forward(m, m->convs[0]));
+  CN_TRY(mark(1));
   for (const Block& bk : m->blocks) {
     const Conv& a = m->convs[bk.a];
     const Conv& b = m->convs[bk.b];
     CN_TRY(wait_layer(a.layer));
     CN_TRY(conv_forward(m, a));
+    CN_TRY(mark(a.layer + 1));
     CN_TRY(wait_layer(b.layer));
     CN_TRY(conv_forward(m, b));
+    CN_TRY(mark(b.layer + 1));
     const void* shortcut = bk.x;
     if (bk.sc >= 0) {
       CN_TRY(wait_layer(m->convs[bk.sc].layer));
       CN_TRY(conv_forward(m, m->convs[bk.sc]));
+      CN_TRY(mark(bk.sc + 1));
       shortcut = m->convs[bk.sc].out;
     }
     const long long n = (long long)m->batch * b.rows() * b.cout;
@@ -557,7 +678,8 @@ dsx_status forward(dsx_cnn* m, bool wait_syncs) {
   c.g.ldc = m->classes;
   c.g.strideC = (long long)m->batch * m->classes;
   ++m->launches;
-  return gemm(c, m->stream, m->nsm);
+  CN_TRY(gemm(c, m->stream, m->nsm));
+  return mark(hl + 1);
 }
 
 long long ld_classes(const dsx_cnn* m) { return m->bf16 ? (m->classes + 7) / 8 * 8 : m->classes; }
@@ -589,8 +711,10 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     loss_mean_kernel<<<m->kl, 256, 0, m->stream>>>(m->loss_part, m->batch, m->loss);
     m->launches += 2;
   }
+  if (m->prof) CN_CUDA(cudaEventRecord(m->pb[m->L], m->stream));
   bool any = false;
   auto done_layer = [&](int l) -> dsx_status {
+    if (m->prof) CN_CUDA(cudaEventRecord(m->pb[l], m->stream));
     const bool sync_l = mask[l + 1] != 0 && m->K > 1;
     m->synced_prev[l] = sync_l ? 1 : 0;
     if (!sync_l) return DSX_OK;
@@ -685,19 +809,16 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     const void* sc_grad = m->ga;  // identity shortcut: dx gets ga
     if (bk.sc >= 0) {
       const Conv& s = m->convs[bk.sc];
-      CN_TRY(conv_backward(m, s, m->ga, true, o, m->sp));
-      CN_TRY(col2im(m, s, m->gsc, nullptr, nullptr));
+      CN_TRY(conv_backward(m, s, m->ga, m->gsc, nullptr, nullptr, o, m->sp));
       sc_grad = m->gsc;
       CN_TRY(done_layer(s.layer));
     }
     // second conv; its input h = relu(first conv): gh = col2im(...) * (h > 0)
-    CN_TRY(conv_backward(m, b, m->ga, true, o, m->sp));
-    CN_TRY(col2im(m, b, m->gh, nullptr, b.in));
+    CN_TRY(conv_backward(m, b, m->ga, m->gh, nullptr, b.in, o, m->sp));
     CN_TRY(done_layer(b.layer));
     // first conv; dx = col2im(...) + shortcut grad -> grad of the previous
     // block's output (its ReLU' is applied by that block)
-    CN_TRY(conv_backward(m, a, m->gh, true, o, m->sp));
-    CN_TRY(col2im(m, a, gnext, sc_grad, nullptr));
+    CN_TRY(conv_backward(m, a, m->gh, gnext, sc_grad, nullptr, o, m->sp));
     CN_TRY(done_layer(a.layer));
     std::swap(gy, gnext);
   }
@@ -707,7 +828,7 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     const long long ns = (long long)m->batch * st.rows() * st.cout;
     if (m->bf16) launch_relu_grad<__nv_bfloat16>(m, gy, st.out, m->ga, ns);
     else launch_relu_grad<float>(m, gy, st.out, m->ga, ns);
-    CN_TRY(conv_backward(m, st, m->ga, false, o, m->sp));
+    CN_TRY(conv_backward(m, st, m->ga, nullptr, nullptr, nullptr, o, m->sp));
     CN_TRY(done_layer(st.layer));
   }
   m->any_synced = any;
@@ -781,6 +902,13 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
     c.H = c.W = H;
     c.Ho = c.Wo = (H + 2 * c.pad - k) / stride + 1;
     c.relu = relu;
+    // DSX_CONV_IMPLICIT=0: every conv through im2col / col2im (A/B measurements)
+    static const bool implicit_ok = [] {
+      const char* e = std::getenv("DSX_CONV_IMPLICIT");
+      return !(e && e[0] == '0');
+    }();
+    c.implicit = implicit_ok && m->bf16 && k == 3 && stride == 1 && cin % 64 == 0 && cout % 64 == 0 && H <= 64 &&
+                 64 % H == 0;
     c.layer = (int)m->convs.size();
     m->convs.push_back(c);
     return (int)m->convs.size() - 1;
@@ -828,9 +956,15 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
   for (const Conv& c : m->convs) {
     act = std::max(act, (long long)m->batch * c.Ho * c.Wo * c.cout);
     act = std::max(act, (long long)m->batch * c.H * c.W * c.cin);
-    col = std::max(col, (long long)m->batch * c.rows() * c.kc());
+    if (!c.implicit) col = std::max(col, (long long)m->batch * c.rows() * c.kc());
   }
   m->act_max = (act + 63) / 64 * 64;
+  long long wpart = 0;
+  for (const Conv& c : m->convs) {
+    int bn = 0, ks = 1;
+    wgrad_plan(m, c, &bn, &ks);
+    if (ks > 1) wpart = std::max(wpart, (long long)ks * m->kl * c.cout * c.kc());
+  }
   m->col_max = (col + 63) / 64 * 64;
   const size_t es = m->bf16 ? 2 : 4;
   auto alloc = [&](void** p, size_t bytes) -> bool {
@@ -847,11 +981,16 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
             (!m->bf16 || alloc((void**)&m->pbf, 2ull * m->P * m->kl)) && alloc(&m->x0, actb);
   for (size_t i = 0; ok && i < m->convs.size(); ++i) {
     Conv& c = m->convs[i];
-    ok = alloc(&c.col, colb) && alloc(&c.out, actb);
+    if (c.implicit) {
+      ok = alloc(&c.out, actb);
+      continue;
+    }
+    c.col_stride = ((long long)m->batch * c.rows() * c.kc() + 63) / 64 * 64;
+    ok = alloc(&c.col, es * c.col_stride * m->kl) && alloc(&c.out, actb);
   }
   for (size_t i = 0; ok && i < m->blocks.size(); ++i) ok = alloc(&m->blocks[i].y, actb);
   ok = ok && alloc(&m->g0, actb) && alloc(&m->g1, actb) && alloc(&m->ga, actb) && alloc(&m->gh, actb) &&
-       alloc(&m->gsc, actb) && alloc(&m->gcol, colb) &&
+       alloc(&m->gsc, actb) && alloc(&m->gcol, colb) && (wpart == 0 || alloc((void**)&m->wpart, 4ull * wpart)) &&
        alloc(&m->pool, es * m->kl * m->batch * cin) && alloc(&m->dpool, es * m->kl * m->batch * cin) &&
        alloc((void**)&m->logits, 4ull * m->kl * m->batch * m->classes) &&
        alloc(&m->dlog, es * m->kl * m->batch * ((m->classes + 7) / 8 * 8)) &&
@@ -1058,6 +1197,89 @@ dsx_status dsx_cnn_event_elapsed(dsx_cnn* m, int a, int b, float* ms) {
   if (!ms || a < 0 || a >= 7 || b < 0 || b >= 7) return cfail(DSX_ERR_ARGUMENT, "bad slots");
   CN_CUDA(cudaEventSynchronize(m->ev[b]));
   CN_CUDA(cudaEventElapsedTime(ms, m->ev[a], m->ev[b]));
+  return DSX_OK;
+}
+
+dsx_status dsx_cnn_profile(dsx_cnn* m, int reps, double* t_fp, double* t_bp, double* t_comm) {
+  CN_TRY(ccheck(m));
+  if (!t_fp || !t_bp || !t_comm) return cfail(DSX_ERR_ARGUMENT, "null out");
+  reps = std::max(1, reps);
+  CN_CUDA(cudaStreamSynchronize(m->side));
+  CN_CUDA(cudaStreamSynchronize(m->stream));
+  // the profile must not change the state: snapshot params / states, steps at lr 0
+  const size_t arena = 4ull * m->P * m->kl;
+  std::vector<std::pair<float*, void*>> keep;
+  for (float* p : {m->params, m->mom, m->var}) {
+    if (!p) continue;
+    void* c = nullptr;
+    CN_CUDA(cudaMalloc(&c, arena));
+    keep.emplace_back(p, c);
+    CN_CUDA(cudaMemcpy(c, p, arena, cudaMemcpyDeviceToDevice));
+  }
+  m->pf.assign(m->L + 1, nullptr);
+  m->pb.assign(m->L + 1, nullptr);
+  for (auto& e : m->pf) CN_CUDA(cudaEventCreate(&e));
+  for (auto& e : m->pb) CN_CUDA(cudaEventCreate(&e));
+  std::vector<std::vector<float>> fp(m->L), bp(m->L), cm(m->L);
+  std::vector<unsigned char> none(m->L + 1, 0);
+  const std::vector<unsigned char> prev = m->synced_prev;
+  std::fill(m->synced_prev.begin(), m->synced_prev.end(), 0);
+  dsx_status st = DSX_OK;
+  m->prof = true;
+  for (int r = 0; r < reps + 1 && st == DSX_OK; ++r) {
+    st = write_step(m, 0.0, 0);
+    if (st == DSX_OK) st = step_impl(m, 0.0, 0, none.data());
+    if (st != DSX_OK) break;
+    CN_CUDA(cudaStreamSynchronize(m->stream));
+    if (r == 0) continue;
+    for (int l = 0; l < m->L; ++l) {
+      float t = 0;
+      CN_CUDA(cudaEventElapsedTime(&t, m->pf[l], m->pf[l + 1]));
+      fp[l].push_back(t);
+      CN_CUDA(cudaEventElapsedTime(&t, m->pb[l + 1 < m->L ? l + 1 : m->L], m->pb[l]));
+      bp[l].push_back(t);
+    }
+  }
+  m->prof = false;
+  cudaEvent_t e0 = m->pf[0], e1 = m->pf[1];
+  for (int r = 0; r < reps + 1 && m->K > 1 && st == DSX_OK; ++r) {
+    for (int l = 0; l < m->L; ++l) {
+      CN_CUDA(cudaEventRecord(e0, m->side));
+      st = average_layer(m, l, m->side);
+      if (st != DSX_OK) break;
+      CN_CUDA(cudaEventRecord(e1, m->side));
+      CN_CUDA(cudaEventSynchronize(e1));
+      float t = 0;
+      CN_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      if (r > 0) cm[l].push_back(t);
+    }
+  }
+  CN_CUDA(cudaStreamSynchronize(m->side));
+  CN_CUDA(cudaStreamSynchronize(m->stream));
+  for (auto& [p, c] : keep) {
+    CN_CUDA(cudaMemcpy(p, c, arena, cudaMemcpyDeviceToDevice));
+    cudaFree(c);
+  }
+  if (m->bf16)
+    cast_bf16_kernel<<<blocks_for(m->P * m->kl, m->nsm), 256, 0, m->stream>>>(m->params, m->pbf, m->P, m->kl, 0,
+                                                                             m->P);
+  CN_CUDA(cudaStreamSynchronize(m->stream));
+  for (auto e : m->pf) cudaEventDestroy(e);
+  for (auto e : m->pb) cudaEventDestroy(e);
+  m->pf.clear();
+  m->pb.clear();
+  m->synced_prev = prev;
+  if (st != DSX_OK) return st;
+  auto med = [](std::vector<float> v) {
+    if (v.empty()) return 0.0;
+    std::sort(v.begin(), v.end());
+    return (double)v[v.size() / 2] * 1e-3;
+  };
+  for (int l = 0; l < m->L; ++l) {
+    t_fp[l] = med(fp[l]);
+    t_bp[l] = med(bp[l]);
+    t_comm[l] = med(cm[l]);
+  }
   return DSX_OK;
 }
 

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "device_once.cuh"
 #include "dsx.h"
@@ -73,10 +74,10 @@ dsx_status make_map(CUtensorMap* map, const void* base, long long inner, long lo
   return DSX_OK;
 }
 
-template <int BN, bool AM, bool BM_, typename TOut>
+template <int BN, bool AM, bool BM_, typename TOut, int CONV = kConvNone>
 dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  auto kern = gemm_tc_kernel<BN, AM, BM_, TOut>;
+  auto kern = gemm_tc_kernel<BN, AM, BM_, TOut, CONV>;
   dsx::once_per_device(attr, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::kSmem);
   });
@@ -84,7 +85,8 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const long long tiles = (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch;
+  const long long tiles =
+      (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
   const int grid = (int)std::min<long long>(tiles, nsm);
   kern<<<grid, 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g);
   NN_CUDA(cudaGetLastError());
@@ -146,11 +148,114 @@ int pick_bn(const GemmArgs& g, int nsm) {
   return 64;
 }
 
+// 5-D activation view (c, w, h, image, worker) of an NHWC tensor whose
+// workers sit `wstride` elements apart; a box covers `pix` consecutive
+// pixels = whole rows of one image, or whole images
+dsx_status make_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int B, int batch, long long wstride,
+                        int pix) {
+  NN_TRY(get_encoder());
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || C % 64 || (wstride * 2) % 16)
+    return nfail(DSX_ERR_ARGUMENT, "conv: activations need 16-B aligned base/stride and 64-channel multiples");
+  int rows = H, imgs = 1;
+  if (H * W >= pix) {
+    if (pix % W) return nfail(DSX_ERR_ARGUMENT, "conv: tile pixels must cover whole image rows");
+    rows = pix / W;
+  } else {
+    if (pix % (H * W)) return nfail(DSX_ERR_ARGUMENT, "conv: tile pixels must cover whole images");
+    imgs = pix / (H * W);
+  }
+  cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)batch};
+  cuuint64_t strides[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2,
+                           (cuuint64_t)wstride * 2};
+  cuuint32_t box[5] = {64, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return nfail(DSX_ERR_CUDA, "cuTensorMapEncodeTiled(5-D) failed (" + std::to_string((int)r) + ")");
+  return DSX_OK;
+}
+
+// 4-D view (c, tap, o, worker) of 3x3 weights W[o][tap][c], workers `wstride` apart
+dsx_status make_tap_map(CUtensorMap* map, const void* base, int cin, int cout, int batch, long long wstride) {
+  NN_TRY(get_encoder());
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (wstride * 2) % 16 || cin % 64)
+    return nfail(DSX_ERR_ARGUMENT, "conv: weights need 16-B aligned base/stride and 64-channel multiples");
+  cuuint64_t dims[4] = {(cuuint64_t)cin, 9, (cuuint64_t)cout, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)cin * 2, (cuuint64_t)9 * cin * 2, (cuuint64_t)wstride * 2};
+  cuuint32_t box[4] = {64, 1, 64, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return nfail(DSX_ERR_CUDA, "cuTensorMapEncodeTiled(4-D) failed (" + std::to_string((int)r) + ")");
+  return DSX_OK;
+}
+
+template <int MODE>
+dsx_status launch_conv_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+  constexpr bool AM = MODE == kConvWgrad, BM_ = MODE != kConvFwd;
+  using T = std::conditional_t<MODE == kConvWgrad, float, __nv_bfloat16>;
+  switch (bn) {
+    case 64: return launch_tc_t<64, AM, BM_, T, MODE>(ta, tb, g, s);
+    case 128: return launch_tc_t<128, AM, BM_, T, MODE>(ta, tb, g, s);
+    default: return launch_tc_t<256, AM, BM_, T, MODE>(ta, tb, g, s);
+  }
+}
+
 }  // namespace
 
+dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int nsm) {
+  GemmArgs g = c.g;
+  if (!c.bf16) return nfail(DSX_ERR_ARGUMENT, "conv_gemm: tensor-core (bf16) path only");
+  if (q.W > 64 || 64 % q.W || q.cin % 64 || q.cout % 64)
+    return nfail(DSX_ERR_ARGUMENT, "conv_gemm: needs W | 64 and 64-channel multiples");
+  g.conv_h = q.H;
+  g.conv_w = q.W;
+  g.conv_cin = q.cin;
+  const int pixels = q.B * q.H * q.W;
+  CUtensorMap ta, tb;
+  if (q.mode == kConvFwd) {
+    g.M = pixels, g.N = q.cout, g.K = 9 * q.cin, g.conv_cpb = q.cin / 64;
+    NN_TRY(make_act_map(&ta, c.A, q.cin, q.W, q.H, q.B, g.batch, c.sA, kBM));
+  } else if (q.mode == kConvWgrad) {
+    g.M = q.cout, g.N = 9 * q.cin, g.K = pixels;
+    NN_TRY(make_map(&ta, c.A, g.M, g.K, g.batch, c.lda, c.sA, kBK));
+    NN_TRY(make_act_map(&tb, c.B, q.cin, q.W, q.H, q.B, g.batch, c.sB, kBK));
+  } else if (q.mode == kConvDgrad) {
+    g.M = pixels, g.N = q.cin, g.K = 9 * q.cout, g.conv_cpb = q.cout / 64;
+    NN_TRY(make_act_map(&ta, c.A, q.cout, q.W, q.H, q.B, g.batch, c.sA, kBM));
+    NN_TRY(make_tap_map(&tb, c.B, q.cin, q.cout, g.batch, c.sB));
+  } else {
+    return nfail(DSX_ERR_ARGUMENT, "conv_gemm: bad mode");
+  }
+  if (g.ksplit > 1) {
+    if (q.mode != kConvWgrad || g.epi != kEpiF32 || g.accumulate)
+      return nfail(DSX_ERR_ARGUMENT, "conv_gemm: split-K only for the fp32 wgrad");
+    const int nk = (g.K + kBK - 1) / kBK;
+    const int kper = (nk + g.ksplit - 1) / g.ksplit;
+    g.ksplit = (nk + kper - 1) / kper;
+  }
+  const int bn = c.bn ? c.bn : pick_bn(g, nsm);
+  if (bn != 64 && bn != 128 && bn != 256) return nfail(DSX_ERR_ARGUMENT, "conv_gemm: bn must be 64, 128 or 256");
+  if (q.mode == kConvFwd) {
+    NN_TRY(make_map(&tb, c.B, g.K, g.N, g.batch, c.ldb, c.sB, bn));
+    return launch_conv_bn<kConvFwd>(bn, ta, tb, g, s);
+  }
+  if (q.mode == kConvWgrad) return launch_conv_bn<kConvWgrad>(bn, ta, tb, g, s);
+  return launch_conv_bn<kConvDgrad>(bn, ta, tb, g, s);
+}
+
 dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm) {
-  const GemmArgs& g = c.g;
+  GemmArgs g = c.g;
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return DSX_OK;
+  if (g.ksplit > 1) {
+    if (!c.bf16 || g.epi != kEpiF32 || g.accumulate)
+      return nfail(DSX_ERR_ARGUMENT, "gemm: split-K needs the tensor-core path, fp32 output, no accumulate");
+    const int nk = (g.K + kBK - 1) / kBK;
+    const int kper = (nk + g.ksplit - 1) / g.ksplit;
+    g.ksplit = (nk + kper - 1) / kper;  // every split non-empty
+  }
   if (!c.bf16) {
     dim3 grid((g.N + 63) / 64, (g.M + 63) / 64, g.batch);
     const float* A = static_cast<const float*>(c.A);
@@ -175,7 +280,7 @@ dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm) {
   const long long tiles2 = (long long)((g.N + bn - 1) / bn) * ((g.M + 2 * kBM - 1) / (2 * kBM)) * g.batch;
   // (measured: 256-wide pairs 1290 -> 1431 TFLOP/s at 8192^3; 128-wide pairs
   // lose to single-CTA 128 tiles, so auto mode pairs only 256-wide tiles)
-  const bool two_sm = bn >= 128 && two_sm_env != 0 &&
+  const bool two_sm = bn >= 128 && two_sm_env != 0 && g.ksplit <= 1 &&
                       (two_sm_env == 1 || (bn == 256 && tiles2 >= nsm / 2));
   CUtensorMap ta, tb;
   if (two_sm) {
@@ -223,6 +328,8 @@ dsx_status dsx_gemm(const dsx_gemm_desc* d) {
   c.sB = d->strideB;
   c.out_bf16 = d->out_dtype == DSX_BF16;
   c.bn = d->bn;
+  c.g.ksplit = d->ksplit;
+  c.g.strideSplit = d->strideSplit;
   c.g.M = d->M;
   c.g.N = d->N;
   c.g.K = d->K;

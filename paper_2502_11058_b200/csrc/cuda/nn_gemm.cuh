@@ -35,7 +35,19 @@ enum : int {
   kEpiF32 = 0,       // C fp32 = acc (+ C if accumulate)
   kEpiBiasAct = 1,   // C = act(acc + bias[n])   (act: none / relu), T out
   kEpiDRelu = 2,     // C = acc * (mask(m,n) > 0), T out (dgrad through relu)
+  kEpiAdd = 3,       // C = acc + mask(m,n), T out (dgrad into a residual sum)
 };
+
+// Implicit-GEMM convolution (3x3, stride 1, pad 1, NHWC, channel counts
+// multiples of 64): the operand tiles are read straight from the activation
+// tensors by 5-D TMA boxes shifted by the filter tap, the padding coming from
+// TMA's out-of-bounds zero fill — no im2col / col2im buffers.
+//   kConvFwd    A(m=pixel, k=(tap,c)) = x[pixel + tap - 1][c]     (5-D map on x)
+//   kConvWgrad  B(n=(tap,c), k=pixel) = x[pixel + tap - 1][c]     (5-D map on x, MN-major)
+//   kConvDgrad  A(m=pixel, k=(tap,o)) = dy[pixel - tap + 1][o]    (5-D map on dy)
+//               B(n=c, k=(tap,o))     = W[o][tap][c]              (4-D map on W, MN-major)
+// A 128-pixel M tile / 64-pixel K block covers whole image rows (W | 64).
+enum : int { kConvNone = 0, kConvFwd = 1, kConvWgrad = 2, kConvDgrad = 3 };
 
 struct GemmArgs {
   int M, N, K, batch;
@@ -46,7 +58,24 @@ struct GemmArgs {
   long long strideBias;
   const void* mask;              // relu' source, same element type as C
   long long ldmask, strideMask;
+  // split-K (tensor-core path, kEpiF32 without accumulate): K is cut into
+  // ksplit ranges of whole k-blocks; split s writes its partial product to
+  // C + s * strideSplit, the caller sums the partials in a fixed order.
+  // 0 / 1: off.
+  int ksplit;
+  long long strideSplit;
+  // implicit conv geometry (CONV != kConvNone): image H x W, 64-channel
+  // chunks of the reduction operand per tap (Cin/64 fwd, Cout/64 dgrad),
+  // input channels (wgrad: the tap of output column n is n / cin)
+  int conv_h, conv_w, conv_cpb, conv_cin;
 };
+
+// pixel index p (multiple of the tile's row span) -> (image, row)
+__device__ __forceinline__ void conv_pix(const GemmArgs& g, int p, int* img, int* h) {
+  const int hw = g.conv_h * g.conv_w;
+  *img = p / hw;
+  *h = (p % hw) / g.conv_w;
+}
 
 // One GEMM call: operands (element pointers, leading dims, per-batch
 // strides), majors, tile width (0: auto) and the epilogue.  gemm() (gemm.cu)
@@ -63,6 +92,14 @@ struct GemmCall {
   GemmArgs g;
 };
 dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm);
+// Implicit-GEMM 3x3 / stride 1 / pad 1 convolution on the tensor cores
+// (see kConv*): B images of H x W, NHWC bf16 activations.  GemmCall carries
+// the operand pointers and per-worker strides (A = x or dy, B = W or x) and
+// the epilogue; M / N / K are derived from the geometry.
+struct ConvGeom {
+  int mode, H, W, B, cin, cout;
+};
+dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int nsm);
 
 constexpr int kBM = 128, kBK = 64, kUmmaK = 16;
 
@@ -86,6 +123,22 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
           su32(dst)),
       "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, "
+      "%7}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -140,9 +193,9 @@ __device__ __forceinline__ void epi_store(const GemmArgs& g, int b, int m, int n
     float v = acc + (g.bias ? g.bias[(long long)b * g.strideBias + n] : 0.f);
     if (g.relu) v = fmaxf(v, 0.f);
     *c = from_f<TOut>(v);
-  } else {  // kEpiDRelu
+  } else {  // kEpiDRelu / kEpiAdd
     const TOut mk = static_cast<const TOut*>(g.mask)[(long long)b * g.strideMask + (long long)m * g.ldmask + n];
-    *c = from_f<TOut>(to_f<TOut>(mk) > 0.f ? acc : 0.f);
+    *c = from_f<TOut>(g.epi == kEpiAdd ? acc + to_f<TOut>(mk) : (to_f<TOut>(mk) > 0.f ? acc : 0.f));
   }
 }
 
@@ -175,9 +228,9 @@ __device__ __forceinline__ float epi_value(const GemmArgs& g, int b, int m, int 
     float v = acc + (g.bias ? g.bias[(long long)b * g.strideBias + n] : 0.f);
     return g.relu ? fmaxf(v, 0.f) : v;
   }
-  if (g.epi == kEpiDRelu) {
+  if (g.epi == kEpiDRelu || g.epi == kEpiAdd) {
     const TOut mk = static_cast<const TOut*>(g.mask)[(long long)b * g.strideMask + (long long)m * g.ldmask + n];
-    return to_f<TOut>(mk) > 0.f ? acc : 0.f;
+    return g.epi == kEpiAdd ? acc + to_f<TOut>(mk) : (to_f<TOut>(mk) > 0.f ? acc : 0.f);
   }
   return acc;
 }
@@ -247,7 +300,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
       if (n1_ok) b1 = bp[1];
     }
     float mk0[16], mk1[16];
-    if (g.epi == kEpiDRelu) {
+    if (g.epi == kEpiDRelu || g.epi == kEpiAdd) {
       if (mwords && n1_ok) {  // prefetched by the caller one chunk ahead
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
@@ -281,6 +334,9 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
         } else if (g.epi == kEpiDRelu) {
           v0 = mk0[i2] > 0.f ? v0 : 0.f;
           v1 = mk1[i2] > 0.f ? v1 : 0.f;
+        } else if (g.epi == kEpiAdd) {
+          v0 += mk0[i2];
+          v1 += mk1[i2];
         }
         if (n1_ok) *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
         else *dst = from_f<TOut>(v0);
@@ -294,7 +350,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
 #pragma unroll
     for (int r0 = 0; r0 < 32; r0 += 8) {
       float mk[8];
-      if (g.epi == kEpiDRelu) {
+      if (g.epi == kEpiDRelu || g.epi == kEpiAdd) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int m = m0 + r0 + u;
@@ -319,6 +375,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
               if (g.relu) o = fmaxf(o, 0.f);
             } else if (g.epi == kEpiDRelu) {
               o = mk[u] > 0.f ? o : 0.f;
+            } else if (g.epi == kEpiAdd) {
+              o += mk[u];
             }
             TOut* dst = static_cast<TOut*>(g.C) + (long long)b * g.strideC + (long long)m * g.ldc + n;
             *dst = from_f<TOut>(o);
@@ -330,7 +388,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
   __syncwarp();
 }
 
-template <int BN, bool A_MN, bool B_MN, typename TOut>
+template <int BN, bool A_MN, bool B_MN, typename TOut, int CONV = kConvNone>
 __global__ void __launch_bounds__(192, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g) {
   using Cfg = TcCfg<BN>;
@@ -343,9 +401,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
   uint64_t* tempty = tfull + 2;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (g.K + kBK - 1) / kBK;
+  const int nk_all = (g.K + kBK - 1) / kBK;
+  const int ks = g.ksplit > 1 ? g.ksplit : 1;
+  const int kper = (nk_all + ks - 1) / ks;  // k-blocks per split (the host keeps every split non-empty)
   const int mt = (g.M + kBM - 1) / kBM, ntl = (g.N + BN - 1) / BN;
-  const int tiles = mt * ntl * g.batch;
+  const int per_split = mt * ntl * g.batch;
+  const int tiles = per_split * ks;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&ta) : "memory");
@@ -376,23 +437,46 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       int it = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         int b, mb, nb;
-        tile_coords(tile, mt, ntl, &b, &mb, &nb);
+        tile_coords(tile % per_split, mt, ntl, &b, &mb, &nb);
         const int m0 = mb * kBM, n0 = nb * BN;
-        for (int k = 0; k < nk; ++k, ++it) {
+        const int kb0 = (tile / per_split) * kper, kb1 = min(nk_all, kb0 + kper);
+        for (int k = kb0; k < kb1; ++k, ++it) {
           const int s = it % Cfg::kStages;
           const unsigned ph = (unsigned)(it / Cfg::kStages) & 1u;
           nn_mbar_wait(&empty[s], ph ^ 1u);
           uint8_t* sa = smem + s * Cfg::kStage;
           uint8_t* sb = sa + Cfg::kABytes;
           nn_mbar_expect_tx(&full[s], Cfg::kStage);
-          if constexpr (!A_MN) {
+          if constexpr (CONV == kConvFwd || CONV == kConvDgrad) {
+            // k-block = (tap, 64-channel chunk); the box is shifted by the tap
+            const int tap = k / g.conv_cpb, cb = k - tap * g.conv_cpb;
+            const int dh = tap / 3 - 1, dw = tap % 3 - 1;
+            int img, h;
+            conv_pix(g, m0, &img, &h);
+            if constexpr (CONV == kConvFwd) tma_load_5d(sa, &ta, &full[s], cb * kBK, dw, h + dh, img, b);
+            else tma_load_5d(sa, &ta, &full[s], cb * kBK, -dw, h - dh, img, b);
+          } else if constexpr (!A_MN) {
             tma_load_3d(sa, &ta, &full[s], k * kBK, m0, b);
           } else {
 #pragma unroll
             for (int i = 0; i < kBM / 64; ++i)
               tma_load_3d(sa + i * 64 * kBK * 2, &ta, &full[s], m0 + 64 * i, k * kBK, b);
           }
-          if constexpr (!B_MN) {
+          if constexpr (CONV == kConvWgrad) {
+            // 64 pixels of the reduction x 64 columns (one tap, 64 channels) per box
+            int img, h;
+            conv_pix(g, k * kBK, &img, &h);
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) {
+              const int n = min(n0 + 64 * i, g.N - 64);  // columns past N: any in-bounds data
+              const int tap = n / g.conv_cin, c0 = n - tap * g.conv_cin;
+              tma_load_5d(sb + i * 64 * kBK * 2, &tb, &full[s], c0, tap % 3 - 1, h + tap / 3 - 1, img, b);
+            }
+          } else if constexpr (CONV == kConvDgrad) {
+            const int tap = k / g.conv_cpb, cb = k - tap * g.conv_cpb;
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) tma_load_4d(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, tap, cb * kBK, b);
+          } else if constexpr (!B_MN) {
             tma_load_3d(sb, &tb, &full[s], k * kBK, n0, b);
           } else {
 #pragma unroll
@@ -414,6 +498,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
         nn_mbar_wait(&tempty[acc], aph ^ 1u);  // the epilogue drained this buffer
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
+        const int nk = min(nk_all, (tile / per_split + 1) * kper) - (tile / per_split) * kper;
         for (int k = 0; k < nk; ++k, ++it) {
           const int s = it % Cfg::kStages;
           const unsigned ph = (unsigned)(it / Cfg::kStages) & 1u;
@@ -442,15 +527,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
     float* st = epi_smem + (warp - 2) * 32 * 33;
     const bool ob = sizeof(TOut) == 2 && g.epi != kEpiF32 && (g.ldc & 1) == 0;
     int tc = 0;
+    GemmArgs gs = g;  // split s writes its partial at C + s * strideSplit
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tc) {
       int b, mb, nb;
-      tile_coords(tile, mt, ntl, &b, &mb, &nb);
+      tile_coords(tile % per_split, mt, ntl, &b, &mb, &nb);
       const int m0 = mb * kBM + 32 * q, n0 = nb * BN;
       const int acc = tc & 1;
+      if (ks > 1) gs.C = static_cast<float*>(g.C) + (long long)(tile / per_split) * g.strideSplit;
       nn_mbar_wait(&tfull[acc], (unsigned)(tc >> 1) & 1u);
       tc_fence_after();
       // bf16 dgrad: the ReLU' mask words of chunk c+1 load while chunk c drains
-      const bool pre = ob && g.epi == kEpiDRelu && (g.ldmask & 1) == 0;
+      const bool pre = ob && (g.epi == kEpiDRelu || g.epi == kEpiAdd) && (g.ldmask & 1) == 0;
       uint32_t mw_cur[16], mw_nxt[16];
       if (pre) load_mask_words<TOut>(g, b, m0, n0 + 2 * (lane & 15), lane, mw_cur);
 #pragma unroll 1
@@ -458,7 +545,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
         if (n0 + c >= g.N) break;
         const bool more = pre && c + 32 < BN && n0 + c + 32 < g.N;
         if (more) load_mask_words<TOut>(g, b, m0, n0 + c + 32 + 2 * (lane & 15), lane, mw_nxt);
-        epi_chunk<TOut>(g, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob,
+        epi_chunk<TOut>(gs, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), st, lane, b, m0, n0 + c, ob,
                         pre ? mw_cur : nullptr);
         if (more)
 #pragma unroll

@@ -258,6 +258,18 @@ __global__ void load_x_kernel(const StepDev* __restrict__ sp, T* __restrict__ y,
 }
 
 
+// split-K partials -> out: out[b*s_out + i] = sum_s part[s*s_split + b*n + i]
+// in split order (deterministic); n elements per batch entry (blockIdx.y)
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int ks, long long s_split, long long n,
+                                     float* __restrict__ out, long long s_out) {
+  const long long b = blockIdx.y;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < ks; ++s) acc += part[s * s_split + b * n + i];
+    out[b * s_out + i] = acc;
+  }
+}
+
 inline int blocks_for(long long n, int nsm) {
   return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, nsm * 8LL));
 }

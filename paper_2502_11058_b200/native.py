@@ -52,7 +52,7 @@ class GemmDescC(C.Structure):
         ("out_dtype", C.c_int), ("epi", C.c_int), ("relu", C.c_int), ("accumulate", C.c_int),
         ("bias", C.c_void_p), ("strideBias", C.c_longlong),
         ("mask", C.c_void_p), ("ldmask", C.c_longlong), ("strideMask", C.c_longlong),
-        ("bn", C.c_int), ("stream", C.c_void_p),
+        ("bn", C.c_int), ("stream", C.c_void_p), ("ksplit", C.c_int), ("strideSplit", C.c_longlong),
     ]
 
 
@@ -163,6 +163,7 @@ _NN_SIGS = {
     "dsx_cnn_event_record": ([C.c_void_p, C.c_int], C.c_int),
     "dsx_cnn_event_elapsed": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "dsx_cnn_launch_count": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
+    "dsx_cnn_profile": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
 }
 _SIGS.update(_NN_SIGS)
 

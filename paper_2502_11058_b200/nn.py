@@ -212,7 +212,7 @@ class Mlp:
 
 def gemm(A, B, C_out, *, M, N_, K, batch=1, a_mn=False, b_mn=False, lda, sA=0, ldb, sB=0, ldc, sC=0,
          epi=N.DSX_EPI_F32, relu=False, bias=None, s_bias=0, mask=None, ldmask=0, s_mask=0,
-         accumulate=False, bn=0, dtype="bf16", stream=0) -> None:
+         accumulate=False, bn=0, dtype="bf16", stream=0, ksplit=0, s_split=0) -> None:
     """dsx_gemm on torch CUDA tensors (test hook for the layer GEMMs)."""
     d = N.GemmDescC()
     d.dtype = N.DSX_BF16 if dtype == "bf16" else N.DSX_F32
@@ -230,4 +230,5 @@ def gemm(A, B, C_out, *, M, N_, K, batch=1, a_mn=False, b_mn=False, lda, sA=0, l
     d.ldmask, d.strideMask = ldmask, s_mask
     d.bn = bn
     d.stream = stream
+    d.ksplit, d.strideSplit = ksplit, s_split
     N.call("dsx_gemm", C.byref(d))

@@ -93,6 +93,18 @@ def test_cnn_bf16_tracks_float64_loss():
         assert _rel(got[k], orc.w[k]) < 2e-2
 
 
+@pytest.mark.parametrize("image", [16, 32])
+def test_cnn_implicit_gemm_convs_track_float64(image):
+    """Width 64: every 3x3 stride-1 conv runs as an implicit GEMM (shifted
+    5-D TMA boxes, no im2col); 3 steps at K = 2 track float64 (images 16:
+    stage grids 16/8/4/2; 32: 32/16/8/4)."""
+    got, orc, losses, _, _ = _run(64, image, 2, 2, 3, "momentum", 0.02, dtype="bf16", bsz=4)
+    for gl, ol in losses:
+        np.testing.assert_allclose(gl, ol, rtol=3e-2)
+    for k in range(2):
+        assert _rel(got[k], orc.w[k]) < 2e-2, (k, _rel(got[k], orc.w[k]))
+
+
 def test_cnn_resnet18_bf16_first_step_loss():
     """Full ResNet-18 geometry, K = 2, batch 8: the tensor-core forward's loss
     within bf16 rounding of float64's, per worker."""

@@ -85,6 +85,28 @@ def test_tc_gemm_wgrad_mn(M, N_, K, batchn, bn):
     assert _rel(C, ref) < 1e-5
 
 
+@pytest.mark.parametrize("M,N_,K,batchn,ks", [(64, 576, 8192, 4, 6), (64, 72, 4000, 2, 7), (128, 1152, 2048, 1, 3)])
+def test_tc_gemm_wgrad_split_k(M, N_, K, batchn, ks):
+    """Split-K wgrad (the conv stack's long B*H*W reductions): every split's
+    partial product lands in its own slot; their sum equals the product."""
+    torch.manual_seed(5)
+    dy = torch.randn(batchn, K, M, device=DEV).bfloat16()
+    x = torch.randn(batchn, K, N_, device=DEV).bfloat16()
+    part = torch.full((ks, batchn, M, N_), float("nan"), device=DEV)
+    gemm(dy, x, part, M=M, N_=N_, K=K, batch=batchn, a_mn=True, b_mn=True, lda=M, sA=K * M, ldb=N_, sB=K * N_,
+         ldc=N_, sC=M * N_, bn=256 if N_ >= 256 else 64, ksplit=ks, s_split=batchn * M * N_)
+    torch.cuda.synchronize()
+    nk = (K + 63) // 64
+    kper = (nk + ks - 1) // ks
+    used = (nk + kper - 1) // kper
+    ref = torch.bmm(dy.float().transpose(1, 2), x.float())
+    assert _rel(part[:used].sum(0), ref) < 1e-5
+    for s in range(used):  # each slot is its own K range
+        lo, hi = s * kper * 64, min(K, (s + 1) * kper * 64)
+        want = torch.bmm(dy.float()[:, lo:hi].transpose(1, 2), x.float()[:, lo:hi])
+        assert _rel(part[s], want) < 1e-5, s
+
+
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True), (True, False)])
 def test_f32_gemm_against_fp64(a_mn, b_mn):
     torch.manual_seed(3)
