@@ -181,6 +181,37 @@ __global__ void col2im_kernel(const T* __restrict__ dcol, T* __restrict__ dx, in
   }
 }
 
+// Column sums of rows [chunk*chunk_rows, +chunk_rows) of dz[b] (C columns,
+// C % 8 == 0, C <= 2048): part[(chunk * kl + b) * C + c].  Each thread sums
+// 8 columns of every rows_par-th row; the row groups combine in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ dz, long long ld, long long s_dz,
+                                                          int rows, int C, int chunk_rows, float* __restrict__ part) {
+  __shared__ float sh[2048];
+  const int b = blockIdx.y;
+  const int tpr = C / 8, rows_par = max(1, 256 / tpr);
+  const int r_off = threadIdx.x / tpr, cv = threadIdx.x % tpr;
+  const int r0 = blockIdx.x * chunk_rows, r1 = min(rows, r0 + chunk_rows);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool active = r_off < rows_par && tpr <= 256;
+  if (active) {
+    const T* p = dz + b * s_dz + cv * 8;
+    for (int r = r0 + r_off; r < r1; r += rows_par) {
+      const Vec8<T> v = ld8(p + (long long)r * ld);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += el(v, j);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sh[r_off * C + cv * 8 + j] = acc[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float t = 0.f;
+    for (int rr = 0; rr < rows_par; ++rr) t += sh[rr * C + c];
+    part[((long long)blockIdx.x * gridDim.y + b) * C + c] = t;
+  }
+}
+
 // y = relu(a + s) (the block output); n elements per worker (multiple of
 // 8), worker blockIdx.y at stride sx
 template <typename T>
@@ -298,6 +329,7 @@ struct dsx_cnn {
   void* dpool = nullptr;         // [kl][B][C]
   void *g0 = nullptr, *g1 = nullptr, *ga = nullptr, *gh = nullptr, *gcol = nullptr, *gsc = nullptr;
   float* wpart = nullptr;  // split-K wgrad partials
+  float* cpart = nullptr;  // bias-gradient column-sum partials [2*nsm][C]
   long long act_max = 0, col_max = 0;  // elements per worker
   float *loss_part = nullptr, *loss = nullptr;
   float* xin = nullptr;
@@ -485,15 +517,22 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
     }
   }
   {
-    dim3 grid((cv.cout + 31) / 32, m->kl);
+    // bias gradient: two-pass column sum over the B*Ho*Wo rows (row chunks
+    // -> per-chunk partials -> fixed-order sum), ~2 blocks per SM
+    const int tpr = cv.cout / 8, rows_par = std::max(1, 256 / tpr);
+    const int nchunks = (int)std::max<long long>(
+        1, std::min<long long>(2LL * m->nsm / m->kl, M / (4LL * rows_par)));
+    const int chunk_rows = (int)((M + nchunks - 1) / nchunks);
+    dim3 grid(nchunks, m->kl);
     if (m->bf16)
-      colsum_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(static_cast<const __nv_bfloat16*>(g), cv.cout,
-                                                                m->act_max, (int)M, cv.cout,
-                                                                m->grads + m->boff[cv.layer], m->P);
+      colsum_part_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(static_cast<const __nv_bfloat16*>(g), cv.cout,
+                                                                     m->act_max, (int)M, cv.cout, chunk_rows, m->cpart);
     else
-      colsum_kernel<float><<<grid, 256, 0, m->stream>>>(static_cast<const float*>(g), cv.cout, m->act_max, (int)M,
-                                                        cv.cout, m->grads + m->boff[cv.layer], m->P);
-    ++m->launches;
+      colsum_part_kernel<float><<<grid, 256, 0, m->stream>>>(static_cast<const float*>(g), cv.cout, m->act_max,
+                                                             (int)M, cv.cout, chunk_rows, m->cpart);
+    splitk_reduce_kernel<<<dim3(1, m->kl), 256, 0, m->stream>>>(m->cpart, nchunks, (long long)m->kl * cv.cout,
+                                                                cv.cout, m->grads + m->boff[cv.layer], m->P);
+    m->launches += 2;
   }
   if (dgrad && cv.implicit) {
     GemmCall c = cbase(m);
@@ -991,6 +1030,7 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
   for (size_t i = 0; ok && i < m->blocks.size(); ++i) ok = alloc(&m->blocks[i].y, actb);
   ok = ok && alloc(&m->g0, actb) && alloc(&m->g1, actb) && alloc(&m->ga, actb) && alloc(&m->gh, actb) &&
        alloc(&m->gsc, actb) && alloc(&m->gcol, colb) && (wpart == 0 || alloc((void**)&m->wpart, 4ull * wpart)) &&
+       alloc((void**)&m->cpart, 4ull * 2 * m->nsm * (m->w0 << 3)) &&
        alloc(&m->pool, es * m->kl * m->batch * cin) && alloc(&m->dpool, es * m->kl * m->batch * cin) &&
        alloc((void**)&m->logits, 4ull * m->kl * m->batch * m->classes) &&
        alloc(&m->dlog, es * m->kl * m->batch * ((m->classes + 7) / 8 * 8)) &&
