@@ -31,3 +31,20 @@ def test_mlp_multirank_matches_single_gpu(world, graphs):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert '"pass": true' in out.stdout
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_cnn_multirank_matches_single_gpu(world, dtype):
+    """The conv stack (BASELINE configs[1] shape) across ranks: fp32 within
+    1e-5 of one GPU and of float64; bf16 (implicit-GEMM convs) within bf16
+    tolerance; averaged layers identical on every worker."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29640 + world + 10 * (dtype == "bf16")),
+           os.path.join(REPO, "tests", "multigpu_cnn.py")]
+    env = dict(os.environ, DSX_TEST_DTYPE=dtype)
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert '"pass": true' in out.stdout
