@@ -67,6 +67,11 @@ typedef struct dsx_gemm_desc {
   void* stream;              /* cudaStream_t (NULL: default stream) */
   int ksplit;                /* split-K (bf16, DSX_EPI_F32, no accumulate): split s of K writes */
   long long strideSplit;     /* its partial at C + s * strideSplit; 0/1: off */
+  /* implicit-GEMM 3x3 / stride 1 / pad 1 convolution (bf16; M, N, K derived):
+   * conv = 1 forward (A = x NHWC, B = W[o][kh][kw][c]), 2 wgrad (A = dy,
+   * B = x), 3 dgrad (A = dy, B = W); strideA / strideB are per batch entry;
+   * 0: plain GEMM */
+  int conv, conv_h, conv_w, conv_images, conv_cin, conv_cout;
 } dsx_gemm_desc;
 dsx_status dsx_gemm(const dsx_gemm_desc* d);
 

@@ -94,10 +94,10 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
 }
 
 // CTA-pair kernel: grid = 2 x clusters (compile-time cluster dims 2x1x1)
-template <int BN, bool AM, bool BM_, typename TOut>
+template <int BN, bool AM, bool BM_, typename TOut, int CONV = kConvNone>
 dsx_status launch_tc2_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  auto kern = gemm_tc2_kernel<BN, AM, BM_, TOut>;
+  auto kern = gemm_tc2_kernel<BN, AM, BM_, TOut, CONV>;
   dsx::once_per_device(attr, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg<BN>::kSmem);
   });
@@ -172,7 +172,16 @@ dsx_status make_act_map(CUtensorMap* map, const void* base, int C, int W, int H,
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return nfail(DSX_ERR_CUDA, "cuTensorMapEncodeTiled(5-D) failed (" + std::to_string((int)r) + ")");
+  if (r != CUDA_SUCCESS) {
+    std::string d = "cuTensorMapEncodeTiled(5-D) failed (" + std::to_string((int)r) + "): dims";
+    for (auto v : dims) d += " " + std::to_string((unsigned long long)v);
+    d += " strides";
+    for (auto v : strides) d += " " + std::to_string((unsigned long long)v);
+    d += " box";
+    for (auto v : box) d += " " + std::to_string(v);
+    d += " base " + std::to_string(reinterpret_cast<uintptr_t>(base));
+    return nfail(DSX_ERR_CUDA, d);
+  }
   return DSX_OK;
 }
 
@@ -193,9 +202,12 @@ dsx_status make_tap_map(CUtensorMap* map, const void* base, int cin, int cout, i
 }
 
 template <int MODE>
-dsx_status launch_conv_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+dsx_status launch_conv_bn(int bn, bool two_sm, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
+                          cudaStream_t s) {
   constexpr bool AM = MODE == kConvWgrad, BM_ = MODE != kConvFwd;
   using T = std::conditional_t<MODE == kConvWgrad, float, __nv_bfloat16>;
+  if (two_sm) return bn == 128 ? launch_tc2_t<128, AM, BM_, T, MODE>(ta, tb, g, s)
+                               : launch_tc2_t<256, AM, BM_, T, MODE>(ta, tb, g, s);
   switch (bn) {
     case 64: return launch_tc_t<64, AM, BM_, T, MODE>(ta, tb, g, s);
     case 128: return launch_tc_t<128, AM, BM_, T, MODE>(ta, tb, g, s);
@@ -238,12 +250,21 @@ dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int n
   }
   const int bn = c.bn ? c.bn : pick_bn(g, nsm);
   if (bn != 64 && bn != 128 && bn != 256) return nfail(DSX_ERR_ARGUMENT, "conv_gemm: bn must be 64, 128 or 256");
+  // CTA pairs (M = 256 MMAs; each SM loads half of B): DSX_CONV_2SM=1.
+  // Off by default: measured 12.73 vs 12.61 ms per ResNet-18 step (pairs
+  // halve the weight traffic, but these short-K tiles are not B-bound).
+  static const bool pairs_ok = [] {
+    const char* e = std::getenv("DSX_CONV_2SM");
+    return e && e[0] == '1';
+  }();
+  const long long tiles2 = (long long)((g.N + bn - 1) / bn) * ((g.M + 2 * kBM - 1) / (2 * kBM)) * g.batch;
+  const bool two_sm = pairs_ok && bn >= 128 && g.ksplit <= 1 && g.M >= 2 * kBM && tiles2 >= nsm / 2;
   if (q.mode == kConvFwd) {
-    NN_TRY(make_map(&tb, c.B, g.K, g.N, g.batch, c.ldb, c.sB, bn));
-    return launch_conv_bn<kConvFwd>(bn, ta, tb, g, s);
+    NN_TRY(make_map(&tb, c.B, g.K, g.N, g.batch, c.ldb, c.sB, two_sm ? bn / 2 : bn));
+    return launch_conv_bn<kConvFwd>(bn, two_sm, ta, tb, g, s);
   }
-  if (q.mode == kConvWgrad) return launch_conv_bn<kConvWgrad>(bn, ta, tb, g, s);
-  return launch_conv_bn<kConvDgrad>(bn, ta, tb, g, s);
+  if (q.mode == kConvWgrad) return launch_conv_bn<kConvWgrad>(bn, two_sm, ta, tb, g, s);
+  return launch_conv_bn<kConvDgrad>(bn, two_sm, ta, tb, g, s);
 }
 
 dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm) {
@@ -346,6 +367,10 @@ dsx_status dsx_gemm(const dsx_gemm_desc* d) {
   c.g.ldmask = d->ldmask;
   c.g.strideMask = d->strideMask;
   if (!c.bf16 && c.out_bf16) return nfail(DSX_ERR_ARGUMENT, "fp32 gemm writes fp32");
+  if (d->conv) {
+    const ConvGeom q{d->conv, d->conv_h, d->conv_w, d->conv_images, d->conv_cin, d->conv_cout};
+    return conv_gemm(c, q, static_cast<cudaStream_t>(d->stream), nsm);
+  }
   return gemm(c, static_cast<cudaStream_t>(d->stream), nsm);
 }
 

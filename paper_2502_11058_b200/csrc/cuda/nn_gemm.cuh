@@ -603,6 +603,22 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* ma
       "l"(map), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6, %7}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 __device__ __forceinline__ void tc2_mma(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
@@ -637,7 +653,7 @@ __device__ __forceinline__ void nn_mbar_wait_bounded(uint64_t* b, unsigned parit
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, typename TOut>
+template <int BN, bool A_MN, bool B_MN, typename TOut, int CONV = kConvNone>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g) {
   using Cfg = Tc2Cfg<BN>;
@@ -695,14 +711,35 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ 
           uint8_t* sa = smem + s * Cfg::kStage;
           uint8_t* sb = sa + Cfg::kABytes;
           if (leader) nn_mbar_expect_tx(&full[s], 2 * Cfg::kStage);
-          if constexpr (!A_MN) {
+          if constexpr (CONV == kConvFwd || CONV == kConvDgrad) {
+            const int tap = k / g.conv_cpb, cb = k - tap * g.conv_cpb;
+            const int dh = tap / 3 - 1, dw = tap % 3 - 1;
+            int img, h;
+            conv_pix(g, m0, &img, &h);
+            if constexpr (CONV == kConvFwd) tma_load_5d_2sm(sa, &ta, &full[s], cb * kBK, dw, h + dh, img, b);
+            else tma_load_5d_2sm(sa, &ta, &full[s], cb * kBK, -dw, h - dh, img, b);
+          } else if constexpr (!A_MN) {
             tma_load_3d_2sm(sa, &ta, &full[s], k * kBK, m0, b);
           } else {
 #pragma unroll
             for (int i = 0; i < kBM / 64; ++i)
               tma_load_3d_2sm(sa + i * 64 * kBK * 2, &ta, &full[s], m0 + 64 * i, k * kBK, b);
           }
-          if constexpr (!B_MN) {
+          if constexpr (CONV == kConvWgrad) {
+            int img, h;
+            conv_pix(g, k * kBK, &img, &h);
+#pragma unroll
+            for (int i = 0; i < BN / 2 / 64; ++i) {
+              const int n = min(n0 + 64 * i, g.N - 64);
+              const int tap = n / g.conv_cin, c0 = n - tap * g.conv_cin;
+              tma_load_5d_2sm(sb + i * 64 * kBK * 2, &tb, &full[s], c0, tap % 3 - 1, h + tap / 3 - 1, img, b);
+            }
+          } else if constexpr (CONV == kConvDgrad) {
+            const int tap = k / g.conv_cpb, cb = k - tap * g.conv_cpb;
+#pragma unroll
+            for (int i = 0; i < BN / 2 / 64; ++i)
+              tma_load_4d_2sm(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, tap, cb * kBK, b);
+          } else if constexpr (!B_MN) {
             tma_load_3d_2sm(sb, &tb, &full[s], k * kBK, n0, b);
           } else {
 #pragma unroll
@@ -758,7 +795,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ 
       nn_mbar_wait_bounded(&tfull[acc], (unsigned)(tc >> 1) & 1u);
       tc_fence_after();
       // bf16 dgrad: the ReLU' mask words of chunk c+1 load while chunk c drains
-      const bool pre = ob && g.epi == kEpiDRelu && (g.ldmask & 1) == 0;
+      const bool pre = ob && (g.epi == kEpiDRelu || g.epi == kEpiAdd) && (g.ldmask & 1) == 0;
       uint32_t mw_cur[16], mw_nxt[16];
       if (pre) load_mask_words<TOut>(g, b, m0, n0 + 2 * (lane & 15), lane, mw_cur);
 #pragma unroll 1

@@ -310,3 +310,72 @@ def test_mlp_cuda_graph_with_empty_masks():
     w = [m.get_params(k) for k in range(K)]
     assert np.array_equal(w[0], w[1])  # the last step averaged everything
     m.close()
+
+
+def _nchw(t, B, H, W):
+    return t.float().view(B, H, W, -1).permute(0, 3, 1, 2)
+
+
+@pytest.mark.parametrize("H,B,cin,cout", [(32, 2, 64, 64), (16, 3, 128, 128), (8, 4, 64, 192), (4, 8, 256, 128),
+                                          (2, 16, 64, 64)])
+def test_implicit_conv_gemms_match_torch_conv2d(H, B, cin, cout):
+    """The implicit-GEMM 3x3 conv (tap-shifted 5-D TMA boxes, zero padding by
+    TMA out-of-bounds fill) against torch's conv2d and its two gradients on
+    the same bf16 operands: forward (bf16 out, bias + ReLU), wgrad (fp32 out,
+    also split-K), dgrad (bf16 out, ReLU' and residual-add epilogues); two
+    workers batched (the CTA-pair kernels: the next test)."""
+    import torch.nn.functional as F
+    torch.manual_seed(7)
+    nb = 2
+    P = B * H * H
+    x = torch.randn(nb, P, cin, device=DEV).bfloat16()
+    w = (torch.randn(nb, cout, 9 * cin, device=DEV) / (3 * cin ** 0.5)).bfloat16()
+    dy = torch.randn(nb, P, cout, device=DEV).bfloat16()
+    bias = torch.randn(nb, cout, device=DEV)
+    mask = torch.randn(nb, P, cin, device=DEV).bfloat16()
+    xs = [_nchw(x[i], B, H, H) for i in range(nb)]
+    ws = [w[i].float().view(cout, 3, 3, cin).permute(0, 3, 1, 2) for i in range(nb)]
+    dys = [_nchw(dy[i], B, H, H) for i in range(nb)]
+    # forward
+    y = torch.zeros(nb, P, cout, device=DEV, dtype=torch.bfloat16)
+    gemm(x, w, y, M=0, N_=0, K=0, batch=nb, lda=cin, sA=P * cin, ldb=9 * cin, sB=cout * 9 * cin, ldc=cout,
+         sC=P * cout, epi=N.DSX_EPI_BIAS_ACT, relu=True, bias=bias, s_bias=cout, conv=(1, H, H, B, cin, cout))
+    torch.cuda.synchronize()
+    for i in range(nb):
+        ref = torch.relu(F.conv2d(xs[i], ws[i], padding=1) + bias[i].view(1, -1, 1, 1))
+        assert _rel(_nchw(y[i], B, H, H), ref.bfloat16().float()) < 1e-2, i
+    # wgrad (plain and split-K partials)
+    for ks in (1, 3):
+        dw = torch.zeros(ks, nb, cout, 9 * cin, device=DEV)
+        gemm(dy, x, dw, M=0, N_=0, K=0, batch=nb, a_mn=True, b_mn=True, lda=cout, sA=P * cout, ldb=cin,
+             sB=P * cin, ldc=9 * cin, sC=cout * 9 * cin, ksplit=ks, s_split=nb * cout * 9 * cin,
+             conv=(2, H, H, B, cin, cout))
+        torch.cuda.synchronize()
+        got = dw.sum(0)
+        for i in range(nb):
+            ref = torch.nn.grad.conv2d_weight(xs[i], (cout, cin, 3, 3), dys[i], padding=1)
+            assert _rel(got[i].view(cout, 3, 3, cin).permute(0, 3, 1, 2), ref) < 1e-5, (ks, i)
+    # dgrad with the ReLU' mask, then with a residual addend
+    for epi in (N.DSX_EPI_DRELU, 3):
+        dx = torch.zeros(nb, P, cin, device=DEV, dtype=torch.bfloat16)
+        gemm(dy, w, dx, M=0, N_=0, K=0, batch=nb, b_mn=True, lda=cout, sA=P * cout, ldb=9 * cin,
+             sB=cout * 9 * cin, ldc=cin, sC=P * cin, epi=epi, mask=mask, ldmask=cin, s_mask=P * cin,
+             conv=(3, H, H, B, cin, cout))
+        torch.cuda.synchronize()
+        for i in range(nb):
+            ref = torch.nn.grad.conv2d_input(xs[i].shape, ws[i], dys[i], padding=1)
+            mk = _nchw(mask[i], B, H, H)
+            ref = ref * (mk > 0) if epi == N.DSX_EPI_DRELU else ref + mk
+            assert _rel(_nchw(dx[i], B, H, H), ref.bfloat16().float()) < 1e-2, (epi, i)
+
+
+def test_implicit_conv_gemms_cta_pairs():
+    """The same checks with the CTA-pair (cta_group::2) conv kernels
+    (DSX_CONV_2SM=1 is read once per process: run in a child)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DSX_CONV_2SM="1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", __file__, "-k",
+                          "implicit_conv_gemms_match"], capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
