@@ -74,8 +74,54 @@ dsx_status make_map(CUtensorMap* map, const void* base, long long inner, long lo
   return DSX_OK;
 }
 
+// bf16 C written by TMA stores (the CST epilogue): C, its strides and the
+// ReLU' / residual operand must be 16-B aligned.  DSX_GEMM_TMA_STORE=0: off.
+bool tma_store_ok(const GemmArgs& g) {
+  static const bool on = [] {
+    const char* e = std::getenv("DSX_GEMM_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || g.epi == kEpiF32 || (reinterpret_cast<uintptr_t>(g.C) & 15) || g.ldc % 8 || g.strideC % 8) return false;
+  if (g.epi == kEpiDRelu || g.epi == kEpiAdd)
+    return !(reinterpret_cast<uintptr_t>(g.mask) & 15) && g.ldmask % 8 == 0 && g.strideMask % 8 == 0;
+  return true;
+}
+
+dsx_status make_c_map(CUtensorMap* map, const GemmArgs& g) {
+  NN_TRY(get_encoder());
+  cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+  cuuint64_t strides[2] = {(cuuint64_t)g.ldc * 2,
+                           (cuuint64_t)std::max<long long>(g.strideC, g.ldc * (long long)g.M) * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, g.C, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return nfail(DSX_ERR_CUDA, "cuTensorMapEncodeTiled(C) failed (" + std::to_string((int)r) + ")");
+  return DSX_OK;
+}
+
 template <int BN, bool AM, bool BM_, typename TOut, int CONV = kConvNone>
 dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+  if constexpr (std::is_same_v<TOut, __nv_bfloat16>) {
+    if (tma_store_ok(g)) {
+      static std::atomic<unsigned long long> attr_c{0};
+      auto kc = gemm_tc_kernel<BN, AM, BM_, TOut, CONV, true>;
+      dsx::once_per_device(attr_c, [&] {
+        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::kSmem);
+      });
+      CUtensorMap tcm;
+      NN_TRY(make_c_map(&tcm, g));
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const long long tiles =
+          (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
+      kc<<<(int)std::min<long long>(tiles, nsm), 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g, tcm);
+      NN_CUDA(cudaGetLastError());
+      return DSX_OK;
+    }
+  }
   static std::atomic<unsigned long long> attr{0};
   auto kern = gemm_tc_kernel<BN, AM, BM_, TOut, CONV>;
   dsx::once_per_device(attr, [&] {
@@ -88,7 +134,8 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   const long long tiles =
       (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
   const int grid = (int)std::min<long long>(tiles, nsm);
-  kern<<<grid, 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g);
+  CUtensorMap unused{};
+  kern<<<grid, 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g, unused);
   NN_CUDA(cudaGetLastError());
   return DSX_OK;
 }

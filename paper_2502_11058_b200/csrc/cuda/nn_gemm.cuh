@@ -388,9 +388,96 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
   __syncwarp();
 }
 
-template <int BN, bool A_MN, bool B_MN, typename TOut, int CONV = kConvNone>
+// TMA-store epilogue of one 32-row x 32-column bf16 chunk (the CST kernels):
+// the accumulator row each lane holds after tcgen05.ld gets bias (one
+// coalesced load + shuffles) / ReLU / ReLU' or the residual addend (the
+// lane's 64-B row segment, vector loads), is packed to bf16 into this warp's
+// staging buffer (64-B rows, double-buffered) and written by one
+// cp.async.bulk.tensor store; TMA clips rows / columns outside C.
+__device__ __forceinline__ void epi_chunk_tma(const GemmArgs& g, const CUtensorMap* tcm, uint32_t taddr,
+                                              uint8_t* stage, int lane, int b, int m0, int n0) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  const int m = m0 + lane;
+  // operands fetched while the TMEM load is in flight
+  float bl = 0.f;
+  if (g.epi == kEpiBiasAct && g.bias && n0 + lane < g.N) bl = g.bias[(long long)b * g.strideBias + n0 + lane];
+  uint4 mw[4] = {};
+  if ((g.epi == kEpiDRelu || g.epi == kEpiAdd) && m < g.M) {
+    const __nv_bfloat16* mp =
+        static_cast<const __nv_bfloat16*>(g.mask) + (long long)b * g.strideMask + (long long)m * g.ldmask + n0;
+    if (n0 + 32 <= g.N) {
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) mw[q4] = reinterpret_cast<const uint4*>(mp)[q4];
+    } else {
+      __nv_bfloat16* mb = reinterpret_cast<__nv_bfloat16*>(mw);
+      for (int j = 0; j < 32 && n0 + j < g.N; ++j) mb[j] = mp[j];
+    }
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (g.epi == kEpiBiasAct) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] += __shfl_sync(0xffffffffu, bl, j);
+      if (g.relu) v[j] = fmaxf(v[j], 0.f);
+    }
+  } else if (g.epi == kEpiDRelu || g.epi == kEpiAdd) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(mw);
+#pragma unroll
+    for (int j2 = 0; j2 < 16; ++j2) {
+      const float lo = __uint_as_float(w[j2] << 16), hi = __uint_as_float(w[j2] & 0xFFFF0000u);
+      if (g.epi == kEpiAdd) {
+        v[2 * j2] += lo;
+        v[2 * j2 + 1] += hi;
+      } else {
+        v[2 * j2] = lo > 0.f ? v[2 * j2] : 0.f;
+        v[2 * j2 + 1] = hi > 0.f ? v[2 * j2 + 1] : 0.f;
+      }
+    }
+  }
+  // the store issued from this buffer two chunks ago must have read it
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+  uint4* dst = reinterpret_cast<uint4*>(stage + lane * 64);
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    uint4 o;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * q4 + 0], v[8 * q4 + 1]);
+    __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * q4 + 2], v[8 * q4 + 3]);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * q4 + 4], v[8 * q4 + 5]);
+    __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * q4 + 6], v[8 * q4 + 7]);
+    o.x = *reinterpret_cast<uint32_t*>(&p0);
+    o.y = *reinterpret_cast<uint32_t*>(&p1);
+    o.z = *reinterpret_cast<uint32_t*>(&p2);
+    o.w = *reinterpret_cast<uint32_t*>(&p3);
+    dst[q4] = o;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tcm),
+        "r"(su32(stage)), "r"(n0), "r"(m0), "r"(b)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, typename TOut, int CONV = kConvNone, bool CST = false>
 __global__ void __launch_bounds__(192, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g) {
+gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g,
+               const __grid_constant__ CUtensorMap tcm) {
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -527,6 +614,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
     float* st = epi_smem + (warp - 2) * 32 * 33;
     const bool ob = sizeof(TOut) == 2 && g.epi != kEpiF32 && (g.ldc & 1) == 0;
     int tc = 0;
+    int chunk_ctr = 0;  // CST: alternates the two staging buffers
     GemmArgs gs = g;  // split s writes its partial at C + s * strideSplit
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tc) {
       int b, mb, nb;
@@ -539,6 +627,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       // bf16 dgrad: the ReLU' mask words of chunk c+1 load while chunk c drains
       const bool pre = ob && (g.epi == kEpiDRelu || g.epi == kEpiAdd) && (g.ldmask & 1) == 0;
       uint32_t mw_cur[16], mw_nxt[16];
+      if constexpr (CST) {
+        uint8_t* stg = reinterpret_cast<uint8_t*>(st);  // 2 x 2 KB staging buffers of this warp
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          if (n0 + c >= g.N) break;
+          epi_chunk_tma(g, &tcm, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c),
+                        stg + (chunk_ctr++ & 1) * 2048, lane, b, m0, n0 + c);
+        }
+        tc_fence_before();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[acc])) : "memory");
+        continue;
+      }
       if (pre) load_mask_words<TOut>(g, b, m0, n0 + 2 * (lane & 15), lane, mw_cur);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -555,6 +655,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       // this warp's TMEM reads of buffer `acc` are complete (wait::ld above)
       tc_fence_before();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[acc])) : "memory");
+    }
+    if constexpr (CST) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   }
   tc_fence_before();
