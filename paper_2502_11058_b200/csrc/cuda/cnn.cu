@@ -212,6 +212,20 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ 
   }
 }
 
+// split-K partials of dW^T [rows = k*k*Cin][Cout] -> dW [Cout][rows]:
+// out[b*s_out + o*rows + r] = sum_s part[s*s_split + (b*rows + r)*cout + o]
+// (split order fixed; reads coalesced over o)
+__global__ void splitk_reduce_t_kernel(const float* __restrict__ part, int ks, long long s_split, int rows, int cout,
+                                       float* __restrict__ out, long long s_out) {
+  const long long b = blockIdx.y, n = (long long)rows * cout;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cout), o = (int)(i % cout);
+    float acc = 0.f;
+    for (int s = 0; s < ks; ++s) acc += part[s * s_split + b * n + i];
+    out[b * s_out + (long long)o * rows + r] = acc;
+  }
+}
+
 // y = relu(a + s) (the block output); n elements per worker (multiple of
 // 8), worker blockIdx.y at stride sx
 template <typename T>
@@ -428,10 +442,23 @@ dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
 // wgrad tiling: the widest tile, and split-K over the B*Ho*Wo reduction when
 // the (Cout x k*k*Cin) output has fewer than two waves of tiles (the 64-wide
 // stage-0 convs: 8 workers x 3 tiles for a 131072-long K)
+// implicit convs with 64 output channels compute dW^T = x-patches^T dy
+// (M = 9*Cin fills the 128-row tiles that Cout = 64 would leave half empty,
+// and the per-k-block traffic halves); the split-K reduce transposes back
+bool wgrad_transposed(const Conv& cv) {
+  static const bool on = [] {
+    const char* e = std::getenv("DSX_CONV_WGRAD_T");
+    return !(e && e[0] == '0');
+  }();
+  return on && cv.implicit && cv.cout == 64;
+}
+
 void wgrad_plan(const dsx_cnn* m, const Conv& cv, int* bn, int* ks) {
   const long long Kc = cv.kc(), Kg = (long long)m->batch * cv.rows();
-  *bn = Kc >= 256 ? 256 : Kc >= 128 ? 128 : 64;
-  const long long units = ((cv.cout + kBM - 1) / kBM) * ((Kc + *bn - 1) / *bn) * m->kl;
+  const bool tr = wgrad_transposed(cv);
+  *bn = tr ? 64 : Kc >= 256 ? 256 : Kc >= 128 ? 128 : 64;
+  const long long units = tr ? ((Kc + kBM - 1) / kBM) * m->kl
+                             : ((cv.cout + kBM - 1) / kBM) * ((Kc + *bn - 1) / *bn) * m->kl;
   const long long nk = (Kg + kBK - 1) / kBK;
   *ks = 1;
   if (m->bf16 && units < 2LL * m->nsm)
@@ -448,7 +475,30 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
                          const OptArgs& o, const StepDev* sp) {
   const long long M = (long long)m->batch * cv.rows(), Kc = cv.kc();
   const bool dgrad = dx != nullptr;
-  if (cv.implicit) {
+  if (wgrad_transposed(cv)) {
+    GemmCall c = cbase(m);
+    c.A = cv.in;
+    c.sA = m->act_max;
+    c.B = g;
+    c.ldb = cv.cout;
+    c.sB = m->act_max;
+    c.g.epi = kEpiF32;
+    int ks = 1;
+    wgrad_plan(m, cv, &c.bn, &ks);
+    c.g.C = m->wpart;
+    c.g.ldc = cv.cout;
+    c.g.strideC = (long long)cv.cout * Kc;
+    c.g.ksplit = ks;
+    c.g.strideSplit = (long long)m->kl * cv.cout * Kc;
+    ++m->launches;
+    CN_TRY(conv_gemm(c, geom(m, cv, kConvWgradT), m->stream, m->nsm));
+    const long long nk = (M + kBK - 1) / kBK, kper = (nk + ks - 1) / ks;
+    const long long n = (long long)cv.cout * Kc;
+    splitk_reduce_t_kernel<<<dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream>>>(
+        m->wpart, (int)((nk + kper - 1) / kper), c.g.strideSplit, (int)Kc, cv.cout, m->grads + m->off[cv.layer],
+        m->P);
+    ++m->launches;
+  } else if (cv.implicit) {
     GemmCall c = cbase(m);
     c.A = g;
     c.lda = cv.cout;
@@ -1002,7 +1052,7 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
   for (const Conv& c : m->convs) {
     int bn = 0, ks = 1;
     wgrad_plan(m, c, &bn, &ks);
-    if (ks > 1) wpart = std::max(wpart, (long long)ks * m->kl * c.cout * c.kc());
+    if (ks > 1 || wgrad_transposed(c)) wpart = std::max(wpart, (long long)ks * m->kl * c.cout * c.kc());
   }
   m->col_max = (col + 63) / 64 * 64;
   const size_t es = m->bf16 ? 2 : 4;

@@ -251,6 +251,10 @@ dsx_status make_tap_map(CUtensorMap* map, const void* base, int cin, int cout, i
 template <int MODE>
 dsx_status launch_conv_bn(int bn, bool two_sm, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
                           cudaStream_t s) {
+  if constexpr (MODE == kConvWgradT) {
+    if (bn != 64) return nfail(DSX_ERR_ARGUMENT, "conv_gemm: the transposed wgrad runs 64-wide tiles");
+    return launch_tc_t<64, true, true, float, kConvWgradT>(ta, tb, g, s);
+  }
   constexpr bool AM = MODE == kConvWgrad, BM_ = MODE != kConvFwd;
   using T = std::conditional_t<MODE == kConvWgrad, float, __nv_bfloat16>;
   if (two_sm) return bn == 128 ? launch_tc2_t<128, AM, BM_, T, MODE>(ta, tb, g, s)
@@ -281,6 +285,11 @@ dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int n
     g.M = q.cout, g.N = 9 * q.cin, g.K = pixels;
     NN_TRY(make_map(&ta, c.A, g.M, g.K, g.batch, c.lda, c.sA, kBK));
     NN_TRY(make_act_map(&tb, c.B, q.cin, q.W, q.H, q.B, g.batch, c.sB, kBK));
+  } else if (q.mode == kConvWgradT) {
+    // dW^T[(tap,c)][o]: A = x (implicit, MN-major), B = dy (MN-major)
+    g.M = 9 * q.cin, g.N = q.cout, g.K = pixels;
+    NN_TRY(make_act_map(&ta, c.A, q.cin, q.W, q.H, q.B, g.batch, c.sA, kBK));
+    NN_TRY(make_map(&tb, c.B, g.N, g.K, g.batch, c.ldb, c.sB, kBK));
   } else if (q.mode == kConvDgrad) {
     g.M = pixels, g.N = q.cin, g.K = 9 * q.cout, g.conv_cpb = q.cout / 64;
     NN_TRY(make_act_map(&ta, c.A, q.cout, q.W, q.H, q.B, g.batch, c.sA, kBM));
@@ -289,7 +298,7 @@ dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int n
     return nfail(DSX_ERR_ARGUMENT, "conv_gemm: bad mode");
   }
   if (g.ksplit > 1) {
-    if (q.mode != kConvWgrad || g.epi != kEpiF32 || g.accumulate)
+    if ((q.mode != kConvWgrad && q.mode != kConvWgradT) || g.epi != kEpiF32 || g.accumulate)
       return nfail(DSX_ERR_ARGUMENT, "conv_gemm: split-K only for the fp32 wgrad");
     const int nk = (g.K + kBK - 1) / kBK;
     const int kper = (nk + g.ksplit - 1) / g.ksplit;
@@ -311,6 +320,7 @@ dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int n
     return launch_conv_bn<kConvFwd>(bn, two_sm, ta, tb, g, s);
   }
   if (q.mode == kConvWgrad) return launch_conv_bn<kConvWgrad>(bn, two_sm, ta, tb, g, s);
+  if (q.mode == kConvWgradT) return launch_conv_bn<kConvWgradT>(64, false, ta, tb, g, s);
   return launch_conv_bn<kConvDgrad>(bn, two_sm, ta, tb, g, s);
 }
 

@@ -47,7 +47,9 @@ enum : int {
 //   kConvDgrad  A(m=pixel, k=(tap,o)) = dy[pixel - tap + 1][o]    (5-D map on dy)
 //               B(n=c, k=(tap,o))     = W[o][tap][c]              (4-D map on W, MN-major)
 // A 128-pixel M tile / 64-pixel K block covers whole image rows (W | 64).
-enum : int { kConvNone = 0, kConvFwd = 1, kConvWgrad = 2, kConvDgrad = 3 };
+//   kConvWgradT A(m=(tap,c), k=pixel) = x[pixel + tap - 1][c]    (5-D map on x, MN-major)
+//               B(n=o, k=pixel)       = dy[pixel][o]              (dW^T: narrow Cout fills M-tiles)
+enum : int { kConvNone = 0, kConvFwd = 1, kConvWgrad = 2, kConvDgrad = 3, kConvWgradT = 4 };
 
 struct GemmArgs {
   int M, N, K, batch;
@@ -542,6 +544,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
             conv_pix(g, m0, &img, &h);
             if constexpr (CONV == kConvFwd) tma_load_5d(sa, &ta, &full[s], cb * kBK, dw, h + dh, img, b);
             else tma_load_5d(sa, &ta, &full[s], cb * kBK, -dw, h - dh, img, b);
+          } else if constexpr (CONV == kConvWgradT) {
+            int img, h;
+            conv_pix(g, k * kBK, &img, &h);
+#pragma unroll
+            for (int i = 0; i < kBM / 64; ++i) {
+              const int mm = min(m0 + 64 * i, g.M - 64);  // rows past M: any in-bounds data
+              const int tap = mm / g.conv_cin, c0 = mm - tap * g.conv_cin;
+              tma_load_5d(sa + i * 64 * kBK * 2, &ta, &full[s], c0, tap % 3 - 1, h + tap / 3 - 1, img, b);
+            }
           } else if constexpr (!A_MN) {
             tma_load_3d(sa, &ta, &full[s], k * kBK, m0, b);
           } else {

@@ -355,6 +355,17 @@ def test_implicit_conv_gemms_match_torch_conv2d(H, B, cin, cout):
         for i in range(nb):
             ref = torch.nn.grad.conv2d_weight(xs[i], (cout, cin, 3, 3), dys[i], padding=1)
             assert _rel(got[i].view(cout, 3, 3, cin).permute(0, 3, 1, 2), ref) < 1e-5, (ks, i)
+    # transposed wgrad (dW^T[(tap,c)][o], the narrow-Cout path), split-K partials
+    for ks in (1, 4):
+        dwt = torch.zeros(ks, nb, 9 * cin, cout, device=DEV)
+        gemm(x, dy, dwt, M=0, N_=0, K=0, batch=nb, a_mn=True, b_mn=True, lda=cin, sA=P * cin, ldb=cout,
+             sB=P * cout, ldc=cout, sC=9 * cin * cout, ksplit=ks, s_split=nb * 9 * cin * cout, bn=64,
+             conv=(4, H, H, B, cin, cout))
+        torch.cuda.synchronize()
+        got = dwt.sum(0)
+        for i in range(nb):
+            ref = torch.nn.grad.conv2d_weight(xs[i], (cout, cin, 3, 3), dys[i], padding=1)
+            assert _rel(got[i].view(3, 3, cin, cout).permute(3, 2, 0, 1), ref) < 1e-5, ("T", ks, i)
     # dgrad with the ReLU' mask, then with a residual addend
     for epi in (N.DSX_EPI_DRELU, 3):
         dx = torch.zeros(nb, P, cin, device=DEV, dtype=torch.bfloat16)

@@ -61,6 +61,10 @@ def run(H, B, cin, cout, nb=8):
         "wgrad": lambda: gemm(dy, x, dw, M=0, N_=0, K=0, a_mn=True, b_mn=True, lda=cout, sA=P * cout, ldb=cin,
                               sB=P * cin, ldc=9 * cin, sC=cout * 9 * cin, conv=(2,) + geo, **kw),
     }
+    dwt = torch.empty(4, nb, 9 * cin, cout, device=dev)
+    variants["wgradT_ks4"] = lambda: gemm(x, dy, dwt, M=0, N_=0, K=0, a_mn=True, b_mn=True, lda=cin, sA=P * cin,
+                                          ldb=cout, sB=P * cout, ldc=cout, sC=9 * cin * cout, ksplit=4,
+                                          s_split=nb * 9 * cin * cout, bn=64, conv=(4,) + geo, **kw)
     for bn in (64, 128, 256):
         if bn <= cout or bn == 64:
             variants[f"fwd_bn{bn}"] = (lambda bn=bn: gemm(
