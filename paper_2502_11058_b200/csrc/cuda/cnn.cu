@@ -221,7 +221,15 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ part, int ks, l
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(i / cout), o = (int)(i % cout);
     float acc = 0.f;
-    for (int s = 0; s < ks; ++s) acc += part[s * s_split + b * n + i];
+    int s = 0;
+    for (; s + 8 <= ks; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(s + u) * s_split + b * n + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; s < ks; ++s) acc += part[s * s_split + b * n + i];
     out[b * s_out + (long long)o * rows + r] = acc;
   }
 }
@@ -580,8 +588,8 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
     else
       colsum_part_kernel<float><<<grid, 256, 0, m->stream>>>(static_cast<const float*>(g), cv.cout, m->act_max,
                                                              (int)M, cv.cout, chunk_rows, m->cpart);
-    splitk_reduce_kernel<<<dim3(1, m->kl), 256, 0, m->stream>>>(m->cpart, nchunks, (long long)m->kl * cv.cout,
-                                                                cv.cout, m->grads + m->boff[cv.layer], m->P);
+    splitk_reduce_kernel<<<dim3((cv.cout + 63) / 64, m->kl), 64, 0, m->stream>>>(
+        m->cpart, nchunks, (long long)m->kl * cv.cout, cv.cout, m->grads + m->boff[cv.layer], m->P);
     m->launches += 2;
   }
   if (dgrad && cv.implicit) {

@@ -356,10 +356,14 @@ dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm) {
     return e ? std::atoi(e) : -1;
   }();
   const long long tiles2 = (long long)((g.N + bn - 1) / bn) * ((g.M + 2 * kBM - 1) / (2 * kBM)) * g.batch;
-  // (measured: 256-wide pairs 1290 -> 1431 TFLOP/s at 8192^3; 128-wide pairs
-  // lose to single-CTA 128 tiles, so auto mode pairs only 256-wide tiles)
+  // (measured: 256-wide pairs 1290 -> 1431 TFLOP/s at 8192^3 with fp32 C;
+  // 128-wide pairs lose to single-CTA 128 tiles; bf16 C goes through the
+  // single-CTA TMA-store epilogue, which beats the pairs: wide MLP 126.5 ->
+  // 129.8 it/s, ResNet-18 step 10.06 -> 9.26 ms — so auto mode pairs only
+  // 256-wide fp32-output tiles)
+  const bool cst = c.out_bf16 && tma_store_ok(g);
   const bool two_sm = bn >= 128 && two_sm_env != 0 && g.ksplit <= 1 &&
-                      (two_sm_env == 1 || (bn == 256 && tiles2 >= nsm / 2));
+                      (two_sm_env == 1 || (bn == 256 && !cst && tiles2 >= nsm / 2));
   CUtensorMap ta, tb;
   if (two_sm) {
     if (!c.a_mn) NN_TRY(make_map(&ta, c.A, g.K, g.M, g.batch, c.lda, c.sA, kBM));

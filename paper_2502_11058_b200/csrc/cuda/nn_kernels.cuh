@@ -264,8 +264,17 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int ks, lon
                                      float* __restrict__ out, long long s_out) {
   const long long b = blockIdx.y;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    // 8 loads in flight, summed in split order
     float acc = 0.f;
-    for (int s = 0; s < ks; ++s) acc += part[s * s_split + b * n + i];
+    int s = 0;
+    for (; s + 8 <= ks; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(s + u) * s_split + b * n + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; s < ks; ++s) acc += part[s * s_split + b * n + i];
     out[b * s_out + i] = acc;
   }
 }
