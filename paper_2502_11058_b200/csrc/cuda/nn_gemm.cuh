@@ -523,12 +523,41 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
+      // conv modes: box coordinates advance incrementally along k (no
+      // divisions in the loop — the single producer thread issues 2-6 TMA
+      // ops per k-block)
+      const int rstep = CONV != kConvNone ? kBK / g.conv_w : 0;             // image rows per 64-pixel block
+      const int istep = CONV != kConvNone && rstep >= g.conv_h ? rstep / g.conv_h : 0;  // or whole images
       int it = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         int b, mb, nb;
         tile_coords(tile % per_split, mt, ntl, &b, &mb, &nb);
         const int m0 = mb * kBM, n0 = nb * BN;
         const int kb0 = (tile / per_split) * kper, kb1 = min(nk_all, kb0 + kper);
+        int ctap = 0, ccb = 0, fimg = 0, fh = 0, pimg = 0, prow = 0;
+        int xtap[4] = {0, 0, 0, 0}, xc0[4] = {0, 0, 0, 0};  // implicit-patch chunks: tap, channel
+        if constexpr (CONV == kConvFwd || CONV == kConvDgrad) {
+          ctap = kb0 / g.conv_cpb;
+          ccb = kb0 - ctap * g.conv_cpb;
+          conv_pix(g, m0, &fimg, &fh);
+        }
+        if constexpr (CONV == kConvWgrad || CONV == kConvWgradT) conv_pix(g, kb0 * kBK, &pimg, &prow);
+        if constexpr (CONV == kConvWgrad) {
+#pragma unroll
+          for (int i = 0; i < BN / 64; ++i) {
+            const int n = min(n0 + 64 * i, g.N - 64);  // columns past N: any in-bounds data
+            xtap[i] = n / g.conv_cin;
+            xc0[i] = n - xtap[i] * g.conv_cin;
+          }
+        }
+        if constexpr (CONV == kConvWgradT) {
+#pragma unroll
+          for (int i = 0; i < kBM / 64; ++i) {
+            const int mm = min(m0 + 64 * i, g.M - 64);  // rows past M: any in-bounds data
+            xtap[i] = mm / g.conv_cin;
+            xc0[i] = mm - xtap[i] * g.conv_cin;
+          }
+        }
         for (int k = kb0; k < kb1; ++k, ++it) {
           const int s = it % Cfg::kStages;
           const unsigned ph = (unsigned)(it / Cfg::kStages) & 1u;
@@ -538,21 +567,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
           nn_mbar_expect_tx(&full[s], Cfg::kStage);
           if constexpr (CONV == kConvFwd || CONV == kConvDgrad) {
             // k-block = (tap, 64-channel chunk); the box is shifted by the tap
-            const int tap = k / g.conv_cpb, cb = k - tap * g.conv_cpb;
-            const int dh = tap / 3 - 1, dw = tap % 3 - 1;
-            int img, h;
-            conv_pix(g, m0, &img, &h);
-            if constexpr (CONV == kConvFwd) tma_load_5d(sa, &ta, &full[s], cb * kBK, dw, h + dh, img, b);
-            else tma_load_5d(sa, &ta, &full[s], cb * kBK, -dw, h - dh, img, b);
+            const int dh = ctap / 3 - 1, dw = ctap % 3 - 1;
+            if constexpr (CONV == kConvFwd) tma_load_5d(sa, &ta, &full[s], ccb * kBK, dw, fh + dh, fimg, b);
+            else tma_load_5d(sa, &ta, &full[s], ccb * kBK, -dw, fh - dh, fimg, b);
           } else if constexpr (CONV == kConvWgradT) {
-            int img, h;
-            conv_pix(g, k * kBK, &img, &h);
 #pragma unroll
-            for (int i = 0; i < kBM / 64; ++i) {
-              const int mm = min(m0 + 64 * i, g.M - 64);  // rows past M: any in-bounds data
-              const int tap = mm / g.conv_cin, c0 = mm - tap * g.conv_cin;
-              tma_load_5d(sa + i * 64 * kBK * 2, &ta, &full[s], c0, tap % 3 - 1, h + tap / 3 - 1, img, b);
-            }
+            for (int i = 0; i < kBM / 64; ++i)
+              tma_load_5d(sa + i * 64 * kBK * 2, &ta, &full[s], xc0[i], xtap[i] % 3 - 1, prow + xtap[i] / 3 - 1, pimg,
+                          b);
           } else if constexpr (!A_MN) {
             tma_load_3d(sa, &ta, &full[s], k * kBK, m0, b);
           } else {
@@ -562,24 +584,34 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
           }
           if constexpr (CONV == kConvWgrad) {
             // 64 pixels of the reduction x 64 columns (one tap, 64 channels) per box
-            int img, h;
-            conv_pix(g, k * kBK, &img, &h);
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) {
-              const int n = min(n0 + 64 * i, g.N - 64);  // columns past N: any in-bounds data
-              const int tap = n / g.conv_cin, c0 = n - tap * g.conv_cin;
-              tma_load_5d(sb + i * 64 * kBK * 2, &tb, &full[s], c0, tap % 3 - 1, h + tap / 3 - 1, img, b);
-            }
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_5d(sb + i * 64 * kBK * 2, &tb, &full[s], xc0[i], xtap[i] % 3 - 1, prow + xtap[i] / 3 - 1, pimg,
+                          b);
           } else if constexpr (CONV == kConvDgrad) {
-            const int tap = k / g.conv_cpb, cb = k - tap * g.conv_cpb;
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load_4d(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, tap, cb * kBK, b);
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_4d(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, ctap, ccb * kBK, b);
           } else if constexpr (!B_MN) {
             tma_load_3d(sb, &tb, &full[s], k * kBK, n0, b);
           } else {
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i)
               tma_load_3d(sb + i * 64 * kBK * 2, &tb, &full[s], n0 + 64 * i, k * kBK, b);
+          }
+          if constexpr (CONV == kConvFwd || CONV == kConvDgrad) {
+            if (++ccb == g.conv_cpb) {
+              ccb = 0;
+              ++ctap;
+            }
+          }
+          if constexpr (CONV == kConvWgrad || CONV == kConvWgradT) {
+            if (istep) {
+              pimg += istep;
+            } else if ((prow += rstep) >= g.conv_h) {
+              prow -= g.conv_h;
+              ++pimg;
+            }
           }
         }
       }
