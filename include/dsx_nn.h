@@ -71,7 +71,8 @@ typedef struct dsx_gemm_desc {
    * conv = 1 forward (A = x NHWC, B = W[o][kh][kw][c]), 2 wgrad (A = dy,
    * B = x), 3 dgrad (A = dy, B = W); strideA / strideB are per batch entry;
    * 0: plain GEMM */
-  int conv, conv_h, conv_w, conv_images, conv_cin, conv_cout;
+  int conv, conv_h, conv_w, conv_images, conv_cin, conv_cout;  /* conv_h / conv_w: input grid */
+  int conv_stride, conv_k;   /* 0 -> 1 / 3; stride 2 (3x3 or 1x1): forward and wgrad */
 } dsx_gemm_desc;
 dsx_status dsx_gemm(const dsx_gemm_desc* d);
 

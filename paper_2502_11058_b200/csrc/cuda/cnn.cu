@@ -307,7 +307,8 @@ __global__ void load_image_kernel(const StepDev* __restrict__ sp, T* __restrict_
 struct Conv {
   int cin, cout, k, stride, pad, H, W, Ho, Wo;
   bool relu;          // epilogue ReLU (stem, first conv of a block)
-  bool implicit = false;  // tensor-core implicit GEMM (3x3 stride 1, 64-channel multiples): no col buffers
+  bool implicit = false;     // forward + wgrad as tensor-core implicit GEMMs (no im2col buffer)
+  bool implicit_dg = false;  // dgrad too (3x3 stride 1; stride-2 convs keep gcol + col2im)
   int layer;          // registered layer (0-based)
   void* in = nullptr;   // input activation (not owned)
   void* col = nullptr;  // im2col buffer (owned), worker stride col_stride
@@ -394,7 +395,10 @@ const void* wptr(const dsx_cnn* m, int l) {
 }
 
 ConvGeom geom(const dsx_cnn* m, const Conv& cv, int mode) {
-  return ConvGeom{mode, cv.H, cv.W, m->batch, cv.cin, cv.cout};
+  ConvGeom q{mode, cv.H, cv.W, m->batch, cv.cin, cv.cout};
+  q.stride = cv.stride;
+  q.k = cv.k;
+  return q;
 }
 
 dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
@@ -592,7 +596,7 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
         m->cpart, nchunks, (long long)m->kl * cv.cout, cv.cout, m->grads + m->boff[cv.layer], m->P);
     m->launches += 2;
   }
-  if (dgrad && cv.implicit) {
+  if (dgrad && cv.implicit_dg) {
     GemmCall c = cbase(m);
     c.A = g;
     c.sA = m->act_max;
@@ -638,7 +642,7 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
                                                 lo, n, o, sp);
   ++m->launches;
   CN_CUDA(cudaGetLastError());
-  if (dgrad && !cv.implicit) return col2im(m, cv, dx, add, mask);
+  if (dgrad && !cv.implicit_dg) return col2im(m, cv, dx, add, mask);
   return DSX_OK;
 }
 
@@ -1004,8 +1008,10 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
       const char* e = std::getenv("DSX_CONV_IMPLICIT");
       return !(e && e[0] == '0');
     }();
-    c.implicit = implicit_ok && m->bf16 && k == 3 && stride == 1 && cin % 64 == 0 && cout % 64 == 0 && H <= 64 &&
-                 64 % H == 0;
+    const int Wo = c.Wo;
+    c.implicit = implicit_ok && m->bf16 && cin % 64 == 0 && cout % 64 == 0 && Wo <= 64 && 64 % Wo == 0 &&
+                 ((k == 3 && (stride == 1 || stride == 2)) || (k == 1 && stride == 2));
+    c.implicit_dg = c.implicit && k == 3 && stride == 1;
     c.layer = (int)m->convs.size();
     m->convs.push_back(c);
     return (int)m->convs.size() - 1;
@@ -1053,7 +1059,7 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
   for (const Conv& c : m->convs) {
     act = std::max(act, (long long)m->batch * c.Ho * c.Wo * c.cout);
     act = std::max(act, (long long)m->batch * c.H * c.W * c.cin);
-    if (!c.implicit) col = std::max(col, (long long)m->batch * c.rows() * c.kc());
+    if (!c.implicit_dg) col = std::max(col, (long long)m->batch * c.rows() * c.kc());
   }
   m->act_max = (act + 63) / 64 * 64;
   long long wpart = 0;

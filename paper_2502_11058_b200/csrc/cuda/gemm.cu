@@ -199,23 +199,26 @@ int pick_bn(const GemmArgs& g, int nsm) {
 // workers sit `wstride` elements apart; a box covers `pix` consecutive
 // pixels = whole rows of one image, or whole images
 dsx_status make_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int B, int batch, long long wstride,
-                        int pix) {
+                        int pix, int stride = 1) {
   NN_TRY(get_encoder());
   if ((reinterpret_cast<uintptr_t>(base) & 15) || C % 64 || (wstride * 2) % 16)
     return nfail(DSX_ERR_ARGUMENT, "conv: activations need 16-B aligned base/stride and 64-channel multiples");
-  int rows = H, imgs = 1;
-  if (H * W >= pix) {
-    if (pix % W) return nfail(DSX_ERR_ARGUMENT, "conv: tile pixels must cover whole image rows");
-    rows = pix / W;
+  // the box covers `pix` OUTPUT pixels; with stride 2 it traverses every
+  // second input row / column (element strides), i.e. 2x the extent
+  const int Wo = W / stride, Ho = H / stride;
+  int rows = Ho, imgs = 1;
+  if (Ho * Wo >= pix) {
+    if (pix % Wo) return nfail(DSX_ERR_ARGUMENT, "conv: tile pixels must cover whole image rows");
+    rows = pix / Wo;
   } else {
-    if (pix % (H * W)) return nfail(DSX_ERR_ARGUMENT, "conv: tile pixels must cover whole images");
-    imgs = pix / (H * W);
+    if (pix % (Ho * Wo)) return nfail(DSX_ERR_ARGUMENT, "conv: tile pixels must cover whole images");
+    imgs = pix / (Ho * Wo);
   }
   cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)batch};
   cuuint64_t strides[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2,
                            (cuuint64_t)wstride * 2};
-  cuuint32_t box[5] = {64, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs, 1};
-  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  cuuint32_t box[5] = {64, (cuuint32_t)(Wo * stride), (cuuint32_t)(rows * stride), (cuuint32_t)imgs, 1};
+  cuuint32_t es[5] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -271,24 +274,30 @@ dsx_status launch_conv_bn(int bn, bool two_sm, const CUtensorMap& ta, const CUte
 dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int nsm) {
   GemmArgs g = c.g;
   if (!c.bf16) return nfail(DSX_ERR_ARGUMENT, "conv_gemm: tensor-core (bf16) path only");
-  if (q.W > 64 || 64 % q.W || q.cin % 64 || q.cout % 64)
-    return nfail(DSX_ERR_ARGUMENT, "conv_gemm: needs W | 64 and 64-channel multiples");
-  g.conv_h = q.H;
-  g.conv_w = q.W;
+  const int st = q.stride > 1 ? q.stride : 1, kk = q.k == 1 ? 1 : 3;
+  const int Ho = q.H / st, Wo = q.W / st;
+  if (Wo > 64 || 64 % Wo || q.cin % 64 || q.cout % 64 || (st != 1 && st != 2) || q.H % st || q.W % st)
+    return nfail(DSX_ERR_ARGUMENT, "conv_gemm: needs W_out | 64, 64-channel multiples, stride 1 or 2");
+  if ((st != 1 || kk != 3) && (q.mode == kConvDgrad || (kk == 1 && st == 1)))
+    return nfail(DSX_ERR_ARGUMENT, "conv_gemm: strided / 1x1 convs: forward and wgrad only (stride 2)");
+  g.conv_h = Ho;
+  g.conv_w = Wo;
   g.conv_cin = q.cin;
-  const int pixels = q.B * q.H * q.W;
+  g.conv_stride = st;
+  g.conv_k = kk;
+  const int pixels = q.B * Ho * Wo;
   CUtensorMap ta, tb;
   if (q.mode == kConvFwd) {
-    g.M = pixels, g.N = q.cout, g.K = 9 * q.cin, g.conv_cpb = q.cin / 64;
-    NN_TRY(make_act_map(&ta, c.A, q.cin, q.W, q.H, q.B, g.batch, c.sA, kBM));
+    g.M = pixels, g.N = q.cout, g.K = kk * kk * q.cin, g.conv_cpb = q.cin / 64;
+    NN_TRY(make_act_map(&ta, c.A, q.cin, q.W, q.H, q.B, g.batch, c.sA, kBM, st));
   } else if (q.mode == kConvWgrad) {
-    g.M = q.cout, g.N = 9 * q.cin, g.K = pixels;
+    g.M = q.cout, g.N = kk * kk * q.cin, g.K = pixels;
     NN_TRY(make_map(&ta, c.A, g.M, g.K, g.batch, c.lda, c.sA, kBK));
-    NN_TRY(make_act_map(&tb, c.B, q.cin, q.W, q.H, q.B, g.batch, c.sB, kBK));
+    NN_TRY(make_act_map(&tb, c.B, q.cin, q.W, q.H, q.B, g.batch, c.sB, kBK, st));
   } else if (q.mode == kConvWgradT) {
     // dW^T[(tap,c)][o]: A = x (implicit, MN-major), B = dy (MN-major)
-    g.M = 9 * q.cin, g.N = q.cout, g.K = pixels;
-    NN_TRY(make_act_map(&ta, c.A, q.cin, q.W, q.H, q.B, g.batch, c.sA, kBK));
+    g.M = kk * kk * q.cin, g.N = q.cout, g.K = pixels;
+    NN_TRY(make_act_map(&ta, c.A, q.cin, q.W, q.H, q.B, g.batch, c.sA, kBK, st));
     NN_TRY(make_map(&tb, c.B, g.N, g.K, g.batch, c.ldb, c.sB, kBK));
   } else if (q.mode == kConvDgrad) {
     g.M = pixels, g.N = q.cin, g.K = 9 * q.cout, g.conv_cpb = q.cout / 64;
@@ -429,7 +438,9 @@ dsx_status dsx_gemm(const dsx_gemm_desc* d) {
   c.g.strideMask = d->strideMask;
   if (!c.bf16 && c.out_bf16) return nfail(DSX_ERR_ARGUMENT, "fp32 gemm writes fp32");
   if (d->conv) {
-    const ConvGeom q{d->conv, d->conv_h, d->conv_w, d->conv_images, d->conv_cin, d->conv_cout};
+    ConvGeom q{d->conv, d->conv_h, d->conv_w, d->conv_images, d->conv_cin, d->conv_cout};
+    q.stride = d->conv_stride > 1 ? d->conv_stride : 1;
+    q.k = d->conv_k == 1 ? 1 : 3;
     return conv_gemm(c, q, static_cast<cudaStream_t>(d->stream), nsm);
   }
   return gemm(c, static_cast<cudaStream_t>(d->stream), nsm);

@@ -70,6 +70,10 @@ struct GemmArgs {
   // chunks of the reduction operand per tap (Cin/64 fwd, Cout/64 dgrad),
   // input channels (wgrad: the tap of output column n is n / cin)
   int conv_h, conv_w, conv_cpb, conv_cin;
+  // stride-2 convs (3x3 pad 1, or 1x1 pad 0: the projection shortcuts),
+  // forward and wgrad only: conv_h / conv_w are the OUTPUT grid, the 5-D
+  // input boxes traverse every second row / column (TMA element strides)
+  int conv_stride, conv_k;
 };
 
 // pixel index p (multiple of the tile's row span) -> (image, row)
@@ -99,7 +103,8 @@ dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm);
 // the operand pointers and per-worker strides (A = x or dy, B = W or x) and
 // the epilogue; M / N / K are derived from the geometry.
 struct ConvGeom {
-  int mode, H, W, B, cin, cout;
+  int mode, H, W, B, cin, cout;  // H, W: the input grid
+  int stride = 1, k = 3;         // stride 2 (3x3 or 1x1): forward / wgrad only
 };
 dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int nsm);
 
@@ -528,6 +533,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       // ops per k-block)
       const int rstep = CONV != kConvNone ? kBK / g.conv_w : 0;             // image rows per 64-pixel block
       const int istep = CONV != kConvNone && rstep >= g.conv_h ? rstep / g.conv_h : 0;  // or whole images
+      const int cs = g.conv_stride > 1 ? g.conv_stride : 1;  // input rows per output row
+      const bool k3 = g.conv_k != 1;                          // 3x3 taps (else 1x1, pad 0)
       int it = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         int b, mb, nb;
@@ -567,14 +574,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
           nn_mbar_expect_tx(&full[s], Cfg::kStage);
           if constexpr (CONV == kConvFwd || CONV == kConvDgrad) {
             // k-block = (tap, 64-channel chunk); the box is shifted by the tap
-            const int dh = ctap / 3 - 1, dw = ctap % 3 - 1;
-            if constexpr (CONV == kConvFwd) tma_load_5d(sa, &ta, &full[s], ccb * kBK, dw, fh + dh, fimg, b);
+            const int dh = k3 ? ctap / 3 - 1 : 0, dw = k3 ? ctap % 3 - 1 : 0;
+            if constexpr (CONV == kConvFwd) tma_load_5d(sa, &ta, &full[s], ccb * kBK, dw, cs * fh + dh, fimg, b);
             else tma_load_5d(sa, &ta, &full[s], ccb * kBK, -dw, fh - dh, fimg, b);
           } else if constexpr (CONV == kConvWgradT) {
 #pragma unroll
             for (int i = 0; i < kBM / 64; ++i)
-              tma_load_5d(sa + i * 64 * kBK * 2, &ta, &full[s], xc0[i], xtap[i] % 3 - 1, prow + xtap[i] / 3 - 1, pimg,
-                          b);
+              tma_load_5d(sa + i * 64 * kBK * 2, &ta, &full[s], xc0[i], k3 ? xtap[i] % 3 - 1 : 0,
+                          cs * prow + (k3 ? xtap[i] / 3 - 1 : 0), pimg, b);
           } else if constexpr (!A_MN) {
             tma_load_3d(sa, &ta, &full[s], k * kBK, m0, b);
           } else {
@@ -586,8 +593,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
             // 64 pixels of the reduction x 64 columns (one tap, 64 channels) per box
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i)
-              tma_load_5d(sb + i * 64 * kBK * 2, &tb, &full[s], xc0[i], xtap[i] % 3 - 1, prow + xtap[i] / 3 - 1, pimg,
-                          b);
+              tma_load_5d(sb + i * 64 * kBK * 2, &tb, &full[s], xc0[i], k3 ? xtap[i] % 3 - 1 : 0,
+                          cs * prow + (k3 ? xtap[i] / 3 - 1 : 0), pimg, b);
           } else if constexpr (CONV == kConvDgrad) {
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i)

@@ -54,7 +54,7 @@ class GemmDescC(C.Structure):
         ("mask", C.c_void_p), ("ldmask", C.c_longlong), ("strideMask", C.c_longlong),
         ("bn", C.c_int), ("stream", C.c_void_p), ("ksplit", C.c_int), ("strideSplit", C.c_longlong),
         ("conv", C.c_int), ("conv_h", C.c_int), ("conv_w", C.c_int), ("conv_images", C.c_int),
-        ("conv_cin", C.c_int), ("conv_cout", C.c_int),
+        ("conv_cin", C.c_int), ("conv_cout", C.c_int), ("conv_stride", C.c_int), ("conv_k", C.c_int),
     ]
 
 

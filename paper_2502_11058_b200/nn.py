@@ -231,6 +231,8 @@ def gemm(A, B, C_out, *, M, N_, K, batch=1, a_mn=False, b_mn=False, lda, sA=0, l
     d.bn = bn
     d.stream = stream
     d.ksplit, d.strideSplit = ksplit, s_split
-    if conv is not None:  # (mode, H, W, images, cin, cout): implicit-GEMM 3x3 conv
-        d.conv, d.conv_h, d.conv_w, d.conv_images, d.conv_cin, d.conv_cout = conv
+    if conv is not None:  # (mode, H, W, images, cin, cout[, stride, k]): implicit-GEMM conv (input grid H x W)
+        d.conv, d.conv_h, d.conv_w, d.conv_images, d.conv_cin, d.conv_cout = conv[:6]
+        if len(conv) > 6:
+            d.conv_stride, d.conv_k = conv[6], conv[7]
     N.call("dsx_gemm", C.byref(d))

@@ -390,3 +390,41 @@ def test_implicit_conv_gemms_cta_pairs():
     out = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", __file__, "-k",
                           "implicit_conv_gemms_match"], capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("H,B,cin,cout,k", [(32, 2, 64, 128, 3), (16, 4, 128, 256, 3), (8, 8, 256, 512, 3),
+                                            (32, 2, 64, 128, 1), (8, 8, 256, 512, 1)])
+def test_implicit_strided_conv_gemms_match_torch(H, B, cin, cout, k):
+    """Stride-2 implicit convs (the stage-entry 3x3 convs and the 1x1
+    projection shortcuts): 5-D input boxes with element strides 2 in h / w,
+    forward (bias + ReLU epilogue) and wgrad (plain and split-K) against
+    torch's conv2d / conv2d_weight on the same bf16 operands."""
+    import torch.nn.functional as F
+    torch.manual_seed(11)
+    nb, pad = 2, (1 if k == 3 else 0)
+    Ho = H // 2
+    P, Po = B * H * H, B * Ho * Ho
+    x = torch.randn(nb, P, cin, device=DEV).bfloat16()
+    w = (torch.randn(nb, cout, k * k * cin, device=DEV) / (k * cin ** 0.5)).bfloat16()
+    dy = torch.randn(nb, Po, cout, device=DEV).bfloat16()
+    bias = torch.randn(nb, cout, device=DEV)
+    geo = (H, H, B, cin, cout, 2, k)
+    y = torch.zeros(nb, Po, cout, device=DEV, dtype=torch.bfloat16)
+    gemm(x, w, y, M=0, N_=0, K=0, batch=nb, lda=cin, sA=P * cin, ldb=k * k * cin, sB=cout * k * k * cin, ldc=cout,
+         sC=Po * cout, epi=N.DSX_EPI_BIAS_ACT, relu=True, bias=bias, s_bias=cout, conv=(1,) + geo)
+    for ks in (1, 3):
+        dw = torch.zeros(ks, nb, cout, k * k * cin, device=DEV)
+        gemm(dy, x, dw, M=0, N_=0, K=0, batch=nb, a_mn=True, b_mn=True, lda=cout, sA=Po * cout, ldb=cin,
+             sB=P * cin, ldc=k * k * cin, sC=cout * k * k * cin, ksplit=ks, s_split=nb * cout * k * k * cin,
+             conv=(2,) + geo)
+        torch.cuda.synchronize()
+        for i in range(nb):
+            xs = _nchw(x[i], B, H, H)
+            ws = w[i].float().view(cout, k, k, cin).permute(0, 3, 1, 2)
+            if ks == 1:
+                ref = torch.relu(F.conv2d(xs, ws, stride=2, padding=pad) + bias[i].view(1, -1, 1, 1))
+                assert _rel(_nchw(y[i], B, Ho, Ho), ref.bfloat16().float()) < 1e-2, i
+            refw = torch.nn.grad.conv2d_weight(xs, (cout, cin, k, k), _nchw(dy[i], B, Ho, Ho), stride=2,
+                                               padding=pad)
+            got = dw.sum(0)[i].view(cout, k, k, cin).permute(0, 3, 1, 2)
+            assert _rel(got, refw) < 1e-5, (ks, i)
