@@ -15,6 +15,7 @@
 #include "dsx.h"
 #include "dsx_nn.h"
 #include "nn_gemm.cuh"
+#include "conv64.cuh"
 
 namespace dsx {
 extern thread_local std::string g_last_error;
@@ -312,6 +313,33 @@ dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int n
     const int nk = (g.K + kBK - 1) / kBK;
     const int kper = (nk + g.ksplit - 1) / g.ksplit;
     g.ksplit = (nk + kper - 1) / kper;
+  }
+  // 64-in / 64-out 3x3 stride-1 convs on 32x32 / 16x16 images: the resident-
+  // weight, halo-staged kernel (conv64.cuh).  DSX_CONV64=0: general path.
+  static const bool c64_ok = [] {
+    const char* e = std::getenv("DSX_CONV64");
+    return !(e && e[0] == '0');
+  }();
+  if (c64_ok && (q.mode == kConvFwd || q.mode == kConvDgrad) && st == 1 && kk == 3 && q.cin == 64 && q.cout == 64 &&
+      (q.W == 32 || q.W == 16) && q.H >= kBM / q.W + 2 && tma_store_ok(g) && c.bn == 0) {
+    CUtensorMap tcm;
+    NN_TRY(make_act_map(&ta, c.A, 64, q.W, q.H, q.B, g.batch, c.sA, (kBM / q.W + 2) * q.W));
+    if (q.mode == kConvFwd) NN_TRY(make_map(&tb, c.B, g.K, g.N, g.batch, c.ldb, c.sB, 64));
+    NN_TRY(make_c_map(&tcm, g));
+    static std::atomic<unsigned long long> attr{0};
+    auto kf = conv64_kernel<kConvFwd>;
+    auto kd = conv64_kernel<kConvDgrad>;
+    dsx::once_per_device(attr, [&] {
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, Conv64Cfg::kSmem);
+      cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, Conv64Cfg::kSmem);
+    });
+    const long long tiles = (long long)((g.M + kBM - 1) / kBM) * g.batch;
+    const int grid = (int)std::min<long long>(tiles, nsm);
+    constexpr int threads = 64 + 32 * Conv64Cfg::kEpiWarps;
+    if (q.mode == kConvFwd) kf<<<grid, threads, Conv64Cfg::kSmem, s>>>(ta, tb, g, tcm);
+    else kd<<<grid, threads, Conv64Cfg::kSmem, s>>>(ta, tb, g, tcm);
+    NN_CUDA(cudaGetLastError());
+    return DSX_OK;
   }
   const int bn = c.bn ? c.bn : pick_bn(g, nsm);
   if (bn != 64 && bn != 128 && bn != 256) return nfail(DSX_ERR_ARGUMENT, "conv_gemm: bn must be 64, 128 or 256");
