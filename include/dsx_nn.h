@@ -46,7 +46,8 @@ enum { DSX_BF16 = 2 };
 enum { DSX_OPT_SGD = 0, DSX_OPT_MOMENTUM = 1, DSX_OPT_ADAM = 2 };
 
 /* ---- GEMM test hook: C[b][m][n] = epi(sum_k A(m,k) B(n,k)) ------------- */
-enum { DSX_EPI_F32 = 0, DSX_EPI_BIAS_ACT = 1, DSX_EPI_DRELU = 2 };
+enum { DSX_EPI_F32 = 0, DSX_EPI_BIAS_ACT = 1, DSX_EPI_DRELU = 2, DSX_EPI_ADD = 3,
+       DSX_EPI_BIAS_ADD_ACT = 4 /* act(acc + bias + mask) */, DSX_EPI_ADD_DRELU = 5 /* (acc + mask) * (mask2 > 0) */ };
 typedef struct dsx_gemm_desc {
   int dtype;                 /* DSX_BF16: tcgen05 kernel, DSX_F32: SIMT kernel */
   int M, N, K, batch;
@@ -73,6 +74,8 @@ typedef struct dsx_gemm_desc {
    * 0: plain GEMM */
   int conv, conv_h, conv_w, conv_images, conv_cin, conv_cout;  /* conv_h / conv_w: input grid */
   int conv_stride, conv_k;   /* 0 -> 1 / 3; stride 2 (3x3 or 1x1): forward and wgrad */
+  const void* mask2;         /* DSX_EPI_ADD_DRELU: the ReLU' operand (mask is the addend) */
+  long long ldmask2, strideMask2;
 } dsx_gemm_desc;
 dsx_status dsx_gemm(const dsx_gemm_desc* d);
 

@@ -234,37 +234,6 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ part, int ks, l
   }
 }
 
-// y = relu(a + s) (the block output); n elements per worker (multiple of
-// 8), worker blockIdx.y at stride sx
-template <typename T>
-__global__ void add_relu_kernel(const T* __restrict__ a, const T* __restrict__ s, T* __restrict__ y, long long n,
-                                long long sx) {
-  const long long o = blockIdx.y * sx;
-  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8; i < n;
-       i += (long long)gridDim.x * blockDim.x * 8) {
-    const Vec8<T> va = ld8(a + o + i), vs = ld8(s + o + i);
-    Vec8<T> out;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) set_el(out, j, fmaxf(el(va, j) + el(vs, j), 0.f));
-    st8(y + o + i, out);
-  }
-}
-
-// out = g * (y > 0), same geometry
-template <typename T>
-__global__ void relu_grad_kernel(const T* __restrict__ g, const T* __restrict__ y, T* __restrict__ out, long long n,
-                                 long long sx) {
-  const long long o = blockIdx.y * sx;
-  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8; i < n;
-       i += (long long)gridDim.x * blockDim.x * 8) {
-    const Vec8<T> vg = ld8(g + o + i), vy = ld8(y + o + i);
-    Vec8<T> r;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) set_el(r, j, el(vy, j) > 0.f ? el(vg, j) : 0.f);
-    st8(out + o + i, r);
-  }
-}
-
 // global average pool: p[w][b][c] = mean over HW of y[w][b][hw][c]
 template <typename T>
 __global__ void pool_fwd_kernel(const T* __restrict__ y, T* __restrict__ p, int B, int HW, int C, long long sy,
@@ -277,15 +246,17 @@ __global__ void pool_fwd_kernel(const T* __restrict__ y, T* __restrict__ p, int 
   }
 }
 
-// its gradient: gy[w][b][hw][c] = dp[w][b][c] / HW
+// its gradient through the last block's ReLU: g[w][b][hw][c] = dp[w][b][c] / HW
+// where y[w][b][hw][c] > 0
 template <typename T>
-__global__ void pool_bwd_kernel(const T* __restrict__ dp, T* __restrict__ gy, int B, int HW, int C, long long sdp,
-                                long long sy) {
+__global__ void pool_bwd_kernel(const T* __restrict__ dp, const T* __restrict__ y, T* __restrict__ gy, int B, int HW,
+                                int C, long long sdp, long long sy) {
   const long long n = (long long)B * HW * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
     const int b = (int)(i / ((long long)HW * C));
-    gy[blockIdx.y * sy + i] = from_f<T>(to_f<T>(dp[blockIdx.y * sdp + (long long)b * C + c]) / (float)HW);
+    const float v = to_f<T>(dp[blockIdx.y * sdp + (long long)b * C + c]) / (float)HW;
+    gy[blockIdx.y * sy + i] = from_f<T>(to_f<T>(y[blockIdx.y * sy + i]) > 0.f ? v : 0.f);
   }
 }
 
@@ -314,6 +285,8 @@ struct Conv {
   void* col = nullptr;  // im2col buffer (owned), worker stride col_stride
   long long col_stride = 0;
   void* out = nullptr;  // output activation (owned)
+  void* dst = nullptr;        // where the forward writes (out, or the block output when fused)
+  const void* res = nullptr;  // residual addend fused into the epilogue: dst = relu(conv + res)
   long long rows() const { return (long long)Ho * Wo; }
   long long kc() const { return (long long)k * k * cin; }
 };
@@ -350,7 +323,7 @@ struct dsx_cnn {
   float* logits = nullptr;       // [kl][B][classes]
   void* dlog = nullptr;          // [kl][B][ldc] T
   void* dpool = nullptr;         // [kl][B][C]
-  void *g0 = nullptr, *g1 = nullptr, *ga = nullptr, *gh = nullptr, *gcol = nullptr, *gsc = nullptr;
+  void *g0 = nullptr, *g1 = nullptr, *gh = nullptr, *gcol = nullptr, *gsc = nullptr;
   float* wpart = nullptr;  // split-K wgrad partials
   float* cpart = nullptr;  // bias-gradient column-sum partials [2*nsm][C]
   long long act_max = 0, col_max = 0;  // elements per worker
@@ -401,6 +374,21 @@ ConvGeom geom(const dsx_cnn* m, const Conv& cv, int mode) {
   return q;
 }
 
+// forward epilogue: bias (+ ReLU); a block's last conv also adds the
+// residual and applies the block ReLU (dst = the block output)
+void fwd_epilogue(const dsx_cnn* m, const Conv& cv, GemmArgs* g) {
+  g->epi = cv.res ? kEpiBiasAddAct : kEpiBiasAct;
+  g->relu = cv.relu ? 1 : 0;
+  g->bias = m->params + m->boff[cv.layer];
+  g->strideBias = m->P;
+  g->mask = cv.res;
+  g->ldmask = cv.cout;
+  g->strideMask = m->act_max;
+  g->C = cv.dst;
+  g->ldc = cv.cout;
+  g->strideC = m->act_max;
+}
+
 dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
   const long long M = (long long)m->batch * cv.rows(), Kc = cv.kc();
   if (cv.implicit) {
@@ -410,13 +398,7 @@ dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
     c.B = wptr(m, cv.layer);
     c.ldb = Kc;
     c.sB = m->P;
-    c.g.epi = kEpiBiasAct;
-    c.g.relu = cv.relu ? 1 : 0;
-    c.g.bias = m->params + m->boff[cv.layer];
-    c.g.strideBias = m->P;
-    c.g.C = cv.out;
-    c.g.ldc = cv.cout;
-    c.g.strideC = m->act_max;
+    fwd_epilogue(m, cv, &c.g);
     ++m->launches;
     return conv_gemm(c, geom(m, cv, kConvFwd), m->stream, m->nsm);
   }
@@ -440,13 +422,7 @@ dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
   c.g.M = (int)M;
   c.g.N = cv.cout;
   c.g.K = (int)Kc;
-  c.g.epi = kEpiBiasAct;
-  c.g.relu = cv.relu ? 1 : 0;
-  c.g.bias = m->params + m->boff[cv.layer];
-  c.g.strideBias = m->P;
-  c.g.C = cv.out;
-  c.g.ldc = cv.cout;
-  c.g.strideC = m->act_max;
+  fwd_epilogue(m, cv, &c.g);
   ++m->launches;
   return gemm(c, m->stream, m->nsm);
 }
@@ -602,12 +578,15 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
     c.sA = m->act_max;
     c.B = wptr(m, cv.layer);
     c.sB = m->P;
-    c.g.epi = add ? kEpiAdd : (mask ? kEpiDRelu : kEpiBiasAct);
+    c.g.epi = add && mask ? kEpiAddDRelu : add ? kEpiAdd : (mask ? kEpiDRelu : kEpiBiasAct);
     c.g.relu = 0;
     c.g.bias = nullptr;
     c.g.mask = add ? add : mask;
     c.g.ldmask = cv.cin;
     c.g.strideMask = m->act_max;
+    c.g.mask2 = add ? mask : nullptr;
+    c.g.ldmask2 = cv.cin;
+    c.g.strideMask2 = m->act_max;
     c.g.C = dx;
     c.g.ldc = cv.cin;
     c.g.strideC = m->act_max;
@@ -664,19 +643,6 @@ dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const v
   return DSX_OK;
 }
 
-dim3 ew_grid(const dsx_cnn* m, long long n) { return dim3(blocks_for(n / 8, m->nsm) / m->kl + 1, m->kl); }
-template <typename T>
-void launch_add_relu(dsx_cnn* m, const void* a, const void* s, void* y, long long n) {
-  add_relu_kernel<T><<<ew_grid(m, n), 256, 0, m->stream>>>(static_cast<const T*>(a), static_cast<const T*>(s),
-                                                           static_cast<T*>(y), n, m->act_max);
-  ++m->launches;
-}
-template <typename T>
-void launch_relu_grad(dsx_cnn* m, const void* g, const void* y, void* out, long long n) {
-  relu_grad_kernel<T><<<ew_grid(m, n), 256, 0, m->stream>>>(static_cast<const T*>(g), static_cast<const T*>(y),
-                                                            static_cast<T*>(out), n, m->act_max);
-  ++m->launches;
-}
 
 dsx_status average_layer(dsx_cnn* m, int l, cudaStream_t s) {
   std::string err;
@@ -735,16 +701,13 @@ dsx_status forward(dsx_cnn* m, bool wait_syncs) {
     CN_TRY(wait_layer(b.layer));
     CN_TRY(conv_forward(m, b));
     CN_TRY(mark(b.layer + 1));
-    const void* shortcut = bk.x;
+    // the block output relu(b + shortcut) comes out of the last conv's
+    // epilogue (conv b with an identity shortcut, else the 1x1 projection)
     if (bk.sc >= 0) {
       CN_TRY(wait_layer(m->convs[bk.sc].layer));
       CN_TRY(conv_forward(m, m->convs[bk.sc]));
       CN_TRY(mark(bk.sc + 1));
-      shortcut = m->convs[bk.sc].out;
     }
-    const long long n = (long long)m->batch * b.rows() * b.cout;
-    if (m->bf16) launch_add_relu<__nv_bfloat16>(m, b.out, shortcut, bk.y, n);
-    else launch_add_relu<float>(m, b.out, shortcut, bk.y, n);
   }
   // global average pool + head
   const Block& last = m->blocks.back();
@@ -888,48 +851,45 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     if (m->bf16)
       pool_bwd_kernel<__nv_bfloat16><<<dim3(blocks_for((long long)m->batch * HW * Cl, m->nsm), m->kl), 256, 0,
                                        m->stream>>>(static_cast<const __nv_bfloat16*>(m->dpool),
+                                                    static_cast<const __nv_bfloat16*>(last.y),
                                                     static_cast<__nv_bfloat16*>(m->g0), m->batch, HW, Cl,
                                                     (long long)m->batch * Cl, m->act_max);
     else
       pool_bwd_kernel<float><<<dim3(blocks_for((long long)m->batch * HW * Cl, m->nsm), m->kl), 256, 0, m->stream>>>(
-          static_cast<const float*>(m->dpool), static_cast<float*>(m->g0), m->batch, HW, Cl,
-          (long long)m->batch * Cl, m->act_max);
+          static_cast<const float*>(m->dpool), static_cast<const float*>(last.y), static_cast<float*>(m->g0),
+          m->batch, HW, Cl, (long long)m->batch * Cl, m->act_max);
     ++m->launches;
   }
-  // blocks, last to first: gy (grad of the block output) lives in g0/g1
-  void* gy = m->g0;
+  // blocks, last to first.  ga = dL/d(block output) * (block output > 0) —
+  // the gradient of the block's last convs — lives in g0/g1: the pool
+  // backward produces the top block's, each block's first-conv dgrad the one
+  // below (epilogue: (dgrad + shortcut gradient) * (block input > 0))
+  void* ga = m->g0;
   void* gnext = m->g1;
   for (int bi = (int)m->blocks.size() - 1; bi >= 0; --bi) {
     const Block& bk = m->blocks[bi];
     const Conv& a = m->convs[bk.a];
     const Conv& b = m->convs[bk.b];
-    // ga = gy * (y > 0): the gradient of both the second conv and the shortcut
-    const long long nb = (long long)m->batch * b.rows() * b.cout;
-    if (m->bf16) launch_relu_grad<__nv_bfloat16>(m, gy, bk.y, m->ga, nb);
-    else launch_relu_grad<float>(m, gy, bk.y, m->ga, nb);
-    const void* sc_grad = m->ga;  // identity shortcut: dx gets ga
+    const void* sc_grad = ga;  // identity shortcut: dx gets ga
     if (bk.sc >= 0) {
       const Conv& s = m->convs[bk.sc];
-      CN_TRY(conv_backward(m, s, m->ga, m->gsc, nullptr, nullptr, o, m->sp));
+      CN_TRY(conv_backward(m, s, ga, m->gsc, nullptr, nullptr, o, m->sp));
       sc_grad = m->gsc;
       CN_TRY(done_layer(s.layer));
     }
-    // second conv; its input h = relu(first conv): gh = col2im(...) * (h > 0)
-    CN_TRY(conv_backward(m, b, m->ga, m->gh, nullptr, b.in, o, m->sp));
+    // second conv; its input h = relu(first conv): gh = dgrad * (h > 0)
+    CN_TRY(conv_backward(m, b, ga, m->gh, nullptr, b.in, o, m->sp));
     CN_TRY(done_layer(b.layer));
-    // first conv; dx = col2im(...) + shortcut grad -> grad of the previous
-    // block's output (its ReLU' is applied by that block)
-    CN_TRY(conv_backward(m, a, m->gh, gnext, sc_grad, nullptr, o, m->sp));
+    // first conv; (dgrad + shortcut grad) * (x > 0), x = the block input =
+    // the previous block's output (or the stem's): that block's ga
+    CN_TRY(conv_backward(m, a, m->gh, gnext, sc_grad, bk.x, o, m->sp));
     CN_TRY(done_layer(a.layer));
-    std::swap(gy, gnext);
+    std::swap(ga, gnext);
   }
-  // stem: its output relu(conv(x0)) gets gy * (out > 0); wgrad only
+  // stem: wgrad only, its output gradient already through its ReLU'
   {
     const Conv& st = m->convs[0];
-    const long long ns = (long long)m->batch * st.rows() * st.cout;
-    if (m->bf16) launch_relu_grad<__nv_bfloat16>(m, gy, st.out, m->ga, ns);
-    else launch_relu_grad<float>(m, gy, st.out, m->ga, ns);
-    CN_TRY(conv_backward(m, st, m->ga, nullptr, nullptr, nullptr, o, m->sp));
+    CN_TRY(conv_backward(m, st, ga, nullptr, nullptr, nullptr, o, m->sp));
     CN_TRY(done_layer(st.layer));
   }
   m->any_synced = any;
@@ -1092,7 +1052,7 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
     ok = alloc(&c.col, es * c.col_stride * m->kl) && alloc(&c.out, actb);
   }
   for (size_t i = 0; ok && i < m->blocks.size(); ++i) ok = alloc(&m->blocks[i].y, actb);
-  ok = ok && alloc(&m->g0, actb) && alloc(&m->g1, actb) && alloc(&m->ga, actb) && alloc(&m->gh, actb) &&
+  ok = ok && alloc(&m->g0, actb) && alloc(&m->g1, actb) && alloc(&m->gh, actb) &&
        alloc(&m->gsc, actb) && alloc(&m->gcol, colb) && (wpart == 0 || alloc((void**)&m->wpart, 4ull * wpart)) &&
        alloc((void**)&m->cpart, 4ull * 2 * m->nsm * (m->w0 << 3)) &&
        alloc(&m->pool, es * m->kl * m->batch * cin) && alloc(&m->dpool, es * m->kl * m->batch * cin) &&
@@ -1105,12 +1065,18 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
   // wire the activations: stem reads x0; block a/sc read the block input;
   // b reads a's output
   m->convs[0].in = m->x0;
+  for (Conv& c : m->convs) c.dst = c.out;
   void* x = m->convs[0].out;
   for (Block& b : m->blocks) {
     b.x = x;
     m->convs[b.a].in = x;
     m->convs[b.b].in = m->convs[b.a].out;
     if (b.sc >= 0) m->convs[b.sc].in = x;
+    // the block's last conv writes relu(conv + residual) = the block output
+    Conv& last = m->convs[b.sc >= 0 ? b.sc : b.b];
+    last.res = b.sc >= 0 ? m->convs[b.b].out : x;
+    last.dst = b.y;
+    last.relu = true;
     x = b.y;
   }
   if (cudaHostAlloc(&m->ring, sizeof(StepDev) * 64, cudaHostAllocDefault) != cudaSuccess)

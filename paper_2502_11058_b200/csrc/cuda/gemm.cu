@@ -83,8 +83,11 @@ bool tma_store_ok(const GemmArgs& g) {
     return !(e && e[0] == '0');
   }();
   if (!on || g.epi == kEpiF32 || (reinterpret_cast<uintptr_t>(g.C) & 15) || g.ldc % 8 || g.strideC % 8) return false;
-  if (g.epi == kEpiDRelu || g.epi == kEpiAdd)
-    return !(reinterpret_cast<uintptr_t>(g.mask) & 15) && g.ldmask % 8 == 0 && g.strideMask % 8 == 0;
+  const auto aligned = [](const void* p, long long ld, long long sb) {
+    return p && !(reinterpret_cast<uintptr_t>(p) & 15) && ld % 8 == 0 && sb % 8 == 0;
+  };
+  if (g.epi >= kEpiDRelu && !aligned(g.mask, g.ldmask, g.strideMask)) return false;
+  if (g.epi == kEpiAddDRelu && !aligned(g.mask2, g.ldmask2, g.strideMask2)) return false;
   return true;
 }
 
@@ -123,6 +126,8 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
       return DSX_OK;
     }
   }
+  if (g.epi >= kEpiBiasAddAct)
+    return nfail(DSX_ERR_ARGUMENT, "gemm: fused residual epilogues need a bf16, 16-B aligned C and operands");
   static std::atomic<unsigned long long> attr{0};
   auto kern = gemm_tc_kernel<BN, AM, BM_, TOut, CONV>;
   dsx::once_per_device(attr, [&] {
@@ -351,7 +356,8 @@ dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int n
     return e && e[0] == '1';
   }();
   const long long tiles2 = (long long)((g.N + bn - 1) / bn) * ((g.M + 2 * kBM - 1) / (2 * kBM)) * g.batch;
-  const bool two_sm = pairs_ok && bn >= 128 && g.ksplit <= 1 && g.M >= 2 * kBM && tiles2 >= nsm / 2;
+  const bool two_sm = pairs_ok && bn >= 128 && g.ksplit <= 1 && g.M >= 2 * kBM && tiles2 >= nsm / 2 &&
+                      g.epi < kEpiBiasAddAct;
   if (q.mode == kConvFwd) {
     NN_TRY(make_map(&tb, c.B, g.K, g.N, g.batch, c.ldb, c.sB, two_sm ? bn / 2 : bn));
     return launch_conv_bn<kConvFwd>(bn, two_sm, ta, tb, g, s);
@@ -399,7 +405,7 @@ dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm) {
   // 129.8 it/s, ResNet-18 step 10.06 -> 9.26 ms — so auto mode pairs only
   // 256-wide fp32-output tiles)
   const bool cst = c.out_bf16 && tma_store_ok(g);
-  const bool two_sm = bn >= 128 && two_sm_env != 0 && g.ksplit <= 1 &&
+  const bool two_sm = bn >= 128 && two_sm_env != 0 && g.ksplit <= 1 && g.epi < kEpiBiasAddAct &&
                       (two_sm_env == 1 || (bn == 256 && !cst && tiles2 >= nsm / 2));
   CUtensorMap ta, tb;
   if (two_sm) {
@@ -449,6 +455,9 @@ dsx_status dsx_gemm(const dsx_gemm_desc* d) {
   c.bn = d->bn;
   c.g.ksplit = d->ksplit;
   c.g.strideSplit = d->strideSplit;
+  c.g.mask2 = d->mask2;
+  c.g.ldmask2 = d->ldmask2;
+  c.g.strideMask2 = d->strideMask2;
   c.g.M = d->M;
   c.g.N = d->N;
   c.g.K = d->K;

@@ -36,6 +36,11 @@ enum : int {
   kEpiBiasAct = 1,   // C = act(acc + bias[n])   (act: none / relu), T out
   kEpiDRelu = 2,     // C = acc * (mask(m,n) > 0), T out (dgrad through relu)
   kEpiAdd = 3,       // C = acc + mask(m,n), T out (dgrad into a residual sum)
+  // the residual block's elementwise ops fused into its GEMMs (TMA-store /
+  // SIMT epilogues only):
+  kEpiBiasAddAct = 4,  // C = act(acc + bias[n] + mask(m,n)): block output relu(conv + shortcut)
+  kEpiAddDRelu = 5,    // C = (acc + mask(m,n)) * (mask2(m,n) > 0): input grad of a block,
+                       //     times the previous block's ReLU'
 };
 
 // Implicit-GEMM convolution (3x3, stride 1, pad 1, NHWC, channel counts
@@ -74,6 +79,8 @@ struct GemmArgs {
   // forward and wgrad only: conv_h / conv_w are the OUTPUT grid, the 5-D
   // input boxes traverse every second row / column (TMA element strides)
   int conv_stride, conv_k;
+  const void* mask2;  // kEpiAddDRelu: the ReLU' source (same layout as mask)
+  long long ldmask2, strideMask2;
 };
 
 // pixel index p (multiple of the tile's row span) -> (image, row)
@@ -200,9 +207,23 @@ __device__ __forceinline__ void epi_store(const GemmArgs& g, int b, int m, int n
     float v = acc + (g.bias ? g.bias[(long long)b * g.strideBias + n] : 0.f);
     if (g.relu) v = fmaxf(v, 0.f);
     *c = from_f<TOut>(v);
-  } else {  // kEpiDRelu / kEpiAdd
-    const TOut mk = static_cast<const TOut*>(g.mask)[(long long)b * g.strideMask + (long long)m * g.ldmask + n];
-    *c = from_f<TOut>(g.epi == kEpiAdd ? acc + to_f<TOut>(mk) : (to_f<TOut>(mk) > 0.f ? acc : 0.f));
+  } else {  // kEpiDRelu / kEpiAdd / kEpiBiasAddAct / kEpiAddDRelu
+    const float mk =
+        to_f<TOut>(static_cast<const TOut*>(g.mask)[(long long)b * g.strideMask + (long long)m * g.ldmask + n]);
+    float v;
+    if (g.epi == kEpiAdd) {
+      v = acc + mk;
+    } else if (g.epi == kEpiBiasAddAct) {
+      v = acc + (g.bias ? g.bias[(long long)b * g.strideBias + n] : 0.f) + mk;
+      if (g.relu) v = fmaxf(v, 0.f);
+    } else if (g.epi == kEpiAddDRelu) {
+      const float m2 = to_f<TOut>(
+          static_cast<const TOut*>(g.mask2)[(long long)b * g.strideMask2 + (long long)m * g.ldmask2 + n]);
+      v = m2 > 0.f ? acc + mk : 0.f;
+    } else {
+      v = mk > 0.f ? acc : 0.f;
+    }
+    *c = from_f<TOut>(v);
   }
 }
 
@@ -416,42 +437,52 @@ __device__ __forceinline__ void epi_chunk_tma(const GemmArgs& g, const CUtensorM
   const int m = m0 + lane;
   // operands fetched while the TMEM load is in flight
   float bl = 0.f;
-  if (g.epi == kEpiBiasAct && g.bias && n0 + lane < g.N) bl = g.bias[(long long)b * g.strideBias + n0 + lane];
-  uint4 mw[4] = {};
-  if ((g.epi == kEpiDRelu || g.epi == kEpiAdd) && m < g.M) {
-    const __nv_bfloat16* mp =
-        static_cast<const __nv_bfloat16*>(g.mask) + (long long)b * g.strideMask + (long long)m * g.ldmask + n0;
+  const bool has_bias = g.epi == kEpiBiasAct || g.epi == kEpiBiasAddAct;
+  if (has_bias && g.bias && n0 + lane < g.N) bl = g.bias[(long long)b * g.strideBias + n0 + lane];
+  // the lane's 32-element row segment of an elementwise operand
+  auto row_seg = [&](const void* base, long long ld, long long sb, uint4 out[4]) {
+    const __nv_bfloat16* mp = static_cast<const __nv_bfloat16*>(base) + (long long)b * sb + (long long)m * ld + n0;
     if (n0 + 32 <= g.N) {
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) mw[q4] = reinterpret_cast<const uint4*>(mp)[q4];
+      for (int q4 = 0; q4 < 4; ++q4) out[q4] = reinterpret_cast<const uint4*>(mp)[q4];
     } else {
-      __nv_bfloat16* mb = reinterpret_cast<__nv_bfloat16*>(mw);
+      __nv_bfloat16* mb = reinterpret_cast<__nv_bfloat16*>(out);
       for (int j = 0; j < 32 && n0 + j < g.N; ++j) mb[j] = mp[j];
     }
-  }
+  };
+  uint4 mw[4] = {}, mw2[4] = {};
+  if (g.epi >= kEpiDRelu && m < g.M) row_seg(g.mask, g.ldmask, g.strideMask, mw);
+  if (g.epi == kEpiAddDRelu && m < g.M) row_seg(g.mask2, g.ldmask2, g.strideMask2, mw2);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-  if (g.epi == kEpiBiasAct) {
+  if (has_bias) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      v[j] += __shfl_sync(0xffffffffu, bl, j);
-      if (g.relu) v[j] = fmaxf(v[j], 0.f);
-    }
-  } else if (g.epi == kEpiDRelu || g.epi == kEpiAdd) {
+    for (int j = 0; j < 32; ++j) v[j] += __shfl_sync(0xffffffffu, bl, j);
+  }
+  if (g.epi >= kEpiDRelu) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(mw);
+    const uint32_t* w2 = reinterpret_cast<const uint32_t*>(mw2);
 #pragma unroll
     for (int j2 = 0; j2 < 16; ++j2) {
       const float lo = __uint_as_float(w[j2] << 16), hi = __uint_as_float(w[j2] & 0xFFFF0000u);
-      if (g.epi == kEpiAdd) {
-        v[2 * j2] += lo;
-        v[2 * j2 + 1] += hi;
-      } else {
+      if (g.epi == kEpiDRelu) {
         v[2 * j2] = lo > 0.f ? v[2 * j2] : 0.f;
         v[2 * j2 + 1] = hi > 0.f ? v[2 * j2 + 1] : 0.f;
+      } else if (g.epi == kEpiAddDRelu) {
+        const float lo2 = __uint_as_float(w2[j2] << 16), hi2 = __uint_as_float(w2[j2] & 0xFFFF0000u);
+        v[2 * j2] = lo2 > 0.f ? v[2 * j2] + lo : 0.f;
+        v[2 * j2 + 1] = hi2 > 0.f ? v[2 * j2 + 1] + hi : 0.f;
+      } else {  // kEpiAdd, kEpiBiasAddAct
+        v[2 * j2] += lo;
+        v[2 * j2 + 1] += hi;
       }
     }
+  }
+  if ((g.epi == kEpiBiasAct || g.epi == kEpiBiasAddAct) && g.relu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
   }
   // the store issued from this buffer two chunks ago must have read it
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");

@@ -16,7 +16,7 @@ DREAMSCHED_PATH = os.path.join(LIB_DIR, "libdreamsched.so")
 DSX_OK, DSX_ERR_ARGUMENT, DSX_ERR_STATE, DSX_ERR_CUDA, DSX_ERR_NCCL = range(5)
 DSX_F64, DSX_F32, DSX_BF16 = 0, 1, 2
 DSX_OPT_SGD, DSX_OPT_MOMENTUM, DSX_OPT_ADAM = 0, 1, 2
-DSX_EPI_F32, DSX_EPI_BIAS_ACT, DSX_EPI_DRELU = 0, 1, 2
+DSX_EPI_F32, DSX_EPI_BIAS_ACT, DSX_EPI_DRELU, DSX_EPI_ADD, DSX_EPI_BIAS_ADD_ACT, DSX_EPI_ADD_DRELU = 0, 1, 2, 3, 4, 5
 DSX_SYNC_PAIRWISE, DSX_SYNC_NCCL_AVG = 0, 1
 
 
@@ -55,6 +55,7 @@ class GemmDescC(C.Structure):
         ("bn", C.c_int), ("stream", C.c_void_p), ("ksplit", C.c_int), ("strideSplit", C.c_longlong),
         ("conv", C.c_int), ("conv_h", C.c_int), ("conv_w", C.c_int), ("conv_images", C.c_int),
         ("conv_cin", C.c_int), ("conv_cout", C.c_int), ("conv_stride", C.c_int), ("conv_k", C.c_int),
+        ("mask2", C.c_void_p), ("ldmask2", C.c_longlong), ("strideMask2", C.c_longlong),
     ]
 
 

@@ -212,7 +212,7 @@ class Mlp:
 
 def gemm(A, B, C_out, *, M, N_, K, batch=1, a_mn=False, b_mn=False, lda, sA=0, ldb, sB=0, ldc, sC=0,
          epi=N.DSX_EPI_F32, relu=False, bias=None, s_bias=0, mask=None, ldmask=0, s_mask=0,
-         accumulate=False, bn=0, dtype="bf16", stream=0, ksplit=0, s_split=0, conv=None) -> None:
+         accumulate=False, bn=0, dtype="bf16", stream=0, ksplit=0, s_split=0, conv=None, mask2=None) -> None:
     """dsx_gemm on torch CUDA tensors (test hook for the layer GEMMs)."""
     d = N.GemmDescC()
     d.dtype = N.DSX_BF16 if dtype == "bf16" else N.DSX_F32
@@ -231,6 +231,8 @@ def gemm(A, B, C_out, *, M, N_, K, batch=1, a_mn=False, b_mn=False, lda, sA=0, l
     d.bn = bn
     d.stream = stream
     d.ksplit, d.strideSplit = ksplit, s_split
+    if mask2 is not None:
+        d.mask2, d.ldmask2, d.strideMask2 = mask2.data_ptr(), ldmask, s_mask
     if conv is not None:  # (mode, H, W, images, cin, cout[, stride, k]): implicit-GEMM conv (input grid H x W)
         d.conv, d.conv_h, d.conv_w, d.conv_images, d.conv_cin, d.conv_cout = conv[:6]
         if len(conv) > 6:

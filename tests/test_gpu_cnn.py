@@ -98,7 +98,9 @@ def test_cnn_implicit_gemm_convs_track_float64(image):
     """Width 64: every 3x3 stride-1 conv runs as an implicit GEMM (shifted
     5-D TMA boxes, no im2col); 3 steps at K = 2 track float64 (images 16:
     stage grids 16/8/4/2; 32: 32/16/8/4)."""
-    got, orc, losses, _, _ = _run(64, image, 2, 2, 3, "momentum", 0.02, dtype="bf16", bsz=4)
+    # lr 0.005: at 0.02 this batch-4 run diverges (loss 2.3 -> 5) and bf16
+    # rounding differences grow with it
+    got, orc, losses, _, _ = _run(64, image, 2, 2, 3, "momentum", 0.005, dtype="bf16", bsz=4)
     for gl, ol in losses:
         np.testing.assert_allclose(gl, ol, rtol=3e-2)
     for k in range(2):

@@ -428,3 +428,34 @@ def test_implicit_strided_conv_gemms_match_torch(H, B, cin, cout, k):
                                                padding=pad)
             got = dw.sum(0)[i].view(cout, k, k, cin).permute(0, 3, 1, 2)
             assert _rel(got, refw) < 1e-5, (ks, i)
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_fused_residual_epilogues(fp32):
+    """The residual block's elementwise ops fused into GEMM epilogues:
+    DSX_EPI_BIAS_ADD_ACT  C = relu(A B^T + bias + R)       (block output)
+    DSX_EPI_ADD_DRELU     C = (A B^T + R) * (Y > 0)         (block input gradient)
+    on the TMA-store (bf16) and SIMT (fp32) paths."""
+    torch.manual_seed(13)
+    M, N_, K, nb = 300, 192, 128, 2
+    dt = torch.float32 if fp32 else torch.bfloat16
+    A = torch.randn(nb, M, K, device=DEV).to(dt)
+    B = torch.randn(nb, N_, K, device=DEV).to(dt)
+    R = torch.randn(nb, M, N_, device=DEV).to(dt)
+    Y = torch.randn(nb, M, N_, device=DEV).to(dt)
+    bias = torch.randn(nb, N_, device=DEV)
+    ref = torch.bmm(A.float(), B.float().transpose(1, 2))
+    kw = dict(M=M, N_=N_, K=K, batch=nb, lda=K, sA=M * K, ldb=K, sB=N_ * K, ldc=N_, sC=M * N_,
+              dtype="f32" if fp32 else "bf16")
+    tol = 1e-5 if fp32 else 1e-2
+    C = torch.zeros(nb, M, N_, device=DEV, dtype=dt)
+    gemm(A, B, C, epi=N.DSX_EPI_BIAS_ADD_ACT, relu=True, bias=bias, s_bias=N_, mask=R, ldmask=N_, s_mask=M * N_,
+         **kw)
+    torch.cuda.synchronize()
+    want = torch.relu(ref + bias[:, None, :] + R.float())
+    assert _rel(C.float(), want.to(dt).float()) < tol
+    C2 = torch.zeros(nb, M, N_, device=DEV, dtype=dt)
+    gemm(A, B, C2, epi=N.DSX_EPI_ADD_DRELU, mask=R, ldmask=N_, s_mask=M * N_, mask2=Y, **kw)
+    torch.cuda.synchronize()
+    want2 = (ref + R.float()) * (Y.float() > 0)
+    assert _rel(C2.float(), want2.to(dt).float()) < tol
