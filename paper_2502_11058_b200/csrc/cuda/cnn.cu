@@ -196,7 +196,17 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ 
   const bool active = r_off < rows_par && tpr <= 256;
   if (active) {
     const T* p = dz + b * s_dz + cv * 8;
-    for (int r = r0 + r_off; r < r1; r += rows_par) {
+    int r = r0 + r_off;
+    for (; r + 3 * rows_par < r1; r += 4 * rows_par) {  // 4 rows in flight, summed in row order
+      Vec8<T> v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ld8(p + (long long)(r + u * rows_par) * ld);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += el(v[u], j);
+    }
+    for (; r < r1; r += rows_par) {
       const Vec8<T> v = ld8(p + (long long)r * ld);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] += el(v, j);
@@ -325,7 +335,7 @@ struct dsx_cnn {
   void* dpool = nullptr;         // [kl][B][C]
   void *g0 = nullptr, *g1 = nullptr, *gh = nullptr, *gcol = nullptr, *gsc = nullptr;
   float* wpart = nullptr;  // split-K wgrad partials
-  float* cpart = nullptr;  // bias-gradient column-sum partials [2*nsm][C]
+  float* cpart = nullptr;  // bias-gradient column-sum partials [4*nsm][C]
   long long act_max = 0, col_max = 0;  // elements per worker
   float *loss_part = nullptr, *loss = nullptr;
   float* xin = nullptr;
@@ -460,7 +470,7 @@ dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const v
 // [B*Ho*Wo][Cout].  Implicit convs produce dx in the dgrad GEMM's epilogue;
 // the others through gcol + col2im.
 dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, const void* add, const void* mask,
-                         const OptArgs& o, const StepDev* sp) {
+                         const OptArgs& o, const StepDev* sp, const float* db_from = nullptr) {
   const long long M = (long long)m->batch * cv.rows(), Kc = cv.kc();
   const bool dgrad = dx != nullptr;
   if (wgrad_transposed(cv)) {
@@ -556,21 +566,27 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
   }
   {
     // bias gradient: two-pass column sum over the B*Ho*Wo rows (row chunks
-    // -> per-chunk partials -> fixed-order sum), ~2 blocks per SM
+    // -> per-chunk partials -> fixed-order sum), ~4 blocks per SM; a
+    // projection block's conv b reuses its shortcut's (same gradient)
     const int tpr = cv.cout / 8, rows_par = std::max(1, 256 / tpr);
     const int nchunks = (int)std::max<long long>(
-        1, std::min<long long>(2LL * m->nsm / m->kl, M / (4LL * rows_par)));
+        1, std::min<long long>(4LL * m->nsm / m->kl, M / (4LL * rows_par)));
     const int chunk_rows = (int)((M + nchunks - 1) / nchunks);
     dim3 grid(nchunks, m->kl);
-    if (m->bf16)
+    if (db_from) {
+      CN_CUDA(cudaMemcpy2DAsync(m->grads + m->boff[cv.layer], 4ull * m->P, db_from, 4ull * m->P, 4ull * cv.cout,
+                                m->kl, cudaMemcpyDeviceToDevice, m->stream));
+    } else if (m->bf16)
       colsum_part_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(static_cast<const __nv_bfloat16*>(g), cv.cout,
                                                                      m->act_max, (int)M, cv.cout, chunk_rows, m->cpart);
     else
       colsum_part_kernel<float><<<grid, 256, 0, m->stream>>>(static_cast<const float*>(g), cv.cout, m->act_max,
                                                              (int)M, cv.cout, chunk_rows, m->cpart);
-    splitk_reduce_kernel<<<dim3((cv.cout + 63) / 64, m->kl), 64, 0, m->stream>>>(
-        m->cpart, nchunks, (long long)m->kl * cv.cout, cv.cout, m->grads + m->boff[cv.layer], m->P);
-    m->launches += 2;
+    if (!db_from) {
+      splitk_reduce_kernel<<<dim3((cv.cout + 63) / 64, m->kl), 64, 0, m->stream>>>(
+          m->cpart, nchunks, (long long)m->kl * cv.cout, cv.cout, m->grads + m->boff[cv.layer], m->P);
+      m->launches += 2;
+    }
   }
   if (dgrad && cv.implicit_dg) {
     GemmCall c = cbase(m);
@@ -878,7 +894,8 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
       CN_TRY(done_layer(s.layer));
     }
     // second conv; its input h = relu(first conv): gh = dgrad * (h > 0)
-    CN_TRY(conv_backward(m, b, ga, m->gh, nullptr, b.in, o, m->sp));
+    CN_TRY(conv_backward(m, b, ga, m->gh, nullptr, b.in, o, m->sp,
+                         bk.sc >= 0 ? m->grads + m->boff[m->convs[bk.sc].layer] : nullptr));
     CN_TRY(done_layer(b.layer));
     // first conv; (dgrad + shortcut grad) * (x > 0), x = the block input =
     // the previous block's output (or the stem's): that block's ga
@@ -1054,7 +1071,7 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
   for (size_t i = 0; ok && i < m->blocks.size(); ++i) ok = alloc(&m->blocks[i].y, actb);
   ok = ok && alloc(&m->g0, actb) && alloc(&m->g1, actb) && alloc(&m->gh, actb) &&
        alloc(&m->gsc, actb) && alloc(&m->gcol, colb) && (wpart == 0 || alloc((void**)&m->wpart, 4ull * wpart)) &&
-       alloc((void**)&m->cpart, 4ull * 2 * m->nsm * (m->w0 << 3)) &&
+       alloc((void**)&m->cpart, 4ull * 4 * m->nsm * (m->w0 << 3)) &&
        alloc(&m->pool, es * m->kl * m->batch * cin) && alloc(&m->dpool, es * m->kl * m->batch * cin) &&
        alloc((void**)&m->logits, 4ull * m->kl * m->batch * m->classes) &&
        alloc(&m->dlog, es * m->kl * m->batch * ((m->classes + 7) / 8 * 8)) &&
