@@ -132,7 +132,8 @@ __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ col, int 
 template <typename T>
 __global__ void col2im_kernel(const T* __restrict__ dcol, T* __restrict__ dx, int B, int H, int W, int C, int Ho,
                               int Wo, int k, int stride, int pad, const T* __restrict__ add,
-                              const T* __restrict__ mask, long long sdcol, long long sx) {
+                              const T* __restrict__ mask, long long sdcol, long long sx,
+                              const T* __restrict__ sub2) {
   const int cv = C / 8;
   const long long Kc = (long long)k * k * C;
   const long long total = (long long)B * H * W * cv;
@@ -164,6 +165,12 @@ __global__ void col2im_kernel(const T* __restrict__ dcol, T* __restrict__ dx, in
       }
     }
     const long long o = (((long long)b * H + hi) * W + wi) * C + c8 * 8;
+    if (sub2 && !(hi & 1) && !(wi & 1)) {  // a 1x1 stride-2 projection's dgrad [B][H/2][W/2][C]
+      const Vec8<T> a = ld8(sub2 + blockIdx.y * sx + (((long long)b * (H >> 1) + (hi >> 1)) * (W >> 1) + (wi >> 1)) * C +
+                            c8 * 8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += el(a, j);
+    }
     if (add) {
       const Vec8<T> a = ld8(add + blockIdx.y * sx + o);
 #pragma unroll
@@ -463,14 +470,19 @@ void wgrad_plan(const dsx_cnn* m, const Conv& cv, int* bn, int* ks) {
     *ks = (int)std::max<long long>(1, std::min<long long>((2LL * m->nsm + units - 1) / units, nk / 8));
 }
 
-dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const void* mask);
+dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const void* mask,
+                  const void* sub2 = nullptr);
 
 // wgrad + bias grad + (dx != null) the input gradient dx = dgrad (+ add)
 // (* (mask > 0)), then the layer's optimizer step; g = dL/d(conv output)
 // [B*Ho*Wo][Cout].  Implicit convs produce dx in the dgrad GEMM's epilogue;
 // the others through gcol + col2im.
+// raw (1x1 convs on the explicit path): dx = the dgrad GEMM's [B*Ho*Wo][Cin]
+// output itself, for the caller's col2im to scatter (sub2); sub2: such a
+// projection gradient folded into this conv's col2im
 dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, const void* add, const void* mask,
-                         const OptArgs& o, const StepDev* sp, const float* db_from = nullptr) {
+                         const OptArgs& o, const StepDev* sp, const float* db_from = nullptr, bool raw = false,
+                         const void* sub2 = nullptr) {
   const long long M = (long long)m->batch * cv.rows(), Kc = cv.kc();
   const bool dgrad = dx != nullptr;
   if (wgrad_transposed(cv)) {
@@ -624,9 +636,9 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
     c.g.epi = kEpiBiasAct;  // plain copy-out (no bias, no ReLU)
     c.g.relu = 0;
     c.g.bias = nullptr;
-    c.g.C = m->gcol;
+    c.g.C = raw ? dx : m->gcol;
     c.g.ldc = Kc;
-    c.g.strideC = m->col_max;
+    c.g.strideC = raw ? m->act_max : m->col_max;
     ++m->launches;
     CN_TRY(gemm(c, m->stream, m->nsm));
   }
@@ -637,23 +649,24 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
                                                 lo, n, o, sp);
   ++m->launches;
   CN_CUDA(cudaGetLastError());
-  if (dgrad && !cv.implicit_dg) return col2im(m, cv, dx, add, mask);
+  if (dgrad && !cv.implicit_dg && !raw) return col2im(m, cv, dx, add, mask, sub2);
   return DSX_OK;
 }
 
 // dx = col2im(gcol) (+ add) (* (mask > 0)) for conv cv's input geometry
-dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const void* mask) {
+dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const void* mask, const void* sub2) {
   const long long total = (long long)m->batch * cv.H * cv.W * (cv.cin / 8);
   const int grid = blocks_for(total, m->nsm) / std::max(1, m->kl) + 1;
   if (m->bf16)
     col2im_kernel<__nv_bfloat16><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
         static_cast<const __nv_bfloat16*>(m->gcol), static_cast<__nv_bfloat16*>(dx), m->batch, cv.H, cv.W, cv.cin,
         cv.Ho, cv.Wo, cv.k, cv.stride, cv.pad, static_cast<const __nv_bfloat16*>(add),
-        static_cast<const __nv_bfloat16*>(mask), m->col_max, m->act_max);
+        static_cast<const __nv_bfloat16*>(mask), m->col_max, m->act_max, static_cast<const __nv_bfloat16*>(sub2));
   else
     col2im_kernel<float><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
         static_cast<const float*>(m->gcol), static_cast<float*>(dx), m->batch, cv.H, cv.W, cv.cin, cv.Ho, cv.Wo, cv.k,
-        cv.stride, cv.pad, static_cast<const float*>(add), static_cast<const float*>(mask), m->col_max, m->act_max);
+        cv.stride, cv.pad, static_cast<const float*>(add), static_cast<const float*>(mask), m->col_max, m->act_max,
+        static_cast<const float*>(sub2));
   ++m->launches;
   CN_CUDA(cudaGetLastError());
   return DSX_OK;
@@ -887,10 +900,15 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     const Conv& a = m->convs[bk.a];
     const Conv& b = m->convs[bk.b];
     const void* sc_grad = ga;  // identity shortcut: dx gets ga
+    const void* sc_raw = nullptr;
     if (bk.sc >= 0) {
       const Conv& s = m->convs[bk.sc];
-      CN_TRY(conv_backward(m, s, ga, m->gsc, nullptr, nullptr, o, m->sp));
-      sc_grad = m->gsc;
+      // a 1x1 stride-2 projection's dgrad stays [B][H/2][W/2][C]; conv a's
+      // col2im adds it at the even pixels
+      const bool fold = s.k == 1 && s.stride == 2 && !a.implicit_dg;
+      CN_TRY(conv_backward(m, s, ga, m->gsc, nullptr, nullptr, o, m->sp, nullptr, fold));
+      if (fold) sc_raw = m->gsc;
+      sc_grad = fold ? nullptr : m->gsc;
       CN_TRY(done_layer(s.layer));
     }
     // second conv; its input h = relu(first conv): gh = dgrad * (h > 0)
@@ -899,7 +917,7 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     CN_TRY(done_layer(b.layer));
     // first conv; (dgrad + shortcut grad) * (x > 0), x = the block input =
     // the previous block's output (or the stem's): that block's ga
-    CN_TRY(conv_backward(m, a, m->gh, gnext, sc_grad, bk.x, o, m->sp));
+    CN_TRY(conv_backward(m, a, m->gh, gnext, sc_grad, bk.x, o, m->sp, nullptr, false, sc_raw));
     CN_TRY(done_layer(a.layer));
     std::swap(ga, gnext);
   }
