@@ -117,7 +117,7 @@ conv64_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
+    {  // MMA issuer: converged warp, elected lane (tc_mma_kblock / tc_commit_elect)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((B_MN ? 1u : 0u) << 16) |
                              ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
       int it = 0, tc = 0, cur_b = -1;
@@ -126,7 +126,7 @@ conv64_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tc) {
         const int b = tile / mt;
         if (b != cur_b) {
-          if (cur_b >= 0) tc_commit(bfree);  // the previous worker's MMAs release the weights
+          if (cur_b >= 0) tc_commit_elect(bfree);  // the previous worker's MMAs release the weights
           nn_mbar_wait(bfull, bfull_ph);
           bfull_ph ^= 1u;
           tc_fence_after();
@@ -147,17 +147,13 @@ conv64_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
             // forward: input row h + kh - 1 = halo row kh; dgrad: dy row h + 1 - kh = halo row 2 - kh
             const unsigned a0 = sa + (unsigned)((MODE == kConvFwd ? kh : 2 - kh) * W * 128);
             const unsigned b0 = bsm + (unsigned)((kh * 3 + kw) * 8192);
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t ad = smem_desc(a0 + kk * kUmmaK * 2, 16, 1024);
-              const uint64_t bd = B_MN ? smem_desc(b0 + kk * kUmmaK * 128, kBK * 128, 1024)
-                                       : smem_desc(b0 + kk * kUmmaK * 2, 16, 1024);
-              tc_mma(d, ad, bd, idesc, (kw | kh | kk) != 0 ? 1u : 0u);
-            }
+            tc_mma_kblock<false, B_MN>(d, smem_desc(a0, 16, 1024),
+                                       B_MN ? smem_desc(b0, kBK * 128, 1024) : smem_desc(b0, 16, 1024), idesc,
+                                       (kw | kh) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty[s]);
+          tc_commit_elect(&empty[s]);
         }
-        tc_commit(&tfull[acc]);
+        tc_commit_elect(&tfull[acc]);
       }
     }
   } else {  // epilogue warps (TMA-store, bf16): lane quarter warp % 4, 64 / (kEpiWarps / 4) columns each

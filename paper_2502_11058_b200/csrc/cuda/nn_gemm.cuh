@@ -169,6 +169,35 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t adesc, uint64_t b
       : "memory");
 }
 
+// The four K=16 MMAs of one 64-wide k-block in ONE asm statement: the MMA
+// thread runs inside a lane-0 branch, where the compiler wraps every
+// uniform-datapath UTCHMMA in its own elect / branch loop (~17 instructions,
+// longer than a 128 x 64 x 16 MMA takes); one statement pays that once.
+// Descriptor k advances: K-major +32 B (2 in 16-B units), MN-major +2 KB.
+// Called by the whole (converged) MMA warp: elect.sync picks the issuing
+// lane inside the statement, so no per-instruction elect loop is generated.
+template <bool A_MN, bool B_MN>
+__device__ __forceinline__ void tc_mma_kblock(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                              uint32_t acc) {
+  constexpr uint64_t da = A_MN ? (16 * 128) >> 4 : 2, db = B_MN ? (16 * 128) >> 4 : 2;
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %6, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %8, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %9, %10, %3, 1;\n}\n" ::"r"(tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "l"(ad + da), "l"(bd + db), "l"(ad + 2 * da), "l"(bd + 2 * db),
+      "l"(ad + 3 * da), "l"(bd + 3 * db)
+      : "memory");
+}
+// tcgen05.commit from one elected lane of a converged warp
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(su32(bar))
+      : "memory");
+}
+
 // Shared-memory matrix descriptor (sm_100 UMMA): start address, leading /
 // stride byte offsets (16-B units), version 1, 128-B swizzle.
 __device__ __forceinline__ uint64_t smem_desc(unsigned addr, unsigned lbo_bytes, unsigned sbo_bytes) {
@@ -655,7 +684,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
+    {  // MMA issuer: the converged warp, one elected lane issues (tc_mma_kblock)
       // instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                              ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
@@ -674,20 +703,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
           tc_fence_after();
           const unsigned sa = su32(smem + s * Cfg::kStage);
           const unsigned sb = sa + Cfg::kABytes;
-#pragma unroll
-          for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
-            // K-major: the 16-element K slice is 32 B into each 128-B swizzled
-            // row (8-row atoms 1024 B apart); MN-major: 16 K rows of 128 B
-            // further, 64-element MN chunks kBK*128 B apart.
-            const uint64_t ad = A_MN ? smem_desc(sa + kk * kUmmaK * 128, kBK * 128, 1024)
-                                     : smem_desc(sa + kk * kUmmaK * 2, 16, 1024);
-            const uint64_t bd = B_MN ? smem_desc(sb + kk * kUmmaK * 128, kBK * 128, 1024)
-                                     : smem_desc(sb + kk * kUmmaK * 2, 16, 1024);
-            tc_mma(d, ad, bd, idesc, (k | kk) != 0 ? 1u : 0u);
-          }
-          tc_commit(&empty[s]);  // frees the stage once these MMAs have read it
+          // K-major: the 16-element K slice is 32 B into each 128-B swizzled
+          // row (8-row atoms 1024 B apart); MN-major: 16 K rows of 128 B
+          // further, 64-element MN chunks kBK*128 B apart.
+          const uint64_t ad = A_MN ? smem_desc(sa, kBK * 128, 1024) : smem_desc(sa, 16, 1024);
+          const uint64_t bd = B_MN ? smem_desc(sb, kBK * 128, 1024) : smem_desc(sb, 16, 1024);
+          tc_mma_kblock<A_MN, B_MN>(d, ad, bd, idesc, k != 0 ? 1u : 0u);
+          tc_commit_elect(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        tc_commit_elect(&tfull[acc]);  // accumulator ready for the epilogue
       }
     }
   } else {  // epilogue warps 2..5
