@@ -14,9 +14,9 @@
 // So a 128-pixel tile moves 3 x (R+2) x W x 128 B (72 KB at W = 32) instead
 // of 9 x 24 KB, all nine taps' MMAs run from three stages.  Warp roles,
 // double-buffered TMEM accumulator and the TMA-store epilogue are those of
-// gemm_tc_kernel (kEpiWarps = 8, two per lane quarter, measured no faster:
-// these N = 64 tiles are bounded by the 128 x 64 MMA shape itself — 570
-// TFLOP/s here vs 488 for the general kernel, 909 at N = 128, 1250 at 256).
+// gemm_tc_kernel, with 8 epilogue warps (two per TMEM lane quarter, one
+// 32-column chunk each): with 9 k-blocks per tile the epilogue's operand
+// loads (ReLU' mask, residual) bound the dgrad otherwise (489 -> 643 TFLOP/s).
 #pragma once
 
 #include "nn_gemm.cuh"
@@ -27,7 +27,7 @@ struct Conv64Cfg {
   static constexpr int kABytesMax = (128 + 2 * 32) * 128;  // W = 32: 6 rows x 32 px x 128 B
   static constexpr int kStages = 5;
   static constexpr int kBBytes = 9 * 64 * 64 * 2;          // resident weights, 9 taps
-  static constexpr int kEpiWarps = 4;                      // one per TMEM lane quarter (8, two per quarter: no faster)
+  static constexpr int kEpiWarps = 8;                      // two per TMEM lane quarter
   static constexpr int kEpiBytes = kEpiWarps * 32 * 33 * 4;
   static constexpr int kSmem = kStages * kABytesMax + kBBytes + kEpiBytes + 1024 + 256;
   static constexpr int kTmemCols = 128;                    // 2 x 64-column accumulators
