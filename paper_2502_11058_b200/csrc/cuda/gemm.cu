@@ -112,7 +112,7 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
       static std::atomic<unsigned long long> attr_c{0};
       auto kc = gemm_tc_kernel<BN, AM, BM_, TOut, CONV, true>;
       dsx::once_per_device(attr_c, [&] {
-        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::kSmem);
+        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN, 8>::kSmem);
       });
       CUtensorMap tcm;
       NN_TRY(make_c_map(&tcm, g));
@@ -121,7 +121,7 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const long long tiles =
           (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
-      kc<<<(int)std::min<long long>(tiles, nsm), 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g, tcm);
+      kc<<<(int)std::min<long long>(tiles, nsm), TcCfg<BN, 8>::kThreads, TcCfg<BN, 8>::kSmem, s>>>(ta, tb, g, tcm);
       NN_CUDA(cudaGetLastError());
       return DSX_OK;
     }

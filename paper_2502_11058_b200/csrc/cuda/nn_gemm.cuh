@@ -268,13 +268,15 @@ __device__ __forceinline__ void epi_store(const GemmArgs& g, int b, int m, int n
 // or 64-B (bf16) row segments per warp instruction, with bias / ReLU / ReLU'
 // applied on the coalesced side.
 // ---------------------------------------------------------------------------
-template <int BN>
+template <int BN, int EW = 4>
 struct TcCfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
-  static constexpr int kEpiBytes = 4 * 32 * 33 * 4;  // per epilogue warp: 32 x 33 fp32
+  static constexpr int kEpiWarps = EW;
+  static constexpr int kThreads = 64 + 32 * EW;
+  static constexpr int kEpiBytes = EW * 32 * 33 * 4;  // per epilogue warp: 32 x 33 fp32
   static constexpr int kSmem = kStages * kStage + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
@@ -541,11 +543,14 @@ __device__ __forceinline__ void epi_chunk_tma(const GemmArgs& g, const CUtensorM
   }
 }
 
+// CST (TMA-store epilogue) kernels run 8 epilogue warps, two per TMEM lane
+// quarter splitting the tile's columns: the epilogue's operand loads
+// otherwise bound short-K tiles (conv64.cuh measured 489 -> 643 TFLOP/s)
 template <int BN, bool A_MN, bool B_MN, typename TOut, int CONV = kConvNone, bool CST = false>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(TcCfg<BN, CST ? 8 : 4>::kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g,
                const __grid_constant__ CUtensorMap tcm) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, CST ? 8 : 4>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_smem = reinterpret_cast<float*>(smem + Cfg::kStages * Cfg::kStage);
@@ -571,7 +576,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
     }
     for (int a = 0; a < 2; ++a) {
       nn_mbar_init(&tfull[a], 1);
-      nn_mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      nn_mbar_init(&tempty[a], Cfg::kEpiWarps);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -734,8 +739,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
       uint32_t mw_cur[16], mw_nxt[16];
       if constexpr (CST) {
         uint8_t* stg = reinterpret_cast<uint8_t*>(st);  // 2 x 2 KB staging buffers of this warp
+        constexpr int kCols = BN / (Cfg::kEpiWarps / 4);  // this warp's share of the tile's columns
+        const int cbeg = ((warp - 2) >> 2) * kCols;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = cbeg; c < cbeg + kCols; c += 32) {
           if (n0 + c >= g.N) break;
           epi_chunk_tma(g, &tcm, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c),
                         stg + (chunk_ctr++ & 1) * 2048, lane, b, m0, n0 + c);
