@@ -105,8 +105,56 @@ dsx_status make_c_map(CUtensorMap* map, const GemmArgs& g) {
   return DSX_OK;
 }
 
+// fp32 C (kEpiF32, no accumulate) through TMA stores: 4-D map (n, m, batch
+// entry, split), 16 x 32 boxes
+bool tma_store_f32_ok(const GemmArgs& g) {
+  static const bool on = [] {
+    const char* e = std::getenv("DSX_GEMM_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  const int ks = std::max(1, g.ksplit);
+  return on && g.epi == kEpiF32 && !g.accumulate && !(reinterpret_cast<uintptr_t>(g.C) & 15) && g.ldc % 4 == 0 &&
+         g.strideC % 4 == 0 && (ks == 1 || g.strideSplit % 4 == 0);
+}
+
+dsx_status make_c_map_f32(CUtensorMap* map, const GemmArgs& g) {
+  NN_TRY(get_encoder());
+  const int ks = std::max(1, g.ksplit);
+  const long long sc = std::max<long long>(g.strideC, g.ldc * (long long)g.M);
+  cuuint64_t dims[4] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch, (cuuint64_t)ks};
+  cuuint64_t strides[3] = {(cuuint64_t)g.ldc * 4, (cuuint64_t)sc * 4,
+                           (cuuint64_t)std::max<long long>(g.strideSplit, sc * g.batch) * 4};
+  cuuint32_t box[4] = {16, 32, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.C, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return nfail(DSX_ERR_CUDA, "cuTensorMapEncodeTiled(C fp32) failed (" + std::to_string((int)r) + ")");
+  return DSX_OK;
+}
+
 template <int BN, bool AM, bool BM_, typename TOut, int CONV = kConvNone>
 dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+  if constexpr (std::is_same_v<TOut, float>) {
+    if (tma_store_f32_ok(g)) {
+      static std::atomic<unsigned long long> attr_c{0};
+      auto kc = gemm_tc_kernel<BN, AM, BM_, TOut, CONV, true>;
+      dsx::once_per_device(attr_c, [&] {
+        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN, 8>::kSmem);
+      });
+      CUtensorMap tcm;
+      NN_TRY(make_c_map_f32(&tcm, g));
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const long long tiles =
+          (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
+      kc<<<(int)std::min<long long>(tiles, nsm), TcCfg<BN, 8>::kThreads, TcCfg<BN, 8>::kSmem, s>>>(ta, tb, g, tcm);
+      NN_CUDA(cudaGetLastError());
+      return DSX_OK;
+    }
+  }
   if constexpr (std::is_same_v<TOut, __nv_bfloat16>) {
     if (tma_store_ok(g)) {
       static std::atomic<unsigned long long> attr_c{0};
@@ -404,7 +452,10 @@ dsx_status gemm(const GemmCall& c, cudaStream_t s, int nsm) {
   // single-CTA TMA-store epilogue, which beats the pairs: wide MLP 126.5 ->
   // 129.8 it/s, ResNet-18 step 10.06 -> 9.26 ms — so auto mode pairs only
   // 256-wide fp32-output tiles)
-  const bool cst = c.out_bf16 && tma_store_ok(g);
+  // fp32 C with MN-major operands (the wgrads) likewise takes the
+  // single-CTA TMA-store kernel (wide wgrad 704 -> 1283 TFLOP/s); K-major
+  // fp32-output GEMMs keep the pairs (8192^3: 1420 vs 1229)
+  const bool cst = c.out_bf16 ? tma_store_ok(g) : (tma_store_f32_ok(g) && (c.a_mn || c.b_mn));
   const bool two_sm = bn >= 128 && two_sm_env != 0 && g.ksplit <= 1 && g.epi < kEpiBiasAddAct &&
                       (two_sm_env == 1 || (bn == 256 && !cst && tiles2 >= nsm / 2));
   CUtensorMap ta, tb;

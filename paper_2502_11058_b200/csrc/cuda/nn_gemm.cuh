@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "dsx.h"
 
@@ -447,6 +448,44 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& g, uint32_t taddr, flo
   __syncwarp();
 }
 
+// fp32 TMA-store epilogue (kEpiF32: the wgrad outputs / split-K partials):
+// the lane's accumulator row goes to this warp's staging buffers as two
+// 16-column halves (64-B rows, the same 2 x 2 KB double buffer as bf16) and
+// leaves by two 4-D tensor stores (n, m, batch entry, split).
+__device__ __forceinline__ void epi_chunk_tma_f32(const CUtensorMap* tcm, uint32_t taddr, uint8_t* stg, int* ctr,
+                                                  int lane, int b, int m0, int n0, int split) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint8_t* stage = stg + ((*ctr)++ & 1) * 2048;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    uint4* dst = reinterpret_cast<uint4*>(stage + lane * 64);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4)
+      dst[q4] = make_uint4(r[16 * h + 4 * q4], r[16 * h + 4 * q4 + 1], r[16 * h + 4 * q4 + 2], r[16 * h + 4 * q4 + 3]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile(
+          "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(tcm),
+          "r"(su32(stage)), "r"(n0 + 16 * h), "r"(m0), "r"(b), "r"(split)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+}
+
 // TMA-store epilogue of one 32-row x 32-column bf16 chunk (the CST kernels):
 // the accumulator row each lane holds after tcgen05.ld gets bias (one
 // coalesced load + shuffles) / ReLU / ReLU' or the residual addend (the
@@ -744,8 +783,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ C
 #pragma unroll 1
         for (int c = cbeg; c < cbeg + kCols; c += 32) {
           if (n0 + c >= g.N) break;
-          epi_chunk_tma(g, &tcm, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c),
-                        stg + (chunk_ctr++ & 1) * 2048, lane, b, m0, n0 + c);
+          if constexpr (std::is_same_v<TOut, float>)
+            epi_chunk_tma_f32(&tcm, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c), stg, &chunk_ctr,
+                              lane, b, m0, n0 + c, tile / per_split);
+          else
+            epi_chunk_tma(g, &tcm, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c),
+                          stg + (chunk_ctr++ & 1) * 2048, lane, b, m0, n0 + c);
         }
         tc_fence_before();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[acc])) : "memory");
