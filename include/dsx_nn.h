@@ -194,6 +194,10 @@ dsx_status dsx_cnn_event_elapsed(dsx_cnn* m, int from_slot, int to_slot, float* 
  * of dsc_write_profile -> the DFS scheduler, as dsx_mlp_profile. */
 dsx_status dsx_cnn_profile(dsx_cnn* m, int reps, double* t_fp, double* t_bp, double* t_comm);
 dsx_status dsx_cnn_launch_count(dsx_cnn* m, uint64_t* out);
+/* Throttled sync link and overlap control, as dsx_mlp_set_link /
+ * dsx_mlp_set_overlap (the four-mode runs of paper_2502_11058_b200/modes.py). */
+dsx_status dsx_cnn_set_link(dsx_cnn* m, double bandwidth, double latency);
+dsx_status dsx_cnn_set_overlap(dsx_cnn* m, int enabled);
 
 #ifdef __cplusplus
 }

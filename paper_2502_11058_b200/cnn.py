@@ -178,6 +178,13 @@ class Cnn:
         """GEMM flops of one local step: forward, wgrad and dgrad (none into the stem's input)."""
         return conv_stack_flops(self.width, self.image, self.classes, self.batch)
 
+    def set_link(self, bandwidth: float, latency: float = 0.0) -> None:
+        """Throttled sync link (bytes/s, s); bandwidth <= 0 disables."""
+        N.call("dsx_cnn_set_link", self.h, bandwidth, latency)
+
+    def set_overlap(self, on: bool) -> None:
+        N.call("dsx_cnn_set_overlap", self.h, int(on))
+
     def record(self, slot: int) -> None:
         N.call("dsx_cnn_event_record", self.h, slot)
 

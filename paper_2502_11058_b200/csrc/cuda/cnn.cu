@@ -361,6 +361,8 @@ struct dsx_cnn {
   std::vector<cudaEvent_t> pf, pb;  // dsx_cnn_profile: after each layer's FP / BP
   bool prof = false;
   bool instrument = false, any_synced = false;
+  double link_bw = 0.0, link_lat = 0.0;  // throttled sync link (bw <= 0: off)
+  bool overlap = true;                   // false: averages after the whole local step
   uint64_t launches = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -806,18 +808,27 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
   }
   if (m->prof) CN_CUDA(cudaEventRecord(m->pb[m->L], m->stream));
   bool any = false;
+  // one layer's sync on the side stream (+ the throttled link's busy time)
+  auto sync_layer = [&](int l) -> dsx_status {
+    if (m->instrument && !any) CN_CUDA(cudaEventRecord(m->ev[7], m->side));
+    CN_TRY(average_layer(m, l, m->side));
+    if (m->link_bw > 0.0) {
+      const double bytes = 4.0 * (double)(m->packed[l + 1] - m->packed[l]);
+      nn_link_spin_kernel<<<1, 1, 0, m->side>>>((unsigned long long)((m->link_lat + bytes / m->link_bw) * 1e9));
+      ++m->launches;
+    }
+    CN_CUDA(cudaEventRecord(m->ev_sync[l], m->side));
+    any = true;
+    return DSX_OK;
+  };
   auto done_layer = [&](int l) -> dsx_status {
     if (m->prof) CN_CUDA(cudaEventRecord(m->pb[l], m->stream));
     const bool sync_l = mask[l + 1] != 0 && m->K > 1;
     m->synced_prev[l] = sync_l ? 1 : 0;
-    if (!sync_l) return DSX_OK;
+    if (!sync_l || !m->overlap) return DSX_OK;
     CN_CUDA(cudaEventRecord(m->ev_upd[l], m->stream));
     CN_CUDA(cudaStreamWaitEvent(m->side, m->ev_upd[l], 0));
-    if (m->instrument && !any) CN_CUDA(cudaEventRecord(m->ev[7], m->side));
-    CN_TRY(average_layer(m, l, m->side));
-    CN_CUDA(cudaEventRecord(m->ev_sync[l], m->side));
-    any = true;
-    return DSX_OK;
+    return sync_layer(l);
   };
   // head: dW = dlog^T pool, db, dpool = dlog W  ->  pool backward into g0
   const int hl = m->L - 1;
@@ -926,6 +937,13 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     const Conv& st = m->convs[0];
     CN_TRY(conv_backward(m, st, ga, nullptr, nullptr, nullptr, o, m->sp));
     CN_TRY(done_layer(st.layer));
+  }
+  if (!m->overlap) {
+    // ssgd / flsgd: the transfers start after the whole local step
+    CN_CUDA(cudaEventRecord(m->ev_upd[0], m->stream));
+    CN_CUDA(cudaStreamWaitEvent(m->side, m->ev_upd[0], 0));
+    for (int l = m->L - 1; l >= 0; --l)
+      if (m->synced_prev[l]) CN_TRY(sync_layer(l));
   }
   m->any_synced = any;
   if (m->instrument) {
@@ -1385,6 +1403,20 @@ dsx_status dsx_cnn_profile(dsx_cnn* m, int reps, double* t_fp, double* t_bp, dou
     t_bp[l] = med(bp[l]);
     t_comm[l] = med(cm[l]);
   }
+  return DSX_OK;
+}
+
+dsx_status dsx_cnn_set_link(dsx_cnn* m, double bandwidth, double latency) {
+  CN_TRY(ccheck(m));
+  if (!(latency >= 0.0)) return cfail(DSX_ERR_ARGUMENT, "latency must be >= 0");
+  m->link_bw = bandwidth > 0.0 ? bandwidth : 0.0;
+  m->link_lat = latency;
+  return DSX_OK;
+}
+
+dsx_status dsx_cnn_set_overlap(dsx_cnn* m, int enabled) {
+  CN_TRY(ccheck(m));
+  m->overlap = enabled != 0;
   return DSX_OK;
 }
 

@@ -148,6 +148,60 @@ def run(block_sizes, workers=4, period=4, bandwidth=None, latency=5e-6, comm_rat
     return res
 
 
+def _four_modes(m, L, sizes, dx, dy, period, lr, comm_ratio, latency, iters, reps, info):
+    """The four modes on a device NN (Mlp or Cnn handle): CUDA-event profile
+    -> write_profile -> schedule_dfs + bubble_fill (plsgd) and simulate_run
+    (the prediction); the sync stream throttled so the whole model's transfer
+    takes comm_ratio x the measured FP + BP."""
+    m.set_batch_ptr(dx[0].data_ptr(), dy[0].data_ptr(), True)
+    t_fp, t_bp, _ = m.profile(reps=reps)
+    pbytes = [4 * s for s in sizes]
+    bandwidth = float(sum(pbytes)) / max(comm_ratio * float(np.sum(t_fp) + np.sum(t_bp)) - L * latency, 1e-6)
+    tmp = tempfile.mkdtemp(prefix="dreamddp_nn_modes_")
+    prof = os.path.join(tmp, "measured.profile")
+    write_profile(prof, pbytes, t_fp, t_bp, None, bandwidth, latency)
+    sets, fills, objective, sched_text = schedule_from_profile(prof, period)
+    res = dict(info)
+    res.update({"profile": prof, "schedule": sched_text, "period": period, "bandwidth_Bps": bandwidth,
+                "latency_s": latency, "iters": iters, "t_fp_total_s": float(np.sum(t_fp)),
+                "t_bp_total_s": float(np.sum(t_bp)), "modes": {}})
+    everything = np.ones(L + 1, dtype=np.uint8)
+    nothing = np.zeros(L + 1, dtype=np.uint8)
+    m.set_link(bandwidth, latency)
+    npool = dx.shape[0]
+    r_global = 0
+    for mode in MODES:
+        predicted, _ = simulate(prof, mode, period, iters)
+        m.set_overlap(mode in ("wfbp", "plsgd"))
+
+        def mask_of(r):
+            if mode in ("ssgd", "wfbp"):
+                return everything
+            if mode == "flsgd":
+                return everything if (r + 1) % period == 0 else nothing
+            return sync_mask("partial", period, r, L, sets, fills)
+        for r in range(period):  # warm-up, same mode
+            m.set_batch_ptr(dx[r % npool].data_ptr(), dy[r % npool].data_ptr(), True)
+            m.step(lr, r_global, mask_of(r))
+            r_global += 1
+        m.sync()
+        m.record(0)
+        for r in range(iters):
+            m.set_batch_ptr(dx[r % npool].data_ptr(), dy[r % npool].data_ptr(), True)
+            m.step(lr, r_global, mask_of(r))
+            r_global += 1
+        m.record(1)
+        measured = m.elapsed_ms(0, 1) * 1e-3
+        m.sync()
+        res["modes"][mode] = {"measured_s": measured, "predicted_s": predicted}
+    m.set_link(0.0, 0.0)
+    mm = res["modes"]
+    for kind in ("measured_s", "predicted_s"):
+        res["S1_" + kind.split("_")[0]] = mm["wfbp"][kind] / mm["plsgd"][kind]
+        res["S2_" + kind.split("_")[0]] = mm["flsgd"][kind] / mm["plsgd"][kind]
+    return res
+
+
 def run_mlp(widths, batch_size=256, workers=4, period=4, optimizer="adam", lr=1e-3, dtype="bf16",
             comm_ratio=2.0, latency=5e-6, iters=None, device=0, reps=5, seed=1):
     """The four modes on the NN local step (the paper's Table 1 experiment on
@@ -171,51 +225,41 @@ def run_mlp(widths, batch_size=256, workers=4, period=4, optimizer="adam", lr=1e
     xs, ys = batch_pool(seed, list(range(workers)), 4, batch_size, widths[0], widths[-1], device)
     dx = torch.from_numpy(xs).to(f"cuda:{device}")
     dy = torch.from_numpy(ys).to(f"cuda:{device}")
-    m.set_batch_ptr(dx[0].data_ptr(), dy[0].data_ptr(), True)
-    t_fp, t_bp, _ = m.profile(reps=reps)
-    sizes = layer_sizes(widths)
-    pbytes = [4 * s for s in sizes]
-    bandwidth = float(sum(pbytes)) / max(comm_ratio * float(np.sum(t_fp) + np.sum(t_bp)) - L * latency, 1e-6)
-    tmp = tempfile.mkdtemp(prefix="dreamddp_nn_modes_")
-    prof = os.path.join(tmp, "measured.profile")
-    write_profile(prof, pbytes, t_fp, t_bp, None, bandwidth, latency)
-    sets, fills, objective, sched_text = schedule_from_profile(prof, period)
-    res = {"profile": prof, "schedule": sched_text, "widths": list(widths), "batch": batch_size,
-           "workers": workers, "period": period, "optimizer": optimizer, "dtype": dtype,
-           "bandwidth_Bps": bandwidth, "latency_s": latency, "iters": iters,
-           "t_fp_total_s": float(np.sum(t_fp)), "t_bp_total_s": float(np.sum(t_bp)), "modes": {}}
-    everything = np.ones(L + 1, dtype=np.uint8)
-    nothing = np.zeros(L + 1, dtype=np.uint8)
-    m.set_link(bandwidth, latency)
-    r_global = 0
-    for mode in MODES:
-        predicted, _ = simulate(prof, mode, period, iters)
-        m.set_overlap(mode in ("wfbp", "plsgd"))
-
-        def mask_of(r):
-            if mode in ("ssgd", "wfbp"):
-                return everything
-            if mode == "flsgd":
-                return everything if (r + 1) % period == 0 else nothing
-            return sync_mask("partial", period, r, L, sets, fills)
-        for r in range(period):  # warm-up, same mode
-            m.set_batch_ptr(dx[r % 4].data_ptr(), dy[r % 4].data_ptr(), True)
-            m.step(lr, r_global, mask_of(r))
-            r_global += 1
-        m.sync()
-        m.record(0)
-        for r in range(iters):
-            m.set_batch_ptr(dx[r % 4].data_ptr(), dy[r % 4].data_ptr(), True)
-            m.step(lr, r_global, mask_of(r))
-            r_global += 1
-        m.record(1)
-        measured = m.elapsed_ms(0, 1) * 1e-3
-        m.sync()
-        res["modes"][mode] = {"measured_s": measured, "predicted_s": predicted}
-    m.set_link(0.0, 0.0)
+    info = {"widths": list(widths), "batch": batch_size, "workers": workers, "optimizer": optimizer,
+            "dtype": dtype}
+    res = _four_modes(m, L, layer_sizes(widths), dx, dy, period, lr, comm_ratio, latency, iters, reps, info)
     m.close()
-    mm = res["modes"]
-    for kind in ("measured_s", "predicted_s"):
-        res["S1_" + kind.split("_")[0]] = mm["wfbp"][kind] / mm["plsgd"][kind]
-        res["S2_" + kind.split("_")[0]] = mm["flsgd"][kind] / mm["plsgd"][kind]
+    return res
+
+
+def run_cnn(batch_size=128, workers=8, period=5, optimizer="momentum", lr=0.01, comm_ratio=2.0, latency=5e-6,
+            iters=None, device=0, reps=5, seed=1):
+    """The four modes on the ResNet-18-shaped conv stack (BASELINE
+    configs[1] as a network; the paper's main model family): K workers on one
+    B200, throttled sync link, same profile -> DFS -> simulate loop as
+    run_mlp."""
+    import torch
+
+    from .cnn import Cnn, batch, init_params, teacher
+    iters = iters or 4 * period
+    m = Cnn(batch_size, workers, dtype="bf16", optimizer=optimizer, device=device)
+    roles = ["stem"]
+    for s_ in range(4):
+        for blk in range(2):
+            roles += ["a", "b"] + (["sc"] if (s_ > 0 and blk == 0) else [])
+    init = init_params(seed, m.layer_sizes(), m.fan_in, roles + ["head"])
+    for k in range(workers):
+        m.set_params(k, init)
+    t = teacher(seed, 32, 3, 10)
+    xs = np.empty((2, workers, batch_size, 32, 32, 3), dtype=np.float32)
+    ys = np.empty((2, workers, batch_size), dtype=np.int32)
+    for p in range(2):
+        for k in range(workers):
+            xs[p, k], ys[p, k] = batch(seed, k, p, batch_size, 32, 3, t)
+    dx = torch.from_numpy(xs).to(f"cuda:{device}")
+    dy = torch.from_numpy(ys).to(f"cuda:{device}")
+    info = {"model": "resnet18-shaped conv stack (21 registered layers)", "batch": batch_size,
+            "workers": workers, "optimizer": optimizer, "dtype": "bf16"}
+    res = _four_modes(m, m.L, m.layer_sizes(), dx, dy, period, lr, comm_ratio, latency, iters, reps, info)
+    m.close()
     return res

@@ -167,6 +167,8 @@ _NN_SIGS = {
     "dsx_cnn_event_elapsed": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "dsx_cnn_launch_count": ([C.c_void_p, C.POINTER(C.c_uint64)], C.c_int),
     "dsx_cnn_profile": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "dsx_cnn_set_link": ([C.c_void_p, C.c_double, C.c_double], C.c_int),
+    "dsx_cnn_set_overlap": ([C.c_void_p, C.c_int], C.c_int),
 }
 _SIGS.update(_NN_SIGS)
 

@@ -58,3 +58,14 @@ def test_four_modes_on_the_nn_local_step():
         assert m[mode]["measured_s"] == pytest.approx(m[mode]["predicted_s"], rel=0.25), (mode, res)
     assert res["S1_measured"] > 1.3 and res["S2_measured"] > 1.1, res
     assert res["S2_measured"] == pytest.approx(res["S2_predicted"], rel=0.2)
+
+
+def test_four_modes_on_the_resnet18_conv_stack():
+    """Table 1 on BASELINE configs[1] as a network: 8 ResNet-18-shaped
+    workers x 128 images on one B200, sync link throttled to 2x compute; the
+    measured modes follow simulate_run and plsgd beats wfbp and flsgd."""
+    res = modes.run_cnn(comm_ratio=2.0)
+    m = res["modes"]
+    for mode in modes.MODES:
+        assert m[mode]["measured_s"] == pytest.approx(m[mode]["predicted_s"], rel=0.25), (mode, res)
+    assert res["S1_measured"] > 1.3 and res["S2_measured"] > 1.1, res

@@ -18,4 +18,10 @@ for name, widths, bsz, ratio in [("mlp_configs0_adam", [1024] * 8 + [10], 256, 2
     print(name, {k: (round(v["measured_s"], 5), round(v["predicted_s"], 5)) for k, v in r["modes"].items()},
           "S1", round(r["S1_measured"], 3), round(r["S1_predicted"], 3), "S2", round(r["S2_measured"], 3),
           round(r["S2_predicted"], 3), file=sys.stderr, flush=True)
+if "--cnn" in sys.argv:
+    for name, ratio in [("resnet18_cnn_momentum", 2.0), ("resnet18_cnn_momentum_ratio1", 1.0)]:
+        out[name] = r = modes.run_cnn(comm_ratio=ratio)
+        print(name, {k: (round(v["measured_s"], 5), round(v["predicted_s"], 5)) for k, v in r["modes"].items()},
+              "S1", round(r["S1_measured"], 3), round(r["S1_predicted"], 3), "S2", round(r["S2_measured"], 3),
+              round(r["S2_predicted"], 3), file=sys.stderr, flush=True)
 print(json.dumps(out, indent=1))
