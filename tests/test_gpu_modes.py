@@ -64,6 +64,7 @@ def test_four_modes_on_the_resnet18_conv_stack():
     """Table 1 on BASELINE configs[1] as a network: 8 ResNet-18-shaped
     workers x 128 images on one B200, sync link throttled to 2x compute; the
     measured modes follow simulate_run and plsgd beats wfbp and flsgd."""
+    from paper_2502_11058_b200 import modes
     res = modes.run_cnn(comm_ratio=2.0)
     m = res["modes"]
     for mode in modes.MODES:
