@@ -8,5 +8,8 @@ timeout 600 python bench.py --config resnet18_cnn --steps 30 --warmup 5 > gpurun
 for n in 2 4; do timeout 600 python bench.py --config resnet18_cnn --gpus $n --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/final_cnn_n$n.json 2> gpurun_out/final_cnn_n$n.err; done
 timeout 600 python bench.py --config mlp > gpurun_out/final_mlp_n1.json 2> gpurun_out/final_mlp_n1.err
 timeout 600 python bench.py --config mlp_wide --no-cpu-baseline > gpurun_out/final_mlpw_n1.json 2> gpurun_out/final_mlpw_n1.err
+for n in 2 4; do timeout 600 python bench.py --config mlp --gpus $n --no-cpu-baseline > gpurun_out/final_mlp_n$n.json 2> gpurun_out/final_mlp_n$n.err; done
+timeout 900 python bench.py --config llama_mlp --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/final_llama_n1.json 2> gpurun_out/final_llama_n1.err
+timeout 900 python tools/run_nn_modes.py --cnn > gpurun_out/final_nn_modes.json 2> gpurun_out/final_nn_modes.err
 bash tools/ncu_cnn.sh
 ls gpurun_out/final_*.json
