@@ -96,22 +96,21 @@ __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ col, int 
                               int k, int stride, int pad, long long sx, long long scol) {
   const int cv = C / 8;
   const long long Kc = (long long)k * k * C;
-  const long long total = (long long)B * Ho * Wo * k * k * cv;
+  const int total = B * Ho * Wo * k * k * cv;  // < 2^31 (host-checked): 32-bit index math
   const T* xw = x + blockIdx.y * sx;
   T* cw = col + blockIdx.y * scol;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    long long t = idx;
-    const int c8 = (int)(t % cv);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    int t = idx;
+    const int c8 = t % cv;
     t /= cv;
-    const int kw = (int)(t % k);
+    const int kw = t % k;
     t /= k;
-    const int kh = (int)(t % k);
+    const int kh = t % k;
     t /= k;
-    const int wo = (int)(t % Wo);
+    const int wo = t % Wo;
     t /= Wo;
-    const int ho = (int)(t % Ho);
-    const int b = (int)(t / Ho);
+    const int ho = t % Ho;
+    const int b = t / Ho;
     const int hi = ho * stride - pad + kh, wi = wo * stride - pad + kw;
     T* dst = cw + ((long long)(b * Ho + ho) * Wo + wo) * Kc + (long long)(kh * k + kw) * C + c8 * 8;
     Vec8<T> v;
@@ -134,20 +133,21 @@ __global__ void col2im_kernel(const T* __restrict__ dcol, T* __restrict__ dx, in
                               int Wo, int k, int stride, int pad, const T* __restrict__ add,
                               const T* __restrict__ mask, long long sdcol, long long sx,
                               const T* __restrict__ sub2) {
+  // 32-bit index math (the host keeps B*H*W*C/8 < 2^31): 64-bit divisions
+  // had made this gather 7x slower than its bytes
   const int cv = C / 8;
   const long long Kc = (long long)k * k * C;
-  const long long total = (long long)B * H * W * cv;
+  const int total = B * H * W * cv;
   const T* dcw = dcol + blockIdx.y * sdcol;
   T* dxw = dx + blockIdx.y * sx;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    long long t = idx;
-    const int c8 = (int)(t % cv);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    int t = idx;
+    const int c8 = t % cv;
     t /= cv;
-    const int wi = (int)(t % W);
+    const int wi = t % W;
     t /= W;
-    const int hi = (int)(t % H);
-    const int b = (int)(t / H);
+    const int hi = t % H;
+    const int b = t / H;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int kh = 0; kh < k; ++kh) {
       const int hs = hi + pad - kh;
@@ -1074,6 +1074,9 @@ dsx_status dsx_cnn_create(const dsx_cnn_desc* d, dsx_cnn** out) {
     act = std::max(act, (long long)m->batch * c.H * c.W * c.cin);
     if (!c.implicit_dg) col = std::max(col, (long long)m->batch * c.rows() * c.kc());
   }
+  // im2col / col2im index one worker's 8-channel vectors with 32-bit ints
+  if (std::max(col, act) / 8 >= (1LL << 31))
+    return cleanup(cfail(DSX_ERR_ARGUMENT, "batch too large: one worker's im2col exceeds 2^34 elements"));
   m->act_max = (act + 63) / 64 * 64;
   long long wpart = 0;
   for (const Conv& c : m->convs) {
