@@ -576,7 +576,7 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
       const double* nb1 = nullptr;
       long long ibound = 0;
       int simple = 1;
-      if constexpr (NM == 2) {
+      if constexpr (NM >= 2) {
         if (lane < KL) {
           const int k = lane;
           const unsigned long long* pf = a.nv.pfx + (long long)k * (a.nv.P + 2);
@@ -601,13 +601,13 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
         if (lane == 0) {
           info[st] = BulkChunk{tile_id, a0, a1, simple, a1 >= hi ? 1 : 0};
           const unsigned row = 8u * (unsigned)(a1 - a0);
-          const unsigned bytes = row * ((stale ? 1u : (unsigned)KL) + ((NM == 2 && simple) ? (unsigned)KL : 0u));
+          const unsigned bytes = row * ((stale ? 1u : (unsigned)KL) + ((NM >= 2 && simple) ? (unsigned)KL : 0u));
           mbar_expect_tx(&full[st], bytes);
           if (stale) bulk_g2s(wbuf(st, 0), a.mean_in + a0, row, &full[st]);
           else
             for (int k = 0; k < KL; ++k) bulk_g2s(wbuf(st, k), a.w + k * a.ld + a0, row, &full[st]);
         }
-        if constexpr (NM == 2) {
+        if constexpr (NM >= 2) {
           if (simple && lane < KL) {
             const int k = lane;
             const long long cut = min(max(ibound, (long long)a0), (long long)a1);
@@ -651,7 +651,7 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
         for (int k = 0; k < KL; ++k) {
           const double2 wv = *reinterpret_cast<const double2*>(wbuf(st, stale ? 0 : k) + 2 * p);
           double2 xv = make_double2(0.0, 0.0);
-          if constexpr (NM == 2) {
+          if constexpr (NM >= 2) {
             if (ci.simple) {
               xv = *reinterpret_cast<const double2*>(xbuf(st, k) + 2 * p);
             } else {
@@ -661,6 +661,9 @@ lab_update_bulk_kernel(UpdateArgs<double> a, int count) {
                                                      2 * (long long)(a.nv.base + ((unsigned long long)i >> 1) - pf[sg]));
             }
           }
+          // raw attempts (DSX_NOISE_RAW): the polar transform here, in the
+          // issue slots the HBM-bound update leaves idle
+          if constexpr (NM == 3) xv = mt_polar_normals(xv.x, xv.y, a.nv.stddev);
           const double g0 = grad_step(wv.x, lam0, opt0, xv.x, a.eta, NOISE, &w0[k]);
           const double g1 = grad_step(wv.y, lam1, opt1, xv.y, a.eta, NOISE, &w1[k]);
           if (in0) nsq[k] += g0 * g0;
@@ -1405,14 +1408,17 @@ void launch_update_t(dsx_lab* lab, cudaStream_t s, int tile_base, int count, int
     // mbarrier round trip: 4 GPUs 0.29 vs 0.17 ms, so 8 rows only by default)
     const int bulk_ctas = bulk_env >= 0 ? bulk_env : (nm == 2 && KL == 8 ? 1 : 0);
     if (bulk_ctas > 0 && (nm == 0 || nm == 2)) {
+      const bool raw = nm == 2 && a.nv.raw;
       constexpr size_t smem = sizeof(double) * kBStages * 2 * KL * bulk_chunk<KL>();
       static std::atomic<unsigned long long> attr{0};
       dsx::once_per_device(attr, [] {
         cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lab_update_bulk_kernel<KL, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       });
       const int grid = std::min(count, bulk_ctas == 1 ? lab->nsm : bulk_ctas);
-      if (nm == 2) lab_update_bulk_kernel<KL, 2><<<grid, kBThreads, smem, s>>>(a, count);
+      if (raw) lab_update_bulk_kernel<KL, 3><<<grid, kBThreads, smem, s>>>(a, count);
+      else if (nm == 2) lab_update_bulk_kernel<KL, 2><<<grid, kBThreads, smem, s>>>(a, count);
       else lab_update_bulk_kernel<KL, 0><<<grid, kBThreads, smem, s>>>(a, count);
       ++lab->launches;
       return;

@@ -128,6 +128,10 @@ struct dsx_mlp {
   // be waited on eagerly afterwards), and the pre-capture drain
   std::vector<cudaEvent_t> gev_upd, gev_sync;
   cudaEvent_t ev_join = nullptr, ev_drain = nullptr;
+  // several ranks: the step graph holds only the compute; it records hev_upd[l]
+  // as external event nodes and the NCCL averages are issued eagerly on the
+  // side stream behind them (capturing the collectives hung at 2 GPUs)
+  std::vector<cudaEvent_t> hev_upd;
 };
 
 namespace dsx_nn {
@@ -303,7 +307,21 @@ dsx_status prepare_input(dsx_mlp* m) {
   return DSX_OK;
 }
 
-dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* mask, bool capturing) {
+// one layer's average on the side stream (+ the throttled link's busy time)
+dsx_status side_sync(dsx_mlp* m, int l) {
+  NN_TRY(average_layer(m, l, m->side));
+  if (m->link_bw > 0.0) {
+    const double bytes = 4.0 * (double)(m->boff[l] + m->widths[l + 1] - m->off[l]);
+    nn_link_spin_kernel<<<1, 1, 0, m->side>>>((unsigned long long)((m->link_lat + bytes / m->link_bw) * 1e9));
+    ++m->launches;
+  }
+  return DSX_OK;
+}
+
+// capturing && hybrid: the compute only, with external event records where
+// the averages start (issued eagerly after the launch: issue_hybrid_syncs)
+dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* mask, bool capturing,
+                     bool hybrid = false) {
   OptArgs o{};
   o.kind = m->opt;
   o.lr = (float)lr;
@@ -345,13 +363,12 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
   std::vector<cudaEvent_t>& ev_sync = capturing ? m->gev_sync : m->ev_sync;
   // one layer's sync on the side stream (+ the throttled link's busy time)
   auto sync_layer = [&](int l) -> dsx_status {
-    if (m->instrument && !any) NN_CUDA(cudaEventRecord(m->ev[7], m->side));
-    NN_TRY(average_layer(m, l, m->side));
-    if (m->link_bw > 0.0) {
-      const double bytes = 4.0 * (double)(m->boff[l] + m->widths[l + 1] - m->off[l]);
-      nn_link_spin_kernel<<<1, 1, 0, m->side>>>((unsigned long long)((m->link_lat + bytes / m->link_bw) * 1e9));
-      ++m->launches;
+    if (hybrid) {
+      any = true;
+      return DSX_OK;
     }
+    if (m->instrument && !any) NN_CUDA(cudaEventRecord(m->ev[7], m->side));
+    NN_TRY(side_sync(m, l));
     NN_CUDA(cudaEventRecord(ev_sync[l], m->side));
     any = true;
     return DSX_OK;
@@ -362,15 +379,23 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
     const bool sync_l = mask[l + 1] != 0 && m->K > 1;
     m->synced_prev[l] = sync_l ? 1 : 0;
     if (sync_l && m->overlap) {
-      NN_CUDA(cudaEventRecord(ev_upd[l], m->stream));
-      NN_CUDA(cudaStreamWaitEvent(m->side, ev_upd[l], 0));
+      if (hybrid) {
+        NN_CUDA(cudaEventRecordWithFlags(m->hev_upd[l], m->stream, cudaEventRecordExternal));
+      } else {
+        NN_CUDA(cudaEventRecord(ev_upd[l], m->stream));
+        NN_CUDA(cudaStreamWaitEvent(m->side, ev_upd[l], 0));
+      }
       NN_TRY(sync_layer(l));
     }
   }
   if (!m->overlap) {
     // ssgd / flsgd: the transfers start after the whole local step
-    NN_CUDA(cudaEventRecord(ev_upd[0], m->stream));
-    NN_CUDA(cudaStreamWaitEvent(m->side, ev_upd[0], 0));
+    if (hybrid) {
+      NN_CUDA(cudaEventRecordWithFlags(m->hev_upd[0], m->stream, cudaEventRecordExternal));
+    } else {
+      NN_CUDA(cudaEventRecord(ev_upd[0], m->stream));
+      NN_CUDA(cudaStreamWaitEvent(m->side, ev_upd[0], 0));
+    }
     for (int l = m->L - 1; l >= 0; --l)
       if (m->synced_prev[l]) NN_TRY(sync_layer(l));
   }
@@ -379,6 +404,34 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
   if (m->instrument) {
     NN_CUDA(cudaEventRecord(m->iev[1], m->stream));
     NN_CUDA(cudaEventRecord(m->iev[2], m->side));
+  }
+  NN_CUDA(cudaGetLastError());
+  return DSX_OK;
+}
+
+// After a hybrid graph launch: the scheduled layers' averages on the side
+// stream, each behind its layer's external event record (backward order, as
+// step_impl issues them eagerly), then joined into the compute stream.
+dsx_status issue_hybrid_syncs(dsx_mlp* m, const unsigned char* mask) {
+  bool any = false;
+  if (m->overlap) {
+    for (int l = m->L - 1; l >= 0; --l) {
+      if (!(mask[l + 1] != 0 && m->K > 1)) continue;
+      NN_CUDA(cudaStreamWaitEvent(m->side, m->hev_upd[l], 0));
+      NN_TRY(side_sync(m, l));
+      any = true;
+    }
+  } else {
+    for (int l = m->L - 1; l >= 0; --l) {
+      if (!(mask[l + 1] != 0 && m->K > 1)) continue;
+      if (!any) NN_CUDA(cudaStreamWaitEvent(m->side, m->hev_upd[0], 0));
+      NN_TRY(side_sync(m, l));
+      any = true;
+    }
+  }
+  if (any) {
+    NN_CUDA(cudaEventRecord(m->ev_join, m->side));
+    NN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_join, 0));
   }
   NN_CUDA(cudaGetLastError());
   return DSX_OK;
@@ -487,6 +540,8 @@ dsx_status dsx_mlp_create(const dsx_mlp_desc* d, dsx_mlp** out) {
   cudaEventCreateWithFlags(&m->ev_drain, cudaEventDisableTiming);
   m->gev_upd.assign(m->L, nullptr);
   m->gev_sync.assign(m->L, nullptr);
+  m->hev_upd.assign(m->L, nullptr);
+  for (auto& e : m->hev_upd) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   for (int l = 0; l < m->L; ++l) {
     cudaEventCreateWithFlags(&m->gev_upd[l], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&m->gev_sync[l], cudaEventDisableTiming);
@@ -526,6 +581,8 @@ dsx_status dsx_mlp_destroy(dsx_mlp* m) {
     if (e) cudaEventDestroy(e);
   if (m->ev_join) cudaEventDestroy(m->ev_join);
   if (m->ev_drain) cudaEventDestroy(m->ev_drain);
+  for (auto e : m->hev_upd)
+    if (e) cudaEventDestroy(e);
   for (auto e : m->gev_upd)
     if (e) cudaEventDestroy(e);
   for (auto e : m->gev_sync)
@@ -611,9 +668,10 @@ dsx_status dsx_mlp_step(dsx_mlp* m, double lr, long long step_index, const unsig
   NN_TRY(check(m));
   if (!mask) return nfail(DSX_ERR_ARGUMENT, "null mask");
   NN_TRY(write_step(m, lr, step_index));
-  // graphs: single rank (capturing the NCCL averages of a multi-rank step
-  // hung at 2 GPUs, so those steps stay eager)
-  if (!m->graphs || m->instrument || m->nranks > 1) return step_impl(m, lr, step_index, mask, false);
+  // graphs: one rank captures the averages too; several ranks capture the
+  // compute only (hybrid) and issue the NCCL averages eagerly behind it
+  if (!m->graphs || m->instrument) return step_impl(m, lr, step_index, mask, false);
+  const bool hybrid = m->nranks > 1;
   // one graph per distinct mask (H of them for a partial schedule), captured
   // on first use; the averages are joined into the compute stream at the end
   const std::string key(reinterpret_cast<const char*>(mask), (size_t)m->L + 1);
@@ -626,8 +684,8 @@ dsx_status dsx_mlp_step(dsx_mlp* m, double lr, long long step_index, const unsig
     NN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_drain, 0));
     const uint64_t before = m->launches;
     NN_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
-    dsx_status st = step_impl(m, lr, step_index, mask, true);
-    if (st == DSX_OK && m->side_used) {  // (a mask with nothing to average never forks)
+    dsx_status st = step_impl(m, lr, step_index, mask, true, hybrid);
+    if (st == DSX_OK && m->side_used && !hybrid) {  // (a mask with nothing to average never forks)
       if (cudaEventRecord(m->ev_join, m->side) != cudaSuccess ||
           cudaStreamWaitEvent(m->stream, m->ev_join, 0) != cudaSuccess)
         st = nfail(DSX_ERR_CUDA, "graph capture: joining the sync stream failed");
@@ -650,6 +708,7 @@ dsx_status dsx_mlp_step(dsx_mlp* m, double lr, long long step_index, const unsig
   }
   NN_CUDA(cudaGraphLaunch(g->exec, m->stream));
   m->launches += g->launches;
+  if (hybrid) NN_TRY(issue_hybrid_syncs(m, mask));
   for (int l = 0; l < m->L; ++l) m->synced_prev[l] = (mask[l + 1] != 0 && m->K > 1) ? 1 : 0;
   return DSX_OK;
 }

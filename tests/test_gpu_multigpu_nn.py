@@ -19,7 +19,7 @@ def _gpus():
         return 0
 
 
-@pytest.mark.parametrize("graphs", [False, True])  # graphs: single-rank only, falls back to eager
+@pytest.mark.parametrize("graphs", [False, True])  # graphs: compute-only step graphs, NCCL averages eager behind external events (several ranks)
 @pytest.mark.parametrize("world", [2, 4])
 def test_mlp_multirank_matches_single_gpu(world, graphs):
     if _gpus() < world:
