@@ -144,8 +144,10 @@ dsx_status dsx_mlp_set_overlap(dsx_mlp* m, int enabled);
 /* Replay the step from CUDA graphs: one captured per distinct sync mask on
  * first use (the step's lr / bias corrections / batch pointers are read from
  * device memory, so every step replays the same graph), the sync stream's
- * averages joined at the end of each.  Single rank; with several ranks the
- * step stays eager (NCCL).  0 disables (default). */
+ * averages joined at the end of each.  With several ranks the graph holds
+ * the compute only (external event records where each scheduled layer's
+ * update ends) and the NCCL averages are enqueued eagerly behind those
+ * events after every launch.  0 disables (default). */
 dsx_status dsx_mlp_set_graphs(dsx_mlp* m, int enabled);
 
 /* ---- conv stack: BASELINE configs[1] (ResNet-18 shape) as a network ----
