@@ -36,7 +36,9 @@ def main():
     dist.broadcast_object_list(uid, src=0)
     m.comm_init(uid[0], world, rank)
     graphs = os.environ.get("DSX_TEST_GRAPHS") == "1"
-    m.set_graphs(graphs)  # NCCL averages captured in the step graphs
+    m.set_graphs(graphs)  # several ranks: compute-only graphs, NCCL averages eager behind them
+    overlap = os.environ.get("DSX_TEST_OVERLAP", "1") == "1"
+    m.set_overlap(overlap)  # 0: every average after the whole local step (ssgd / flsgd modes)
     for k in range(kl):
         m.set_params(k, init)
     for r in range(steps):
@@ -48,7 +50,7 @@ def main():
     allp = [None] * world
     dist.all_gather_object(allp, mine)
     ok = True
-    res = {"world": world, "workers_per_rank": kl, "graphs": graphs}
+    res = {"world": world, "workers_per_rank": kl, "graphs": graphs, "overlap": overlap}
     if rank == 0:
         got = [w for part in allp for w in part]
         one = Mlp(widths, bsz, K, device=dev)

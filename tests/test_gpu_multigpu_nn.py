@@ -33,6 +33,20 @@ def test_mlp_multirank_matches_single_gpu(world, graphs):
     assert '"pass": true' in out.stdout
 
 
+def test_mlp_multirank_graphs_without_overlap():
+    """Hybrid graphs with every average after the whole local step (the
+    ssgd / flsgd modes): the external event sits at the end of the BP."""
+    if _gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29637",
+           os.path.join(REPO, "tests", "multigpu_mlp.py")]
+    env = dict(os.environ, DSX_TEST_GRAPHS="1", DSX_TEST_OVERLAP="0")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert '"pass": true' in out.stdout
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_cnn_multirank_matches_single_gpu(world, dtype):
