@@ -489,8 +489,22 @@ extern "C" {
 dsx_status dsx_gemm(const dsx_gemm_desc* d) {
   if (!d) return nfail(DSX_ERR_ARGUMENT, "null gemm desc");
   if (d->dtype != DSX_BF16 && d->dtype != DSX_F32) return nfail(DSX_ERR_ARGUMENT, "gemm dtype");
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
+  // run on the device that owns C (not whatever device an earlier call on
+  // this thread left current: a launch there would reach C over peer
+  // access, unordered with the owner's default stream)
+  int prev = 0, dev = 0, nsm = 148;
+  cudaGetDevice(&prev);
+  dev = prev;
+  cudaPointerAttributes pa{};
+  if (d->C && cudaPointerGetAttributes(&pa, d->C) == cudaSuccess && pa.type == cudaMemoryTypeDevice) dev = pa.device;
+  cudaGetLastError();
+  if (dev != prev) NN_CUDA(cudaSetDevice(dev));
+  struct Restore {
+    int prev, dev;
+    ~Restore() {
+      if (dev != prev) cudaSetDevice(prev);
+    }
+  } restore{prev, dev};
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   GemmCall c{};
   c.bf16 = d->dtype == DSX_BF16;
