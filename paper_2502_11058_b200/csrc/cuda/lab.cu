@@ -2882,7 +2882,16 @@ dsx_status dsx_lab_comm_init(dsx_lab* lab, const unsigned char id[128], int nran
   return comm_finish(lab, ok, nranks);
 }
 
+// Restores the calling thread's current device when a multi-device entry
+// point returns (callers such as torch keep using the device they had).
+struct CurrentDeviceGuard {
+  int dev = 0;
+  CurrentDeviceGuard() { cudaGetDevice(&dev); }
+  ~CurrentDeviceGuard() { cudaSetDevice(dev); }
+};
+
 dsx_status dsx_lab_comm_init_local(dsx_lab* const* labs, int n, int sync_algo) {
+  const CurrentDeviceGuard keep_device;
   if (!labs || n < 1 || n > kMaxProg) return fail(DSX_ERR_ARGUMENT, "bad lab group");
   if (sync_algo != DSX_SYNC_PAIRWISE && sync_algo != DSX_SYNC_NCCL_AVG)
     return fail(DSX_ERR_ARGUMENT, "bad sync algorithm");
@@ -2940,6 +2949,7 @@ dsx_status dsx_lab_comm_init_local(dsx_lab* const* labs, int n, int sync_algo) {
 }
 
 dsx_status dsx_p2p_average_selftest(int nranks, long long n, double* max_abs_err) {
+  const CurrentDeviceGuard keep_device;
   if (!max_abs_err || nranks < 1 || nranks > kMaxProg || n < 1) return fail(DSX_ERR_ARGUMENT, "bad selftest args");
   *max_abs_err = -1.0;
   int ndev = 0;
