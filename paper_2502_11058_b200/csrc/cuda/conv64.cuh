@@ -83,6 +83,7 @@ conv64_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_enter();
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer

@@ -23,6 +23,29 @@ extern thread_local std::string g_last_error;
 
 namespace dsx_nn {
 
+// Launches a tensor-core GEMM / conv kernel with programmatic stream
+// serialization (PDL): it may start while the previous kernel on the stream
+// drains and waits in pdl_enter() (griddepcontrol.wait) before its first
+// global access.  DSX_PDL=0: plain launches.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args&&... args) {
+  static const bool on = [] {
+    const char* e = std::getenv("DSX_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = on ? at : nullptr;
+  cfg.numAttrs = on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 
 namespace {
 
@@ -150,7 +173,7 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const long long tiles =
           (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
-      kc<<<(int)std::min<long long>(tiles, nsm), TcCfg<BN, 8>::kThreads, TcCfg<BN, 8>::kSmem, s>>>(ta, tb, g, tcm);
+      NN_CUDA(launch_pdl(kc, (int)std::min<long long>(tiles, nsm), TcCfg<BN, 8>::kThreads, TcCfg<BN, 8>::kSmem, s, ta, tb, g, tcm));
       NN_CUDA(cudaGetLastError());
       return DSX_OK;
     }
@@ -169,7 +192,7 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const long long tiles =
           (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
-      kc<<<(int)std::min<long long>(tiles, nsm), TcCfg<BN, 8>::kThreads, TcCfg<BN, 8>::kSmem, s>>>(ta, tb, g, tcm);
+      NN_CUDA(launch_pdl(kc, (int)std::min<long long>(tiles, nsm), TcCfg<BN, 8>::kThreads, TcCfg<BN, 8>::kSmem, s, ta, tb, g, tcm));
       NN_CUDA(cudaGetLastError());
       return DSX_OK;
     }
@@ -189,7 +212,7 @@ dsx_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
       (long long)((g.N + BN - 1) / BN) * ((g.M + kBM - 1) / kBM) * g.batch * std::max(1, g.ksplit);
   const int grid = (int)std::min<long long>(tiles, nsm);
   CUtensorMap unused{};
-  kern<<<grid, 192, TcCfg<BN>::kSmem, s>>>(ta, tb, g, unused);
+  NN_CUDA(launch_pdl(kern, grid, 192, TcCfg<BN>::kSmem, s, ta, tb, g, unused));
   NN_CUDA(cudaGetLastError());
   return DSX_OK;
 }
@@ -207,7 +230,7 @@ dsx_status launch_tc2_t(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (long long)((g.N + BN - 1) / BN) * ((g.M + 2 * kBM - 1) / (2 * kBM)) * g.batch;
   const int clusters = (int)std::min<long long>(tiles, nsm / 2);
-  kern<<<2 * clusters, 192, Tc2Cfg<BN>::kSmem, s>>>(ta, tb, g);
+  NN_CUDA(launch_pdl(kern, 2 * clusters, 192, Tc2Cfg<BN>::kSmem, s, ta, tb, g));
   NN_CUDA(cudaGetLastError());
   return DSX_OK;
 }
@@ -389,8 +412,8 @@ dsx_status conv_gemm(const GemmCall& c, const ConvGeom& q, cudaStream_t s, int n
     const long long tiles = (long long)((g.M + kBM - 1) / kBM) * g.batch;
     const int grid = (int)std::min<long long>(tiles, nsm);
     constexpr int threads = 64 + 32 * Conv64Cfg::kEpiWarps;
-    if (q.mode == kConvFwd) kf<<<grid, threads, Conv64Cfg::kSmem, s>>>(ta, tb, g, tcm);
-    else kd<<<grid, threads, Conv64Cfg::kSmem, s>>>(ta, tb, g, tcm);
+    if (q.mode == kConvFwd) NN_CUDA(launch_pdl(kf, grid, threads, Conv64Cfg::kSmem, s, ta, tb, g, tcm));
+    else NN_CUDA(launch_pdl(kd, grid, threads, Conv64Cfg::kSmem, s, ta, tb, g, tcm));
     NN_CUDA(cudaGetLastError());
     return DSX_OK;
   }
