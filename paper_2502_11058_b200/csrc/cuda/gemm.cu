@@ -23,29 +23,6 @@ extern thread_local std::string g_last_error;
 
 namespace dsx_nn {
 
-// Launches a tensor-core GEMM / conv kernel with programmatic stream
-// serialization (PDL): it may start while the previous kernel on the stream
-// drains and waits in pdl_enter() (griddepcontrol.wait) before its first
-// global access.  DSX_PDL=0: plain launches.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args&&... args) {
-  static const bool on = [] {
-    const char* e = std::getenv("DSX_PDL");
-    return !(e && e[0] == '0');
-  }();
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3((unsigned)block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = on ? at : nullptr;
-  cfg.numAttrs = on ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-
 
 namespace {
 

@@ -232,13 +232,13 @@ dsx_status backward_layer(dsx_mlp* m, int l, void* dz_cur, void* dz_prev, const 
   {
     dim3 grid((out + 31) / 32, m->kl);
     if (m->bf16)
-      colsum_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(static_cast<const __nv_bfloat16*>(dz_cur), ld_cur,
+      NN_CUDA(launch_pdl(colsum_kernel<__nv_bfloat16>, grid, 256, 0, m->stream, static_cast<const __nv_bfloat16*>(dz_cur), ld_cur,
                                                                 (long long)m->batch * m->maxw, m->batch, out,
-                                                                m->grads + m->boff[l], m->P);
+                                                                m->grads + m->boff[l], m->P));
     else
-      colsum_kernel<float><<<grid, 256, 0, m->stream>>>(static_cast<const float*>(dz_cur), ld_cur,
+      NN_CUDA(launch_pdl(colsum_kernel<float>, grid, 256, 0, m->stream, static_cast<const float*>(dz_cur), ld_cur,
                                                         (long long)m->batch * m->maxw, m->batch, out,
-                                                        m->grads + m->boff[l], m->P);
+                                                        m->grads + m->boff[l], m->P));
     ++m->launches;
   }
   // dgrad through the ReLU of layer l-1's output: dz_prev = (dz W) * (x > 0)
@@ -270,8 +270,8 @@ dsx_status backward_layer(dsx_mlp* m, int l, void* dz_cur, void* dz_prev, const 
   // ~4 resident blocks per SM over all workers, each thread 2 x 16 B per pass
   const long long want = (n / 8 + 255) / 256;
   dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(want, (long long)m->nsm * 8 / m->kl)), m->kl);
-  optimizer_kernel<<<grid, 256, 0, m->stream>>>(m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P,
-                                                lo, n, o, sp);
+  NN_CUDA(launch_pdl(optimizer_kernel, grid, 256, 0, m->stream, m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P,
+                                                lo, n, o, sp));
   ++m->launches;
   NN_CUDA(cudaGetLastError());
   return DSX_OK;
@@ -299,10 +299,10 @@ dsx_status write_step(dsx_mlp* m, double lr, long long t) {
 dsx_status prepare_input(dsx_mlp* m) {
   const long long n = (long long)m->kl * m->batch * m->widths[0];
   if (m->bf16)
-    load_x_kernel<__nv_bfloat16><<<blocks_for(n, m->nsm), 256, 0, m->stream>>>(
-        m->sp, static_cast<__nv_bfloat16*>(m->act[0]), n);
+    NN_CUDA(launch_pdl(load_x_kernel<__nv_bfloat16>, blocks_for(n, m->nsm), 256, 0, m->stream, 
+        m->sp, static_cast<__nv_bfloat16*>(m->act[0]), n));
   else
-    load_x_kernel<float><<<blocks_for(n, m->nsm), 256, 0, m->stream>>>(m->sp, static_cast<float*>(m->act[0]), n);
+    NN_CUDA(launch_pdl(load_x_kernel<float>, blocks_for(n, m->nsm), 256, 0, m->stream, m->sp, static_cast<float*>(m->act[0]), n));
   ++m->launches;
   return DSX_OK;
 }
@@ -345,14 +345,14 @@ dsx_status step_impl(dsx_mlp* m, double lr, long long t, const unsigned char* ma
     const int C = m->widths[m->L];
     dim3 grid((m->batch * 32 + 255) / 256, m->kl);
     if (m->bf16)
-      softmax_xent_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(
+      NN_CUDA(launch_pdl(softmax_xent_kernel<__nv_bfloat16>, grid, 256, 0, m->stream, 
           m->logits, C, (long long)m->batch * C, nullptr, m->batch, C, static_cast<__nv_bfloat16*>(m->dz[0]), ldz(m, m->L),
-          (long long)m->batch * m->maxw, m->loss_part, m->sp);
+          (long long)m->batch * m->maxw, m->loss_part, m->sp));
     else
-      softmax_xent_kernel<float><<<grid, 256, 0, m->stream>>>(m->logits, C, (long long)m->batch * C, nullptr,
+      NN_CUDA(launch_pdl(softmax_xent_kernel<float>, grid, 256, 0, m->stream, m->logits, C, (long long)m->batch * C, nullptr,
                                                               m->batch, C, static_cast<float*>(m->dz[0]), ldz(m, m->L),
-                                                              (long long)m->batch * m->maxw, m->loss_part, m->sp);
-    loss_mean_kernel<<<m->kl, 256, 0, m->stream>>>(m->loss_part, m->batch, m->loss);
+                                                              (long long)m->batch * m->maxw, m->loss_part, m->sp));
+    NN_CUDA(launch_pdl(loss_mean_kernel, m->kl, 256, 0, m->stream, m->loss_part, m->batch, m->loss));
     m->launches += 2;
   }
   // BP L..1 with the optimizer fused per layer; a masked layer's average
@@ -818,13 +818,13 @@ dsx_status dsx_mlp_profile(dsx_mlp* m, int reps, double* t_fp, double* t_bp, dou
     const int C = m->widths[m->L];
     dim3 grid((m->batch * 32 + 255) / 256, m->kl);
     if (m->bf16)
-      softmax_xent_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(
+      NN_CUDA(launch_pdl(softmax_xent_kernel<__nv_bfloat16>, grid, 256, 0, m->stream, 
           m->logits, C, (long long)m->batch * C, nullptr, m->batch, C, static_cast<__nv_bfloat16*>(m->dz[0]), ldz(m, m->L),
-          (long long)m->batch * m->maxw, m->loss_part, m->sp);
+          (long long)m->batch * m->maxw, m->loss_part, m->sp));
     else
-      softmax_xent_kernel<float><<<grid, 256, 0, m->stream>>>(m->logits, C, (long long)m->batch * C, nullptr,
+      NN_CUDA(launch_pdl(softmax_xent_kernel<float>, grid, 256, 0, m->stream, m->logits, C, (long long)m->batch * C, nullptr,
                                                               m->batch, C, static_cast<float*>(m->dz[0]), ldz(m, m->L),
-                                                              (long long)m->batch * m->maxw, m->loss_part, m->sp);
+                                                              (long long)m->batch * m->maxw, m->loss_part, m->sp));
     NN_CUDA(cudaEventRecord(e[m->L + 1], m->stream));
     int cur = 0;
     for (int l = m->L - 1; l >= 0; --l) {

@@ -19,6 +19,8 @@
 // MN-major operands are read by TMA in 64-element-wide boxes and described
 // to the MMA as MN-major canonical layouts, so no transposed copies exist.
 #pragma once
+#include <cstdlib>
+#include <utility>
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -165,6 +167,30 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+
+// Launches a kernel that starts with pdl_enter() with programmatic stream
+// serialization (PDL): it may start while the previous kernel on the stream
+// drains and waits in pdl_enter() (griddepcontrol.wait) before its first
+// global access.  DSX_PDL=0: plain launches.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  static const bool on = [] {
+    const char* e = std::getenv("DSX_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = on ? at : nullptr;
+  cfg.numAttrs = on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))

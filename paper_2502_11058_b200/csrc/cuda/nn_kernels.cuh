@@ -40,6 +40,7 @@ __global__ void softmax_xent_kernel(const float* __restrict__ logits, long long 
                                     const int* __restrict__ labels_arg, int batch, int C, T* __restrict__ dz,
                                     long long ld_dz, long long s_dz, float* __restrict__ loss_part,
                                     const StepDev* __restrict__ sp) {
+  pdl_enter();
   const int* __restrict__ labels = sp ? sp->labels : labels_arg;
   const int b = blockIdx.y;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -64,6 +65,7 @@ __global__ void softmax_xent_kernel(const float* __restrict__ logits, long long 
 
 // loss[b] = mean over the batch of loss_part (fixed order)
 __global__ void loss_mean_kernel(const float* __restrict__ part, int batch, float* __restrict__ loss) {
+  pdl_enter();
   const int b = blockIdx.x;
   __shared__ float sh[256];
   float s = 0.f;
@@ -83,6 +85,7 @@ __global__ void loss_mean_kernel(const float* __restrict__ part, int batch, floa
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ dz, long long ld, long long s_dz, int rows,
                                                      int n_out, float* __restrict__ db, long long s_db) {
+  pdl_enter();
   __shared__ float part[8][33];
   const int b = blockIdx.y;
   const int cx = threadIdx.x & 31, rg = threadIdx.x >> 5;
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(256) optimizer_kernel(float* __restrict__ w, c
                                                         float* __restrict__ m, float* __restrict__ v,
                                                         __nv_bfloat16* __restrict__ wb, long long ld, long long lo,
                                                         long long n, OptArgs o, const StepDev* __restrict__ sp) {
+  pdl_enter();
   if (sp) {
     o.lr = sp->lr;
     o.bc1 = sp->bc1;
@@ -252,6 +256,7 @@ __global__ void nn_link_spin_kernel(unsigned long long ns) {
 // the step's input batch -> act[0] (bf16 for the tensor-core path)
 template <typename T>
 __global__ void load_x_kernel(const StepDev* __restrict__ sp, T* __restrict__ y, long long n) {
+  pdl_enter();
   const float* __restrict__ x = sp->x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] = from_f<T>(x[i]);
