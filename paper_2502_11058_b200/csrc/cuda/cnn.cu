@@ -94,6 +94,7 @@ __device__ __forceinline__ void set_el(Vec8<T>& v, int j, float x) {
 template <typename T>
 __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ col, int B, int H, int W, int C, int Ho, int Wo,
                               int k, int stride, int pad, long long sx, long long scol) {
+  pdl_enter();
   const int cv = C / 8;
   const long long Kc = (long long)k * k * C;
   const int total = B * Ho * Wo * k * k * cv;  // < 2^31 (host-checked): 32-bit index math
@@ -133,6 +134,7 @@ __global__ void col2im_kernel(const T* __restrict__ dcol, T* __restrict__ dx, in
                               int Wo, int k, int stride, int pad, const T* __restrict__ add,
                               const T* __restrict__ mask, long long sdcol, long long sx,
                               const T* __restrict__ sub2) {
+  pdl_enter();
   // 32-bit index math (the host keeps B*H*W*C/8 < 2^31): 64-bit divisions
   // had made this gather 7x slower than its bytes
   const int cv = C / 8;
@@ -194,6 +196,7 @@ __global__ void col2im_kernel(const T* __restrict__ dcol, T* __restrict__ dx, in
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ dz, long long ld, long long s_dz,
                                                           int rows, int C, int chunk_rows, float* __restrict__ part) {
+  pdl_enter();
   __shared__ float sh[2048];
   const int b = blockIdx.y;
   const int tpr = C / 8, rows_par = max(1, 256 / tpr);
@@ -234,6 +237,7 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ 
 // (split order fixed; reads coalesced over o)
 __global__ void splitk_reduce_t_kernel(const float* __restrict__ part, int ks, long long s_split, int rows, int cout,
                                        float* __restrict__ out, long long s_out) {
+  pdl_enter();
   const long long b = blockIdx.y, n = (long long)rows * cout;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(i / cout), o = (int)(i % cout);
@@ -255,6 +259,7 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ part, int ks, l
 template <typename T>
 __global__ void pool_fwd_kernel(const T* __restrict__ y, T* __restrict__ p, int B, int HW, int C, long long sy,
                                 long long sp) {
+  pdl_enter();
   const int b = blockIdx.x, w = blockIdx.y;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float s = 0.f;
@@ -268,6 +273,7 @@ __global__ void pool_fwd_kernel(const T* __restrict__ y, T* __restrict__ p, int 
 template <typename T>
 __global__ void pool_bwd_kernel(const T* __restrict__ dp, const T* __restrict__ y, T* __restrict__ gy, int B, int HW,
                                 int C, long long sdp, long long sy) {
+  pdl_enter();
   const long long n = (long long)B * HW * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
@@ -282,6 +288,7 @@ __global__ void pool_bwd_kernel(const T* __restrict__ dp, const T* __restrict__ 
 template <typename T>
 __global__ void load_image_kernel(const StepDev* __restrict__ sp, T* __restrict__ x0, long long pixels, int cin,
                                   int cp, long long sx) {
+  pdl_enter();
   const float* __restrict__ x = sp->x + blockIdx.y * pixels * cin;
   T* __restrict__ xw = x0 + blockIdx.y * sx;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < pixels * cp;
@@ -423,13 +430,13 @@ dsx_status conv_forward(dsx_cnn* m, const Conv& cv) {
   }
   const int grid = blocks_for(M * cv.k * cv.k * (cv.cin / 8), m->nsm) / std::max(1, m->kl) + 1;
   if (m->bf16)
-    im2col_kernel<__nv_bfloat16><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
+    CN_CUDA(launch_pdl(im2col_kernel<__nv_bfloat16>, dim3(grid, m->kl), 256, 0, m->stream, 
         static_cast<const __nv_bfloat16*>(cv.in), static_cast<__nv_bfloat16*>(cv.col), m->batch, cv.H, cv.W, cv.cin,
-        cv.Ho, cv.Wo, cv.k, cv.stride, cv.pad, m->act_max, cv.col_stride);
+        cv.Ho, cv.Wo, cv.k, cv.stride, cv.pad, m->act_max, cv.col_stride));
   else
-    im2col_kernel<float><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
+    CN_CUDA(launch_pdl(im2col_kernel<float>, dim3(grid, m->kl), 256, 0, m->stream, 
         static_cast<const float*>(cv.in), static_cast<float*>(cv.col), m->batch, cv.H, cv.W, cv.cin, cv.Ho, cv.Wo,
-        cv.k, cv.stride, cv.pad, m->act_max, cv.col_stride);
+        cv.k, cv.stride, cv.pad, m->act_max, cv.col_stride));
   ++m->launches;
   GemmCall c = cbase(m);
   c.A = cv.col;
@@ -506,9 +513,9 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
     CN_TRY(conv_gemm(c, geom(m, cv, kConvWgradT), m->stream, m->nsm));
     const long long nk = (M + kBK - 1) / kBK, kper = (nk + ks - 1) / ks;
     const long long n = (long long)cv.cout * Kc;
-    splitk_reduce_t_kernel<<<dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream>>>(
+    CN_CUDA(launch_pdl(splitk_reduce_t_kernel, dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream, 
         m->wpart, (int)((nk + kper - 1) / kper), c.g.strideSplit, (int)Kc, cv.cout, m->grads + m->off[cv.layer],
-        m->P);
+        m->P));
     ++m->launches;
   } else if (cv.implicit) {
     GemmCall c = cbase(m);
@@ -535,8 +542,8 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
     if (ks > 1) {
       const long long nk = (M + kBK - 1) / kBK, kper = (nk + ks - 1) / ks;
       const long long n = (long long)cv.cout * Kc;
-      splitk_reduce_kernel<<<dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream>>>(
-          m->wpart, (int)((nk + kper - 1) / kper), c.g.strideSplit, n, m->grads + m->off[cv.layer], m->P);
+      CN_CUDA(launch_pdl(splitk_reduce_kernel, dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream, 
+          m->wpart, (int)((nk + kper - 1) / kper), c.g.strideSplit, n, m->grads + m->off[cv.layer], m->P));
       ++m->launches;
     }
   } else {
@@ -573,8 +580,8 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
       const long long nk = ((long long)M + kBK - 1) / kBK, kper = (nk + ks - 1) / ks;
       const int ks_eff = (int)((nk + kper - 1) / kper);
       const long long n = (long long)cv.cout * Kc;
-      splitk_reduce_kernel<<<dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream>>>(
-          m->wpart, ks_eff, c.g.strideSplit, n, m->grads + m->off[cv.layer], m->P);
+      CN_CUDA(launch_pdl(splitk_reduce_kernel, dim3(blocks_for(n, m->nsm) / m->kl + 1, m->kl), 256, 0, m->stream, 
+          m->wpart, ks_eff, c.g.strideSplit, n, m->grads + m->off[cv.layer], m->P));
       ++m->launches;
     }
   }
@@ -591,14 +598,14 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
       CN_CUDA(cudaMemcpy2DAsync(m->grads + m->boff[cv.layer], 4ull * m->P, db_from, 4ull * m->P, 4ull * cv.cout,
                                 m->kl, cudaMemcpyDeviceToDevice, m->stream));
     } else if (m->bf16)
-      colsum_part_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(static_cast<const __nv_bfloat16*>(g), cv.cout,
-                                                                     m->act_max, (int)M, cv.cout, chunk_rows, m->cpart);
+      CN_CUDA(launch_pdl(colsum_part_kernel<__nv_bfloat16>, grid, 256, 0, m->stream, static_cast<const __nv_bfloat16*>(g), cv.cout,
+                                                                     m->act_max, (int)M, cv.cout, chunk_rows, m->cpart));
     else
-      colsum_part_kernel<float><<<grid, 256, 0, m->stream>>>(static_cast<const float*>(g), cv.cout, m->act_max,
-                                                             (int)M, cv.cout, chunk_rows, m->cpart);
+      CN_CUDA(launch_pdl(colsum_part_kernel<float>, grid, 256, 0, m->stream, static_cast<const float*>(g), cv.cout, m->act_max,
+                                                             (int)M, cv.cout, chunk_rows, m->cpart));
     if (!db_from) {
-      splitk_reduce_kernel<<<dim3((cv.cout + 63) / 64, m->kl), 64, 0, m->stream>>>(
-          m->cpart, nchunks, (long long)m->kl * cv.cout, cv.cout, m->grads + m->boff[cv.layer], m->P);
+      CN_CUDA(launch_pdl(splitk_reduce_kernel, dim3((cv.cout + 63) / 64, m->kl), 64, 0, m->stream, 
+          m->cpart, nchunks, (long long)m->kl * cv.cout, cv.cout, m->grads + m->boff[cv.layer], m->P));
       m->launches += 2;
     }
   }
@@ -647,8 +654,8 @@ dsx_status conv_backward(dsx_cnn* m, const Conv& cv, const void* g, void* dx, co
   const long long lo = m->off[cv.layer], n = m->boff[cv.layer] + cv.cout - lo;
   const long long want = (n / 8 + 255) / 256;
   dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(want, (long long)m->nsm * 8 / m->kl)), m->kl);
-  optimizer_kernel<<<grid, 256, 0, m->stream>>>(m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P,
-                                                lo, n, o, sp);
+  CN_CUDA(launch_pdl(optimizer_kernel, grid, 256, 0, m->stream, m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P,
+                                                lo, n, o, sp));
   ++m->launches;
   CN_CUDA(cudaGetLastError());
   if (dgrad && !cv.implicit_dg && !raw) return col2im(m, cv, dx, add, mask, sub2);
@@ -660,15 +667,15 @@ dsx_status col2im(dsx_cnn* m, const Conv& cv, void* dx, const void* add, const v
   const long long total = (long long)m->batch * cv.H * cv.W * (cv.cin / 8);
   const int grid = blocks_for(total, m->nsm) / std::max(1, m->kl) + 1;
   if (m->bf16)
-    col2im_kernel<__nv_bfloat16><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
+    CN_CUDA(launch_pdl(col2im_kernel<__nv_bfloat16>, dim3(grid, m->kl), 256, 0, m->stream, 
         static_cast<const __nv_bfloat16*>(m->gcol), static_cast<__nv_bfloat16*>(dx), m->batch, cv.H, cv.W, cv.cin,
         cv.Ho, cv.Wo, cv.k, cv.stride, cv.pad, static_cast<const __nv_bfloat16*>(add),
-        static_cast<const __nv_bfloat16*>(mask), m->col_max, m->act_max, static_cast<const __nv_bfloat16*>(sub2));
+        static_cast<const __nv_bfloat16*>(mask), m->col_max, m->act_max, static_cast<const __nv_bfloat16*>(sub2)));
   else
-    col2im_kernel<float><<<dim3(grid, m->kl), 256, 0, m->stream>>>(
+    CN_CUDA(launch_pdl(col2im_kernel<float>, dim3(grid, m->kl), 256, 0, m->stream, 
         static_cast<const float*>(m->gcol), static_cast<float*>(dx), m->batch, cv.H, cv.W, cv.cin, cv.Ho, cv.Wo, cv.k,
         cv.stride, cv.pad, static_cast<const float*>(add), static_cast<const float*>(mask), m->col_max, m->act_max,
-        static_cast<const float*>(sub2));
+        static_cast<const float*>(sub2)));
   ++m->launches;
   CN_CUDA(cudaGetLastError());
   return DSX_OK;
@@ -705,11 +712,11 @@ dsx_status forward(dsx_cnn* m, bool wait_syncs) {
   const long long pixels = (long long)m->batch * m->image * m->image;
   const dim3 lgrid(blocks_for(pixels * m->cp, m->nsm) / m->kl + 1, m->kl);
   if (m->bf16)
-    load_image_kernel<__nv_bfloat16><<<lgrid, 256, 0, m->stream>>>(m->sp, static_cast<__nv_bfloat16*>(m->x0),
-                                                                   pixels, m->cin, m->cp, m->act_max);
+    CN_CUDA(launch_pdl(load_image_kernel<__nv_bfloat16>, lgrid, 256, 0, m->stream, m->sp, static_cast<__nv_bfloat16*>(m->x0),
+                                                                   pixels, m->cin, m->cp, m->act_max));
   else
-    load_image_kernel<float><<<lgrid, 256, 0, m->stream>>>(m->sp, static_cast<float*>(m->x0), pixels, m->cin,
-                                                           m->cp, m->act_max);
+    CN_CUDA(launch_pdl(load_image_kernel<float>, lgrid, 256, 0, m->stream, m->sp, static_cast<float*>(m->x0), pixels, m->cin,
+                                                           m->cp, m->act_max));
   ++m->launches;
   auto wait_layer = [&](int l) -> dsx_status {
     if (wait_syncs && m->synced_prev[l]) CN_CUDA(cudaStreamWaitEvent(m->stream, m->ev_sync[l], 0));
@@ -745,13 +752,13 @@ dsx_status forward(dsx_cnn* m, bool wait_syncs) {
   const Conv& lc = m->convs[last.b];
   const int C = lc.cout, HW = lc.Ho * lc.Wo;
   if (m->bf16)
-    pool_fwd_kernel<__nv_bfloat16><<<dim3(m->batch, m->kl), 256, 0, m->stream>>>(
+    CN_CUDA(launch_pdl(pool_fwd_kernel<__nv_bfloat16>, dim3(m->batch, m->kl), 256, 0, m->stream, 
         static_cast<const __nv_bfloat16*>(last.y), static_cast<__nv_bfloat16*>(m->pool), m->batch, HW, C, m->act_max,
-        (long long)m->batch * C);
+        (long long)m->batch * C));
   else
-    pool_fwd_kernel<float><<<dim3(m->batch, m->kl), 256, 0, m->stream>>>(
+    CN_CUDA(launch_pdl(pool_fwd_kernel<float>, dim3(m->batch, m->kl), 256, 0, m->stream, 
         static_cast<const float*>(last.y), static_cast<float*>(m->pool), m->batch, HW, C, m->act_max,
-        (long long)m->batch * C);
+        (long long)m->batch * C));
   ++m->launches;
   const int hl = m->L - 1;
   CN_TRY(wait_layer(hl));
@@ -796,14 +803,14 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
   {
     dim3 grid((m->batch * 32 + 255) / 256, m->kl);
     if (m->bf16)
-      softmax_xent_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(
+      CN_CUDA(launch_pdl(softmax_xent_kernel<__nv_bfloat16>, grid, 256, 0, m->stream, 
           m->logits, C, (long long)m->batch * C, nullptr, m->batch, C, static_cast<__nv_bfloat16*>(m->dlog),
-          ld_classes(m), (long long)m->batch * ld_classes(m), m->loss_part, m->sp);
+          ld_classes(m), (long long)m->batch * ld_classes(m), m->loss_part, m->sp));
     else
-      softmax_xent_kernel<float><<<grid, 256, 0, m->stream>>>(m->logits, C, (long long)m->batch * C, nullptr, m->batch,
+      CN_CUDA(launch_pdl(softmax_xent_kernel<float>, grid, 256, 0, m->stream, m->logits, C, (long long)m->batch * C, nullptr, m->batch,
                                                               C, static_cast<float*>(m->dlog), ld_classes(m),
-                                                              (long long)m->batch * ld_classes(m), m->loss_part, m->sp);
-    loss_mean_kernel<<<m->kl, 256, 0, m->stream>>>(m->loss_part, m->batch, m->loss);
+                                                              (long long)m->batch * ld_classes(m), m->loss_part, m->sp));
+    CN_CUDA(launch_pdl(loss_mean_kernel, m->kl, 256, 0, m->stream, m->loss_part, m->batch, m->loss));
     m->launches += 2;
   }
   if (m->prof) CN_CUDA(cudaEventRecord(m->pb[m->L], m->stream));
@@ -855,13 +862,13 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     CN_TRY(gemm(c, m->stream, m->nsm));
     dim3 grid((C + 31) / 32, m->kl);
     if (m->bf16)
-      colsum_kernel<__nv_bfloat16><<<grid, 256, 0, m->stream>>>(static_cast<const __nv_bfloat16*>(m->dlog),
+      CN_CUDA(launch_pdl(colsum_kernel<__nv_bfloat16>, grid, 256, 0, m->stream, static_cast<const __nv_bfloat16*>(m->dlog),
                                                                 ld_classes(m), (long long)m->batch * ld_classes(m),
-                                                                m->batch, C, m->grads + m->boff[hl], m->P);
+                                                                m->batch, C, m->grads + m->boff[hl], m->P));
     else
-      colsum_kernel<float><<<grid, 256, 0, m->stream>>>(static_cast<const float*>(m->dlog), ld_classes(m),
+      CN_CUDA(launch_pdl(colsum_kernel<float>, grid, 256, 0, m->stream, static_cast<const float*>(m->dlog), ld_classes(m),
                                                         (long long)m->batch * ld_classes(m), m->batch, C,
-                                                        m->grads + m->boff[hl], m->P);
+                                                        m->grads + m->boff[hl], m->P));
     ++m->launches;
     GemmCall d = cbase(m);
     d.a_mn = false;
@@ -884,20 +891,20 @@ dsx_status step_impl(dsx_cnn* m, double lr, long long t, const unsigned char* ma
     ++m->launches;
     CN_TRY(gemm(d, m->stream, m->nsm));
     const long long lo = m->off[hl], n = m->packed[hl + 1] - m->packed[hl];
-    optimizer_kernel<<<dim3((unsigned)std::max<long long>(1, (n / 8 + 255) / 256), m->kl), 256, 0, m->stream>>>(
-        m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P, lo, n, o, m->sp);
+    CN_CUDA(launch_pdl(optimizer_kernel, dim3((unsigned)std::max<long long>(1, (n / 8 + 255) / 256), m->kl), 256, 0, m->stream, 
+        m->params, m->grads, m->mom, m->var, m->bf16 ? m->pbf : nullptr, m->P, lo, n, o, m->sp));
     ++m->launches;
     CN_TRY(done_layer(hl));
     if (m->bf16)
-      pool_bwd_kernel<__nv_bfloat16><<<dim3(blocks_for((long long)m->batch * HW * Cl, m->nsm), m->kl), 256, 0,
-                                       m->stream>>>(static_cast<const __nv_bfloat16*>(m->dpool),
+      CN_CUDA(launch_pdl(pool_bwd_kernel<__nv_bfloat16>, dim3(blocks_for((long long)m->batch * HW * Cl, m->nsm), m->kl), 256, 0,
+                                       m->stream, static_cast<const __nv_bfloat16*>(m->dpool),
                                                     static_cast<const __nv_bfloat16*>(last.y),
                                                     static_cast<__nv_bfloat16*>(m->g0), m->batch, HW, Cl,
-                                                    (long long)m->batch * Cl, m->act_max);
+                                                    (long long)m->batch * Cl, m->act_max));
     else
-      pool_bwd_kernel<float><<<dim3(blocks_for((long long)m->batch * HW * Cl, m->nsm), m->kl), 256, 0, m->stream>>>(
+      CN_CUDA(launch_pdl(pool_bwd_kernel<float>, dim3(blocks_for((long long)m->batch * HW * Cl, m->nsm), m->kl), 256, 0, m->stream, 
           static_cast<const float*>(m->dpool), static_cast<const float*>(last.y), static_cast<float*>(m->g0),
-          m->batch, HW, Cl, (long long)m->batch * Cl, m->act_max);
+          m->batch, HW, Cl, (long long)m->batch * Cl, m->act_max));
     ++m->launches;
   }
   // blocks, last to first.  ga = dL/d(block output) * (block output > 0) —

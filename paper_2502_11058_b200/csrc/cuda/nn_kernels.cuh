@@ -267,6 +267,7 @@ __global__ void load_x_kernel(const StepDev* __restrict__ sp, T* __restrict__ y,
 // in split order (deterministic); n elements per batch entry (blockIdx.y)
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int ks, long long s_split, long long n,
                                      float* __restrict__ out, long long s_out) {
+  pdl_enter();
   const long long b = blockIdx.y;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     // 8 loads in flight, summed in split order
